@@ -33,7 +33,7 @@ CORE     := $(PKG)/_core$(PY_EXT)
 PARITY   := $(PKG)/libparity.so
 ORACLE   := oracle/liboracle.so
 
-all: $(LIB) $(CORE) $(PARITY) $(ORACLE)
+all: $(LIB) $(PARITY) $(ORACLE)
 
 build/host/%.o: $(CSRC)/host/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
@@ -48,7 +48,7 @@ build/kernels/%.o: $(CSRC)/kernels/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(LIB): $(HOST_OBJ) $(ENG_OBJ) $(KER_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -soname=libklotski.so -lcudart_static -lcuda -ldl -lrt -lpthread \
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -soname=libklotski.so -lcudart_static -ldl -lrt -lpthread \
 	    -L$(CUDA)/lib64/stubs
 
 $(CORE): $(CSRC)/bindings/core.cpp $(LIB) $(HDRS)

@@ -1,0 +1,158 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * klotski/kernels.h — C-ABI of the hand-written sm_100a kernels behind the
+ * Klotski layer-execution path. One entry point per compute op kind of the
+ * reference schedule (proj/include/moesim/schedule.hpp:32-45), which the
+ * reference only *prices* in its simulator (proj/src/simulator.cpp:13-17):
+ *
+ *   compute_gate      (schedule.cpp:340-353)  -> kl_gate_topk
+ *   compute_expert    (schedule.cpp:355-372)  -> kl_permute + kl_expert_ffn + kl_combine
+ *   compute_attention (schedule.cpp:313-338)  -> kl_rmsnorm, kl_gemm_bf16, kl_rope_kv_append,
+ *                                                kl_attn_decode / kl_attn_prefill
+ *   update_table / predict_hot (correlation.cpp:74-140, invoked from
+ *   make_table_prefetcher, schedule.cpp:60-91) -> kl_coact_update, kl_predict_scores
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers and sizes; bf16 tensors are passed as uint16_t*;
+ *   - caller-owned buffers, no hidden allocation, no host synchronisation;
+ *   - enqueue-only on `stream`; not thread-safe per stream;
+ *   - return 0 on success, a positive cudaError_t value on a CUDA failure,
+ *     or a negative KL_E* code for invalid arguments (no exceptions cross
+ *     the ABI; the C++ layer maps codes to moesim exceptions).
+ *   - row-major layouts; "K-major" weights are [out_features, in_features].
+ */
+#ifndef KLOTSKI_KERNELS_H
+#define KLOTSKI_KERNELS_H
+
+#include <stdint.h>
+
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KL_OK 0
+#define KL_EINVAL (-1)      /* bad shape / pointer / alignment */
+#define KL_EUNSUPPORTED (-2) /* shape outside what the kernel implements */
+#define KL_ENODEV (-3)      /* no sm_100 device / driver entry point missing */
+
+/* Version / capability probe. Returns the compiled ABI version. */
+int kl_abi_version(void);
+/* 1 if the current device is sm_100 and the kernels can launch, else 0. */
+int kl_device_supported(void);
+/* Human-readable message for a return code (static storage). */
+const char* kl_error_string(int code);
+
+/* ---- dense / grouped GEMM on tcgen05 (TMEM accumulators, TMA operands) ----
+ * C[M,N] = A[M,K] * B[N,K]^T, bf16 in, fp32 accumulate.
+ * epilogue: 0 = store bf16 C
+ *           1 = store bf16 (C + R)          (R: bf16 [M,N], may alias C)
+ *           2 = SwiGLU: B holds [W1; W3] stacked as two [N/2, K] halves at
+ *               b and b + (N/2)*K; out[m, j] = silu(acc1) * acc3, C is [M, N/2]
+ * Requirements: K % 64 == 0, N % 64 == 0 (N % 256 == 0 for epilogue 2),
+ * lda == K, ldb == K (contiguous rows), 16-byte aligned pointers.
+ * row_offset selects rows [row_offset, row_offset + M) of a taller A whose
+ * total row count is a_rows (used for expert-major permuted activations). */
+int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                 const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
+                 int epilogue, cudaStream_t stream);
+
+/* One expert's SwiGLU FFN over its contiguous rows of the permuted buffer:
+ *   H = silu(X W1^T) * (X W3^T)   (bf16 [M, f] scratch)
+ *   Y = H W2^T                     (bf16 rows [row_offset, row_offset+M) of y)
+ * w13 = [W1 (f x d); W3 (f x d)], w2 = d x f, all bf16 and contiguous
+ * (exactly moesim ModelSpec::expert_bytes = 3*d*f*2 bytes starting at w13
+ * when w2 == w13 + 2*f*d). h_scratch must hold M*f bf16. */
+int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
+                  int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
+                  uint16_t* y, cudaStream_t stream);
+
+/* ---- routing ----
+ * Fused RMSNorm + router + top-k for T tokens (one warp per token):
+ *   x2[t]   = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * norm_w)      (stored)
+ *   logit[t,e] = sum_i x2[t,i] * wg[e,i]   (fp32, fixed FMA + butterfly order,
+ *                                           mirrored bit-exactly by the oracle)
+ *   idx[t, 0..k-1]: top-k by logit, ties -> lower expert id
+ *   weight: score_mode 0 = softmax over the k selected logits (Mixtral),
+ *           score_mode 1 = softmax over all E logits, selected probs (DeepSeek)
+ * Also accumulates hist[e] += count (int32, atomics) if hist != NULL and
+ * records first_pos[e] = min token-major position (t*k+j) if first_pos != NULL
+ * (initialise first_pos to INT32_MAX). logits (fp32 [T,E]) may be NULL.
+ * Requirements: d % 256 == 0, E <= 64, k <= 8. */
+int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uint16_t* wg, int T, int d,
+                 int E, int k, float eps, int score_mode, uint16_t* x2, float* logits,
+                 int32_t* idx, float* weight, int32_t* hist, int32_t* first_pos,
+                 cudaStream_t stream);
+
+/* Stable counting sort of the R = T*k routed rows into expert-major order:
+ *   counts[e], offsets[e] (exclusive scan, offsets[E] = R),
+ *   pos[r] = offsets[e_r] + #{r' < r : e_r' == e_r},   row_token[pos[r]] = r / k,
+ *   xp[pos[r], :] = x2[r / k, :]   (vectorised 16-byte copies; xp may be NULL).
+ * workspace: >= kl_permute_workspace_bytes(R, E) bytes. */
+int64_t kl_permute_workspace_bytes(int64_t R, int E);
+int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uint16_t* x2, int d,
+               int32_t* counts, int32_t* offsets, int32_t* pos, int32_t* row_token,
+               uint16_t* xp, void* workspace, cudaStream_t stream);
+
+/* Weighted combine with residual:
+ *   out[t] = bf16( float(resid[t]) + sum_{j<k} weight[t,j] * float(y[pos[t*k+j]]) )
+ * accumulated in fp32 in j order (fmaf), mirrored bit-exactly by the oracle.
+ * out may alias resid. */
+int kl_combine(const uint16_t* y, const int32_t* pos, const float* weight,
+               const uint16_t* resid, int64_t T, int k, int d, uint16_t* out,
+               cudaStream_t stream);
+
+/* ---- correlation-aware prefetcher statistics (exact integer atomics) ----
+ * layer == 0: marginal[e] += 1 for every id in cur (prev ignored).
+ * layer  > 0: table[(layer-1)][a][b] += 1 for every token and every
+ *             (a in prev[t, :k], b in cur[t, :k]).  table: int64 [L-1][E][E]. */
+int kl_coact_update(const int32_t* prev, const int32_t* cur, int64_t T, int k, int E, int layer,
+                    int64_t* table, int64_t* marginal, cudaStream_t stream);
+/* score[b] = sum_a hist[a] * table[(layer-1)][a][b]  (layer > 0), int64. */
+int kl_predict_scores(const int32_t* hist, const int64_t* table, int E, int layer,
+                      int64_t* score, cudaStream_t stream);
+
+/* ---- attention block pieces ---- */
+/* out[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * w), d % 256 == 0. */
+int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps,
+               uint16_t* out, cudaStream_t stream);
+
+/* Rotary embedding on q/k of a fused qkv row [Hq*hd | Hkv*hd | Hkv*hd] at the
+ * token's absolute position, rope applied in place to q; roped k and v are
+ * written to the KV cache slot of that position. Cache layout per layer:
+ *   k_cache/v_cache: [n_seq][cap][Hkv][hd] bf16,
+ *   slot(p) = p < sink ? p : sink + (p - sink) % (cap - sink).
+ * pos[t] = absolute position, seq[t] = cache sequence index. For a prefill
+ * chunk whose last position is chunk_last_pos, only positions still retained
+ * after the chunk are written (p < sink or p > chunk_last_pos - (cap-sink)),
+ * so ring slots are never written twice; pass -1 for decode. */
+int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int hd, const int32_t* pos,
+                      const int32_t* seq, float rope_theta, uint16_t* k_cache,
+                      uint16_t* v_cache, int cap, int sink, int chunk_last_pos,
+                      cudaStream_t stream);
+
+/* Decode attention (one query token per sequence), GQA, over the retained
+ * slots of each sequence: min(pos+1, cap) slots (sink + sliding window).
+ * q: [T][Hq*hd] (stride q_stride elements), out: [T][Hq*hd] bf16. hd == 128. */
+int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
+                   int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache,
+                   const uint16_t* v_cache, int cap, int sink, float scale, uint16_t* out,
+                   cudaStream_t stream);
+
+/* Prefill (chunk) attention: T = n_seq * L query rows laid out [seq][L]; keys
+ * and values read from the same qkv rows (post-rope), causal with the same
+ * sink + window retention mask as decode (window = cap - sink). hd == 128. */
+int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap,
+                    int sink, float scale, uint16_t* out, cudaStream_t stream);
+
+/* Deterministic synthetic bf16 init on device: v[i] = N(0, std) from a
+ * SplitMix64 stream keyed by (seed, i) (Box-Muller), for weights/inputs. */
+int kl_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, float std_dev,
+                        cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KLOTSKI_KERNELS_H */

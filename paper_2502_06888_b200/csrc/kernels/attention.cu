@@ -1,0 +1,235 @@
+// SPDX-License-Identifier: Apache-2.0
+// K6: attention pieces for compute_attention (reference schedule.cpp:313-338,
+// priced as token_count * attn_per_token in simulator.cpp:15). The reference
+// models KV retention only as a cache-size cap (model.hpp:60-73,
+// KvRetentionPolicy::retained); here it is executed: each sequence keeps
+// `sink` leading positions plus a ring of `cap - sink` most recent ones, and
+// attention reads exactly the retained slots.
+//
+// Decode attention is HBM-bound (K and V of the retained slots are read once
+// per (token, kv head); query heads of one GQA group share the reads through
+// L1): algorithmic bytes per (sequence, layer) = retained * Hkv*hd*2 * 2.
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace kl {
+namespace {
+
+__device__ __forceinline__ int slot_of(int p, int cap, int sink) {
+    return p < sink ? p : sink + (p - sink) % (cap - sink);
+}
+
+// qkv row layout: [Hq*hd | Hkv*hd | Hkv*hd]. One thread per (token, head, pair).
+__global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq, int Hkv, int hd,
+                                   const int32_t* __restrict__ pos, const int32_t* __restrict__ seq, float theta,
+                                   uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int cap, int sink,
+                                   int chunk_last_pos) {
+    const int half = hd / 2;
+    const int heads = Hq + Hkv;
+    const int64_t per_tok = static_cast<int64_t>(heads) * half + static_cast<int64_t>(Hkv) * half;
+    const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= T * per_tok) return;
+    const int64_t t = id / per_tok;
+    int64_t rem = id % per_tok;
+    const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * hd;
+    uint16_t* row = qkv + t * width;
+    const int p = pos[t];
+    const int slot = slot_of(p, cap, sink);
+    const bool to_cache = chunk_last_pos < 0 || p < sink || p > chunk_last_pos - (cap - sink);
+    const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot) * Hkv * hd;
+    if (rem < static_cast<int64_t>(heads) * half) {
+        const int head = static_cast<int>(rem / half);
+        const int i = static_cast<int>(rem % half);
+        const float inv = powf(theta, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
+        float sn, cs;
+        sincosf(static_cast<float>(p) * inv, &sn, &cs);
+        uint16_t* base = row + static_cast<int64_t>(head) * hd;
+        const float a = bf2f(base[i]), b = bf2f(base[i + half]);
+        const uint16_t ra = f2bf(a * cs - b * sn);
+        const uint16_t rb = f2bf(b * cs + a * sn);
+        base[i] = ra;
+        base[i + half] = rb;
+        if (head >= Hq && to_cache) {  // rotated key -> cache
+            uint16_t* dst = kc + cache_row + static_cast<int64_t>(head - Hq) * hd;
+            dst[i] = ra;
+            dst[i + half] = rb;
+        }
+    } else {
+        rem -= static_cast<int64_t>(heads) * half;
+        if (!to_cache) return;
+        const int kvh = static_cast<int>(rem / half);
+        const int i = static_cast<int>(rem % half);
+        const uint16_t* src = row + static_cast<int64_t>(Hq + Hkv + kvh) * hd;
+        uint16_t* dst = vc + cache_row + static_cast<int64_t>(kvh) * hd;
+        dst[i] = src[i];
+        dst[i + half] = src[i + half];
+    }
+}
+
+// One CTA per (token, kv head); warp g handles query head kvh*G + g.
+// Phase 1: lane-per-slot scores; phase 2: warp softmax; phase 3: P.V with
+// each lane owning 4 of the 128 head dims.
+__global__ void attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
+                                   const int32_t* __restrict__ seq, int Hq, int Hkv, const uint16_t* __restrict__ kc,
+                                   const uint16_t* __restrict__ vc, int cap, int sink, float scale,
+                                   uint16_t* __restrict__ out) {
+    constexpr int HD = 128;
+    extern __shared__ float sc[];  // [G][cap]
+    const int t = blockIdx.x;
+    const int kvh = blockIdx.y;
+    const int G = Hq / Hkv;
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qh = kvh * G + g;
+    const int p = pos[t];
+    const int n = p + 1 < cap ? p + 1 : cap;  // retained slots (all valid)
+    const int64_t seq_base = static_cast<int64_t>(seq[t]) * cap * Hkv * HD;
+    float* s = sc + g * cap;
+
+    // Query head in registers (fp32), 128 dims.
+    const uint16_t* qp = q + static_cast<int64_t>(t) * q_stride + static_cast<int64_t>(qh) * HD;
+    float qv[HD];
+#pragma unroll
+    for (int c = 0; c < HD; c += 8) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(qp + c));
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            qv[c + 2 * i] = bf2f(static_cast<uint16_t>(ws[i] & 0xffffu)) * scale;
+            qv[c + 2 * i + 1] = bf2f(static_cast<uint16_t>(ws[i] >> 16)) * scale;
+        }
+    }
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) {
+        const uint16_t* kp = kc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD;
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < HD; c += 8) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(kp + c));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc = fmaf(qv[c + 2 * i], bf2f(static_cast<uint16_t>(ws[i] & 0xffffu)), acc);
+                acc = fmaf(qv[c + 2 * i + 1], bf2f(static_cast<uint16_t>(ws[i] >> 16)), acc);
+            }
+        }
+        s[j] = acc;
+        mx = fmaxf(mx, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j = lane; j < n; j += 32) {
+        const float e = __expf(s[j] - mx);
+        s[j] = e;
+        sum += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncwarp();
+    const float inv = 1.0f / sum;
+    float o4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < n; ++j) {
+        const uint16_t* vp = vc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD + lane * 4;
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(vp));
+        const float pj = s[j];
+        o4[0] = fmaf(pj, bf2f(static_cast<uint16_t>(w.x & 0xffffu)), o4[0]);
+        o4[1] = fmaf(pj, bf2f(static_cast<uint16_t>(w.x >> 16)), o4[1]);
+        o4[2] = fmaf(pj, bf2f(static_cast<uint16_t>(w.y & 0xffffu)), o4[2]);
+        o4[3] = fmaf(pj, bf2f(static_cast<uint16_t>(w.y >> 16)), o4[3]);
+    }
+    uint16_t* op = out + static_cast<int64_t>(t) * Hq * HD + static_cast<int64_t>(qh) * HD + lane * 4;
+    *reinterpret_cast<uint2*>(op) = make_uint2(pack2(o4[0] * inv, o4[1] * inv), pack2(o4[2] * inv, o4[3] * inv));
+}
+
+// Prefill: one warp per (query row, q head); keys from the same chunk's qkv
+// rows; causal with sink + sliding-window retention; online softmax.
+__global__ void attn_prefill_kernel(const uint16_t* __restrict__ qkv, int n_seq, int L, int Hq, int Hkv, int cap,
+                                    int sink, float scale, uint16_t* __restrict__ out) {
+    constexpr int HD = 128;
+    const int64_t wid = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = static_cast<int64_t>(n_seq) * L;
+    if (wid >= rows * Hq) return;
+    const int64_t row = wid / Hq;
+    const int qh = static_cast<int>(wid % Hq);
+    const int sq = static_cast<int>(row / L), i = static_cast<int>(row % L);
+    const int kvh = qh / (Hq / Hkv);
+    const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * HD;
+    const uint16_t* qp = qkv + row * width + static_cast<int64_t>(qh) * HD + lane * 4;
+    const uint2 qw = *reinterpret_cast<const uint2*>(qp);
+    const float q0 = bf2f(qw.x & 0xffffu) * scale, q1 = bf2f(qw.x >> 16) * scale;
+    const float q2 = bf2f(qw.y & 0xffffu) * scale, q3 = bf2f(qw.y >> 16) * scale;
+    const int window = cap - sink;
+    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    for (int j = 0; j <= i; ++j) {
+        const bool kept = j < sink || j > i - window;
+        if (!kept) continue;
+        const int64_t krow = (static_cast<int64_t>(sq) * L + j) * width;
+        const uint2 kw = *reinterpret_cast<const uint2*>(qkv + krow + static_cast<int64_t>(Hq + kvh) * HD + lane * 4);
+        float dot = q0 * bf2f(kw.x & 0xffffu) + q1 * bf2f(kw.x >> 16) + q2 * bf2f(kw.y & 0xffffu) +
+                    q3 * bf2f(kw.y >> 16);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const float nm = fmaxf(m, dot);
+        const float corr = __expf(m - nm), pj = __expf(dot - nm);
+        const uint2 vw =
+            *reinterpret_cast<const uint2*>(qkv + krow + static_cast<int64_t>(Hq + Hkv + kvh) * HD + lane * 4);
+        o0 = o0 * corr + pj * bf2f(vw.x & 0xffffu);
+        o1 = o1 * corr + pj * bf2f(vw.x >> 16);
+        o2 = o2 * corr + pj * bf2f(vw.y & 0xffffu);
+        o3 = o3 * corr + pj * bf2f(vw.y >> 16);
+        l = l * corr + pj;
+        m = nm;
+    }
+    const float inv = 1.0f / l;
+    uint16_t* op = out + row * Hq * HD + static_cast<int64_t>(qh) * HD + lane * 4;
+    *reinterpret_cast<uint2*>(op) = make_uint2(pack2(o0 * inv, o1 * inv), pack2(o2 * inv, o3 * inv));
+}
+
+}  // namespace
+}  // namespace kl
+
+using namespace kl;
+
+extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int hd, const int32_t* pos,
+                                 const int32_t* seq, float rope_theta, uint16_t* k_cache, uint16_t* v_cache, int cap,
+                                 int sink, int chunk_last_pos, cudaStream_t stream) {
+    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || hd % 2 || cap <= sink || sink < 0) return KL_EINVAL;
+    if (!qkv || !pos || !seq || !k_cache || !v_cache) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
+    rope_append_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(qkv, T, Hq, Hkv, hd, pos, seq,
+                                                                               rope_theta, k_cache, v_cache, cap, sink,
+                                                                               chunk_last_pos);
+    return check_launch();
+}
+
+extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq, int64_t T,
+                              int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache, int cap,
+                              int sink, float scale, uint16_t* out, cudaStream_t stream) {
+    if (hd != 128) return KL_EUNSUPPORTED;
+    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 32 || cap <= sink || !q || !pos || !seq || !out)
+        return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int G = Hq / Hkv;
+    const size_t smem = static_cast<size_t>(G) * cap * sizeof(float);
+    if (smem > 200 * 1024) return KL_EUNSUPPORTED;
+    if (smem > 48 * 1024)
+        KL_CUDA_TRY(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    attn_decode_kernel<<<dim3(static_cast<unsigned>(T), Hkv), 32 * G, smem, stream>>>(
+        q, q_stride, pos, seq, Hq, Hkv, k_cache, v_cache, cap, sink, scale, out);
+    return check_launch();
+}
+
+extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap, int sink,
+                               float scale, uint16_t* out, cudaStream_t stream) {
+    if (hd != 128) return KL_EUNSUPPORTED;
+    if (n_seq < 0 || L < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || !qkv || !out) return KL_EINVAL;
+    const int64_t warps = static_cast<int64_t>(n_seq) * L * Hq;
+    if (warps == 0) return KL_OK;
+    attn_prefill_kernel<<<static_cast<int>((warps + 7) / 8), 256, 0, stream>>>(qkv, n_seq, L, Hq, Hkv, cap, sink,
+                                                                              scale, out);
+    return check_launch();
+}

@@ -1,0 +1,434 @@
+// SPDX-License-Identifier: Apache-2.0
+// Routing-path kernels (all HBM/latency bound, CUDA cores):
+//   K1 kl_gate_topk      fused RMSNorm + router logits + top-k + weights +
+//                        per-batch histogram / first-demand positions
+//                        (reference op compute_gate, schedule.cpp:340-353;
+//                         first-demand order = batch_demand, schedule.cpp:448-454)
+//   K4 kl_permute        stable counting sort into expert-major rows
+//                        (histogram = expert_load, trace.cpp:380-389)
+//   K7 kl_combine        weighted sum of expert rows + residual
+//   K2 kl_coact_update   co-activation counts (update_table, correlation.cpp:123-140)
+//   K3 kl_predict_scores hist . C_j (predict_hot 'sum' scores, correlation.cpp:74-121)
+//   kl_rmsnorm, kl_fill_normal_bf16
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace kl {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ void load8(const uint16_t* p, float (&v)[8]) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = bf2f(static_cast<uint16_t>(w[i] & 0xffffu));
+        v[2 * i + 1] = bf2f(static_cast<uint16_t>(w[i] >> 16));
+    }
+}
+
+// Warp-wide RMS of a bf16 row: sum of squares in a fixed order (lane-strided
+// 8-element chunks, then xor butterfly), returns rsqrt(mean + eps).
+__device__ __forceinline__ float row_rstd(const uint16_t* x, int d, float eps, int lane) {
+    float ss = 0.f;
+    for (int c = lane * 8; c < d; c += 256) {
+        float v[8];
+        load8(x + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    return rsqrtf(ss / static_cast<float>(d) + eps);
+}
+
+// Normalised row written as bf16: out = bf16((x * rstd) * w).
+__device__ __forceinline__ void write_normed(const uint16_t* x, const uint16_t* w, uint16_t* out, int d, float rstd,
+                                             int lane) {
+    for (int c = lane * 8; c < d; c += 256) {
+        float v[8], g[8];
+        load8(x + c, v);
+        load8(w + c, g);
+        uint4 o;
+        o.x = pack2(__fmul_rn(__fmul_rn(v[0], rstd), g[0]), __fmul_rn(__fmul_rn(v[1], rstd), g[1]));
+        o.y = pack2(__fmul_rn(__fmul_rn(v[2], rstd), g[2]), __fmul_rn(__fmul_rn(v[3], rstd), g[3]));
+        o.z = pack2(__fmul_rn(__fmul_rn(v[4], rstd), g[4]), __fmul_rn(__fmul_rn(v[5], rstd), g[5]));
+        o.w = pack2(__fmul_rn(__fmul_rn(v[6], rstd), g[6]), __fmul_rn(__fmul_rn(v[7], rstd), g[7]));
+        *reinterpret_cast<uint4*>(out + c) = o;
+    }
+}
+
+// One warp per token. Logit order (mirrored in oracle/numerics.c): lane l
+// accumulates fmaf over its chunks c = l*8 + 256*j, elements in order, then
+// an xor butterfly 16,8,4,2,1 with round-to-nearest adds.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ norm_w,
+                 const uint16_t* __restrict__ wg, int T, int d, int E, int k, float eps, int score_mode,
+                 uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
+                 float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp >= T) return;
+    const uint16_t* hrow = h + static_cast<int64_t>(warp) * d;
+    uint16_t* xrow = x2 + static_cast<int64_t>(warp) * d;
+    const float rstd = row_rstd(hrow, d, eps, lane);
+    write_normed(hrow, norm_w, xrow, d, rstd, lane);
+    __syncwarp();
+
+    __shared__ float sh_logit[kWarpsPerBlock][64];
+    float* lg = sh_logit[threadIdx.x >> 5];
+    for (int e0 = 0; e0 < E; e0 += 8) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int ne = E - e0 < 8 ? E - e0 : 8;
+        for (int c = lane * 8; c < d; c += 256) {
+            float xv[8];
+            // Re-read the just-written normalised row (same warp, after syncwarp).
+            const uint4 q = *reinterpret_cast<const uint4*>(xrow + c);
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                xv[2 * i] = bf2f(static_cast<uint16_t>(w4[i] & 0xffffu));
+                xv[2 * i + 1] = bf2f(static_cast<uint16_t>(w4[i] >> 16));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < ne) {
+                    float wv[8];
+                    load8(wg + static_cast<int64_t>(e0 + j) * d + c, wv);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[j] = fmaf(xv[i], wv[i], acc[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[j] = __fadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+            if (lane == 0 && j < ne) lg[e0 + j] = acc[j];
+        }
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    if (logits_out != nullptr)
+        for (int e = 0; e < E; ++e) logits_out[static_cast<int64_t>(warp) * E + e] = lg[e];
+    // Top-k: repeated arg-max, strict '>' so ties keep the lower expert id.
+    uint64_t taken = 0;
+    int sel[8];
+    float val[8];
+    for (int j = 0; j < k; ++j) {
+        int best = -1;
+        float bv = 0.f;
+        for (int e = 0; e < E; ++e) {
+            if ((taken >> e) & 1ull) continue;
+            if (best < 0 || lg[e] > bv) {
+                best = e;
+                bv = lg[e];
+            }
+        }
+        taken |= 1ull << best;
+        sel[j] = best;
+        val[j] = bv;
+    }
+    float wsum = 0.f;
+    float p[8];
+    if (score_mode == 0) {
+        for (int j = 0; j < k; ++j) {
+            p[j] = expf(val[j] - val[0]);
+            wsum += p[j];
+        }
+    } else {
+        float mx = lg[0];
+        for (int e = 1; e < E; ++e) mx = fmaxf(mx, lg[e]);
+        for (int e = 0; e < E; ++e) wsum += expf(lg[e] - mx);
+        for (int j = 0; j < k; ++j) p[j] = expf(val[j] - mx);
+    }
+    for (int j = 0; j < k; ++j) {
+        const int64_t r = static_cast<int64_t>(warp) * k + j;
+        idx[r] = sel[j];
+        weight[r] = p[j] / wsum;
+        if (hist != nullptr) atomicAdd(&hist[sel[j]], 1);
+        if (first_pos != nullptr) atomicMin(&first_pos[sel[j]], static_cast<int32_t>(r));
+    }
+}
+
+__global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int64_t T, int d,
+                               float eps, uint16_t* __restrict__ out) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const float rstd = row_rstd(x + row * d, d, eps, lane);
+    write_normed(x + row * d, w, out + row * d, d, rstd, lane);
+}
+
+// ---------------------------------------------------------------- permute --
+// Chunk of 1024 routed rows per CTA (32 warps): per-warp match_any ranks,
+// per-expert warp prefix in smem -> stable local rank within the chunk.
+constexpr int kChunk = 1024;
+
+__global__ void __launch_bounds__(kChunk)
+permute_rank_kernel(const int32_t* __restrict__ idx, int64_t R, int E, int32_t* __restrict__ chunk_counts,
+                    int32_t* __restrict__ local_rank) {
+    __shared__ int32_t warp_cnt[32][64];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
+    for (int i = threadIdx.x; i < 32 * 64; i += blockDim.x) (&warp_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const bool valid = r < R;
+    const int e = valid ? idx[r] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) warp_cnt[warp][e] = __popc(peers);
+    __syncthreads();
+    // Exclusive prefix over warps per expert (thread e scans column e).
+    if (threadIdx.x < E) {
+        int run = 0;
+        for (int w = 0; w < 32; ++w) {
+            const int c = warp_cnt[w][threadIdx.x];
+            warp_cnt[w][threadIdx.x] = run;
+            run += c;
+        }
+        chunk_counts[static_cast<int64_t>(blockIdx.x) * E + threadIdx.x] = run;
+    }
+    __syncthreads();
+    if (valid) local_rank[r] = warp_cnt[warp][e] + rank;
+}
+
+// One thread per expert: totals, exclusive offsets, per-chunk bases.
+__global__ void permute_scan_kernel(int32_t* __restrict__ chunk_counts, int64_t n_chunks, int E,
+                                    int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+    __shared__ int32_t total[64];
+    const int e = threadIdx.x;
+    if (e < E) {
+        int32_t run = 0;
+        for (int64_t c = 0; c < n_chunks; ++c) {
+            const int32_t v = chunk_counts[c * E + e];
+            chunk_counts[c * E + e] = run;  // becomes the within-expert chunk base
+            run += v;
+        }
+        total[e] = run;
+        if (counts != nullptr) counts[e] = run;
+    }
+    __syncthreads();
+    if (e == 0) {
+        int32_t acc = 0;
+        for (int i = 0; i < E; ++i) {
+            offsets[i] = acc;
+            acc += total[i];
+        }
+        offsets[E] = acc;
+    }
+    __syncthreads();
+    if (e < E) {
+        const int32_t base = offsets[e];
+        for (int64_t c = 0; c < n_chunks; ++c) chunk_counts[c * E + e] += base;
+    }
+}
+
+// One warp per routed row: position, inverse map, 16-byte vector row copy.
+__global__ void permute_scatter_kernel(const int32_t* __restrict__ idx, int64_t R, int k, int E,
+                                       const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ local_rank,
+                                       const uint16_t* __restrict__ x2, int d, int32_t* __restrict__ pos,
+                                       int32_t* __restrict__ row_token, uint16_t* __restrict__ xp) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const int e = idx[r];
+    const int32_t p = chunk_base[(r / kChunk) * E + e] + local_rank[r];
+    const int64_t t = r / k;
+    if (lane == 0) {
+        pos[r] = p;
+        if (row_token != nullptr) row_token[p] = static_cast<int32_t>(t);
+    }
+    if (xp != nullptr) {
+        const uint4* src = reinterpret_cast<const uint4*>(x2 + t * d);
+        uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<int64_t>(p) * d);
+        for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
+    }
+}
+
+// ---------------------------------------------------------------- combine --
+__global__ void combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
+                               const float* __restrict__ weight, const uint16_t* resid, int64_t T, int k, int d,
+                               uint16_t* out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    int32_t p[8];
+    float w[8];
+    for (int j = 0; j < k; ++j) {
+        p[j] = pos[t * k + j];
+        w[j] = weight[t * k + j];
+    }
+    for (int c = lane * 8; c < d; c += 256) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < k; ++j) {
+            float v[8];
+            load8(y + static_cast<int64_t>(p[j]) * d + c, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[j], v[i], acc[i]);
+        }
+        float rv[8];
+        const uint4 q = *reinterpret_cast<const uint4*>(resid + t * d + c);
+        const uint32_t rw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            rv[2 * i] = bf2f(static_cast<uint16_t>(rw[i] & 0xffffu));
+            rv[2 * i + 1] = bf2f(static_cast<uint16_t>(rw[i] >> 16));
+        }
+        uint4 o;
+        o.x = pack2(__fadd_rn(rv[0], acc[0]), __fadd_rn(rv[1], acc[1]));
+        o.y = pack2(__fadd_rn(rv[2], acc[2]), __fadd_rn(rv[3], acc[3]));
+        o.z = pack2(__fadd_rn(rv[4], acc[4]), __fadd_rn(rv[5], acc[5]));
+        o.w = pack2(__fadd_rn(rv[6], acc[6]), __fadd_rn(rv[7], acc[7]));
+        *reinterpret_cast<uint4*>(out + t * d + c) = o;
+    }
+}
+
+// ------------------------------------------------------------ prefetcher --
+__global__ void coact_kernel(const int32_t* __restrict__ prev, const int32_t* __restrict__ cur, int64_t T, int k,
+                             int E, int layer, int64_t* __restrict__ table, int64_t* __restrict__ marginal) {
+    extern __shared__ int32_t cnt[];  // E*E (or E for the marginal)
+    const int cells = layer == 0 ? E : E * E;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < T;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (layer == 0) {
+            for (int j = 0; j < k; ++j) atomicAdd(&cnt[cur[t * k + j]], 1);
+        } else {
+            for (int a = 0; a < k; ++a) {
+                const int pa = prev[t * k + a];
+                for (int b = 0; b < k; ++b) atomicAdd(&cnt[pa * E + cur[t * k + b]], 1);
+            }
+        }
+    }
+    __syncthreads();
+    int64_t* dst = layer == 0 ? marginal : table + static_cast<int64_t>(layer - 1) * E * E;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x)
+        if (cnt[i] != 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(dst + i), static_cast<unsigned long long>(cnt[i]));
+}
+
+__global__ void predict_kernel(const int32_t* __restrict__ hist, const int64_t* __restrict__ table, int E,
+                               int layer, int64_t* __restrict__ score) {
+    const int b = threadIdx.x;
+    if (b >= E) return;
+    const int64_t* tab = table + static_cast<int64_t>(layer - 1) * E * E;
+    int64_t s = 0;
+    for (int a = 0; a < E; ++a) s += static_cast<int64_t>(hist[a]) * tab[a * E + b];
+    score[b] = s;
+}
+
+// ------------------------------------------------------------ synthetic init --
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+__global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64_t seed, float sd) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t z = splitmix(seed ^ (static_cast<uint64_t>(i >> 1) * 0xd1b54a32d192ed03ULL));
+        const float u1 = (static_cast<float>(z >> 40) + 1.0f) * (1.0f / 16777217.0f);
+        const float u2 = static_cast<float>((z >> 16) & 0xffffffu) * (1.0f / 16777216.0f);
+        const float rad = sqrtf(-2.0f * logf(u1));
+        const float ang = 6.283185307179586f * u2;
+        const float v = (i & 1) ? rad * sinf(ang) : rad * cosf(ang);
+        dst[i] = f2bf(v * sd);
+    }
+}
+
+int grid_for(int64_t items, int per_block) {
+    const int64_t g = (items + per_block - 1) / per_block;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+}  // namespace kl
+
+using namespace kl;
+
+extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uint16_t* wg, int T, int d, int E, int k,
+                            float eps, int score_mode, uint16_t* x2, float* logits, int32_t* idx, float* weight,
+                            int32_t* hist, int32_t* first_pos, cudaStream_t stream) {
+    if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 64 || k < 1 || k > 8 || k > E) return KL_EINVAL;
+    if (!h || !norm_w || !wg || !x2 || !idx || !weight) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    gate_topk_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(
+        h, norm_w, wg, T, d, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);
+    return check_launch();
+}
+
+extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps, uint16_t* out,
+                          cudaStream_t stream) {
+    if (T < 0 || d <= 0 || d % 256 != 0 || !x || !w || !out) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    rmsnorm_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(x, w, T, d, eps, out);
+    return check_launch();
+}
+
+extern "C" int64_t kl_permute_workspace_bytes(int64_t R, int E) {
+    const int64_t chunks = (R + kChunk - 1) / kChunk;
+    return (chunks * E + R) * static_cast<int64_t>(sizeof(int32_t)) + 256;
+}
+
+extern "C" int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uint16_t* x2, int d, int32_t* counts,
+                          int32_t* offsets, int32_t* pos, int32_t* row_token, uint16_t* xp, void* workspace,
+                          cudaStream_t stream) {
+    if (T < 0 || k < 1 || E < 1 || E > 64 || !idx || !offsets || !pos || !workspace) return KL_EINVAL;
+    if (xp != nullptr && (x2 == nullptr || d % 8 != 0)) return KL_EINVAL;
+    const int64_t R = T * k;
+    const int64_t chunks = (R + kChunk - 1) / kChunk;
+    int32_t* chunk_counts = static_cast<int32_t*>(workspace);
+    int32_t* local_rank = chunk_counts + chunks * E;
+    if (R > 0) {
+        permute_rank_kernel<<<static_cast<int>(chunks), kChunk, 0, stream>>>(idx, R, E, chunk_counts, local_rank);
+        KL_CUDA_TRY(cudaGetLastError());
+    }
+    permute_scan_kernel<<<1, 64, 0, stream>>>(chunk_counts, chunks, E, counts, offsets);
+    KL_CUDA_TRY(cudaGetLastError());
+    if (R == 0) return KL_OK;
+    permute_scatter_kernel<<<grid_for(R, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(
+        idx, R, k, E, chunk_counts, local_rank, x2, d, pos, row_token, xp);
+    return check_launch();
+}
+
+extern "C" int kl_combine(const uint16_t* y, const int32_t* pos, const float* weight, const uint16_t* resid, int64_t T,
+                          int k, int d, uint16_t* out, cudaStream_t stream) {
+    if (T < 0 || k < 1 || k > 8 || d % 256 != 0 || !y || !pos || !weight || !resid || !out) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    combine_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(y, pos, weight, resid, T, k, d,
+                                                                                    out);
+    return check_launch();
+}
+
+extern "C" int kl_coact_update(const int32_t* prev, const int32_t* cur, int64_t T, int k, int E, int layer,
+                               int64_t* table, int64_t* marginal, cudaStream_t stream) {
+    if (T < 0 || k < 1 || E < 1 || E > 64 || layer < 0 || !cur) return KL_EINVAL;
+    if (layer == 0 ? marginal == nullptr : (table == nullptr || prev == nullptr)) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int cells = layer == 0 ? E : E * E;
+    const int blocks = static_cast<int>(T / 256 + 1 < 148 ? T / 256 + 1 : 148);
+    coact_kernel<<<blocks, 256, cells * sizeof(int32_t), stream>>>(prev, cur, T, k, E, layer, table, marginal);
+    return check_launch();
+}
+
+extern "C" int kl_predict_scores(const int32_t* hist, const int64_t* table, int E, int layer, int64_t* score,
+                                 cudaStream_t stream) {
+    if (E < 1 || E > 1024 || layer < 1 || !hist || !table || !score) return KL_EINVAL;
+    predict_kernel<<<1, E < 32 ? 32 : E, 0, stream>>>(hist, table, E, layer, score);
+    return check_launch();
+}
+
+extern "C" int kl_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, float std_dev, cudaStream_t stream) {
+    if (n < 0 || (n > 0 && dst == nullptr)) return KL_EINVAL;
+    if (n == 0) return KL_OK;
+    const int64_t blocks = (n + 255) / 256;
+    fill_normal_kernel<<<static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, stream>>>(dst, n, seed,
+                                                                                                      std_dev);
+    return check_launch();
+}

@@ -1,0 +1,164 @@
+"""ctypes bindings for include/klotski/kernels.h (the kernel C-ABI).
+
+Every function takes torch CUDA tensors, passes raw pointers + sizes to the
+C entry point on the current torch stream (or an explicit `stream` handle)
+and raises KernelError on a non-zero return code. No CPU fallback exists.
+"""
+import ctypes as C
+
+import torch
+
+from . import load_native
+
+_lib = load_native()
+
+_P = C.c_void_p
+_I = C.c_int
+_L = C.c_int64
+_F = C.c_float
+_U64 = C.c_uint64
+
+
+def _sig(name, args, res=C.c_int):
+    fn = getattr(_lib, name)
+    fn.argtypes = args
+    fn.restype = res
+    return fn
+
+
+_lib.kl_error_string.restype = C.c_char_p
+_lib.kl_error_string.argtypes = [_I]
+_gemm = _sig("kl_gemm_bf16", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P])
+_ffn = _sig("kl_expert_ffn", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P])
+_gate = _sig("kl_gate_topk", [_P, _P, _P, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P, _P])
+_perm_ws = _sig("kl_permute_workspace_bytes", [_L, _I], C.c_int64)
+_perm = _sig("kl_permute", [_P, _L, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P])
+_comb = _sig("kl_combine", [_P, _P, _P, _P, _L, _I, _I, _P, _P])
+_coact = _sig("kl_coact_update", [_P, _P, _L, _I, _I, _I, _P, _P, _P])
+_pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
+_rms = _sig("kl_rmsnorm", [_P, _P, _L, _I, _F, _P, _P])
+_rope = _sig("kl_rope_kv_append", [_P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _I, _I, _P])
+_dec = _sig("kl_attn_decode", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P])
+_pre = _sig("kl_attn_prefill", [_P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P])
+_fill = _sig("kl_fill_normal_bf16", [_P, _L, _U64, _F, _P])
+abi_version = _sig("kl_abi_version", [])
+device_supported = _sig("kl_device_supported", [])
+
+
+class KernelError(RuntimeError):
+    pass
+
+
+def _chk(rc, name):
+    if rc != 0:
+        raise KernelError(f"{name}: {_lib.kl_error_string(rc).decode()} (code {rc})")
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _s(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    return C.c_void_p(stream)
+
+
+def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None):
+    """C = A[row_offset:row_offset+m] @ B^T (bf16, fp32 accumulate) on tcgen05."""
+    m = a.shape[0] - row_offset if m is None else m
+    K = a.shape[1]
+    N = b.shape[0]
+    n_out = N // 2 if epilogue == 2 else N
+    if c is None:
+        c = torch.empty(m, n_out, dtype=torch.bfloat16, device=a.device)
+    _chk(_gemm(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue,
+               _s(stream)), "kl_gemm_bf16")
+    return c
+
+
+def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None):
+    d = xp.shape[1]
+    f = w2.shape[1]
+    _chk(_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _s(stream)),
+         "kl_expert_ffn")
+
+
+def gate_topk(h, norm_w, wg, k, eps=1e-5, score_mode=0, x2=None, logits=None, hist=None, first_pos=None,
+              stream=None):
+    T, d = h.shape
+    E = wg.shape[0]
+    dev = h.device
+    x2 = torch.empty_like(h) if x2 is None else x2
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    w = torch.empty(T, k, dtype=torch.float32, device=dev)
+    _chk(_gate(_p(h), _p(norm_w), _p(wg), T, d, E, k, eps, score_mode, _p(x2), _p(logits), _p(idx), _p(w),
+               _p(hist), _p(first_pos), _s(stream)), "kl_gate_topk")
+    return x2, idx, w
+
+
+def permute(idx, E, x2=None, stream=None, with_rows=True):
+    T, k = idx.shape
+    dev = idx.device
+    R = T * k
+    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    pos = torch.empty(R, dtype=torch.int32, device=dev)
+    row_token = torch.empty(R, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(_perm_ws(R, E)), dtype=torch.uint8, device=dev)
+    xp = None
+    d = 0
+    if x2 is not None and with_rows:
+        d = x2.shape[1]
+        xp = torch.empty(R, d, dtype=x2.dtype, device=dev)
+    _chk(_perm(_p(idx), T, k, E, _p(x2), d, _p(counts), _p(offsets), _p(pos), _p(row_token), _p(xp), _p(ws),
+               _s(stream)), "kl_permute")
+    return counts, offsets, pos, row_token, xp
+
+
+def combine(y, pos, weight, resid, out=None, stream=None):
+    T, k = weight.shape
+    d = resid.shape[1]
+    out = torch.empty_like(resid) if out is None else out
+    _chk(_comb(_p(y), _p(pos), _p(weight), _p(resid), T, k, d, _p(out), _s(stream)), "kl_combine")
+    return out
+
+
+def coact_update(prev, cur, E, layer, table, marginal, stream=None):
+    T, k = cur.shape
+    _chk(_coact(_p(prev), _p(cur), T, k, E, layer, _p(table), _p(marginal), _s(stream)), "kl_coact_update")
+
+
+def predict_scores(hist, table, E, layer, stream=None):
+    score = torch.empty(E, dtype=torch.int64, device=hist.device)
+    _chk(_pred(_p(hist), _p(table), E, layer, _p(score), _s(stream)), "kl_predict_scores")
+    return score
+
+
+def rmsnorm(x, w, eps=1e-5, out=None, stream=None):
+    out = torch.empty_like(x) if out is None else out
+    _chk(_rms(_p(x), _p(w), x.shape[0], x.shape[1], eps, _p(out), _s(stream)), "kl_rmsnorm")
+    return out
+
+
+def rope_kv_append(qkv, Hq, Hkv, hd, pos, seq, theta, k_cache, v_cache, cap, sink, chunk_last_pos=-1,
+                   stream=None):
+    _chk(_rope(_p(qkv), qkv.shape[0], Hq, Hkv, hd, _p(pos), _p(seq), theta, _p(k_cache), _p(v_cache), cap, sink,
+               chunk_last_pos, _s(stream)), "kl_rope_kv_append")
+
+
+def attn_decode(q, q_stride, pos, seq, Hq, Hkv, hd, k_cache, v_cache, cap, sink, scale, out, stream=None):
+    T = pos.shape[0]
+    _chk(_dec(_p(q), q_stride, _p(pos), _p(seq), T, Hq, Hkv, hd, _p(k_cache), _p(v_cache), cap, sink, scale,
+              _p(out), _s(stream)), "kl_attn_decode")
+    return out
+
+
+def attn_prefill(qkv, n_seq, L, Hq, Hkv, hd, cap, sink, scale, out, stream=None):
+    _chk(_pre(_p(qkv), n_seq, L, Hq, Hkv, hd, cap, sink, scale, _p(out), _s(stream)), "kl_attn_prefill")
+    return out
+
+
+def fill_normal(t, seed, std, stream=None):
+    _chk(_fill(_p(t), t.numel(), seed, std, _s(stream)), "kl_fill_normal_bf16")
+    return t
