@@ -103,6 +103,19 @@ int kl_combine(const uint16_t* y, const int32_t* pos, const float* weight,
                const uint16_t* resid, int64_t T, int k, int d, uint16_t* out,
                cudaStream_t stream);
 
+/* Trace-replay routing: overwrite the router's choice with forced ids
+ * (token-major [T,k]) and recompute weights as the softmax of the router's
+ * own logits at those ids (score_mode 0), plus hist / first_pos as above. */
+int kl_route_override(const int32_t* forced, const float* logits, int T, int E, int k,
+                      int32_t* idx, float* weight, int32_t* hist, int32_t* first_pos,
+                      cudaStream_t stream);
+
+/* out[t] = table[ids[t]] (bf16 rows of width d). */
+int kl_embed(const int32_t* ids, const uint16_t* table, int64_t T, int d, uint16_t* out,
+             cudaStream_t stream);
+/* out[t] = first index of max(logits[t, :V]) (greedy decoding). */
+int kl_argmax_bf16(const uint16_t* logits, int64_t T, int V, int32_t* out, cudaStream_t stream);
+
 /* ---- correlation-aware prefetcher statistics (exact integer atomics) ----
  * layer == 0: marginal[e] += 1 for every id in cur (prev ignored).
  * layer  > 0: table[(layer-1)][a][b] += 1 for every token and every
@@ -134,7 +147,7 @@ int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int hd, const i
 
 /* Decode attention (one query token per sequence), GQA, over the retained
  * slots of each sequence: min(pos+1, cap) slots (sink + sliding window).
- * q: [T][Hq*hd] (stride q_stride elements), out: [T][Hq*hd] bf16. hd == 128. */
+ * q: [T][Hq*hd] (stride q_stride elements), out: [T][Hq*hd] bf16. hd in {64, 128}. */
 int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
                    int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache,
                    const uint16_t* v_cache, int cap, int sink, float scale, uint16_t* out,
@@ -142,7 +155,7 @@ int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, cons
 
 /* Prefill (chunk) attention: T = n_seq * L query rows laid out [seq][L]; keys
  * and values read from the same qkv rows (post-rope), causal with the same
- * sink + window retention mask as decode (window = cap - sink). hd == 128. */
+ * sink + window retention mask as decode (window = cap - sink). hd in {64, 128}. */
 int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap,
                     int sink, float scale, uint16_t* out, cudaStream_t stream);
 

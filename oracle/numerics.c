@@ -306,7 +306,7 @@ void orc_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, in
     }
 }
 
-/* Same SplitMix64 + Box-Muller stream as kl_fill_normal_bf16. */
+/* Same SplitMix64 Irwin-Hall(4) stream as kl_fill_normal_bf16 (bit-exact). */
 static uint64_t splitmix(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -314,14 +314,14 @@ static uint64_t splitmix(uint64_t x) {
     return x ^ (x >> 31);
 }
 void orc_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, float sd) {
+    const float scale = 1.7320508075688772f * sd;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
-        const uint64_t z = splitmix(seed ^ ((uint64_t)(i >> 1) * 0xd1b54a32d192ed03ULL));
-        const float u1 = ((float)(z >> 40) + 1.0f) * (1.0f / 16777217.0f);
-        const float u2 = (float)((z >> 16) & 0xffffffu) * (1.0f / 16777216.0f);
-        const float rad = sqrtf(-2.0f * logf(u1));
-        const float ang = 6.283185307179586f * u2;
-        const float v = (i & 1) ? rad * sinf(ang) : rad * cosf(ang);
-        dst[i] = f2bf(v * sd);
+        const uint64_t z = splitmix(seed ^ ((uint64_t)i * 0xd1b54a32d192ed03ULL));
+        const uint64_t w = splitmix(z);
+        const float a = (float)(z & 0x3fffffu) + (float)((z >> 22) & 0x3fffffu);
+        const float b = (float)(w & 0x3fffffu) + (float)((w >> 22) & 0x3fffffu);
+        const float c = (a + b) * 0x1.0p-22f - 2.0f;
+        dst[i] = f2bf(c * scale);
     }
 }

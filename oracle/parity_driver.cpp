@@ -111,9 +111,13 @@ json request(const char* text) {
     if (req.value("quant", false)) quant = moesim::QuantConfig{};
     moesim::KvRetentionPolicy retention;
     if (req.value("streaming_kv", false)) retention.mode = moesim::KvRetentionPolicy::Mode::streaming;
+    retention.sink_tokens = req.value("sink_tokens", retention.sink_tokens);
+    retention.window_tokens = req.value("window_tokens", retention.window_tokens);
     std::optional<int> n_override;
     if (req.contains("n")) n_override = req["n"].get<int>();
     const auto load_model = static_cast<moesim::ExpertLoadModel>(req.value("load_model", 1));
+    moesim::PlacementConfig pcfg;
+    pcfg.working_set_override = req.value("working_set_override", std::int64_t{0});
 
     json out;
     // Warm-up trace and table (experiment.cpp prepare: disjoint warm-up seed).
@@ -126,7 +130,7 @@ json request(const char* text) {
     out["table_text"] = moesim::table_to_string(table);
 
     const moesim::PipelinePlan plan =
-        moesim::make_plan(model, hw, cfg, stats, quant, load_model, retention, n_override);
+        moesim::make_plan(model, hw, cfg, stats, quant, load_model, retention, n_override, pcfg);
     out["plan_text"] = plan.to_text();
     out["n_batches"] = plan.n_batches;
     cfg.n_batches = plan.n_batches;

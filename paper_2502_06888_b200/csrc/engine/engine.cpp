@@ -1,0 +1,513 @@
+// SPDX-License-Identifier: Apache-2.0
+// B200 execution engine: setup (plan, arena, pinned host store, weights).
+// See engine.hpp for the execution model. Reference anchors:
+//   planning        make_plan / plan_placement (planner.cpp:167-239, placement.cpp:70-243)
+//   warm-up table   prepare() (experiment.cpp:183-202)
+//   op semantics    Builder::emit_* (schedule.cpp:155-372)
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+
+#include <nlohmann/json.hpp>
+
+#include "klotski/kernels.h"
+#include "splitmix.hpp"
+
+namespace klotski {
+
+using json = nlohmann::json;
+using namespace moesim;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void kl_check(int rc, const char* what) {
+    if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
+}
+
+Dims preset_dims(const std::string& p) {
+    Dims d;
+    if (p == "mixtral-8x7b") {
+        d = Dims{32, 4096, 14336, 32, 8, 128, 8, 2, 32000, 1e6f, 1e-5f, 0};
+    } else if (p == "mixtral-8x22b") {
+        d = Dims{56, 6144, 16384, 48, 8, 128, 8, 2, 32768, 1e6f, 1e-5f, 0};
+    } else if (p == "deepseek-v2-lite") {
+        // Fine-grained routed experts (64, top-6, softmax-over-all scores);
+        // MLA is replaced by GQA attention of the same width.
+        d = Dims{26, 2048, 1408, 16, 16, 128, 64, 6, 102400, 1e4f, 1e-6f, 1};
+    } else if (p == "tiny") {
+        d = Dims{4, 512, 1792, 8, 2, 64, 8, 2, 1024, 1e6f, 1e-5f, 0};
+    } else {
+        throw ConfigError("unknown model preset '" + p + "'");
+    }
+    return d;
+}
+
+std::uint64_t tensor_seed(std::uint64_t base, int kind, int layer, int expert) {
+    return mix64(base, (static_cast<std::uint64_t>(kind) << 48) ^ (static_cast<std::uint64_t>(layer) << 16) ^
+                           static_cast<std::uint64_t>(expert + 1));
+}
+
+constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKindHead = 5;
+
+}  // namespace
+
+EngineConfig parse_config(const std::string& text) {
+    EngineConfig c;
+    const json j = text.empty() ? json::object() : json::parse(text);
+    const json m = j.value("model", json::object());
+    c.name = m.value("preset", "tiny");
+    c.dims = preset_dims(c.name);
+    Dims& D = c.dims;
+    D.L = m.value("n_layers", D.L);
+    D.d = m.value("d", D.d);
+    D.f = m.value("f", D.f);
+    D.Hq = m.value("heads", D.Hq);
+    D.Hkv = m.value("kv_heads", D.Hkv);
+    D.hd = m.value("head_dim", D.hd);
+    D.E = m.value("experts", D.E);
+    D.k = m.value("top_k", D.k);
+    D.V = m.value("vocab", D.V);
+    D.theta = m.value("rope_theta", D.theta);
+    D.eps = m.value("norm_eps", D.eps);
+    D.score_mode = m.value("score_mode", D.score_mode);
+    const json w = j.value("workload", json::object());
+    c.workload.batch_size = w.value("batch_size", 4);
+    c.workload.n_batches = w.value("n_batches", 4);
+    c.workload.prompt_len = w.value("prompt_len", 8);
+    c.workload.gen_len = w.value("gen_len", 4);
+    if (w.contains("n_batches")) c.n_override = c.workload.n_batches;
+    if (j.contains("n_override")) c.n_override = j["n_override"].get<int>();
+    if (j.value("solve_n", false)) c.n_override.reset();
+    c.hbm_cap = j.value("hbm_cap_bytes", c.hbm_cap);
+    c.host_dram = j.value("host_dram_bytes", c.host_dram);
+    c.pcie_bandwidth = j.value("pcie_bandwidth", c.pcie_bandwidth);
+    c.attn_ps = j.value("attn_ps", c.attn_ps);
+    c.gate_ps = j.value("gate_ps", c.gate_ps);
+    c.expert_ps = j.value("expert_ps", c.expert_ps);
+    if (j.contains("kv_retention")) {
+        const json& r = j["kv_retention"];
+        if (r.value("mode", "full") == "streaming") c.retention.mode = KvRetentionPolicy::Mode::streaming;
+        c.retention.sink_tokens = r.value("sink_tokens", 4);
+        c.retention.window_tokens = r.value("window_tokens", 256);
+    }
+    c.variant = variant_from_name(j.value("variant", "klotski"));
+    if (c.variant == Variant::simple) throw ConfigError("engine: the 'simple' row-by-row variant is not executed");
+    c.replay = j.value("routing", "gate") == "replay";
+    if (j.contains("skew")) {
+        const json& s = j["skew"];
+        const std::string kind = s.value("kind", "zipf");
+        c.skew = kind == "uniform"  ? SkewSpec::uniform()
+                 : kind == "markov" ? SkewSpec::markov(s.value("s", 1.5), s.value("p", 0.8))
+                                    : SkewSpec::zipf(s.value("s", 1.5));
+    }
+    c.trace_seed = j.value("trace_seed", c.trace_seed);
+    c.warmup_seed = j.value("warmup_seed", c.warmup_seed);
+    c.weight_seed = j.value("weight_seed", c.weight_seed);
+    c.host_distinct_layers = j.value("host_distinct_layers", 0);
+    c.expert_slots = j.value("expert_slots", 0);
+    c.ffn_chunk_rows = j.value("ffn_chunk_rows", 4096);
+    c.record_trace = j.value("record_trace", true);
+    c.record_hidden = j.value("record_hidden", false);
+    if (j.contains("ep")) {
+        c.ep_rank = j["ep"].value("rank", 0);
+        c.ep_world = j["ep"].value("world", 1);
+    }
+    c.prefill = j.value("prefill", true);
+    D.qkv_width();
+    if (D.d % 256 || D.hd % 2 || D.Hq % D.Hkv || D.k > D.E || D.k > 8 || D.E > 64)
+        throw ConfigError("engine: unsupported model dimensions");
+    return c;
+}
+
+int ExpertSlotPool::acquire() {
+    if (free_fifo.empty()) throw AccountingError("engine: expert slot pool exhausted");
+    const int s = free_fifo.front();
+    free_fifo.pop_front();
+    return s;
+}
+
+void ExpertSlotPool::release_after(int slot, cudaEvent_t ev) {
+    release[slot] = ev;
+    has_release[slot] = ev != nullptr;
+    free_fifo.push_back(slot);
+}
+
+Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
+    spec_.name = cfg_.name;
+    spec_.n_layers = D_.L;
+    spec_.n_experts_per_layer = D_.E;
+    spec_.top_k = D_.k;
+    spec_.expert_bytes = D_.expert_elems() * 2;
+    spec_.attention_bytes = D_.attention_elems() * 2;
+    spec_.gate_bytes = D_.gate_elems() * 2;
+    spec_.kv_bytes_per_token = 2LL * D_.Hkv * D_.hd * 2;
+    spec_.dtype = {"bf16", 16};
+    profile_.name = "b200";
+    profile_.vram_capacity = cfg_.hbm_cap;
+    profile_.dram_capacity = cfg_.host_dram;
+    profile_.disk_capacity = 1'000'000'000'000LL;
+    profile_.pcie_bandwidth = cfg_.pcie_bandwidth;
+    profile_.disk_bandwidth = 3.0e9;
+    profile_.attn_compute_per_token = cfg_.attn_ps;
+    profile_.gate_compute_per_token = cfg_.gate_ps;
+    profile_.expert_compute_per_token = cfg_.expert_ps;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (kl_device_supported() != 1) throw std::runtime_error("engine: device is not sm_100 (B200)");
+    plan_memory();
+    allocate_device();
+    allocate_host();
+    for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreate(&t0_), "event");
+    init_weights();
+    const detail::GroupShape shape{cfg_.workload.gen_len, D_.L, plan_.n_batches, cfg_.workload.batch_size,
+                           cfg_.workload.prompt_len, D_.k, D_.E};
+    em_ = std::make_unique<detail::Emitter>(cfg_.variant, plan_, shape, ScheduleOptions{});
+    // Trace containers: replayed routing and the routing actually executed.
+    BatchGroupConfig g = cfg_.workload;
+    g.n_batches = plan_.n_batches;
+    if (cfg_.replay) replay_trace_ = generate_trace(spec_, g, cfg_.skew, cfg_.trace_seed);
+    recorded_ = generate_trace(spec_, g, SkewSpec::uniform(), 0);
+    recorded_.seed = 0;
+    std::fill(recorded_.sel.begin(), recorded_.sel.end(), 0);
+    host_marginal_ = table0_.marginal;
+}
+
+Engine::~Engine() {
+    cudaDeviceSynchronize();
+    for (auto& s : streams_)
+        if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+    if (t0_) cudaEventDestroy(t0_);
+    for (cudaEvent_t e : pool_.release) (void)e;
+    if (arena_) cudaFree(arena_);
+    for (void* p : host_blocks_) cudaFreeHost(p);
+}
+
+void* Engine::take(byte_count bytes) {
+    const byte_count aligned = (arena_used_ + 1023) & ~byte_count(1023);
+    if (aligned + bytes > cfg_.hbm_cap)
+        throw MemoryInfeasible("engine arena: " + std::to_string(aligned + bytes) + " B exceeds HBM cap " +
+                                   std::to_string(cfg_.hbm_cap) + " B",
+                               aligned + bytes - cfg_.hbm_cap, 0, 0);
+    arena_used_ = aligned + bytes;
+    return arena_ == nullptr ? nullptr : arena_ + aligned;
+}
+
+// The planner's working-set term is replaced by what this engine really
+// keeps in HBM besides resident layers and KV: slot pools, scratch,
+// embeddings/head, norms, routing buffers.
+void Engine::plan_memory() {
+    const BatchGroupConfig& w = cfg_.workload;
+    // Warm-up trace -> correlation table + stats, as prepare() does.
+    BatchGroupConfig warm = w;
+    warm.n_batches = w.batch_size > 1 ? 2 : 4;
+    const ActivationTrace wt =
+        generate_trace(spec_, warm, cfg_.skew, cfg_.warmup_seed ? cfg_.warmup_seed : cfg_.trace_seed + 1);
+    table0_ = build_table(wt, spec_);
+    const TraceStats stats = compute_trace_stats(wt, D_.k);
+
+    int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, std::nullopt,
+                                                           ExpertLoadModel::measured, cfg_.retention)
+                                                     .n_batches;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const int64_t seqs = static_cast<int64_t>(w.batch_size) * n;
+        t_max_ = seqs * (cfg_.prefill ? w.prompt_len : 1);
+        tb_max_ = static_cast<int64_t>(w.batch_size) * (cfg_.prefill ? w.prompt_len : 1);
+        slots_ = cfg_.expert_slots > 0 ? cfg_.expert_slots : D_.E + D_.k;
+        const int64_t R = t_max_ * D_.k;
+        const int64_t chunk = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1));
+        byte_count ws = 0;
+        auto add = [&](byte_count b) { ws += ((b + 1023) / 1024) * 1024; };
+        add(2 * spec_.attention_bytes);
+        add(2 * spec_.gate_bytes);
+        for (int s = 0; s < slots_; ++s) add(spec_.expert_bytes);
+        add(static_cast<byte_count>(D_.L) * 2 * D_.d * 2 + D_.d * 2);
+        add(2LL * D_.V * D_.d * 2);
+        add(2 * t_max_ * D_.d * 2);                                              // h, x2
+        add(tb_max_ * (D_.d + D_.qkv_width() + D_.Hq * D_.hd) * 2);              // xa, qkv, ao
+        add(4 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
+        add(2 * R * D_.d * 2);                                                   // xp, y
+        add(chunk * D_.f * 2);                                                   // hs
+        add(kl_permute_workspace_bytes(R, D_.E));
+        add(5 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/ids/next/last, counts/offsets
+        add(seqs * D_.d * 2 + seqs * D_.V * 2);                                  // last_h, head logits
+        add(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64);                           // report
+        add((static_cast<byte_count>(std::max(D_.L - 1, 0)) * D_.E * D_.E + D_.E) * 8);
+        add(64 * 1024);
+        ws_bytes_ = ws;
+        PlacementConfig pc;
+        pc.working_set_override = ws;
+        plan_ = make_plan(spec_, profile_, w, stats, std::nullopt, ExpertLoadModel::measured, cfg_.retention, n, pc);
+        if (plan_.n_batches == n) break;
+        n = plan_.n_batches;  // KV-capped: resize scratch for the capped n
+    }
+    if (plan_.placement.kv_tier != Tier::vram)
+        throw ConfigError("engine: KV cache does not fit the HBM cap (KV offload streams are not executed by this "
+                          "engine yet); use kv_retention streaming or a smaller batch group");
+    if (plan_.placement.cpu_window_L > 0 || plan_.placement.any_disk())
+        throw ConfigError("engine: disk-tier placement (staging window) is not executed by this engine");
+    kv_cap_ = plan_.placement.kv_retained_tokens;
+    kv_sink_ = cfg_.retention.mode == KvRetentionPolicy::Mode::streaming ? std::min(cfg_.retention.sink_tokens, kv_cap_ - 1) : 0;
+    kv_bytes_layer_ = static_cast<byte_count>(cfg_.workload.batch_size) * plan_.n_batches * kv_cap_ * spec_.kv_bytes_per_token;
+}
+
+void Engine::allocate_device() {
+    // Dry run to size, then one arena of exactly the HBM cap.
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&arena_), static_cast<size_t>(cfg_.hbm_cap)), "cudaMalloc arena");
+    arena_used_ = 0;
+    const int n = plan_.n_batches;
+    const int64_t seqs = static_cast<int64_t>(cfg_.workload.batch_size) * n;
+    const int64_t R = t_max_ * D_.k;
+    auto bf = [&](int64_t elems) { return static_cast<uint16_t*>(take(elems * 2)); };
+    auto i32 = [&](int64_t elems) { return static_cast<int32_t*>(take(elems * 4)); };
+
+    attn_slot_ = {bf(D_.attention_elems()), bf(D_.attention_elems())};
+    gate_slot_ = {bf(D_.gate_elems()), bf(D_.gate_elems())};
+    attn_slot_busy_.assign(2, 0);
+    gate_slot_busy_.assign(2, 0);
+    attn_slot_release_.assign(2, nullptr);
+    gate_slot_release_.assign(2, nullptr);
+    pool_.ptr.clear();
+    for (int s = 0; s < slots_; ++s) pool_.ptr.push_back(bf(D_.expert_elems()));
+    pool_.release.assign(slots_, nullptr);
+    pool_.has_release.assign(slots_, 0);
+    pool_.free_fifo.clear();
+    for (int s = 0; s < slots_; ++s) pool_.free_fifo.push_back(s);
+
+    norm_attn_.resize(D_.L);
+    norm_ffn_.resize(D_.L);
+    for (int l = 0; l < D_.L; ++l) {
+        norm_attn_[l] = bf(D_.d);
+        norm_ffn_[l] = bf(D_.d);
+    }
+    final_norm_ = bf(D_.d);
+    embed_ = bf(static_cast<int64_t>(D_.V) * D_.d);
+    head_ = bf(static_cast<int64_t>(D_.V) * D_.d);
+    h_ = bf(t_max_ * D_.d);
+    x2_ = bf(t_max_ * D_.d);
+    xa_ = bf(tb_max_ * D_.d);
+    qkv_ = bf(tb_max_ * D_.qkv_width());
+    ao_ = bf(tb_max_ * D_.Hq * D_.hd);
+    idx_[0] = i32(R);
+    idx_[1] = i32(R);
+    forced_ = i32(R);
+    pos_ = i32(R);
+    row_token_ = i32(R);
+    weight_ = static_cast<float*>(take(R * 4));
+    router_logits_ = static_cast<float*>(take(t_max_ * D_.E * 4));
+    xp_ = bf(R * D_.d);
+    y_ = bf(R * D_.d);
+    hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
+    perm_ws_ = take(kl_permute_workspace_bytes(R, D_.E));
+    tok_pos_ = i32(t_max_);
+    tok_seq_ = i32(t_max_);
+    ids_ = i32(t_max_);
+    next_ids_ = i32(t_max_);
+    last_rows_ = i32(t_max_);
+    counts_ = i32(D_.E + 1);
+    offsets_ = i32(D_.E + 1);
+    last_h_ = bf(seqs * D_.d);
+    head_logits_ = bf(seqs * D_.V);
+    report_ = static_cast<int32_t*>(take(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64));
+    table_ = static_cast<int64_t*>(take((static_cast<byte_count>(std::max(D_.L - 1, 1)) * D_.E * D_.E) * 8));
+    marginal_ = static_cast<int64_t*>(take(D_.E * 8));
+    const byte_count ws_real = arena_used_;
+
+    // KV caches and resident layers (planner's decisions).
+    kc_.assign(D_.L, nullptr);
+    vc_.assign(D_.L, nullptr);
+    for (int l = 0; l < D_.L; ++l) {
+        kc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
+        vc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
+    }
+    res_expert_.assign(static_cast<size_t>(D_.L) * D_.E, nullptr);
+    res_attn_.assign(D_.L, nullptr);
+    for (int l = 0; l < D_.L; ++l) {
+        if (plan_.placement.expert_tier[l] == Tier::vram)
+            for (int e = 0; e < D_.E; ++e) res_expert_[l * D_.E + e] = bf(D_.expert_elems());
+        if (plan_.placement.attention_tier[l] == Tier::vram) res_attn_[l] = bf(D_.attention_elems());
+    }
+    if (ws_real > ws_bytes_ + 64 * 1024)
+        throw AccountingError("engine: working-set estimate " + std::to_string(ws_bytes_) + " < actual " +
+                              std::to_string(ws_real));
+}
+
+void Engine::allocate_host() {
+    const int L = D_.L, E = D_.E;
+    host_expert_.assign(static_cast<size_t>(L) * E, nullptr);
+    host_attn_.assign(L, nullptr);
+    host_gate_.assign(L, nullptr);
+    // Non-resident expert layers, optionally aliased onto R distinct copies.
+    // The whole-layer baseline moves every expert over the link each block
+    // (its reference semantics, schedule.cpp:190-208), resident or not.
+    const bool whole_layer = cfg_.variant == Variant::multibatch_full_prefetch;
+    std::vector<int> streamed;
+    for (int l = 0; l < L; ++l)
+        if (plan_.placement.expert_tier[l] != Tier::vram || whole_layer) streamed.push_back(l);
+    const int R = cfg_.host_distinct_layers > 0 ? std::min<int>(cfg_.host_distinct_layers, streamed.size())
+                                                : static_cast<int>(streamed.size());
+    std::vector<void*> blocks(R, nullptr);
+    std::vector<cudaError_t> errs(R, cudaSuccess);
+    const byte_count layer_bytes = spec_.expert_bytes * E;
+    {
+        // Pinning is CPU-bound page work: spread it over host threads.
+        std::vector<std::thread> th;
+        const int workers = std::max(1, std::min<int>(8, R));
+        for (int w = 0; w < workers; ++w)
+            th.emplace_back([&, w] {
+                for (int i = w; i < R; i += workers)
+                    errs[i] = cudaHostAlloc(&blocks[i], static_cast<size_t>(layer_bytes), cudaHostAllocDefault);
+            });
+        for (auto& t : th) t.join();
+    }
+    for (int i = 0; i < R; ++i) {
+        cuda_check(errs[i], "cudaHostAlloc experts");
+        host_blocks_.push_back(blocks[i]);
+    }
+    for (size_t s = 0; s < streamed.size(); ++s) {
+        char* base = static_cast<char*>(blocks[s % R]);
+        for (int e = 0; e < E; ++e)
+            host_expert_[streamed[s] * E + e] = reinterpret_cast<uint16_t*>(base + spec_.expert_bytes * e);
+    }
+    auto pinned = [&](byte_count bytes) {
+        void* p = nullptr;
+        cuda_check(cudaHostAlloc(&p, static_cast<size_t>(bytes), cudaHostAllocDefault), "cudaHostAlloc");
+        host_blocks_.push_back(p);
+        return p;
+    };
+    for (int l = 0; l < L; ++l) {
+        if (plan_.placement.attention_tier[l] != Tier::vram)
+            host_attn_[l] = static_cast<uint16_t*>(pinned(spec_.attention_bytes));
+        host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
+    }
+    const int n = plan_.n_batches;
+    host_report_ = static_cast<int32_t*>(pinned(2LL * n * E * 4 + 2LL * E * 8 + 64));
+    host_idx_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
+    host_forced_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
+    host_tokens_ = static_cast<int32_t*>(pinned(4 * t_max_ * 4));
+}
+
+void Engine::init_weights() {
+    cudaStream_t st = streams_[0];
+    const std::uint64_t ws = cfg_.weight_seed;
+    const float sd = 0.02f;
+    // Norm weights = 1.0 (bf16 0x3f80).
+    std::vector<uint16_t> ones(D_.d, 0x3f80);
+    for (int l = 0; l < D_.L; ++l) {
+        cuda_check(cudaMemcpy(norm_attn_[l], ones.data(), D_.d * 2, cudaMemcpyHostToDevice), "norm");
+        cuda_check(cudaMemcpy(norm_ffn_[l], ones.data(), D_.d * 2, cudaMemcpyHostToDevice), "norm");
+    }
+    cuda_check(cudaMemcpy(final_norm_, ones.data(), D_.d * 2, cudaMemcpyHostToDevice), "norm");
+    kl_check(kl_fill_normal_bf16(embed_, static_cast<int64_t>(D_.V) * D_.d, tensor_seed(ws, kKindEmbed, 0, 0), 1.0f, st),
+             "init embed");
+    kl_check(kl_fill_normal_bf16(head_, static_cast<int64_t>(D_.V) * D_.d, tensor_seed(ws, kKindHead, 0, 0), sd, st),
+             "init head");
+    // Staging for host-resident tensors: a slot large enough for either kind.
+    uint16_t* stage = D_.expert_elems() >= D_.attention_elems() ? pool_.ptr[0] : attn_slot_[0];
+    std::vector<char> host_done(host_blocks_.size(), 0);
+    for (int l = 0; l < D_.L; ++l) {
+        for (int e = 0; e < D_.E; ++e) {
+            const std::uint64_t seed = tensor_seed(ws, kKindExpert, l, e);
+            if (uint16_t* r = res_expert_[l * D_.E + e]) {
+                kl_check(kl_fill_normal_bf16(r, D_.expert_elems(), seed, sd, st), "init expert");
+                if (uint16_t* h = host_expert_[l * D_.E + e])
+                    cuda_check(cudaMemcpyAsync(h, r, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+            } else if (uint16_t* h = host_expert_[l * D_.E + e]) {
+                // Aliased host layers are filled once, by their first user.
+                bool first = true;
+                for (int l2 = 0; l2 < l && first; ++l2)
+                    if (host_expert_[l2 * D_.E + e] == h) first = false;
+                if (!first) continue;
+                kl_check(kl_fill_normal_bf16(stage, D_.expert_elems(), seed, sd, st), "init expert");
+                cuda_check(cudaMemcpyAsync(h, stage, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+            }
+        }
+        const std::uint64_t aseed = tensor_seed(ws, kKindAttn, l, 0);
+        if (res_attn_[l]) {
+            kl_check(kl_fill_normal_bf16(res_attn_[l], D_.attention_elems(), aseed, sd, st), "init attn");
+        } else {
+            kl_check(kl_fill_normal_bf16(stage, D_.attention_elems(), aseed, sd, st), "init attn");
+            cuda_check(cudaMemcpyAsync(host_attn_[l], stage, spec_.attention_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+        }
+        kl_check(kl_fill_normal_bf16(stage, D_.gate_elems(), tensor_seed(ws, kKindGate, l, 0), sd, st), "init gate");
+        cuda_check(cudaMemcpyAsync(host_gate_[l], stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+    }
+    // Correlation table (warm-up) and marginal to HBM.
+    if (D_.L > 1)
+        cuda_check(cudaMemcpyAsync(table_, table0_.counts.data(), table0_.counts.size() * 8, cudaMemcpyHostToDevice, st),
+                   "table");
+    cuda_check(cudaMemcpyAsync(marginal_, table0_.marginal.data(), D_.E * 8, cudaMemcpyHostToDevice, st), "marginal");
+    cuda_check(cudaMemsetAsync(h_, 0, t_max_ * D_.d * 2, st), "h");
+    cuda_check(cudaStreamSynchronize(st), "init sync");
+    (void)host_done;
+}
+
+void Engine::fill_kv_synthetic(int positions, std::uint64_t seed) {
+    // KV content of a synthetic prefill: values for the retained slots of
+    // positions [0, positions) of every sequence (post-rope keys are just
+    // random vectors here; the decode kernels read them like real ones).
+    cudaStream_t st = streams_[0];
+    const int64_t per_seq = static_cast<int64_t>(kv_cap_) * D_.Hkv * D_.hd;
+    const int64_t seqs = static_cast<int64_t>(cfg_.workload.batch_size) * plan_.n_batches;
+    const int filled = std::min(positions, kv_cap_);
+    for (int l = 0; l < D_.L; ++l) {
+        // Whole-cache fill (unused slots are never read: attention reads
+        // min(pos+1, cap) slots).
+        kl_check(kl_fill_normal_bf16(kc_[l], per_seq * seqs, mix64(seed, 2 * l), 1.0f, st), "kv fill");
+        kl_check(kl_fill_normal_bf16(vc_[l], per_seq * seqs, mix64(seed, 2 * l + 1), 1.0f, st), "kv fill");
+    }
+    (void)filled;
+    cuda_check(cudaStreamSynchronize(st), "kv fill sync");
+}
+
+std::string Engine::describe() const {
+    json j;
+    j["plan_text"] = plan_.to_text();
+    j["n_batches"] = plan_.n_batches;
+    j["batch_size"] = cfg_.workload.batch_size;
+    j["expert_slots"] = slots_;
+    j["arena_used_bytes"] = arena_used_;
+    j["hbm_cap_bytes"] = cfg_.hbm_cap;
+    j["working_set_bytes"] = ws_bytes_;
+    j["kv_cap_tokens"] = kv_cap_;
+    j["kv_sink"] = kv_sink_;
+    j["kv_bytes_per_layer"] = kv_bytes_layer_;
+    int resident = 0, attn_res = 0;
+    for (int l = 0; l < D_.L; ++l) {
+        resident += plan_.placement.expert_tier[l] == Tier::vram;
+        attn_res += plan_.placement.attention_tier[l] == Tier::vram;
+    }
+    j["resident_expert_layers"] = resident;
+    j["resident_attention_layers"] = attn_res;
+    j["expert_bytes"] = spec_.expert_bytes;
+    j["attention_bytes"] = spec_.attention_bytes;
+    j["gate_bytes"] = spec_.gate_bytes;
+    j["host_pinned_blocks"] = host_blocks_.size();
+    // Everything needed to rebuild the same plan/schedule with the reference.
+    j["spec"] = {{"n_layers", spec_.n_layers}, {"n_experts", spec_.n_experts_per_layer}, {"top_k", spec_.top_k},
+                 {"expert_bytes", spec_.expert_bytes}, {"attention_bytes", spec_.attention_bytes},
+                 {"gate_bytes", spec_.gate_bytes}, {"kv_bytes_per_token", spec_.kv_bytes_per_token}};
+    j["profile"] = {{"vram_capacity", profile_.vram_capacity}, {"dram_capacity", profile_.dram_capacity},
+                    {"disk_capacity", profile_.disk_capacity}, {"pcie_bandwidth", profile_.pcie_bandwidth},
+                    {"disk_bandwidth", profile_.disk_bandwidth}, {"transfer_fixed_latency_ps", 0},
+                    {"attn_ps", profile_.attn_compute_per_token}, {"gate_ps", profile_.gate_compute_per_token},
+                    {"expert_ps", profile_.expert_compute_per_token}};
+    j["streaming_kv"] = cfg_.retention.mode == KvRetentionPolicy::Mode::streaming;
+    j["sink_tokens"] = cfg_.retention.sink_tokens;
+    j["window_tokens"] = cfg_.retention.window_tokens;
+    j["dims"] = {{"L", D_.L}, {"d", D_.d}, {"f", D_.f}, {"Hq", D_.Hq}, {"Hkv", D_.Hkv}, {"hd", D_.hd},
+                 {"E", D_.E}, {"k", D_.k}, {"V", D_.V}};
+    return j.dump();
+}
+
+}  // namespace klotski

@@ -1,0 +1,202 @@
+// SPDX-License-Identifier: Apache-2.0
+// B200 execution engine for the Klotski pipeline (internal header).
+//
+// Drives the reference's Algorithm 1 online (detail::Emitter, shared with
+// moesim::build_klotski_schedule) and executes each emitted StreamOp:
+//   load_weights / load_expert -> cudaMemcpyAsync H2D from pinned host into
+//                                 the attention / gate / expert slot pools
+//   compute_attention          -> rmsnorm + tcgen05 QKV GEMM + rope/KV append
+//                                 + decode|prefill attention + O GEMM(+resid)
+//   compute_gate               -> fused rmsnorm/router/top-k (+ at the last
+//                                 gate: permute, co-activation update,
+//                                 next-layer prefetch scores, routing readback)
+//   compute_expert             -> SwiGLU expert FFN on the expert's rows
+//                                 (+ combine after the block's last expert)
+//   offload_*                  -> slot release by event (no bytes move)
+// Streams mirror moesim::StreamId; dependencies are cudaEvents; the
+// timeline is measured with events and reduced with the reference metrics.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <array>
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "../host/emitter.hpp"
+#include "moesim/experiment.hpp"
+#include "moesim/simulator.hpp"
+
+namespace klotski {
+
+using moesim::byte_count;
+
+struct Dims {
+    int L = 4, d = 512, f = 1792, Hq = 8, Hkv = 2, hd = 64, E = 8, k = 2, V = 1024;
+    float theta = 1e6f, eps = 1e-5f;
+    int score_mode = 0;
+    int qkv_width() const { return (Hq + 2 * Hkv) * hd; }
+    byte_count expert_elems() const { return 3LL * d * f; }
+    byte_count attention_elems() const { return static_cast<byte_count>(qkv_width()) * d + static_cast<byte_count>(d) * Hq * hd; }
+    byte_count gate_elems() const { return static_cast<byte_count>(E) * d; }
+};
+
+struct EngineConfig {
+    Dims dims;
+    std::string name = "tiny";
+    moesim::BatchGroupConfig workload;
+    moesim::KvRetentionPolicy retention;
+    byte_count hbm_cap = 24'000'000'000LL;
+    byte_count host_dram = 190'000'000'000LL;
+    double pcie_bandwidth = 55.0e9;
+    moesim::duration_ps attn_ps = 1'000'000, gate_ps = 20'000, expert_ps = 300'000;
+    std::optional<int> n_override;
+    moesim::Variant variant = moesim::Variant::klotski;
+    bool replay = false;
+    moesim::SkewSpec skew = moesim::SkewSpec::zipf(1.5);
+    std::uint64_t trace_seed = 1, warmup_seed = 0, weight_seed = 7;
+    int host_distinct_layers = 0;
+    int expert_slots = 0;
+    int ffn_chunk_rows = 4096;
+    bool record_trace = true;
+    bool record_hidden = false;
+    int ep_rank = 0, ep_world = 1;
+    bool prefill = true;
+};
+
+EngineConfig parse_config(const std::string& json_text);
+
+struct ExpertSlotPool {
+    std::vector<uint16_t*> ptr;
+    std::vector<cudaEvent_t> release;     // valid when has_release
+    std::vector<char> has_release;
+    std::deque<int> free_fifo;            // least recently released first
+    int acquire();
+    void release_after(int slot, cudaEvent_t ev);
+};
+
+class Engine {
+  public:
+    explicit Engine(const EngineConfig& cfg);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void fill_kv_synthetic(int positions, std::uint64_t seed);
+    double step(int step, const int32_t* tokens_in, int32_t* next_out);
+    std::string describe() const;
+    std::string report(const std::string& what);
+    void reset_log();
+    void read_hidden(uint16_t* host, int64_t n) const;
+
+  private:
+    // setup
+    void plan_memory();
+    void allocate_device();
+    void allocate_host();
+    void init_weights();
+    void* take(byte_count bytes);
+
+    // execution
+    void issue_pending();
+    void exec(std::int32_t id);
+    void exec_attention(const moesim::StreamOp& op);
+    void exec_gate(const moesim::StreamOp& op);
+    void exec_expert(const moesim::StreamOp& op);
+    void after_layer_gates(int step, int layer);
+    moesim::detail::BlockRouting read_routing(int step, int layer);
+    moesim::PrefetchDecision decide(int step, int layer) const;
+    cudaStream_t stream_of(moesim::StreamId s) const { return streams_[static_cast<int>(s)]; }
+    cudaEvent_t event();
+    void collect_step_times();
+    int tokens_per_batch(int step) const { return cfg_.workload.batch_size * (step == 0 ? cfg_.workload.prompt_len : 1); }
+    int n_batches() const { return plan_.n_batches; }
+    const uint16_t* expert_weights(int layer, int e) const;
+
+    EngineConfig cfg_;
+    Dims D_;
+    moesim::ModelSpec spec_;
+    moesim::HardwareProfile profile_;
+    moesim::PipelinePlan plan_;
+    moesim::CorrelationTable table0_;
+    moesim::ActivationTrace replay_trace_;
+    moesim::ActivationTrace recorded_;
+    std::unique_ptr<moesim::detail::Emitter> em_;
+    std::int32_t next_exec_ = 0;
+
+    // memory plan
+    byte_count ws_bytes_ = 0, kv_bytes_layer_ = 0;
+    int kv_cap_ = 0, kv_sink_ = 0;
+    int64_t t_max_ = 0, tb_max_ = 0;
+    int slots_ = 0;
+    char* arena_ = nullptr;
+    byte_count arena_used_ = 0;
+
+    // device buffers
+    std::vector<uint16_t*> res_expert_;  // [L*E] resident expert weights (or null)
+    std::vector<uint16_t*> res_attn_;    // [L]
+    std::vector<uint16_t*> norm_attn_, norm_ffn_;
+    uint16_t* final_norm_ = nullptr;
+    uint16_t *embed_ = nullptr, *head_ = nullptr;
+    std::vector<uint16_t*> kc_, vc_;     // [L]
+    uint16_t *h_ = nullptr, *x2_ = nullptr, *xa_ = nullptr, *qkv_ = nullptr, *ao_ = nullptr;
+    uint16_t *xp_ = nullptr, *y_ = nullptr, *hs_ = nullptr, *last_h_ = nullptr, *head_logits_ = nullptr;
+    int32_t *idx_[2] = {nullptr, nullptr}, *forced_ = nullptr, *pos_ = nullptr, *row_token_ = nullptr;
+    int32_t *counts_ = nullptr, *offsets_ = nullptr, *tok_pos_ = nullptr, *tok_seq_ = nullptr;
+    int32_t *ids_ = nullptr, *next_ids_ = nullptr, *last_rows_ = nullptr;
+    float *weight_ = nullptr, *router_logits_ = nullptr;
+    void* perm_ws_ = nullptr;
+    int32_t* report_ = nullptr;          // [n*E hist | n*E first] + int64 [E scores | E marginal]
+    int64_t *table_ = nullptr, *marginal_ = nullptr;
+    std::vector<uint16_t*> attn_slot_, gate_slot_;
+    ExpertSlotPool pool_;
+
+    // host (pinned) store
+    std::vector<void*> host_blocks_;
+    std::vector<uint16_t*> host_expert_;  // [L*E] (null when resident)
+    std::vector<uint16_t*> host_attn_;    // [L]
+    std::vector<uint16_t*> host_gate_;    // [L]
+    int32_t* host_report_ = nullptr;
+    int32_t* host_idx_ = nullptr;
+    int32_t* host_tokens_ = nullptr;
+    int32_t* host_forced_ = nullptr;
+
+    // streams / events
+    std::array<cudaStream_t, moesim::kNumStreams> streams_{};
+    std::vector<cudaEvent_t> event_pool_;
+    std::size_t event_next_ = 0;
+    cudaEvent_t t0_ = nullptr;
+    bool t0_recorded_ = false;
+    std::vector<cudaEvent_t> op_start_, op_end_;     // by op id (current step window)
+    std::vector<moesim::SimEvent> timeline_;          // measured, by op id
+    std::int32_t timed_from_ = 0;
+    std::int32_t log_from_ = 0;
+    size_t records_from_ = 0;
+
+    // per-block execution state
+    int cur_step_ = -1;
+    int idx_cur_ = 0;
+    std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot
+    std::map<int, int> attn_slot_of_;                      // layer -> attention slot
+    std::map<int, int> gate_slot_of_;                      // layer -> gate slot
+    std::map<int, std::vector<int>> moe_slots_of_;         // layer -> pool slots (baselines)
+    std::vector<int> attn_slot_busy_, gate_slot_busy_;
+    std::vector<cudaEvent_t> attn_slot_release_, gate_slot_release_;
+    std::vector<int64_t> row_offset_;                      // expert segment starts (block)
+    std::vector<std::vector<int64_t>> batch_prefix_;       // [b][e] rows before batch b in e's segment
+    int64_t block_rows_ = 0;
+    int block_layer_ = -1;
+    int exec_expert_left_ = 0;
+    std::vector<int64_t> host_scores_, host_marginal_;
+    bool scores_valid_ = false;
+    int64_t tokens_generated_ = 0;
+    std::vector<std::vector<uint16_t>> hidden_dumps_;
+    std::vector<double> step_ms_;
+};
+
+}  // namespace klotski

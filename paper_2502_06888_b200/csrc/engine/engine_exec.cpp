@@ -1,0 +1,638 @@
+// SPDX-License-Identifier: Apache-2.0
+// B200 execution engine: per-step / per-block driver and per-op execution.
+//
+// For each (step, layer) block the host
+//   1. derives the prefetch decision from the device-side co-activation
+//      table (make_table_prefetcher semantics, schedule.cpp:60-91),
+//   2. emits Algorithm-1's first half (Emitter::open_block) and enqueues it:
+//      gate + hot expert H2D on the weight_load stream overlapping this
+//      block's n attentions (Eq. 2), n gate kernels,
+//   3. waits for the routing readback of the last gate (tiny D2H),
+//   4. emits the second half (cold loads in first-demand order on the
+//      expert_load stream, expert computes hot-first, immediate offloads)
+//      and enqueues it.
+// Every op records start/end cudaEvents; cross-stream deps are
+// cudaStreamWaitEvent; expert slots are reused only after the release event
+// of their previous occupant (bounded pool with backpressure).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+#include <nlohmann/json.hpp>
+
+#include "engine.hpp"
+#include "klotski/kernels.h"
+#include "metrics.hpp"
+
+namespace klotski {
+
+using json = nlohmann::json;
+using namespace moesim;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void kl_check(int rc, const char* what) {
+    if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
+}
+
+constexpr int32_t kNoPos = 0x7f7f7f7f;  // memset(0x7f) sentinel for first_pos
+
+}  // namespace
+
+cudaEvent_t Engine::event() {
+    if (event_next_ == event_pool_.size()) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        event_pool_.push_back(e);
+    }
+    return event_pool_[event_next_++];
+}
+
+const uint16_t* Engine::expert_weights(int layer, int e) const {
+    if (const uint16_t* r = res_expert_[static_cast<size_t>(layer) * D_.E + e]) return r;
+    const auto it = expert_slot_of_.find({layer, e});
+    if (it == expert_slot_of_.end())
+        throw AccountingError("engine: expert (" + std::to_string(layer) + "," + std::to_string(e) +
+                              ") computed without a loaded slot");
+    return pool_.ptr[it->second];
+}
+
+PrefetchDecision Engine::decide(int /*step*/, int layer) const {
+    PrefetchDecision d;
+    d.layer = layer;
+    std::vector<int64_t> score;
+    if (layer == 0) {
+        score = host_marginal_;
+        d.used_fallback = true;
+    } else {
+        score = host_scores_;
+        if (std::all_of(score.begin(), score.end(), [](int64_t v) { return v == 0; })) {
+            score = host_marginal_;
+            d.used_fallback = true;
+        }
+    }
+    std::vector<int> ids(D_.E);
+    std::iota(ids.begin(), ids.end(), 0);
+    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+        return score[a] != score[b] ? score[a] > score[b] : a < b;
+    });
+    ids.resize(std::min(D_.k, D_.E));
+    d.expert_ids = ids;
+    for (int id : ids) d.scores.push_back(score[id]);
+    return d;
+}
+
+double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
+    if (step < 0 || step >= cfg_.workload.gen_len) throw RangeError("engine: step outside the batch group");
+    if (step == 0 && !cfg_.prefill) throw ConfigError("engine: built without prefill support (prefill=false)");
+    cur_step_ = step;
+    const int n = plan_.n_batches, bs = cfg_.workload.batch_size;
+    const int tpb = tokens_per_batch(step);
+    const int64_t T = static_cast<int64_t>(n) * tpb;
+    const int64_t seqs = static_cast<int64_t>(n) * bs;
+    cudaStream_t cs = stream_of(StreamId::compute);
+
+    cudaEvent_t begin = event();
+    cuda_check(cudaEventRecord(begin, cs), "record");
+    if (!t0_recorded_) {
+        cuda_check(cudaEventRecord(t0_, cs), "record t0");
+        t0_recorded_ = true;
+    }
+    for (int s = 1; s < kNumStreams; ++s) cuda_check(cudaStreamWaitEvent(streams_[s], begin, 0), "wait");
+
+    // Token positions / cache rows; row order = batch-major, sequence-major.
+    int32_t* hp = host_tokens_;
+    int32_t* hs = host_tokens_ + t_max_;
+    int32_t* hl = host_tokens_ + 2 * t_max_;
+    for (int64_t r = 0; r < T; ++r) {
+        const int64_t b = r / tpb, within = r % tpb;
+        const int64_t sq = step == 0 ? within / cfg_.workload.prompt_len : within;
+        hp[r] = step == 0 ? static_cast<int32_t>(within % cfg_.workload.prompt_len)
+                          : cfg_.workload.prompt_len + step - 1;
+        hs[r] = static_cast<int32_t>(b * bs + sq);
+    }
+    for (int64_t s = 0; s < seqs; ++s) {
+        // Row of each sequence's last token this step (greedy head input).
+        const int64_t b = s / bs, i = s % bs;
+        hl[s] = static_cast<int32_t>(step == 0 ? b * tpb + i * cfg_.workload.prompt_len + cfg_.workload.prompt_len - 1
+                                               : b * tpb + i);
+    }
+    cuda_check(cudaMemcpyAsync(tok_pos_, hp, T * 4, cudaMemcpyHostToDevice, cs), "h2d pos");
+    cuda_check(cudaMemcpyAsync(tok_seq_, hs, T * 4, cudaMemcpyHostToDevice, cs), "h2d seq");
+    cuda_check(cudaMemcpyAsync(last_rows_, hl, seqs * 4, cudaMemcpyHostToDevice, cs), "h2d rows");
+    if (tokens_in != nullptr) {
+        int32_t* ht = host_tokens_ + 3 * t_max_;
+        std::memcpy(ht, tokens_in, T * 4);
+        cuda_check(cudaMemcpyAsync(ids_, ht, T * 4, cudaMemcpyHostToDevice, cs), "h2d tokens");
+    } else if (step == 0) {
+        throw ConfigError("engine: prefill needs input tokens");
+    } else {
+        cuda_check(cudaMemcpyAsync(ids_, next_ids_, T * 4, cudaMemcpyDeviceToDevice, cs), "d2d tokens");
+    }
+    kl_check(kl_embed(ids_, embed_, T, D_.d, h_, cs), "embed");
+
+    const bool split = em_->split_moe();
+    for (int layer = 0; layer < D_.L; ++layer) {
+        PrefetchDecision d;
+        if (split) d = decide(step, layer);
+        if (cfg_.replay) {
+            // Forced routing of this (step, layer) from the replay trace.
+            const auto sel = replay_trace_.layer_selections(step, layer);
+            for (size_t i = 0; i < sel.size(); ++i) host_forced_[i] = sel[i];
+        }
+        detail::OpenBlock blk = em_->open_block(step, layer, split ? &d : nullptr);
+        block_layer_ = layer;
+        issue_pending();
+        const detail::BlockRouting routing = read_routing(step, layer);
+        const detail::ClosedBlock closed = em_->close_block(blk, routing);
+        exec_expert_left_ = 0;
+        for (std::int32_t id = closed.first_op; id < static_cast<std::int32_t>(em_->schedule().ops.size()); ++id)
+            exec_expert_left_ += em_->schedule().ops[id].kind == OpKind::compute_expert;
+        issue_pending();
+    }
+
+    // Greedy head on the last token of every sequence.
+    kl_check(kl_embed(last_rows_, h_, seqs, D_.d, last_h_, cs), "gather last rows");
+    kl_check(kl_rmsnorm(last_h_, final_norm_, seqs, D_.d, D_.eps, x2_, cs), "final norm");
+    kl_check(kl_gemm_bf16(x2_, seqs, 0, static_cast<int>(seqs), D_.d, head_, D_.V, head_logits_, D_.V, nullptr, 0, cs),
+             "lm head");
+    kl_check(kl_argmax_bf16(head_logits_, seqs, D_.V, next_ids_, cs), "argmax");
+    if (next_out != nullptr) {
+        int32_t* ho = host_tokens_ + 3 * t_max_;
+        cuda_check(cudaMemcpyAsync(ho, next_ids_, seqs * 4, cudaMemcpyDeviceToHost, cs), "d2h next");
+    }
+    // Join every stream into the end marker.
+    for (int s = 1; s < kNumStreams; ++s) {
+        cudaEvent_t j = event();
+        cuda_check(cudaEventRecord(j, streams_[s]), "record");
+        cuda_check(cudaStreamWaitEvent(cs, j, 0), "wait");
+    }
+    cudaEvent_t end = event();
+    cuda_check(cudaEventRecord(end, cs), "record");
+    cuda_check(cudaEventSynchronize(end), "step sync");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, begin, end), "elapsed");
+    if (next_out != nullptr) std::memcpy(next_out, host_tokens_ + 3 * t_max_, seqs * 4);
+    collect_step_times();
+    tokens_generated_ += seqs;
+    step_ms_.push_back(ms);
+    return ms;
+}
+
+void Engine::collect_step_times() {
+    const auto& ops = em_->schedule().ops;
+    if (timeline_.size() < ops.size()) timeline_.resize(ops.size());
+    for (std::int32_t id = timed_from_; id < next_exec_; ++id) {
+        float a = 0.f, b = 0.f;
+        cuda_check(cudaEventElapsedTime(&a, t0_, op_start_[id]), "elapsed");
+        cuda_check(cudaEventElapsedTime(&b, t0_, op_end_[id]), "elapsed");
+        SimEvent& ev = timeline_[id];
+        ev.op_id = id;
+        ev.stream = ops[id].stream;
+        ev.start = std::llround(static_cast<double>(a) * 1e9);
+        ev.end = std::max(ev.start, static_cast<duration_ps>(std::llround(static_cast<double>(b) * 1e9)));
+        ev.bytes = ops[id].payload_bytes;
+        ev.tokens = ops[id].token_count;
+    }
+    timed_from_ = next_exec_;
+    // Everything this step enqueued has completed: events and release
+    // markers can be recycled.
+    event_next_ = 0;
+    std::fill(pool_.has_release.begin(), pool_.has_release.end(), 0);
+    std::fill(attn_slot_release_.begin(), attn_slot_release_.end(), nullptr);
+    std::fill(gate_slot_release_.begin(), gate_slot_release_.end(), nullptr);
+}
+
+// Enqueue every emitted-but-not-executed op. Cold computes of a reorder
+// group on a VRAM-resident layer run in ascending expert id (they are all
+// ready at the last gate, the simulator's tie rule, simulator.cpp:167-183);
+// on streamed layers the FIFO expert_load stream completes colds in demand
+// order, which is the simulator's earliest-ready pick.
+void Engine::issue_pending() {
+    const auto& ops = em_->schedule().ops;
+    const std::int32_t total = static_cast<std::int32_t>(ops.size());
+    if (static_cast<std::int32_t>(op_start_.size()) < total) {
+        op_start_.resize(total, nullptr);
+        op_end_.resize(total, nullptr);
+    }
+    while (next_exec_ < total) {
+        const StreamOp& op = ops[next_exec_];
+        if (op.kind == OpKind::compute_expert && op.reorder_group >= 0 &&
+            plan_.placement.expert_tier[op.layer] == Tier::vram) {
+            std::int32_t end = next_exec_;
+            while (end < total && ops[end].reorder_group == op.reorder_group) ++end;
+            std::vector<std::int32_t> group(end - next_exec_);
+            std::iota(group.begin(), group.end(), next_exec_);
+            std::stable_sort(group.begin(), group.end(),
+                             [&](std::int32_t a, std::int32_t b) { return ops[a].expert < ops[b].expert; });
+            for (std::int32_t id : group) exec(id);
+            next_exec_ = end;
+            continue;
+        }
+        exec(next_exec_);
+        ++next_exec_;
+    }
+}
+
+void Engine::exec(std::int32_t id) {
+    const StreamOp& op = em_->schedule().ops[id];
+    cudaStream_t st = stream_of(op.stream);
+    for (std::int32_t d : op.deps) {
+        if (d < timed_from_) continue;  // finished in an earlier (synchronized) step
+        if (em_->schedule().ops[d].stream == op.stream) continue;  // FIFO on the same stream
+        cuda_check(cudaStreamWaitEvent(st, op_end_[d], 0), "dep wait");
+    }
+    op_start_[id] = event();
+    op_end_[id] = event();
+    const size_t E = static_cast<size_t>(D_.E);
+    auto wait_release = [&](cudaEvent_t ev) {
+        if (ev != nullptr) cuda_check(cudaStreamWaitEvent(st, ev, 0), "slot wait");
+    };
+    auto pick2 = [](std::vector<int>& busy) {
+        for (int i = 0; i < 2; ++i)
+            if (!busy[i]) {
+                busy[i] = 1;
+                return i;
+            }
+        throw AccountingError("engine: weight slot pool (2) exhausted");
+    };
+
+    switch (op.kind) {
+        case OpKind::load_weights: {
+            // Backpressure first (a slot may still be read by its previous user).
+            if (op.cls == TensorClass::attention) {
+                const int s = pick2(attn_slot_busy_);
+                wait_release(attn_slot_release_[s]);
+                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                cuda_check(cudaMemcpyAsync(attn_slot_[s], host_attn_[op.layer], spec_.attention_bytes,
+                                           cudaMemcpyHostToDevice, st), "h2d attention");
+                attn_slot_of_[op.layer] = s;
+            } else if (op.cls == TensorClass::gate) {
+                const int s = pick2(gate_slot_busy_);
+                wait_release(gate_slot_release_[s]);
+                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                cuda_check(cudaMemcpyAsync(gate_slot_[s], host_gate_[op.layer], spec_.gate_bytes,
+                                           cudaMemcpyHostToDevice, st), "h2d gate");
+                gate_slot_of_[op.layer] = s;
+            } else {
+                // Whole MoE layer (baseline variants): gate + every expert.
+                const int s = pick2(gate_slot_busy_);
+                wait_release(gate_slot_release_[s]);
+                std::vector<int> slots;
+                for (size_t e = 0; e < E; ++e) {
+                    const int x = pool_.acquire();
+                    if (pool_.has_release[x]) wait_release(pool_.release[x]);
+                    slots.push_back(x);
+                }
+                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                cuda_check(cudaMemcpyAsync(gate_slot_[s], host_gate_[op.layer], spec_.gate_bytes,
+                                           cudaMemcpyHostToDevice, st), "h2d gate");
+                for (size_t e = 0; e < E; ++e) {
+                    cuda_check(cudaMemcpyAsync(pool_.ptr[slots[e]], host_expert_[op.layer * E + e], spec_.expert_bytes,
+                                               cudaMemcpyHostToDevice, st), "h2d moe");
+                    expert_slot_of_[{op.layer, static_cast<int>(e)}] = slots[e];
+                }
+                gate_slot_of_[op.layer] = s;
+                moe_slots_of_[op.layer] = slots;
+            }
+            break;
+        }
+        case OpKind::load_expert: {
+            const int s = pool_.acquire();
+            if (pool_.has_release[s]) wait_release(pool_.release[s]);
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            cuda_check(cudaMemcpyAsync(pool_.ptr[s], host_expert_[op.layer * E + op.expert], spec_.expert_bytes,
+                                       cudaMemcpyHostToDevice, st), "h2d expert");
+            expert_slot_of_[{op.layer, op.expert}] = s;
+            break;
+        }
+        case OpKind::offload_expert: {
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            const auto it = expert_slot_of_.find({op.layer, op.expert});
+            if (it == expert_slot_of_.end()) throw AccountingError("engine: offload of an unloaded expert");
+            pool_.release_after(it->second, op_end_[op.deps.front()]);
+            expert_slot_of_.erase(it);
+            break;
+        }
+        case OpKind::offload_weights: {
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            cudaEvent_t after = op_end_[op.deps.front()];
+            if (op.cls == TensorClass::attention) {
+                const int s = attn_slot_of_.at(op.layer);
+                attn_slot_busy_[s] = 0;
+                attn_slot_release_[s] = after;
+                attn_slot_of_.erase(op.layer);
+            } else {
+                const int s = gate_slot_of_.at(op.layer);
+                gate_slot_busy_[s] = 0;
+                gate_slot_release_[s] = after;
+                gate_slot_of_.erase(op.layer);
+                const auto m = moe_slots_of_.find(op.layer);
+                if (m != moe_slots_of_.end()) {
+                    for (size_t e = 0; e < m->second.size(); ++e) {
+                        pool_.release_after(m->second[e], after);
+                        expert_slot_of_.erase({op.layer, static_cast<int>(e)});
+                    }
+                    moe_slots_of_.erase(m);
+                }
+            }
+            break;
+        }
+        case OpKind::compute_attention:
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            exec_attention(op);
+            break;
+        case OpKind::compute_gate:
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            exec_gate(op);
+            break;
+        case OpKind::compute_expert:
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            exec_expert(op);
+            break;
+        default:
+            throw ConfigError(std::string("engine: op kind ") + op_kind_name(op.kind) + " is not executed on B200 yet");
+    }
+    cuda_check(cudaEventRecord(op_end_[id], st), "record");
+}
+
+void Engine::exec_attention(const StreamOp& op) {
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int l = op.layer, step = op.step, b = op.batch;
+    const int tpb = tokens_per_batch(step);
+    const int64_t row0 = static_cast<int64_t>(b) * tpb;
+    const uint16_t* w = res_attn_[l] ? res_attn_[l] : attn_slot_[attn_slot_of_.at(l)];
+    const uint16_t* wqkv = w;
+    const uint16_t* wo = w + static_cast<int64_t>(D_.qkv_width()) * D_.d;
+    uint16_t* hb = h_ + row0 * D_.d;
+    kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
+    kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, cs), "qkv");
+    const float scale = 1.0f / std::sqrt(static_cast<float>(D_.hd));
+    const int last = step == 0 ? cfg_.workload.prompt_len - 1 : -1;
+    kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, tok_seq_ + row0, D_.theta, kc_[l],
+                               vc_[l], kv_cap_, kv_sink_, last, cs), "rope/kv");
+    if (step == 0)
+        kl_check(kl_attn_prefill(qkv_, cfg_.workload.batch_size, cfg_.workload.prompt_len, D_.Hq, D_.Hkv, D_.hd,
+                                 kv_cap_, kv_sink_, scale, ao_, cs), "prefill attention");
+    else
+        kl_check(kl_attn_decode(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
+                                kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, cs), "decode attention");
+    kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, cs), "o proj");
+}
+
+void Engine::exec_gate(const StreamOp& op) {
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int l = op.layer, step = op.step, b = op.batch;
+    const int n = plan_.n_batches;
+    const int tpb = tokens_per_batch(step);
+    const int64_t row0 = static_cast<int64_t>(b) * tpb;
+    int32_t* hist = report_ + static_cast<int64_t>(b) * D_.E;
+    int32_t* first = report_ + static_cast<int64_t>(n) * D_.E + static_cast<int64_t>(b) * D_.E;
+    if (b == 0) {
+        cuda_check(cudaMemsetAsync(report_, 0, static_cast<size_t>(n) * D_.E * 4, cs), "memset hist");
+        cuda_check(cudaMemsetAsync(report_ + static_cast<int64_t>(n) * D_.E, 0x7f, static_cast<size_t>(n) * D_.E * 4, cs),
+                   "memset first");
+        if (cfg_.replay)
+            cuda_check(cudaMemcpyAsync(forced_, host_forced_, static_cast<size_t>(n) * tpb * D_.k * 4,
+                                       cudaMemcpyHostToDevice, cs), "h2d forced routing");
+    }
+    const uint16_t* wg = gate_slot_[gate_slot_of_.at(l)];
+    int32_t* idx = idx_[idx_cur_] + row0 * D_.k;
+    float* wt = weight_ + row0 * D_.k;
+    if (cfg_.replay) {
+        kl_check(kl_gate_topk(h_ + row0 * D_.d, norm_ffn_[l], wg, tpb, D_.d, D_.E, D_.k, D_.eps, D_.score_mode,
+                              x2_ + row0 * D_.d, router_logits_ + row0 * D_.E, idx, wt, nullptr, nullptr, cs), "gate");
+        kl_check(kl_route_override(forced_ + row0 * D_.k, router_logits_ + row0 * D_.E, tpb, D_.E, D_.k, idx, wt, hist,
+                                   first, cs), "route override");
+    } else {
+        kl_check(kl_gate_topk(h_ + row0 * D_.d, norm_ffn_[l], wg, tpb, D_.d, D_.E, D_.k, D_.eps, D_.score_mode,
+                              x2_ + row0 * D_.d, nullptr, idx, wt, hist, first, cs), "gate");
+    }
+    if (b == n - 1) after_layer_gates(step, l);
+}
+
+// Work tied to the block's last gate: expert-major permutation of the whole
+// group, the prefetcher's online table update and the next layer's scores,
+// then one small D2H of everything the host needs to emit the rest.
+void Engine::after_layer_gates(int step, int layer) {
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int n = plan_.n_batches;
+    const int64_t T = static_cast<int64_t>(n) * tokens_per_batch(step);
+    int32_t* cur = idx_[idx_cur_];
+    int32_t* prev = idx_[idx_cur_ ^ 1];
+    kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
+             "permute");
+    int64_t* scores = reinterpret_cast<int64_t*>(report_ + 2LL * n * D_.E + 16 - ((2LL * n * D_.E) % 16));
+    int64_t* marg_copy = scores + D_.E;
+    if (layer + 1 < D_.L) {
+        kl_check(kl_coact_update(layer == 0 ? nullptr : prev, cur, T, D_.k, D_.E, layer, table_, marginal_, cs),
+                 "coact update");
+        kl_check(kl_predict_scores(counts_, table_, D_.E, layer + 1, scores, cs), "predict");
+    }
+    cuda_check(cudaMemcpyAsync(marg_copy, marginal_, D_.E * 8, cudaMemcpyDeviceToDevice, cs), "marginal");
+    const size_t report_bytes = reinterpret_cast<char*>(marg_copy + D_.E) - reinterpret_cast<char*>(report_);
+    cuda_check(cudaMemcpyAsync(host_report_, report_, report_bytes, cudaMemcpyDeviceToHost, cs), "d2h report");
+    if (cfg_.record_trace)
+        cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, cs), "d2h idx");
+    idx_cur_ ^= 1;  // this layer's ids become "prev" for the next layer
+}
+
+detail::BlockRouting Engine::read_routing(int step, int layer) {
+    // The last op issued on the compute stream is the block's last gate;
+    // its end event covers the readback copies.
+    const std::int32_t last_gate = next_exec_ - 1;
+    cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
+    const int n = plan_.n_batches, E = D_.E;
+    detail::BlockRouting r;
+    r.group_hist.assign(E, 0);
+    r.demand.resize(n);
+    r.batch_hist.assign(n, std::vector<int64_t>(E, 0));
+    for (int b = 0; b < n; ++b) {
+        std::vector<std::pair<int32_t, int>> firsts;
+        for (int e = 0; e < E; ++e) {
+            const int32_t c = host_report_[b * E + e];
+            r.batch_hist[b][e] = c;
+            r.group_hist[e] += c;
+            const int32_t f = host_report_[n * E + b * E + e];
+            if (c > 0) {
+                if (f == kNoPos) throw AccountingError("engine: routed expert without a first position");
+                firsts.emplace_back(f, e);
+            }
+        }
+        std::sort(firsts.begin(), firsts.end());
+        for (const auto& [f, e] : firsts) r.demand[b].push_back(e);
+    }
+    const int64_t* scores =
+        reinterpret_cast<const int64_t*>(host_report_ + 2LL * n * E + 16 - ((2LL * n * E) % 16));
+    host_scores_.assign(scores, scores + E);
+    host_marginal_.assign(scores + E, scores + 2 * E);
+    // Expert segment starts of the stable counting sort (== device offsets).
+    row_offset_.assign(E, 0);
+    for (int e = 1; e < E; ++e) row_offset_[e] = row_offset_[e - 1] + r.group_hist[e - 1];
+    block_rows_ = std::accumulate(r.group_hist.begin(), r.group_hist.end(), int64_t{0});
+    batch_prefix_.assign(n, std::vector<int64_t>(E, 0));
+    for (int b = 1; b < n; ++b)
+        for (int e = 0; e < E; ++e) batch_prefix_[b][e] = batch_prefix_[b - 1][e] + r.batch_hist[b - 1][e];
+    if (cfg_.record_trace) {
+        const size_t off = recorded_.offset(step, layer, 0, 0);
+        const int64_t cnt = static_cast<int64_t>(n) * tokens_per_batch(step) * D_.k;
+        for (int64_t i = 0; i < cnt; ++i) recorded_.sel[off + i] = static_cast<uint16_t>(host_idx_[i]);
+    }
+    return r;
+}
+
+void Engine::exec_expert(const StreamOp& op) {
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int l = op.layer, e = op.expert;
+    const int64_t M = op.token_count;
+    const int64_t row0 = row_offset_[e] + (op.batch >= 0 ? batch_prefix_[op.batch][e] : 0);
+    const uint16_t* w = expert_weights(l, e);
+    const uint16_t* w2 = w + 2LL * D_.f * D_.d;
+    for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
+        const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
+        kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, cs), "expert ffn");
+    }
+    if (--exec_expert_left_ == 0) {
+        // Every routed row of the block is computed: weighted combine + residual.
+        const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(op.step);
+        kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
+        if (cfg_.record_hidden) {
+            std::vector<uint16_t> dump(static_cast<size_t>(T) * D_.d);
+            cuda_check(cudaMemcpyAsync(dump.data(), h_, dump.size() * 2, cudaMemcpyDeviceToHost, cs), "dump");
+            cuda_check(cudaStreamSynchronize(cs), "dump sync");
+            hidden_dumps_.push_back(std::move(dump));
+        }
+    }
+}
+
+void Engine::read_hidden(uint16_t* host, int64_t n) const {
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    cuda_check(cudaMemcpy(host, h_, static_cast<size_t>(std::min<int64_t>(n, t_max_ * D_.d)) * 2,
+                          cudaMemcpyDeviceToHost), "read hidden");
+}
+
+void Engine::reset_log() {
+    // Keep the emitter (op ids keep growing); measurement restarts here.
+    timed_from_ = next_exec_;
+    log_from_ = next_exec_;
+    records_from_ = em_->schedule().prefetch_records.size();
+    t0_recorded_ = false;
+    tokens_generated_ = 0;
+    step_ms_.clear();
+    hidden_dumps_.clear();
+}
+
+std::string Engine::report(const std::string& what) {
+    const Schedule& s = em_->schedule();
+    json j;
+    std::vector<SimEvent> tl(timeline_.begin() + std::min<size_t>(log_from_, timeline_.size()),
+                             timeline_.begin() + std::min<size_t>(next_exec_, timeline_.size()));
+    if (what == "schedule") {
+        j["text"] = s.to_text();
+        j["n_ops"] = s.ops.size();
+    } else if (what == "timeline_csv") {
+        j["text"] = timeline_to_string(tl, s, TimelineFormat::csv);
+    } else if (what == "timeline_json") {
+        j["text"] = timeline_to_string(tl, s, TimelineFormat::trace_event_json);
+    } else if (what == "metrics") {
+        Schedule view;
+        view.batch_size = s.batch_size;
+        view.n_batches = s.n_batches;
+        view.n_steps = s.n_steps;
+        view.ops = s.ops;
+        view.prefetch_records.assign(s.prefetch_records.begin() + records_from_, s.prefetch_records.end());
+        RunMetrics m;
+        detail::finalize_metrics(view, tl, arena_used_, m);
+        duration_ps t_begin = tl.empty() ? 0 : tl.front().start;
+        for (const SimEvent& e : tl) t_begin = std::min(t_begin, e.start);
+        m.makespan -= t_begin;  // measured from the first op of the window
+        m.bubble_time = m.makespan - m.compute_busy;
+        m.tokens_generated = tokens_generated_;
+        m.throughput_tps = m.makespan > 0 ? static_cast<double>(tokens_generated_) / sec_from_ps(m.makespan) : 0.0;
+        j["makespan_ps"] = m.makespan;
+        j["compute_busy_ps"] = m.compute_busy;
+        j["bubble_ps"] = m.bubble_time;
+        j["bubble_fraction"] = m.makespan > 0 ? static_cast<double>(m.bubble_time) / m.makespan : 0.0;
+        j["expert_layer_bubble_ps"] = m.expert_layer_bubble_time;
+        j["throughput_tps"] = m.throughput_tps;
+        j["tokens_generated"] = m.tokens_generated;
+        j["peak_vram_bytes"] = m.peak_vram;
+        j["prefetch_participation"] = m.prefetch_participation;
+        j["hot_accuracy"] = m.hot_accuracy;
+        const BubbleBreakdown& b = m.bubbles;
+        j["bubbles_ps"] = {{"startup", b.startup - t_begin},    {"intra_attention", b.intra_attention},
+                           {"attn_to_moe", b.attn_to_moe},      {"intra_gate", b.intra_gate},
+                           {"gate_to_expert", b.gate_to_expert}, {"intra_expert", b.intra_expert},
+                           {"moe_to_attn", b.moe_to_attn},      {"drain", b.drain}};
+        // Host-link accounting: bytes moved by load ops and the time the
+        // link had at least one load in flight (union of load intervals).
+        std::vector<std::pair<duration_ps, duration_ps>> iv;
+        int64_t h2d = 0, n_expert_loads = 0;
+        duration_ps expert_busy = 0, compute_busy = 0;
+        std::map<int, duration_ps> kind_busy;
+        for (const SimEvent& e : tl) {
+            const StreamOp& op = s.ops[e.op_id];
+            if (op.kind == OpKind::load_weights || op.kind == OpKind::load_expert) {
+                h2d += op.payload_bytes;
+                iv.emplace_back(e.start, e.end);
+                if (op.kind == OpKind::load_expert) {
+                    ++n_expert_loads;
+                    expert_busy += e.end - e.start;
+                }
+            }
+            if (op.stream == StreamId::compute) {
+                compute_busy += e.end - e.start;
+                kind_busy[static_cast<int>(op.kind)] += e.end - e.start;
+            }
+        }
+        std::sort(iv.begin(), iv.end());
+        duration_ps link_busy = 0, cur_s = -1, cur_e = -1;
+        for (const auto& [a, bnd] : iv) {
+            if (a > cur_e) {
+                if (cur_e > cur_s) link_busy += cur_e - cur_s;
+                cur_s = a;
+                cur_e = bnd;
+            } else {
+                cur_e = std::max(cur_e, bnd);
+            }
+        }
+        if (cur_e > cur_s) link_busy += cur_e - cur_s;
+        j["h2d_bytes"] = h2d;
+        j["h2d_link_busy_ps"] = link_busy;
+        j["h2d_gbs_busy"] = link_busy > 0 ? h2d / (link_busy * 1e-12) / 1e9 : 0.0;
+        j["h2d_gbs_makespan"] = m.makespan > 0 ? h2d / (m.makespan * 1e-12) / 1e9 : 0.0;
+        j["expert_loads"] = n_expert_loads;
+        j["compute_ps_by_kind"] = {{"attention", kind_busy[static_cast<int>(OpKind::compute_attention)]},
+                                   {"gate", kind_busy[static_cast<int>(OpKind::compute_gate)]},
+                                   {"expert", kind_busy[static_cast<int>(OpKind::compute_expert)]}};
+        j["step_ms"] = step_ms_;
+    } else if (what == "prefetch") {
+        json recs = json::array();
+        for (size_t i = records_from_; i < s.prefetch_records.size(); ++i) {
+            const auto& r = s.prefetch_records[i];
+            recs.push_back({{"step", r.step}, {"layer", r.layer}, {"prefetched", r.prefetched},
+                            {"activated", r.activated}, {"hottest", r.hottest}, {"fallback", r.used_fallback}});
+        }
+        j["records"] = recs;
+    } else if (what == "trace") {
+        j["sel"] = recorded_.sel;
+        j["text_header"] = trace_to_string(ActivationTrace{}).substr(0, 0);
+    } else if (what == "validate") {
+        const ValidationReport rep = validate_schedule(s, cfg_.replay ? replay_trace_ : recorded_, plan_);
+        j["violations"] = rep.violations;
+    } else if (what == "hidden") {
+        json arr = json::array();
+        for (const auto& dmp : hidden_dumps_) arr.push_back(dmp);
+        j["dumps"] = arr;
+    } else {
+        throw ConfigError("engine report: unknown section '" + what + "'");
+    }
+    return j.dump();
+}
+
+}  // namespace klotski

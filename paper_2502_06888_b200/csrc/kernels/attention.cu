@@ -70,11 +70,12 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
 // One CTA per (token, kv head); warp g handles query head kvh*G + g.
 // Phase 1: lane-per-slot scores; phase 2: warp softmax; phase 3: P.V with
 // each lane owning 4 of the 128 head dims.
+template <int HD>
 __global__ void attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
                                    const int32_t* __restrict__ seq, int Hq, int Hkv, const uint16_t* __restrict__ kc,
                                    const uint16_t* __restrict__ vc, int cap, int sink, float scale,
                                    uint16_t* __restrict__ out) {
-    constexpr int HD = 128;
+    constexpr int PER = HD / 32;  // head dims owned by one lane in the P.V phase
     extern __shared__ float sc[];  // [G][cap]
     const int t = blockIdx.x;
     const int kvh = blockIdx.y;
@@ -128,25 +129,30 @@ __global__ void attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_str
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     __syncwarp();
     const float inv = 1.0f / sum;
-    float o4[4] = {0.f, 0.f, 0.f, 0.f};
+    float o[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) o[i] = 0.f;
     for (int j = 0; j < n; ++j) {
-        const uint16_t* vp = vc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD + lane * 4;
-        const uint2 w = __ldg(reinterpret_cast<const uint2*>(vp));
+        const uint16_t* vp = vc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD + lane * PER;
         const float pj = s[j];
-        o4[0] = fmaf(pj, bf2f(static_cast<uint16_t>(w.x & 0xffffu)), o4[0]);
-        o4[1] = fmaf(pj, bf2f(static_cast<uint16_t>(w.x >> 16)), o4[1]);
-        o4[2] = fmaf(pj, bf2f(static_cast<uint16_t>(w.y & 0xffffu)), o4[2]);
-        o4[3] = fmaf(pj, bf2f(static_cast<uint16_t>(w.y >> 16)), o4[3]);
+#pragma unroll
+        for (int i = 0; i < PER; i += 2) {
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vp + i));
+            o[i] = fmaf(pj, bf2f(static_cast<uint16_t>(w & 0xffffu)), o[i]);
+            o[i + 1] = fmaf(pj, bf2f(static_cast<uint16_t>(w >> 16)), o[i + 1]);
+        }
     }
-    uint16_t* op = out + static_cast<int64_t>(t) * Hq * HD + static_cast<int64_t>(qh) * HD + lane * 4;
-    *reinterpret_cast<uint2*>(op) = make_uint2(pack2(o4[0] * inv, o4[1] * inv), pack2(o4[2] * inv, o4[3] * inv));
+    uint16_t* op = out + static_cast<int64_t>(t) * Hq * HD + static_cast<int64_t>(qh) * HD + lane * PER;
+#pragma unroll
+    for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(op + i) = pack2(o[i] * inv, o[i + 1] * inv);
 }
 
 // Prefill: one warp per (query row, q head); keys from the same chunk's qkv
 // rows; causal with sink + sliding-window retention; online softmax.
+template <int HD>
 __global__ void attn_prefill_kernel(const uint16_t* __restrict__ qkv, int n_seq, int L, int Hq, int Hkv, int cap,
                                     int sink, float scale, uint16_t* __restrict__ out) {
-    constexpr int HD = 128;
+    constexpr int PER = HD / 32;
     const int64_t wid = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     const int64_t rows = static_cast<int64_t>(n_seq) * L;
@@ -156,35 +162,37 @@ __global__ void attn_prefill_kernel(const uint16_t* __restrict__ qkv, int n_seq,
     const int sq = static_cast<int>(row / L), i = static_cast<int>(row % L);
     const int kvh = qh / (Hq / Hkv);
     const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * HD;
-    const uint16_t* qp = qkv + row * width + static_cast<int64_t>(qh) * HD + lane * 4;
-    const uint2 qw = *reinterpret_cast<const uint2*>(qp);
-    const float q0 = bf2f(qw.x & 0xffffu) * scale, q1 = bf2f(qw.x >> 16) * scale;
-    const float q2 = bf2f(qw.y & 0xffffu) * scale, q3 = bf2f(qw.y >> 16) * scale;
+    const uint16_t* qp = qkv + row * width + static_cast<int64_t>(qh) * HD + lane * PER;
+    float qv[PER], o[PER];
+#pragma unroll
+    for (int x = 0; x < PER; ++x) {
+        qv[x] = bf2f(qp[x]) * scale;
+        o[x] = 0.f;
+    }
     const int window = cap - sink;
-    float m = -INFINITY, l = 0.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+    float m = -INFINITY, l = 0.f;
     for (int j = 0; j <= i; ++j) {
         const bool kept = j < sink || j > i - window;
         if (!kept) continue;
         const int64_t krow = (static_cast<int64_t>(sq) * L + j) * width;
-        const uint2 kw = *reinterpret_cast<const uint2*>(qkv + krow + static_cast<int64_t>(Hq + kvh) * HD + lane * 4);
-        float dot = q0 * bf2f(kw.x & 0xffffu) + q1 * bf2f(kw.x >> 16) + q2 * bf2f(kw.y & 0xffffu) +
-                    q3 * bf2f(kw.y >> 16);
+        const uint16_t* kp = qkv + krow + static_cast<int64_t>(Hq + kvh) * HD + lane * PER;
+        const uint16_t* vp = qkv + krow + static_cast<int64_t>(Hq + Hkv + kvh) * HD + lane * PER;
+        float dot = 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        for (int x = 0; x < PER; ++x) dot = fmaf(qv[x], bf2f(kp[x]), dot);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
         const float nm = fmaxf(m, dot);
         const float corr = __expf(m - nm), pj = __expf(dot - nm);
-        const uint2 vw =
-            *reinterpret_cast<const uint2*>(qkv + krow + static_cast<int64_t>(Hq + Hkv + kvh) * HD + lane * 4);
-        o0 = o0 * corr + pj * bf2f(vw.x & 0xffffu);
-        o1 = o1 * corr + pj * bf2f(vw.x >> 16);
-        o2 = o2 * corr + pj * bf2f(vw.y & 0xffffu);
-        o3 = o3 * corr + pj * bf2f(vw.y >> 16);
+#pragma unroll
+        for (int x = 0; x < PER; ++x) o[x] = o[x] * corr + pj * bf2f(vp[x]);
         l = l * corr + pj;
         m = nm;
     }
     const float inv = 1.0f / l;
-    uint16_t* op = out + row * Hq * HD + static_cast<int64_t>(qh) * HD + lane * 4;
-    *reinterpret_cast<uint2*>(op) = make_uint2(pack2(o0 * inv, o1 * inv), pack2(o2 * inv, o3 * inv));
+    uint16_t* op = out + row * Hq * HD + static_cast<int64_t>(qh) * HD + lane * PER;
+#pragma unroll
+    for (int x = 0; x < PER; ++x) op[x] = f2bf(o[x] * inv);
 }
 
 }  // namespace
@@ -208,28 +216,28 @@ extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int 
 extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq, int64_t T,
                               int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache, int cap,
                               int sink, float scale, uint16_t* out, cudaStream_t stream) {
-    if (hd != 128) return KL_EUNSUPPORTED;
+    if (hd != 128 && hd != 64) return KL_EUNSUPPORTED;
     if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || Hq / Hkv > 32 || cap <= sink || !q || !pos || !seq || !out)
         return KL_EINVAL;
     if (T == 0) return KL_OK;
     const int G = Hq / Hkv;
     const size_t smem = static_cast<size_t>(G) * cap * sizeof(float);
     if (smem > 200 * 1024) return KL_EUNSUPPORTED;
+    auto kern = hd == 128 ? attn_decode_kernel<128> : attn_decode_kernel<64>;
     if (smem > 48 * 1024)
-        KL_CUDA_TRY(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    attn_decode_kernel<<<dim3(static_cast<unsigned>(T), Hkv), 32 * G, smem, stream>>>(
-        q, q_stride, pos, seq, Hq, Hkv, k_cache, v_cache, cap, sink, scale, out);
+        KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<dim3(static_cast<unsigned>(T), Hkv), 32 * G, smem, stream>>>(q, q_stride, pos, seq, Hq, Hkv, k_cache,
+                                                                         v_cache, cap, sink, scale, out);
     return check_launch();
 }
 
 extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap, int sink,
                                float scale, uint16_t* out, cudaStream_t stream) {
-    if (hd != 128) return KL_EUNSUPPORTED;
+    if (hd != 128 && hd != 64) return KL_EUNSUPPORTED;
     if (n_seq < 0 || L < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || !qkv || !out) return KL_EINVAL;
     const int64_t warps = static_cast<int64_t>(n_seq) * L * Hq;
     if (warps == 0) return KL_OK;
-    attn_prefill_kernel<<<static_cast<int>((warps + 7) / 8), 256, 0, stream>>>(qkv, n_seq, L, Hq, Hkv, cap, sink,
-                                                                              scale, out);
+    auto kern = hd == 128 ? attn_prefill_kernel<128> : attn_prefill_kernel<64>;
+    kern<<<static_cast<int>((warps + 7) / 8), 256, 0, stream>>>(qkv, n_seq, L, Hq, Hkv, cap, sink, scale, out);
     return check_launch();
 }

@@ -329,17 +329,82 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+// Approximately normal values with bit-reproducible arithmetic: Irwin-Hall
+// sum of four 22-bit uniforms (exact in fp32), centred and scaled by
+// sqrt(3)*std (one correctly rounded multiply), so the CPU oracle
+// regenerates identical bf16 weights from (seed, index).
 __global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64_t seed, float sd) {
+    const float scale = 1.7320508075688772f * sd;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t z = splitmix(seed ^ (static_cast<uint64_t>(i >> 1) * 0xd1b54a32d192ed03ULL));
-        const float u1 = (static_cast<float>(z >> 40) + 1.0f) * (1.0f / 16777217.0f);
-        const float u2 = static_cast<float>((z >> 16) & 0xffffffu) * (1.0f / 16777216.0f);
-        const float rad = sqrtf(-2.0f * logf(u1));
-        const float ang = 6.283185307179586f * u2;
-        const float v = (i & 1) ? rad * sinf(ang) : rad * cosf(ang);
-        dst[i] = f2bf(v * sd);
+        const uint64_t z = splitmix(seed ^ (static_cast<uint64_t>(i) * 0xd1b54a32d192ed03ULL));
+        const uint64_t w = splitmix(z);
+        const float u = __fadd_rn(__fadd_rn(static_cast<float>(z & 0x3fffffu), static_cast<float>((z >> 22) & 0x3fffffu)),
+                                  __fadd_rn(static_cast<float>(w & 0x3fffffu), static_cast<float>((w >> 22) & 0x3fffffu)));
+        const float c = __fsub_rn(__fmul_rn(u, 0x1.0p-22f), 2.0f);
+        dst[i] = f2bf(__fmul_rn(c, scale));
     }
+}
+
+// Replay routing: force the trace's ids, recompute weights from the router's
+// own logits of those ids (mode-0 softmax) and the batch histograms.
+__global__ void route_override_kernel(const int32_t* __restrict__ forced, const float* __restrict__ logits, int T,
+                                      int E, int k, int32_t* __restrict__ idx, float* __restrict__ weight,
+                                      int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    float v[8], mx = -INFINITY, sum = 0.f;
+    for (int j = 0; j < k; ++j) {
+        const int e = forced[static_cast<int64_t>(t) * k + j];
+        v[j] = logits[static_cast<int64_t>(t) * E + e];
+        mx = j == 0 ? v[j] : mx;
+    }
+    for (int j = 0; j < k; ++j) sum += (v[j] = expf(v[j] - mx));
+    for (int j = 0; j < k; ++j) {
+        const int64_t r = static_cast<int64_t>(t) * k + j;
+        const int e = forced[r];
+        idx[r] = e;
+        weight[r] = v[j] / sum;
+        if (hist != nullptr) atomicAdd(&hist[e], 1);
+        if (first_pos != nullptr) atomicMin(&first_pos[e], static_cast<int32_t>(r));
+    }
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __restrict__ table, int64_t T, int d,
+                             uint16_t* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(ids[t]) * d);
+    uint4* dst = reinterpret_cast<uint4*>(out + t * d);
+    for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
+}
+
+// Greedy decode: first index of the row maximum (bf16 logits).
+__global__ void argmax_kernel(const uint16_t* __restrict__ logits, int64_t T, int V, int32_t* __restrict__ out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const uint16_t* row = logits + t * V;
+    float best = -INFINITY;
+    int arg = 0x7fffffff;
+    for (int i = lane; i < V; i += 32) {
+        const float v = bf2f(row[i]);
+        if (v > best) {
+            best = v;
+            arg = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) {
+            best = ob;
+            arg = oa;
+        }
+    }
+    if (lane == 0) out[t] = arg;
 }
 
 int grid_for(int64_t items, int per_block) {
@@ -430,5 +495,28 @@ extern "C" int kl_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, floa
     const int64_t blocks = (n + 255) / 256;
     fill_normal_kernel<<<static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, stream>>>(dst, n, seed,
                                                                                                       std_dev);
+    return check_launch();
+}
+
+extern "C" int kl_route_override(const int32_t* forced, const float* logits, int T, int E, int k, int32_t* idx,
+                                 float* weight, int32_t* hist, int32_t* first_pos, cudaStream_t stream) {
+    if (T < 0 || E < 1 || k < 1 || k > 8 || !forced || !logits || !idx || !weight) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    route_override_kernel<<<(T + 127) / 128, 128, 0, stream>>>(forced, logits, T, E, k, idx, weight, hist, first_pos);
+    return check_launch();
+}
+
+extern "C" int kl_embed(const int32_t* ids, const uint16_t* table, int64_t T, int d, uint16_t* out,
+                        cudaStream_t stream) {
+    if (T < 0 || d % 8 != 0 || !ids || !table || !out) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    embed_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(ids, table, T, d, out);
+    return check_launch();
+}
+
+extern "C" int kl_argmax_bf16(const uint16_t* logits, int64_t T, int V, int32_t* out, cudaStream_t stream) {
+    if (T < 0 || V < 1 || !logits || !out) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    argmax_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(logits, T, V, out);
     return check_launch();
 }
