@@ -59,7 +59,7 @@ $(PARITY): oracle/parity_driver.cpp $(LIB) $(HDRS)
 	$(CXX) $(CXXFLAGS) -shared $< -o $@ -L$(PKG) -lklotski -Wl,-rpath,'$$ORIGIN'
 
 $(ORACLE): oracle/numerics.c
-	gcc -std=c11 -O2 -fPIC -ffp-contract=off -fopenmp -shared $< -o $@ -lm
+	gcc -std=c11 -O3 -mavx2 -mfma -fPIC -ffp-contract=off -fopenmp -shared $< -o $@ -lm
 
 ref:
 	oracle/build_ref.sh $(REF)

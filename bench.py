@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Headline benchmark: Mixtral-8x7B bf16 decode under a capped HBM budget with
+experts streamed from pinned host memory (BASELINE.json configs[1]):
+batch 64 x n=8 batch group, 24e9-byte HBM arena, StreamingLLM KV retention
+(sink 4 + window 256, the reference's KvRetentionPolicy) so the KV cache stays
+in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0. A "step" = one decode step of the whole batch group
+(n*bs = 512 tokens) through all 32 layers: attention, router, expert-major
+permutation, every active expert's SwiGLU FFN (weights H2D-streamed by the
+Klotski schedule), combine, greedy head.
+  value : decode tokens/s with the step's inputs already in HBM (device events)
+  e2e   : the same through the public C-ABI (kl_engine_step) with host token
+          ids in and host next-token ids out, copies inside the timed region
+The reference arm (--impl reference) times the CPU port of the same decode
+step (oracle/cpu_port.py, C oracle kernels, all host threads) on a bounded
+sample: the reference itself (proj/) is a simulator with no numeric path.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s (Mixtral-8x7B, capped HBM)"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("hbm_gbs", 6650.0), "measured"
+    except (OSError, ValueError):
+        return 6650.0, "fallback"
+
+
+def link_peak_gbs(torch, dev):
+    """Pinned H2D copy bandwidth of this box (the streaming roofline)."""
+    n = 512 * 1024 * 1024
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(6):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    return 6 * n / (s.elapsed_time(e) / 1e3) / 1e9
+
+
+def engine_config(args, rank, world):
+    gen = 1 + args.warmup + 2 * args.steps
+    cfg = {
+        "model": {"preset": args.model},
+        "workload": {"batch_size": args.batch_size, "n_batches": args.n_batches, "prompt_len": args.prompt_len,
+                     "gen_len": gen},
+        "hbm_cap_bytes": int(args.hbm_cap),
+        "kv_retention": {"mode": "streaming", "sink_tokens": 4, "window_tokens": 256},
+        "routing": "gate",
+        "prefill": False,
+        "record_trace": False,
+        "host_distinct_layers": args.host_distinct_layers,
+        "weight_seed": 7 + rank,
+    }
+    return cfg
+
+
+def cpu_baseline(args, warmup=0, repeats=1):
+    from oracle import cpu_port
+    r = cpu_port.measure(args.model, args.n_batches, args.batch_size, cap=260, repeats=repeats, warmup=warmup)
+    return r
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    times = []
+    from oracle import cpu_port
+    D = cpu_port.mixtral_dims(args.model)
+    layer = cpu_port.LayerSample(D, args.n_batches, args.batch_size, 260)
+    for _ in range(args.warmup):
+        layer.decode_layer(600)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        layer.decode_layer(600)
+        times.append((time.perf_counter() - t0) * D["L"])  # one layer sampled, x L layers
+    step_s = statistics.median(times)
+    toks = args.n_batches * args.batch_size
+    value = toks / step_s
+    sample = (f"each step: 1 of {D['L']} layers of one {args.model} decode step ({args.n_batches}x{args.batch_size} "
+              f"tokens, 260 retained KV slots), extrapolated x{D['L']}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.model} decode, batch {args.batch_size} x n={args.n_batches}, CPU port",
+                   "batch_size": args.batch_size, "n_batches": args.n_batches},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference proj/ is a discrete-event simulator without numerics; its CPU path is the oracle port",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_2502_06888_b200.engine import Engine
+
+    link = link_peak_gbs(torch, dev)
+    t_setup = time.perf_counter()
+    eng = Engine(engine_config(args, rank, world))
+    eng.fill_kv_synthetic(args.prompt_len)
+    setup_s = time.perf_counter() - t_setup
+    seqs = eng.n_seqs
+    step = 1
+    for _ in range(args.warmup):
+        eng.step(step, None, want_next=False)
+        step += 1
+    eng.reset_log()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    # Timed region 1: inputs resident in HBM (device-fed greedy tokens).
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    dev_ms = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, ms = eng.step(step, None, want_next=False)
+        dev_ms.append(ms)
+        step += 1
+    barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    metrics = eng.report("metrics")
+    total_ms = sum(dev_ms)
+
+    # Timed region 2: end to end through the C-ABI with host buffers.
+    rng = np.random.default_rng(rank)
+    tokens = rng.integers(0, eng.info["dims"]["V"], seqs, dtype=np.int32)
+    barrier()
+    e2e_ms = []
+    t1 = time.perf_counter()
+    for _ in range(args.steps):
+        tokens, ms = eng.step(step, tokens, want_next=True)
+        e2e_ms.append(ms)
+        step += 1
+    barrier()
+    e2e_wall = time.perf_counter() - t1
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    total_ms = max_over_ranks(total_ms)
+    e2e_total_ms = max_over_ranks(max(sum(e2e_ms), e2e_wall * 1e3))
+    value = args.steps * seqs * world / (total_ms / 1e3)
+    e2e_value = args.steps * seqs * world / (e2e_total_ms / 1e3)
+
+    # Roofline of the dominant kernel (expert FFN = 2 tcgen05 GEMMs per op):
+    # algorithmic bytes per op = expert weights + routed activations in/out.
+    D = eng.info["dims"]
+    hbm_peak, peak_kind = measured_peaks()
+    n_ops = max(metrics["expert_ops"], 1)
+    rows = metrics["expert_rows"]
+    algo_bytes = n_ops * metrics["expert_bytes"] + rows * (2 * D["d"] * 2 + 2 * D["f"] * 2)
+    expert_s = metrics["compute_ps_by_kind"]["expert"] * 1e-12
+    achieved = algo_bytes / expert_s / 1e9 if expert_s > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_expert_ffn.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_op")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_baseline(args)
+            cpu = {"value": r["tok_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random-init bf16 weights of the Mixtral-8x7B architecture, random token ids, "
+                    "synthetic prefilled KV of 512 positions)",
+            "config": {
+                "workload": f"{args.model} bf16 decode, batch {args.batch_size} x n={eng.n_batches}, "
+                            f"HBM cap {args.hbm_cap:.3g} B, experts streamed from pinned host",
+                "model": args.model, "batch_size": args.batch_size, "n_batches": eng.n_batches,
+                "prompt_len": args.prompt_len, "kv_retention": "streaming sink 4 + window 256",
+                "hbm_cap_bytes": int(args.hbm_cap), "expert_slots": eng.info["expert_slots"],
+                "resident_expert_layers": eng.info["resident_expert_layers"],
+                "resident_attention_layers": eng.info["resident_attention_layers"],
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "l2": "inputs larger than L2 (each step streams the experts of every layer)",
+                "host_distinct_layers": args.host_distinct_layers or "all",
+            },
+            "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": seqs * 4,
+                    "d2h_bytes_per_step": seqs * 4},
+            "gpu_launches": metrics["launches"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "expert FFN (tcgen05 SwiGLU GEMM + down GEMM), per compute_expert op",
+                         "algorithmic_bytes_per_op": algo_bytes / n_ops},
+            "cpu_baseline": cpu,
+            "pipeline": {
+                "bubble_fraction": metrics["bubble_fraction"],
+                "bubbles_ps": metrics["bubbles_ps"],
+                "compute_busy_ms": metrics["compute_busy_ps"] / 1e9,
+                "makespan_ms": metrics["makespan_ps"] / 1e9,
+                "h2d_gb_per_step": metrics["h2d_bytes"] / args.steps / 1e9,
+                "h2d_gbs_link_busy": metrics["h2d_gbs_busy"],
+                "h2d_gbs_over_makespan": metrics["h2d_gbs_makespan"],
+                "link_peak_gbs_measured": link,
+                "h2d_frac_of_link_peak": metrics["h2d_gbs_busy"] / link,
+                "expert_loads_per_step": metrics["expert_loads"] / args.steps,
+                "prefetch_participation": metrics["prefetch_participation"],
+                "hot_accuracy": metrics["hot_accuracy"],
+                "link_bound_ceiling_tok_s": seqs / (metrics["h2d_bytes"] / args.steps / (link * 1e9)),
+            },
+            "setup_s": setup_s,
+            "wall_s_timed": wall,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="mixtral-8x7b")
+    ap.add_argument("--batch-size", type=int, default=64)
+    ap.add_argument("--n-batches", type=int, default=8)
+    ap.add_argument("--prompt-len", type=int, default=512)
+    ap.add_argument("--hbm-cap", type=float, default=24e9)
+    ap.add_argument("--host-distinct-layers", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -22,6 +22,7 @@
  *
  * Compiled with -ffp-contract=off so only the explicit fmaf() calls fuse.
  */
+#include <immintrin.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -175,20 +176,53 @@ void orc_predict_scores(const int32_t* hist, const int64_t* table, int E, int la
     }
 }
 
-/* C[M,N] = A[M,K] . B[N,K]^T in fp32 (bf16 inputs). */
+/* C[M,N] = A[M,K] . B[N,K]^T in fp32 (bf16 inputs). Eight interleaved
+ * partial sums per dot product (vectorisable without reassociation flags);
+ * each thread converts one B row to fp32 and reuses it for every A row. */
 void orc_gemm_f32(const uint16_t* a, const uint16_t* b, int64_t M, int64_t N, int64_t K, float* c) {
+    float* af = (float*)malloc(sizeof(float) * M * K);
 #pragma omp parallel for schedule(static)
-    for (int64_t m = 0; m < M; ++m) {
-        float* arow = (float*)malloc(sizeof(float) * K);
-        for (int64_t i = 0; i < K; ++i) arow[i] = bf2f(a[m * K + i]);
+    for (int64_t i = 0; i < M * K; ++i) af[i] = bf2f(a[i]);
+    const int64_t K8 = K & ~(int64_t)7;
+#pragma omp parallel
+    {
+        float* brow = (float*)malloc(sizeof(float) * (K + 8));
+#pragma omp for schedule(static)
         for (int64_t n = 0; n < N; ++n) {
-            const uint16_t* br = b + n * K;
-            float acc = 0.f;
-            for (int64_t i = 0; i < K; ++i) acc += arow[i] * bf2f(br[i]);
-            c[m * N + n] = acc;
+            for (int64_t i = 0; i < K; ++i) brow[i] = bf2f(b[n * K + i]);
+            int64_t m = 0;
+            for (; m + 4 <= M; m += 4) {  /* 4 A rows share each B load */
+                const float* a0 = af + m * K;
+                __m256 s0 = _mm256_setzero_ps(), s1 = s0, s2 = s0, s3 = s0;
+                for (int64_t i = 0; i < K8; i += 8) {
+                    const __m256 bv = _mm256_loadu_ps(brow + i);
+                    s0 = _mm256_fmadd_ps(_mm256_loadu_ps(a0 + i), bv, s0);
+                    s1 = _mm256_fmadd_ps(_mm256_loadu_ps(a0 + K + i), bv, s1);
+                    s2 = _mm256_fmadd_ps(_mm256_loadu_ps(a0 + 2 * K + i), bv, s2);
+                    s3 = _mm256_fmadd_ps(_mm256_loadu_ps(a0 + 3 * K + i), bv, s3);
+                }
+                float out[4][8];
+                _mm256_storeu_ps(out[0], s0);
+                _mm256_storeu_ps(out[1], s1);
+                _mm256_storeu_ps(out[2], s2);
+                _mm256_storeu_ps(out[3], s3);
+                for (int r = 0; r < 4; ++r) {
+                    float s = 0.f;
+                    for (int j = 0; j < 8; ++j) s += out[r][j];
+                    for (int64_t i = K8; i < K; ++i) s += a0[r * K + i] * brow[i];
+                    c[(m + r) * N + n] = s;
+                }
+            }
+            for (; m < M; ++m) {
+                const float* ar = af + m * K;
+                float s = 0.f;
+                for (int64_t i = 0; i < K; ++i) s += ar[i] * brow[i];
+                c[m * N + n] = s;
+            }
         }
-        free(arow);
+        free(brow);
     }
+    free(af);
 }
 
 /* One expert: H = bf16(silu(X W1^T) * (X W3^T)), Y = bf16(H W2^T). */

@@ -195,6 +195,7 @@ class Engine {
     std::vector<int64_t> host_scores_, host_marginal_;
     bool scores_valid_ = false;
     int64_t tokens_generated_ = 0;
+    int64_t launches_ = 0;  // sm_100a kernel launches since the last reset
     std::vector<std::vector<uint16_t>> hidden_dumps_;
     std::vector<double> step_ms_;
 };

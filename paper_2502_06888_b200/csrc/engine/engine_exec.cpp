@@ -36,9 +36,12 @@ namespace {
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
-void kl_check(int rc, const char* what) {
+void kl_check_impl(int rc, const char* what) {
     if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
 }
+// Every kernel entry point goes through here (inside Engine members), which
+// also counts launches for the bench's gpu_launches claim.
+#define kl_check(rc, what) (++launches_, kl_check_impl((rc), (what)))
 
 constexpr int32_t kNoPos = 0x7f7f7f7f;  // memset(0x7f) sentinel for first_pos
 
@@ -427,6 +430,7 @@ void Engine::after_layer_gates(int step, int layer) {
     int32_t* prev = idx_[idx_cur_ ^ 1];
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
+    launches_ += 2;  // rank + scan + scatter kernels
     int64_t* scores = reinterpret_cast<int64_t*>(report_ + 2LL * n * D_.E + 16 - ((2LL * n * D_.E) % 16));
     int64_t* marg_copy = scores + D_.E;
     if (layer + 1 < D_.L) {
@@ -496,6 +500,7 @@ void Engine::exec_expert(const StreamOp& op) {
     for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
         kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, cs), "expert ffn");
+        ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
     if (--exec_expert_left_ == 0) {
         // Every routed row of the block is computed: weighted combine + residual.
@@ -523,6 +528,7 @@ void Engine::reset_log() {
     records_from_ = em_->schedule().prefetch_records.size();
     t0_recorded_ = false;
     tokens_generated_ = 0;
+    launches_ = 0;
     step_ms_.clear();
     hidden_dumps_.clear();
 }
@@ -607,6 +613,17 @@ std::string Engine::report(const std::string& what) {
         j["h2d_gbs_busy"] = link_busy > 0 ? h2d / (link_busy * 1e-12) / 1e9 : 0.0;
         j["h2d_gbs_makespan"] = m.makespan > 0 ? h2d / (m.makespan * 1e-12) / 1e9 : 0.0;
         j["expert_loads"] = n_expert_loads;
+        j["expert_load_busy_ps"] = expert_busy;
+        j["launches"] = launches_;
+        int64_t n_expert_ops = 0, expert_rows = 0;
+        for (const SimEvent& e : tl)
+            if (s.ops[e.op_id].kind == OpKind::compute_expert) {
+                ++n_expert_ops;
+                expert_rows += s.ops[e.op_id].token_count;
+            }
+        j["expert_ops"] = n_expert_ops;
+        j["expert_rows"] = expert_rows;
+        j["expert_bytes"] = spec_.expert_bytes;
         j["compute_ps_by_kind"] = {{"attention", kind_busy[static_cast<int>(OpKind::compute_attention)]},
                                    {"gate", kind_busy[static_cast<int>(OpKind::compute_gate)]},
                                    {"expert", kind_busy[static_cast<int>(OpKind::compute_expert)]}};
