@@ -53,20 +53,25 @@ const char* kl_error_string(int code);
  * Requirements: K % 64 == 0, N % 64 == 0 (N % 256 == 0 for epilogue 2),
  * lda == K, ldb == K (contiguous rows), 16-byte aligned pointers.
  * row_offset selects rows [row_offset, row_offset + M) of a taller A whose
- * total row count is a_rows (used for expert-major permuted activations). */
+ * total row count is a_rows (used for expert-major permuted activations).
+ * workspace (may be NULL): fp32 scratch enabling deterministic K-splits for
+ * small-M (weight-streaming) shapes; kl_gemm_workspace_bytes() is the size
+ * the split heuristic would like (less -> fewer splits, never an error). */
+int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
-                 int epilogue, cudaStream_t stream);
+                 int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
 /* One expert's SwiGLU FFN over its contiguous rows of the permuted buffer:
  *   H = silu(X W1^T) * (X W3^T)   (bf16 [M, f] scratch)
  *   Y = H W2^T                     (bf16 rows [row_offset, row_offset+M) of y)
  * w13 = [W1 (f x d); W3 (f x d)], w2 = d x f, all bf16 and contiguous
  * (exactly moesim ModelSpec::expert_bytes = 3*d*f*2 bytes starting at w13
- * when w2 == w13 + 2*f*d). h_scratch must hold M*f bf16. */
+ * when w2 == w13 + 2*f*d). h_scratch must hold M*f bf16. workspace as for
+ * kl_gemm_bf16 (shared by both GEMMs, used sequentially). */
 int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
                   int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
-                  uint16_t* y, cudaStream_t stream);
+                  uint16_t* y, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
 /* ---- routing ----
  * Fused RMSNorm + router + top-k for T tokens (one warp per token):

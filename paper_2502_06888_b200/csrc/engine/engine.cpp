@@ -56,6 +56,7 @@ std::uint64_t tensor_seed(std::uint64_t base, int kind, int layer, int expert) {
                            static_cast<std::uint64_t>(expert + 1));
 }
 
+constexpr byte_count kGemmWorkspace = 32LL << 20;  // split-K partials for decode-shaped GEMMs
 constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKindHead = 5;
 
 }  // namespace
@@ -239,6 +240,7 @@ void Engine::plan_memory() {
         add(2 * R * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
         add(kl_permute_workspace_bytes(R, D_.E));
+        add(kGemmWorkspace);
         add(5 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/ids/next/last, counts/offsets
         add(seqs * D_.d * 2 + seqs * D_.V * 2);                                  // last_h, head logits
         add(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64);                           // report
@@ -309,6 +311,8 @@ void Engine::allocate_device() {
     y_ = bf(R * D_.d);
     hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
     perm_ws_ = take(kl_permute_workspace_bytes(R, D_.E));
+    gemm_ws_bytes_ = kGemmWorkspace;
+    gemm_ws_ = take(gemm_ws_bytes_);
     tok_pos_ = i32(t_max_);
     tok_seq_ = i32(t_max_);
     ids_ = i32(t_max_);

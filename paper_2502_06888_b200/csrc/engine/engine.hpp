@@ -151,6 +151,8 @@ class Engine {
     int32_t *ids_ = nullptr, *next_ids_ = nullptr, *last_rows_ = nullptr;
     float *weight_ = nullptr, *router_logits_ = nullptr;
     void* perm_ws_ = nullptr;
+    void* gemm_ws_ = nullptr;            // split-K fp32 partials (decode GEMMs)
+    int64_t gemm_ws_bytes_ = 0;
     int32_t* report_ = nullptr;          // [n*E hist | n*E first] + int64 [E scores | E marginal]
     int64_t *table_ = nullptr, *marginal_ = nullptr;
     std::vector<uint16_t*> attn_slot_, gate_slot_;

@@ -162,7 +162,7 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     // Greedy head on the last token of every sequence.
     kl_check(kl_embed(last_rows_, h_, seqs, D_.d, last_h_, cs), "gather last rows");
     kl_check(kl_rmsnorm(last_h_, final_norm_, seqs, D_.d, D_.eps, x2_, cs), "final norm");
-    kl_check(kl_gemm_bf16(x2_, seqs, 0, static_cast<int>(seqs), D_.d, head_, D_.V, head_logits_, D_.V, nullptr, 0, cs),
+    kl_check(kl_gemm_bf16(x2_, seqs, 0, static_cast<int>(seqs), D_.d, head_, D_.V, head_logits_, D_.V, nullptr, 0, gemm_ws_, gemm_ws_bytes_, cs),
              "lm head");
     kl_check(kl_argmax_bf16(head_logits_, seqs, D_.V, next_ids_, cs), "argmax");
     if (next_out != nullptr) {
@@ -374,7 +374,8 @@ void Engine::exec_attention(const StreamOp& op) {
     const uint16_t* wo = w + static_cast<int64_t>(D_.qkv_width()) * D_.d;
     uint16_t* hb = h_ + row0 * D_.d;
     kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
-    kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, cs), "qkv");
+    kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
+                          gemm_ws_bytes_, cs), "qkv");
     const float scale = 1.0f / std::sqrt(static_cast<float>(D_.hd));
     const int last = step == 0 ? cfg_.workload.prompt_len - 1 : -1;
     kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, tok_seq_ + row0, D_.theta, kc_[l],
@@ -385,7 +386,7 @@ void Engine::exec_attention(const StreamOp& op) {
     else
         kl_check(kl_attn_decode(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
                                 kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, cs), "decode attention");
-    kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, cs), "o proj");
+    kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs), "o proj");
 }
 
 void Engine::exec_gate(const StreamOp& op) {
@@ -499,7 +500,8 @@ void Engine::exec_expert(const StreamOp& op) {
     const uint16_t* w2 = w + 2LL * D_.f * D_.d;
     for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
-        kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, cs), "expert ffn");
+        kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
+                               gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
     if (--exec_expert_left_ == 0) {

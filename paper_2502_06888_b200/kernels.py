@@ -28,8 +28,9 @@ def _sig(name, args, res=C.c_int):
 
 _lib.kl_error_string.restype = C.c_char_p
 _lib.kl_error_string.argtypes = [_I]
-_gemm = _sig("kl_gemm_bf16", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P])
-_ffn = _sig("kl_expert_ffn", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P])
+_gemm = _sig("kl_gemm_bf16", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P, _L, _P])
+_gemm_ws = _sig("kl_gemm_workspace_bytes", [_I, _I, _I, _I], C.c_int64)
+_ffn = _sig("kl_expert_ffn", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P, _L, _P])
 _gate = _sig("kl_gate_topk", [_P, _P, _P, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P, _P])
 _perm_ws = _sig("kl_permute_workspace_bytes", [_L, _I], C.c_int64)
 _perm = _sig("kl_permute", [_P, _L, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P])
@@ -64,7 +65,24 @@ def _s(stream):
     return C.c_void_p(stream)
 
 
-def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None):
+_ws_cache = {}
+
+
+def workspace(nbytes, device):
+    """Reusable fp32 split-K workspace (caller-owned per the C-ABI)."""
+    key = (str(device),)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def workspace_bytes(M, N, K, epilogue=0):
+    return int(_gemm_ws(M, N, K, epilogue))
+
+
+def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None, split_k=True):
     """C = A[row_offset:row_offset+m] @ B^T (bf16, fp32 accumulate) on tcgen05."""
     m = a.shape[0] - row_offset if m is None else m
     K = a.shape[1]
@@ -72,16 +90,20 @@ def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=N
     n_out = N // 2 if epilogue == 2 else N
     if c is None:
         c = torch.empty(m, n_out, dtype=torch.bfloat16, device=a.device)
-    _chk(_gemm(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue,
-               _s(stream)), "kl_gemm_bf16")
+    wsb = workspace_bytes(m, N, K, epilogue) if split_k else 0
+    ws = workspace(wsb, a.device) if wsb else None
+    _chk(_gemm(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue, _p(ws),
+               wsb, _s(stream)), "kl_gemm_bf16")
     return c
 
 
-def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None):
+def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None, split_k=True):
     d = xp.shape[1]
     f = w2.shape[1]
-    _chk(_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _s(stream)),
-         "kl_expert_ffn")
+    wsb = max(workspace_bytes(m, 2 * f, d, 2), workspace_bytes(m, d, f, 0)) if split_k else 0
+    ws = workspace(wsb, xp.device) if wsb else None
+    _chk(_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _p(ws), wsb,
+              _s(stream)), "kl_expert_ffn")
 
 
 def gate_topk(h, norm_w, wg, k, eps=1e-5, score_mode=0, x2=None, logits=None, hist=None, first_pos=None,

@@ -1,0 +1,114 @@
+"""Decode-shaped microbenchmarks of every kernel on the Mixtral-8x7B path
+(through the C-ABI), timed with CUDA events on the launching stream after
+warm-up, inputs larger than L2 where it matters (each expert call uses a
+different 352 MB weight buffer). Also the target for `ncu --set full`.
+
+    python tools/profile_kernels.py [--only ffn] [--iters N] [--json out.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2502_06888_b200 import kernels as K  # noqa: E402
+
+d, f, E, k, Hq, Hkv, hd = 4096, 14336, 8, 2, 32, 8, 128
+bs, n = 64, 8
+T = bs * n
+
+
+def timed(fn, iters, stream):
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        fn(0)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for i in range(iters):
+        fn(i)
+    e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e-3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--rows", type=int, default=128)
+    ap.add_argument("--json", default="")
+    args = ap.parse_args()
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream()
+    res = {}
+    bf = torch.bfloat16
+    # Expert FFN: 8 distinct experts (2.8 GB) so weights stream from HBM, not L2.
+    if not args.only or args.only == "ffn":
+        M = args.rows
+        ws = [torch.randn(3 * d * f, dtype=bf, device=dev) * 0.02 for _ in range(E)]
+        xp = torch.randn(T * k, d, dtype=bf, device=dev)
+        y = torch.empty(T * k, d, dtype=bf, device=dev)
+        h = torch.empty(max(M, 1), f, dtype=bf, device=dev)
+
+        def ffn(i):
+            w = ws[i % E]
+            K.expert_ffn(xp, (i % E) * M % (T * k - M + 1), M, w[: 2 * f * d].view(2 * f, d),
+                         w[2 * f * d:].view(d, f), y, h)
+        t = timed(ffn, args.iters, st)
+        byt = 3 * d * f * 2 + M * (2 * d * 2 + 2 * f * 2)
+        res["expert_ffn"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9, "TFLOPs": 6 * M * d * f / t / 1e12}
+
+        def g1(i):
+            w = ws[i % E]
+            K.gemm(xp, w[: 2 * f * d].view(2 * f, d), c=h, epilogue=2, row_offset=0, m=M)
+        t = timed(g1, args.iters, st)
+        res["gemm_swiglu"] = {"M": M, "us": t * 1e6, "GBs": (2 * d * f * 2) / t / 1e9}
+
+        def g2(i):
+            w = ws[i % E]
+            K.gemm(h, w[2 * f * d:].view(d, f), c=y[:M], m=M)
+        t = timed(g2, args.iters, st)
+        res["gemm_down"] = {"M": M, "us": t * 1e6, "GBs": (d * f * 2) / t / 1e9}
+        del ws
+    if not args.only or args.only == "attn":
+        width = (Hq + 2 * Hkv) * hd
+        wqkv = [torch.randn(width, d, dtype=bf, device=dev) * 0.02 for _ in range(4)]
+        x = torch.randn(bs, d, dtype=bf, device=dev)
+        qkv = torch.empty(bs, width, dtype=bf, device=dev)
+        t = timed(lambda i: K.gemm(x, wqkv[i % 4], c=qkv), args.iters, st)
+        res["gemm_qkv_M64"] = {"us": t * 1e6, "GBs": width * d * 2 / t / 1e9}
+        cap = 260
+        kc = torch.randn(T * cap * Hkv * hd, dtype=bf, device=dev)
+        vc = torch.randn_like(kc)
+        pos = torch.full((bs,), 600, dtype=torch.int32, device=dev)
+        seq = torch.arange(bs, dtype=torch.int32, device=dev)
+        out = torch.empty(bs, Hq * hd, dtype=bf, device=dev)
+
+        def att(i):
+            K.attn_decode(qkv, width, pos, seq + (i % n) * bs, Hq, Hkv, hd, kc, vc, cap, 4, hd ** -0.5, out)
+        t = timed(att, args.iters, st)
+        res["attn_decode_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+    if not args.only or args.only == "route":
+        h = torch.randn(T, d, dtype=bf, device=dev)
+        nw = torch.ones(d, dtype=bf, device=dev)
+        wg = torch.randn(E, d, dtype=bf, device=dev) * 0.02
+        x2 = torch.empty_like(h)
+        t = timed(lambda i: K.gate_topk(h[:bs], nw, wg, k, x2=x2[:bs]), args.iters, st)
+        res["gate_topk_b64"] = {"us": t * 1e6}
+        _, idx, wt = K.gate_topk(h, nw, wg, k, x2=x2)
+        t = timed(lambda i: K.permute(idx, E, x2=x2), args.iters, st)
+        res["permute_T512"] = {"us": t * 1e6, "GBs": (T * d * 2 + T * k * d * 2) / t / 1e9}
+        _, _, p, _, xp = K.permute(idx, E, x2=x2)
+        t = timed(lambda i: K.combine(xp, p, wt, h, out=x2), args.iters, st)
+        res["combine_T512"] = {"us": t * 1e6, "GBs": (k * T * d * 2 + 2 * T * d * 2) / t / 1e9}
+    print(json.dumps(res, indent=1))
+    if args.json:
+        with open(args.json, "w") as fh:
+            json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
