@@ -240,7 +240,19 @@ void Engine::plan_memory() {
         add(2 * R * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
         add(kl_permute_workspace_bytes(R, D_.E));
-        add(kGemmWorkspace);
+        // Split-K partials: the largest request of any small-M GEMM we issue.
+        gemm_ws_bytes_ = 0;
+        for (int64_t m : {int64_t{32}, int64_t{64}, int64_t{128}, int64_t{192}, int64_t{256}, tb_max_, seqs}) {
+            if (m > std::max<int64_t>(R, tb_max_)) continue;
+            const int mi = static_cast<int>(m);
+            gemm_ws_bytes_ = std::max({gemm_ws_bytes_, kl_gemm_workspace_bytes(mi, 2 * D_.f, D_.d, 2),
+                                       kl_gemm_workspace_bytes(mi, D_.d, D_.f, 0),
+                                       kl_gemm_workspace_bytes(mi, D_.qkv_width(), D_.d, 0),
+                                       kl_gemm_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1),
+                                       kl_gemm_workspace_bytes(mi, D_.V, D_.d, 0)});
+        }
+        gemm_ws_bytes_ = std::min<int64_t>(gemm_ws_bytes_, kGemmWorkspace);
+        add(gemm_ws_bytes_);
         add(5 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/ids/next/last, counts/offsets
         add(seqs * D_.d * 2 + seqs * D_.V * 2);                                  // last_h, head logits
         add(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64);                           // report
@@ -311,8 +323,7 @@ void Engine::allocate_device() {
     y_ = bf(R * D_.d);
     hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
     perm_ws_ = take(kl_permute_workspace_bytes(R, D_.E));
-    gemm_ws_bytes_ = kGemmWorkspace;
-    gemm_ws_ = take(gemm_ws_bytes_);
+    gemm_ws_ = gemm_ws_bytes_ > 0 ? take(gemm_ws_bytes_) : nullptr;
     tok_pos_ = i32(t_max_);
     tok_seq_ = i32(t_max_);
     ids_ = i32(t_max_);

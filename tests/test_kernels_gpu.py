@@ -54,6 +54,29 @@ def test_gemm_store(K, cuda, M, N, Kd):
     close_bf16(to_bits(c), orc.gemm_f32(a, b))
 
 
+@pytest.mark.parametrize("split", [True, False])
+def test_gemm_residual_split_k(K, cuda, split):
+    M, N, Kd = 64, 4096, 4096
+    a = orc.normal_bf16(M * Kd, 24, 1.0).reshape(M, Kd)
+    b = orc.normal_bf16(N * Kd, 25, 0.02).reshape(N, Kd)
+    r = orc.normal_bf16(M * N, 26, 1.0).reshape(M, N)
+    rd = to_dev(r, cuda)
+    assert K.workspace_bytes(M, N, Kd, 1) > 0  # this shape takes the split-K path
+    c = K.gemm(to_dev(a, cuda), to_dev(b, cuda), c=rd, residual=rd, epilogue=1, split_k=split)
+    torch.cuda.synchronize()
+    close_bf16(to_bits(c), orc.gemm_f32(a, b) + orc.bits_to_f32(r))
+
+
+def test_gemm_split_k_is_deterministic(K, cuda):
+    M, N, Kd = 100, 1024, 8192
+    a = to_dev(orc.normal_bf16(M * Kd, 27, 1.0).reshape(M, Kd), cuda)
+    b = to_dev(orc.normal_bf16(N * Kd, 28, 0.02).reshape(N, Kd), cuda)
+    x = K.gemm(a, b)
+    y = K.gemm(a, b)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+
+
 def test_gemm_residual_and_row_offset(K, cuda):
     rows, M, off, N, Kd = 500, 130, 77, 384, 512
     a = orc.normal_bf16(rows * Kd, 21, 1.0).reshape(rows, Kd)
@@ -66,7 +89,8 @@ def test_gemm_residual_and_row_offset(K, cuda):
     close_bf16(to_bits(c), ref)
 
 
-@pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048)])
+@pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048), (128, 4096, 1024),
+                                   (64, 2048, 1408), (300, 512, 1792)])
 def test_expert_ffn(K, cuda, M, d, f):
     rows, off = M + 50, 19
     x = orc.normal_bf16(rows * d, 31, 1.0).reshape(rows, d)
