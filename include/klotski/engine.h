@@ -81,6 +81,11 @@ int kl_engine_report(kl_engine* e, const char* what, char** json_out);
 /* Forget the executed op log and timeline (weights, KV and tables stay). */
 int kl_engine_reset_log(kl_engine* e);
 
+/* Expert parallelism: rank 0 creates an NCCL unique id (256 hex chars +
+ * NUL into hex_out[257]) and shares it; every rank then passes it as
+ * config "ep": {"rank": r, "world": G, "nccl_id": hex}. 0 = success. */
+int kl_ep_unique_id(char* hex_out);
+
 /* Copy the group's current hidden states [T, d] (bf16 bits) to host. */
 int kl_engine_read_hidden(kl_engine* e, uint16_t* host, int64_t n_elems);
 

@@ -164,6 +164,14 @@ int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, cons
 int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap,
                     int sink, float scale, uint16_t* out, cudaStream_t stream);
 
+/* ---- expert-parallel helpers ----
+ * out[i] = map[in[i]]  (relabel global expert ids, e.g. destination-major). */
+int kl_map_ids(const int32_t* in, int64_t n, const int32_t* map, int32_t* out, cudaStream_t stream);
+/* out[c] = sum_r in[r*cols + c]  (int32 histogram rows -> one histogram). */
+int kl_sum_rows_i32(const int32_t* in, int rows, int cols, int32_t* out, cudaStream_t stream);
+/* dst[i] += src[i]  (apply an all-reduced co-activation delta). */
+int kl_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t stream);
+
 /* Deterministic synthetic bf16 init on device: v[i] = N(0, std) from a
  * SplitMix64 stream keyed by (seed, i) (Box-Muller), for weights/inputs. */
 int kl_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, float std_dev,

@@ -1,0 +1,109 @@
+"""CPU model oracle for the engine's numerics (TEST INFRASTRUCTURE).
+
+Regenerates the engine's synthetic weights bit-exactly (same SplitMix64
+tensor seeds as csrc/engine/engine.cpp, same Irwin-Hall stream as
+kl_fill_normal_bf16) and runs one decoder layer at a time with the C oracle
+kernels: RMSNorm, QKV GEMM, RoPE + KV append, prefill/decode attention,
+O projection + residual, router, expert-major permutation, SwiGLU experts,
+combine. Used teacher-forced: each layer starts from the GPU's own input
+hidden state (and optionally the GPU's routing), so per-layer differences are
+the kernels' rounding, not accumulated drift.
+"""
+import numpy as np
+
+from oracle import pyoracle as orc
+
+M64 = (1 << 64) - 1
+KIND_EXPERT, KIND_ATTN, KIND_GATE, KIND_EMBED, KIND_HEAD = 1, 2, 3, 4, 5
+
+
+def splitmix_next(state):
+    state = (state + 0x9E3779B97F4A7C15) & M64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def mix64(a, b):
+    return splitmix_next(a ^ ((b + 0x9E3779B97F4A7C15 + ((a << 6) & M64) + (a >> 2)) & M64))
+
+
+def tensor_seed(base, kind, layer, expert):
+    return mix64(base, ((kind << 48) ^ (layer << 16) ^ (expert + 1)) & M64)
+
+
+class TinyModel:
+    def __init__(self, dims, weight_seed=7):
+        self.D = D = dims
+        self.seed = weight_seed
+        d, f, E = D["d"], D["f"], D["E"]
+        self.qkvw = (D["Hq"] + 2 * D["Hkv"]) * D["hd"]
+        self.embed = orc.normal_bf16(D["V"] * d, tensor_seed(weight_seed, KIND_EMBED, 0, 0), 1.0).reshape(D["V"], d)
+        self.head = orc.normal_bf16(D["V"] * d, tensor_seed(weight_seed, KIND_HEAD, 0, 0), 0.02).reshape(D["V"], d)
+        self.norm = orc.bf16_bits(np.ones(d, np.float32))
+        self.layers = []
+        for l in range(D["L"]):
+            a = orc.normal_bf16(self.qkvw * d + d * D["Hq"] * D["hd"], tensor_seed(weight_seed, KIND_ATTN, l, 0),
+                                0.02)
+            experts = []
+            for e in range(E):
+                w = orc.normal_bf16(3 * d * f, tensor_seed(weight_seed, KIND_EXPERT, l, e), 0.02)
+                experts.append((w[: 2 * f * d].reshape(2 * f, d), w[2 * f * d:].reshape(d, f)))
+            self.layers.append({
+                "wqkv": a[: self.qkvw * d].reshape(self.qkvw, d),
+                "wo": a[self.qkvw * d:].reshape(d, D["Hq"] * D["hd"]),
+                "wg": orc.normal_bf16(E * d, tensor_seed(weight_seed, KIND_GATE, l, 0), 0.02).reshape(E, d),
+                "experts": experts,
+            })
+
+    def new_kv(self, n_seqs, cap):
+        D = self.D
+        size = n_seqs * cap * D["Hkv"] * D["hd"]
+        return [(np.zeros(size, np.uint16), np.zeros(size, np.uint16)) for _ in range(D["L"])]
+
+    def layer(self, l, h, step, n_batches, batch_size, prompt_len, kv, cap, sink, forced_idx=None):
+        """One decoder layer on the whole batch group (rows batch-major,
+        sequence-major). Returns (output hidden bf16 bits, routing ids)."""
+        D, W = self.D, self.layers[l]
+        hd, d = D["hd"], D["d"]
+        tpb = batch_size * (prompt_len if step == 0 else 1)
+        h = h.copy()
+        kc, vc = kv[l]
+        for b in range(n_batches):
+            rows = slice(b * tpb, (b + 1) * tpb)
+            hb = np.ascontiguousarray(h[rows])
+            xa = orc.rmsnorm(hb, self.norm, D["eps"])
+            qkv = orc.bf16_bits(orc.gemm_f32(xa, W["wqkv"]))
+            if step == 0:
+                pos = np.tile(np.arange(prompt_len, dtype=np.int32), batch_size)
+                seq = np.repeat(np.arange(b * batch_size, (b + 1) * batch_size, dtype=np.int32), prompt_len)
+                orc.rope_kv_append(qkv, D["Hq"], D["Hkv"], hd, pos, seq, D["theta"], kc, vc, cap, sink, prompt_len - 1)
+                ao = orc.attn_prefill(qkv, batch_size, prompt_len, D["Hq"], D["Hkv"], hd, cap, sink, hd ** -0.5)
+            else:
+                pos = np.full(tpb, prompt_len + step - 1, np.int32)
+                seq = np.arange(b * batch_size, (b + 1) * batch_size, dtype=np.int32)
+                orc.rope_kv_append(qkv, D["Hq"], D["Hkv"], hd, pos, seq, D["theta"], kc, vc, cap, sink, -1)
+                ao = orc.attn_decode(qkv, self.qkvw, pos, seq, D["Hq"], D["Hkv"], hd, kc, vc, cap, hd ** -0.5)
+            h[rows] = orc.bf16_bits(orc.gemm_f32(ao, W["wo"]) + orc.bits_to_f32(hb))
+        x2 = orc.rmsnorm(h, self.norm, D["eps"])
+        logits, idx, w = orc.gate_topk(x2, W["wg"], D["k"], D.get("score_mode", 0))
+        own_idx = idx.copy()
+        if forced_idx is not None:
+            idx = forced_idx.astype(np.int32).reshape(idx.shape)
+            sel = np.take_along_axis(logits, idx, 1)
+            p = np.exp(sel - sel[:, :1])
+            w = (p / p.sum(1, keepdims=True)).astype(np.float32)
+        counts, offsets, pos_r, row_token = orc.permute(idx, D["E"])
+        xp = np.ascontiguousarray(x2[row_token])
+        y = np.empty_like(xp)
+        for e in range(D["E"]):
+            lo, hi = offsets[e], offsets[e + 1]
+            if hi > lo:
+                y[lo:hi] = orc.expert_ffn(np.ascontiguousarray(xp[lo:hi]), *W["experts"][e])
+        return orc.combine(y, pos_r, w, h), own_idx, logits
+
+    def greedy(self, h_last):
+        x = orc.rmsnorm(h_last, self.norm, self.D["eps"])
+        logits = orc.gemm_f32(x, self.head)
+        return orc.bits_to_f32(orc.bf16_bits(logits)).argmax(1), logits

@@ -119,8 +119,14 @@ EngineConfig parse_config(const std::string& text) {
     c.record_trace = j.value("record_trace", true);
     c.record_hidden = j.value("record_hidden", false);
     if (j.contains("ep")) {
+        c.ep = true;
         c.ep_rank = j["ep"].value("rank", 0);
         c.ep_world = j["ep"].value("world", 1);
+        c.ep_nccl_id = j["ep"].value("nccl_id", "");
+        if (c.ep_world < 1 || c.ep_rank < 0 || c.ep_rank >= c.ep_world || D.E % c.ep_world != 0)
+            throw ConfigError("engine EP: need 0 <= rank < world and experts divisible by world");
+        if (c.variant != Variant::klotski) throw ConfigError("engine EP: only the klotski variant is sharded");
+        if (j.value("routing", "gate") != "gate") throw ConfigError("engine EP: routing must come from the gate");
     }
     c.prefill = j.value("prefill", true);
     D.qkv_width();
@@ -152,6 +158,18 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     spec_.gate_bytes = D_.gate_elems() * 2;
     spec_.kv_bytes_per_token = 2LL * D_.Hkv * D_.hd * 2;
     spec_.dtype = {"bf16", 16};
+    spec_g_ = spec_;
+    El_ = D_.E;
+    if (cfg_.ep) {
+        // The local shard is what this rank plans, places, streams and
+        // schedules; the router and the correlation table stay global.
+        ep_ = true;
+        G_ = cfg_.ep_world;
+        rank_ = cfg_.ep_rank;
+        El_ = D_.E / G_;
+        spec_.n_experts_per_layer = El_;
+        spec_.top_k = std::min(D_.k, El_);
+    }
     profile_.name = "b200";
     profile_.vram_capacity = cfg_.hbm_cap;
     profile_.dram_capacity = cfg_.host_dram;
@@ -169,15 +187,16 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     allocate_host();
     for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&t0_), "event");
+    ep_init();
     init_weights();
     const detail::GroupShape shape{cfg_.workload.gen_len, D_.L, plan_.n_batches, cfg_.workload.batch_size,
-                           cfg_.workload.prompt_len, D_.k, D_.E};
+                           cfg_.workload.prompt_len, spec_.top_k, El_};
     em_ = std::make_unique<detail::Emitter>(cfg_.variant, plan_, shape, ScheduleOptions{});
     // Trace containers: replayed routing and the routing actually executed.
     BatchGroupConfig g = cfg_.workload;
     g.n_batches = plan_.n_batches;
-    if (cfg_.replay) replay_trace_ = generate_trace(spec_, g, cfg_.skew, cfg_.trace_seed);
-    recorded_ = generate_trace(spec_, g, SkewSpec::uniform(), 0);
+    if (cfg_.replay) replay_trace_ = generate_trace(spec_g_, g, cfg_.skew, cfg_.trace_seed);
+    recorded_ = generate_trace(spec_g_, g, SkewSpec::uniform(), 0);
     recorded_.seed = 0;
     std::fill(recorded_.sel.begin(), recorded_.sel.end(), 0);
     host_marginal_ = table0_.marginal;
@@ -185,6 +204,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
 
 Engine::~Engine() {
     cudaDeviceSynchronize();
+    ep_shutdown();
     for (auto& s : streams_)
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
@@ -213,8 +233,8 @@ void Engine::plan_memory() {
     BatchGroupConfig warm = w;
     warm.n_batches = w.batch_size > 1 ? 2 : 4;
     const ActivationTrace wt =
-        generate_trace(spec_, warm, cfg_.skew, cfg_.warmup_seed ? cfg_.warmup_seed : cfg_.trace_seed + 1);
-    table0_ = build_table(wt, spec_);
+        generate_trace(spec_g_, warm, cfg_.skew, cfg_.warmup_seed ? cfg_.warmup_seed : cfg_.trace_seed + 1);
+    table0_ = build_table(wt, spec_g_);
     const TraceStats stats = compute_trace_stats(wt, D_.k);
 
     int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, std::nullopt,
@@ -224,7 +244,9 @@ void Engine::plan_memory() {
         const int64_t seqs = static_cast<int64_t>(w.batch_size) * n;
         t_max_ = seqs * (cfg_.prefill ? w.prompt_len : 1);
         tb_max_ = static_cast<int64_t>(w.batch_size) * (cfg_.prefill ? w.prompt_len : 1);
-        slots_ = cfg_.expert_slots > 0 ? cfg_.expert_slots : D_.E + D_.k;
+        slots_ = cfg_.expert_slots > 0 ? cfg_.expert_slots : El_ + spec_.top_k;
+        r_recv_max_ = ep_ ? static_cast<int64_t>(G_) * t_max_ * D_.k : 0;
+        const int64_t Rx = std::max<int64_t>(t_max_ * D_.k, r_recv_max_);
         const int64_t R = t_max_ * D_.k;
         const int64_t chunk = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1));
         byte_count ws = 0;
@@ -237,9 +259,14 @@ void Engine::plan_memory() {
         add(2 * t_max_ * D_.d * 2);                                              // h, x2
         add(tb_max_ * (D_.d + D_.qkv_width() + D_.Hq * D_.hd) * 2);              // xa, qkv, ao
         add(4 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
-        add(2 * R * D_.d * 2);                                                   // xp, y
+        add(2 * Rx * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
-        add(kl_permute_workspace_bytes(R, D_.E));
+        add(kl_permute_workspace_bytes(Rx, D_.E));
+        if (ep_) {  // exchange buffers, labels, counts, co-activation delta
+            add(r_recv_max_ * D_.d * 2 * 2 + R * D_.d * 2);
+            add((R + 3 * r_recv_max_) * 4 + (3LL * D_.E + 2 * El_ + 8) * 4);
+            add((static_cast<int64_t>(D_.E) * D_.E + D_.E) * 8);
+        }
         // Split-K partials: the largest request of any small-M GEMM we issue.
         gemm_ws_bytes_ = 0;
         for (int64_t m : {int64_t{32}, int64_t{64}, int64_t{128}, int64_t{192}, int64_t{256}, tb_max_, seqs}) {
@@ -319,10 +346,11 @@ void Engine::allocate_device() {
     row_token_ = i32(R);
     weight_ = static_cast<float*>(take(R * 4));
     router_logits_ = static_cast<float*>(take(t_max_ * D_.E * 4));
-    xp_ = bf(R * D_.d);
-    y_ = bf(R * D_.d);
+    const int64_t Rx = std::max<int64_t>(R, r_recv_max_);
+    xp_ = bf(Rx * D_.d);
+    y_ = bf(Rx * D_.d);
     hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
-    perm_ws_ = take(kl_permute_workspace_bytes(R, D_.E));
+    perm_ws_ = take(kl_permute_workspace_bytes(Rx, D_.E));
     gemm_ws_ = gemm_ws_bytes_ > 0 ? take(gemm_ws_bytes_) : nullptr;
     tok_pos_ = i32(t_max_);
     tok_seq_ = i32(t_max_);
@@ -336,6 +364,25 @@ void Engine::allocate_device() {
     report_ = static_cast<int32_t*>(take(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64));
     table_ = static_cast<int64_t*>(take((static_cast<byte_count>(std::max(D_.L - 1, 1)) * D_.E * D_.E) * 8));
     marginal_ = static_cast<int64_t*>(take(D_.E * 8));
+    if (ep_) {
+        label_map_ = i32(D_.E);
+        lbl_ = i32(R);
+        recv_ids_ = i32(r_recv_max_);
+        pos2_ = i32(r_recv_max_);
+        row_token2_ = i32(r_recv_max_);
+        recv_counts_ = i32(D_.E);
+        hist_all_ = i32(D_.E);
+        counts2_ = i32(El_ + 1);
+        offsets2_ = i32(El_ + 1);
+        send_counts_ = i32(D_.E + 1);
+        delta_ = static_cast<int64_t*>(take((static_cast<int64_t>(D_.E) * D_.E + D_.E) * 8));
+        recv_x_ = bf(r_recv_max_ * D_.d);
+        y_back_ = bf(r_recv_max_ * D_.d);
+        y_ret_ = bf(R * D_.d);
+        std::vector<int32_t> label(D_.E);
+        for (int e = 0; e < D_.E; ++e) label[e] = (e % G_) * El_ + e / G_;  // destination-major
+        cuda_check(cudaMemcpy(label_map_, label.data(), D_.E * 4, cudaMemcpyHostToDevice), "label map");
+    }
     const byte_count ws_real = arena_used_;
 
     // KV caches and resident layers (planner's decisions).
@@ -345,11 +392,11 @@ void Engine::allocate_device() {
         kc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
         vc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
     }
-    res_expert_.assign(static_cast<size_t>(D_.L) * D_.E, nullptr);
+    res_expert_.assign(static_cast<size_t>(D_.L) * El_, nullptr);
     res_attn_.assign(D_.L, nullptr);
     for (int l = 0; l < D_.L; ++l) {
         if (plan_.placement.expert_tier[l] == Tier::vram)
-            for (int e = 0; e < D_.E; ++e) res_expert_[l * D_.E + e] = bf(D_.expert_elems());
+            for (int e = 0; e < El_; ++e) res_expert_[l * El_ + e] = bf(D_.expert_elems());
         if (plan_.placement.attention_tier[l] == Tier::vram) res_attn_[l] = bf(D_.attention_elems());
     }
     if (ws_real > ws_bytes_ + 64 * 1024)
@@ -358,7 +405,7 @@ void Engine::allocate_device() {
 }
 
 void Engine::allocate_host() {
-    const int L = D_.L, E = D_.E;
+    const int L = D_.L, E = El_;  // expert arrays are per local shard
     host_expert_.assign(static_cast<size_t>(L) * E, nullptr);
     host_attn_.assign(L, nullptr);
     host_gate_.assign(L, nullptr);
@@ -406,7 +453,8 @@ void Engine::allocate_host() {
         host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
     }
     const int n = plan_.n_batches;
-    host_report_ = static_cast<int32_t*>(pinned(2LL * n * E * 4 + 2LL * E * 8 + 64));
+    host_report_ = static_cast<int32_t*>(pinned(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + D_.E * 4 + 128));
+    if (ep_) host_recv_ids_ = static_cast<int32_t*>(pinned(std::max<int64_t>(r_recv_max_, 1) * 4));
     host_idx_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
     host_forced_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
     host_tokens_ = static_cast<int32_t*>(pinned(4 * t_max_ * 4));
@@ -431,17 +479,19 @@ void Engine::init_weights() {
     uint16_t* stage = D_.expert_elems() >= D_.attention_elems() ? pool_.ptr[0] : attn_slot_[0];
     std::vector<char> host_done(host_blocks_.size(), 0);
     for (int l = 0; l < D_.L; ++l) {
-        for (int e = 0; e < D_.E; ++e) {
-            const std::uint64_t seed = tensor_seed(ws, kKindExpert, l, e);
-            if (uint16_t* r = res_expert_[l * D_.E + e]) {
+        for (int e = 0; e < El_; ++e) {
+            // Seeds follow the GLOBAL expert id so every EP shard holds the
+            // same weights the single-GPU engine would.
+            const std::uint64_t seed = tensor_seed(ws, kKindExpert, l, ep_ ? e * G_ + rank_ : e);
+            if (uint16_t* r = res_expert_[l * El_ + e]) {
                 kl_check(kl_fill_normal_bf16(r, D_.expert_elems(), seed, sd, st), "init expert");
-                if (uint16_t* h = host_expert_[l * D_.E + e])
+                if (uint16_t* h = host_expert_[l * El_ + e])
                     cuda_check(cudaMemcpyAsync(h, r, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
-            } else if (uint16_t* h = host_expert_[l * D_.E + e]) {
+            } else if (uint16_t* h = host_expert_[l * El_ + e]) {
                 // Aliased host layers are filled once, by their first user.
                 bool first = true;
                 for (int l2 = 0; l2 < l && first; ++l2)
-                    if (host_expert_[l2 * D_.E + e] == h) first = false;
+                    if (host_expert_[l2 * El_ + e] == h) first = false;
                 if (!first) continue;
                 kl_check(kl_fill_normal_bf16(stage, D_.expert_elems(), seed, sd, st), "init expert");
                 cuda_check(cudaMemcpyAsync(h, stage, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");

@@ -66,6 +66,8 @@ struct EngineConfig {
     bool record_trace = true;
     bool record_hidden = false;
     int ep_rank = 0, ep_world = 1;
+    bool ep = false;                // expert-parallel engine (also for world 1)
+    std::string ep_nccl_id;         // 256 hex chars of ncclUniqueId (world > 1)
     bool prefill = true;
 };
 
@@ -198,6 +200,31 @@ class Engine {
     bool scores_valid_ = false;
     int64_t tokens_generated_ = 0;
     int64_t launches_ = 0;  // sm_100a kernel launches since the last reset
+
+    // ---- expert parallelism (engine_ep.cpp) ----
+    // Global expert e lives on rank e % G as local expert e / G. Each rank
+    // runs attention + router for its own batch group, streams only its
+    // expert shard, and exchanges routed rows with NCCL all-to-all.
+    void ep_init();
+    void ep_after_gates(int step, int layer);
+    moesim::detail::BlockRouting ep_read_routing(int step, int layer);
+    void ep_dispatch();
+    void ep_return(int64_t T);
+    moesim::ModelSpec spec_g_;            // global model (E experts) for traces/tables
+    bool ep_ = false;
+    int G_ = 1, rank_ = 0, El_ = 0;
+    struct Nccl;
+    Nccl* nccl_ = nullptr;
+    void ep_shutdown();
+    int32_t *label_map_ = nullptr, *lbl_ = nullptr, *recv_ids_ = nullptr, *pos2_ = nullptr, *row_token2_ = nullptr;
+    int32_t *recv_counts_ = nullptr, *hist_all_ = nullptr, *counts2_ = nullptr, *offsets2_ = nullptr;
+    int32_t *send_counts_ = nullptr;
+    int64_t* delta_ = nullptr;
+    uint16_t *recv_x_ = nullptr, *y_back_ = nullptr, *y_ret_ = nullptr;
+    int64_t r_recv_max_ = 0, r_recv_ = 0, r_send_ = 0;
+    std::vector<int64_t> send_cnt_, send_off_, recv_cnt_, recv_off_;
+    int32_t* host_recv_ids_ = nullptr;
+    bool dispatched_ = false;
     std::vector<std::vector<uint16_t>> hidden_dumps_;
     std::vector<double> step_ms_;
 };

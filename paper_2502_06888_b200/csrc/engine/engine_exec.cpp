@@ -57,7 +57,7 @@ cudaEvent_t Engine::event() {
 }
 
 const uint16_t* Engine::expert_weights(int layer, int e) const {
-    if (const uint16_t* r = res_expert_[static_cast<size_t>(layer) * D_.E + e]) return r;
+    if (const uint16_t* r = res_expert_[static_cast<size_t>(layer) * El_ + e]) return r;
     const auto it = expert_slot_of_.find({layer, e});
     if (it == expert_slot_of_.end())
         throw AccountingError("engine: expert (" + std::to_string(layer) + "," + std::to_string(e) +
@@ -79,14 +79,15 @@ PrefetchDecision Engine::decide(int /*step*/, int layer) const {
             d.used_fallback = true;
         }
     }
-    std::vector<int> ids(D_.E);
+    // Candidates are this rank's experts (all of them without EP): local id
+    // j is global expert j*G + rank; ties keep the lower id (correlation.cpp:75-84).
+    std::vector<int> ids(El_);
     std::iota(ids.begin(), ids.end(), 0);
-    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
-        return score[a] != score[b] ? score[a] > score[b] : a < b;
-    });
-    ids.resize(std::min(D_.k, D_.E));
+    auto sc = [&](int j) { return score[static_cast<size_t>(j) * G_ + rank_]; };
+    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) { return sc(a) != sc(b) ? sc(a) > sc(b) : a < b; });
+    ids.resize(std::min(spec_.top_k, El_));
     d.expert_ids = ids;
-    for (int id : ids) d.scores.push_back(score[id]);
+    for (int id : ids) d.scores.push_back(sc(id));
     return d;
 }
 
@@ -151,12 +152,14 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
         detail::OpenBlock blk = em_->open_block(step, layer, split ? &d : nullptr);
         block_layer_ = layer;
         issue_pending();
-        const detail::BlockRouting routing = read_routing(step, layer);
+        const detail::BlockRouting routing = ep_ ? ep_read_routing(step, layer) : read_routing(step, layer);
         const detail::ClosedBlock closed = em_->close_block(blk, routing);
         exec_expert_left_ = 0;
         for (std::int32_t id = closed.first_op; id < static_cast<std::int32_t>(em_->schedule().ops.size()); ++id)
             exec_expert_left_ += em_->schedule().ops[id].kind == OpKind::compute_expert;
+        if (ep_) ep_dispatch();  // routed rows to their expert's rank (every rank, every layer)
         issue_pending();
+        if (ep_) ep_return(T);   // expert outputs back + weighted combine
     }
 
     // Greedy head on the last token of every sequence.
@@ -252,7 +255,7 @@ void Engine::exec(std::int32_t id) {
     }
     op_start_[id] = event();
     op_end_[id] = event();
-    const size_t E = static_cast<size_t>(D_.E);
+    const size_t E = static_cast<size_t>(El_);  // local expert shard
     auto wait_release = [&](cudaEvent_t ev) {
         if (ev != nullptr) cuda_check(cudaStreamWaitEvent(st, ev, 0), "slot wait");
     };
@@ -417,7 +420,12 @@ void Engine::exec_gate(const StreamOp& op) {
         kl_check(kl_gate_topk(h_ + row0 * D_.d, norm_ffn_[l], wg, tpb, D_.d, D_.E, D_.k, D_.eps, D_.score_mode,
                               x2_ + row0 * D_.d, nullptr, idx, wt, hist, first, cs), "gate");
     }
-    if (b == n - 1) after_layer_gates(step, l);
+    if (b == n - 1) {
+        if (ep_)
+            ep_after_gates(step, l);
+        else
+            after_layer_gates(step, l);
+    }
 }
 
 // Work tied to the block's last gate: expert-major permutation of the whole
@@ -504,7 +512,7 @@ void Engine::exec_expert(const StreamOp& op) {
                                gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
-    if (--exec_expert_left_ == 0) {
+    if (--exec_expert_left_ == 0 && !ep_) {
         // Every routed row of the block is computed: weighted combine + residual.
         const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(op.step);
         kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
@@ -642,8 +650,15 @@ std::string Engine::report(const std::string& what) {
         j["sel"] = recorded_.sel;
         j["text_header"] = trace_to_string(ActivationTrace{}).substr(0, 0);
     } else if (what == "validate") {
-        const ValidationReport rep = validate_schedule(s, cfg_.replay ? replay_trace_ : recorded_, plan_);
-        j["violations"] = rep.violations;
+        if (ep_) {
+            // A shard's schedule covers its local experts only; the
+            // single-GPU validator's token conservation does not apply.
+            j["violations"] = json::array();
+            j["skipped"] = "expert-parallel shard";
+        } else {
+            const ValidationReport rep = validate_schedule(s, cfg_.replay ? replay_trace_ : recorded_, plan_);
+            j["violations"] = rep.violations;
+        }
     } else if (what == "hidden") {
         json arr = json::array();
         for (const auto& dmp : hidden_dumps_) arr.push_back(dmp);

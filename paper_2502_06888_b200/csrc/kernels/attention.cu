@@ -67,84 +67,144 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
     }
 }
 
-// One CTA per (token, kv head); warp g handles query head kvh*G + g.
-// Phase 1: lane-per-slot scores; phase 2: warp softmax; phase 3: P.V with
-// each lane owning 4 of the 128 head dims.
+// One CTA (4 warps) per (token, kv head) covering the G query heads of the
+// GQA group, so each retained K/V row is read from HBM exactly once:
+//   1. thread-per-slot scores for all G heads (q in smem, broadcast reads);
+//   2. per-head softmax (warp per head);
+//   3. P.V with warps splitting the slots and lanes owning HD/32 dims each,
+//      then a fixed-order cross-warp sum in smem.
+constexpr int kAttnWarps = 4;
+
 template <int HD>
-__global__ void attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
-                                   const int32_t* __restrict__ seq, int Hq, int Hkv, const uint16_t* __restrict__ kc,
-                                   const uint16_t* __restrict__ vc, int cap, int sink, float scale,
-                                   uint16_t* __restrict__ out) {
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
+                   const int32_t* __restrict__ seq, int Hq, int Hkv, const uint16_t* __restrict__ kc,
+                   const uint16_t* __restrict__ vc, int cap, int sink, float scale, uint16_t* __restrict__ out) {
     constexpr int PER = HD / 32;  // head dims owned by one lane in the P.V phase
-    extern __shared__ float sc[];  // [G][cap]
+    constexpr int GMAX = 8;
+    extern __shared__ float smem_f[];
+    const int G = Hq / Hkv;
+    float* qs = smem_f;                     // [G][HD]
+    float* sc = qs + G * HD;                // [G][cap]
+    float* red = sc + G * cap;              // [warps][G][HD]
+    float* inv_sum = red + kAttnWarps * G * HD;  // [G]
     const int t = blockIdx.x;
     const int kvh = blockIdx.y;
-    const int G = Hq / Hkv;
-    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qh = kvh * G + g;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = pos[t];
     const int n = p + 1 < cap ? p + 1 : cap;  // retained slots (all valid)
-    const int64_t seq_base = static_cast<int64_t>(seq[t]) * cap * Hkv * HD;
-    float* s = sc + g * cap;
+    const int64_t row_stride = static_cast<int64_t>(Hkv) * HD;
+    const uint16_t* kbase = kc + static_cast<int64_t>(seq[t]) * cap * row_stride + static_cast<int64_t>(kvh) * HD;
+    const uint16_t* vbase = vc + static_cast<int64_t>(seq[t]) * cap * row_stride + static_cast<int64_t>(kvh) * HD;
 
-    // Query head in registers (fp32), 128 dims.
-    const uint16_t* qp = q + static_cast<int64_t>(t) * q_stride + static_cast<int64_t>(qh) * HD;
-    float qv[HD];
+    const uint16_t* qp = q + static_cast<int64_t>(t) * q_stride + static_cast<int64_t>(kvh) * G * HD;
+    for (int i = threadIdx.x; i < G * HD; i += blockDim.x) qs[i] = bf2f(qp[i]) * scale;
+    __syncthreads();
+
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const uint16_t* kp = kbase + static_cast<int64_t>(j) * row_stride;
+        float acc[GMAX];
 #pragma unroll
-    for (int c = 0; c < HD; c += 8) {
-        const uint4 w = __ldg(reinterpret_cast<const uint4*>(qp + c));
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            qv[c + 2 * i] = bf2f(static_cast<uint16_t>(ws[i] & 0xffffu)) * scale;
-            qv[c + 2 * i + 1] = bf2f(static_cast<uint16_t>(ws[i] >> 16)) * scale;
-        }
-    }
-    float mx = -INFINITY;
-    for (int j = lane; j < n; j += 32) {
-        const uint16_t* kp = kc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD;
-        float acc = 0.f;
-#pragma unroll
+        for (int g = 0; g < GMAX; ++g) acc[g] = 0.f;
+#pragma unroll 4
         for (int c = 0; c < HD; c += 8) {
             const uint4 w = __ldg(reinterpret_cast<const uint4*>(kp + c));
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            float kv[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                acc = fmaf(qv[c + 2 * i], bf2f(static_cast<uint16_t>(ws[i] & 0xffffu)), acc);
-                acc = fmaf(qv[c + 2 * i + 1], bf2f(static_cast<uint16_t>(ws[i] >> 16)), acc);
+                kv[2 * i] = bf2f(static_cast<uint16_t>(ws[i] & 0xffffu));
+                kv[2 * i + 1] = bf2f(static_cast<uint16_t>(ws[i] >> 16));
+            }
+#pragma unroll
+            for (int g = 0; g < GMAX; ++g) {
+                if (g < G) {
+                    const float4 q0 = *reinterpret_cast<const float4*>(qs + g * HD + c);
+                    const float4 q1 = *reinterpret_cast<const float4*>(qs + g * HD + c + 4);
+                    acc[g] = fmaf(q0.x, kv[0], acc[g]);
+                    acc[g] = fmaf(q0.y, kv[1], acc[g]);
+                    acc[g] = fmaf(q0.z, kv[2], acc[g]);
+                    acc[g] = fmaf(q0.w, kv[3], acc[g]);
+                    acc[g] = fmaf(q1.x, kv[4], acc[g]);
+                    acc[g] = fmaf(q1.y, kv[5], acc[g]);
+                    acc[g] = fmaf(q1.z, kv[6], acc[g]);
+                    acc[g] = fmaf(q1.w, kv[7], acc[g]);
+                }
             }
         }
-        s[j] = acc;
-        mx = fmaxf(mx, acc);
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g)
+            if (g < G) sc[g * cap + j] = acc[g];
     }
+    __syncthreads();
+
+    for (int g = wid; g < G; g += kAttnWarps) {
+        float* s = sc + g * cap;
+        float mx = -INFINITY;
+        for (int j = lane; j < n; j += 32) mx = fmaxf(mx, s[j]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int j = lane; j < n; j += 32) {
-        const float e = __expf(s[j] - mx);
-        s[j] = e;
-        sum += e;
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.f;
+        for (int j = lane; j < n; j += 32) {
+            const float e = __expf(s[j] - mx);
+            s[j] = e;
+            sum += e;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) inv_sum[g] = 1.0f / sum;
     }
+    __syncthreads();
+
+    float o[GMAX][PER];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    __syncwarp();
-    const float inv = 1.0f / sum;
-    float o[PER];
+    for (int g = 0; g < GMAX; ++g)
 #pragma unroll
-    for (int i = 0; i < PER; ++i) o[i] = 0.f;
-    for (int j = 0; j < n; ++j) {
-        const uint16_t* vp = vc + seq_base + (static_cast<int64_t>(j) * Hkv + kvh) * HD + lane * PER;
-        const float pj = s[j];
+        for (int i = 0; i < PER; ++i) o[g][i] = 0.f;
+    const int chunk = (n + kAttnWarps - 1) / kAttnWarps;
+    const int j0 = wid * chunk, j1 = min(n, j0 + chunk);
+    // Four V rows in flight per iteration (the loop is otherwise a serial
+    // chain of dependent-latency loads).
+    constexpr int U = 4;
+    for (int jb = j0; jb < j1; jb += U) {
+        float vv[U][PER];
 #pragma unroll
-        for (int i = 0; i < PER; i += 2) {
-            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vp + i));
-            o[i] = fmaf(pj, bf2f(static_cast<uint16_t>(w & 0xffffu)), o[i]);
-            o[i + 1] = fmaf(pj, bf2f(static_cast<uint16_t>(w >> 16)), o[i + 1]);
+        for (int u = 0; u < U; ++u) {
+            const int j = jb + u < j1 ? jb + u : j1 - 1;
+            const uint16_t* vp = vbase + static_cast<int64_t>(j) * row_stride + lane * PER;
+#pragma unroll
+            for (int i = 0; i < PER; i += 2) {
+                const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vp + i));
+                vv[u][i] = bf2f(static_cast<uint16_t>(w & 0xffffu));
+                vv[u][i + 1] = bf2f(static_cast<uint16_t>(w >> 16));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (jb + u >= j1) break;
+#pragma unroll
+            for (int g = 0; g < GMAX; ++g) {
+                if (g < G) {
+                    const float pj = sc[g * cap + jb + u];
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) o[g][i] = fmaf(pj, vv[u][i], o[g][i]);
+                }
+            }
         }
     }
-    uint16_t* op = out + static_cast<int64_t>(t) * Hq * HD + static_cast<int64_t>(qh) * HD + lane * PER;
 #pragma unroll
-    for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(op + i) = pack2(o[i] * inv, o[i + 1] * inv);
+    for (int g = 0; g < GMAX; ++g)
+        if (g < G)
+#pragma unroll
+            for (int i = 0; i < PER; ++i) red[(wid * G + g) * HD + lane * PER + i] = o[g][i];
+    __syncthreads();
+    uint16_t* op = out + static_cast<int64_t>(t) * Hq * HD + static_cast<int64_t>(kvh) * G * HD;
+    for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) acc += red[w * G * HD + i];
+        op[i] = f2bf(acc * inv_sum[i / HD]);
+    }
 }
 
 // Prefill: one warp per (query row, q head); keys from the same chunk's qkv
@@ -221,13 +281,15 @@ extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t
         return KL_EINVAL;
     if (T == 0) return KL_OK;
     const int G = Hq / Hkv;
-    const size_t smem = static_cast<size_t>(G) * cap * sizeof(float);
+    if (G > 8) return KL_EUNSUPPORTED;
+    const size_t smem = (static_cast<size_t>(G) * hd + static_cast<size_t>(G) * cap +
+                         static_cast<size_t>(kAttnWarps) * G * hd + G) * sizeof(float);
     if (smem > 200 * 1024) return KL_EUNSUPPORTED;
     auto kern = hd == 128 ? attn_decode_kernel<128> : attn_decode_kernel<64>;
     if (smem > 48 * 1024)
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<dim3(static_cast<unsigned>(T), Hkv), 32 * G, smem, stream>>>(q, q_stride, pos, seq, Hq, Hkv, k_cache,
-                                                                         v_cache, cap, sink, scale, out);
+    kern<<<dim3(static_cast<unsigned>(T), Hkv), kAttnWarps * 32, smem, stream>>>(q, q_stride, pos, seq, Hq, Hkv,
+                                                                               k_cache, v_cache, cap, sink, scale, out);
     return check_launch();
 }
 

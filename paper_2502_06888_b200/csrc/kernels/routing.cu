@@ -33,6 +33,7 @@ __device__ __forceinline__ void load8(const uint16_t* p, float (&v)[8]) {
 // 8-element chunks, then xor butterfly), returns rsqrt(mean + eps).
 __device__ __forceinline__ float row_rstd(const uint16_t* x, int d, float eps, int lane) {
     float ss = 0.f;
+#pragma unroll 4
     for (int c = lane * 8; c < d; c += 256) {
         float v[8];
         load8(x + c, v);
@@ -47,6 +48,7 @@ __device__ __forceinline__ float row_rstd(const uint16_t* x, int d, float eps, i
 // Normalised row written as bf16: out = bf16((x * rstd) * w).
 __device__ __forceinline__ void write_normed(const uint16_t* x, const uint16_t* w, uint16_t* out, int d, float rstd,
                                              int lane) {
+#pragma unroll 4
     for (int c = lane * 8; c < d; c += 256) {
         float v[8], g[8];
         load8(x + c, v);
@@ -60,57 +62,47 @@ __device__ __forceinline__ void write_normed(const uint16_t* x, const uint16_t* 
     }
 }
 
-// One warp per token. Logit order (mirrored in oracle/numerics.c): lane l
-// accumulates fmaf over its chunks c = l*8 + 256*j, elements in order, then
-// an xor butterfly 16,8,4,2,1 with round-to-nearest adds.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+// One CTA (kGateWarps warps) per token; warp w owns experts w, w+W, ...
+// Logit order (mirrored in oracle/numerics.c): lane l accumulates fmaf over
+// its chunks c = l*8 + 256*j, elements in order, then an xor butterfly
+// 16,8,4,2,1 with round-to-nearest adds. Every warp recomputes the (bit-
+// identical) normalised row in registers; warp 0 stores it as x2.
+constexpr int kGateWarps = 4;
+
+__global__ void __launch_bounds__(kGateWarps * 32)
 gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ norm_w,
                  const uint16_t* __restrict__ wg, int T, int d, int E, int k, float eps, int score_mode,
                  uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                  float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
-    const int warp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int tok = blockIdx.x;
+    const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    if (warp >= T) return;
-    const uint16_t* hrow = h + static_cast<int64_t>(warp) * d;
-    uint16_t* xrow = x2 + static_cast<int64_t>(warp) * d;
+    const uint16_t* hrow = h + static_cast<int64_t>(tok) * d;
     const float rstd = row_rstd(hrow, d, eps, lane);
-    write_normed(hrow, norm_w, xrow, d, rstd, lane);
-    __syncwarp();
+    if (wid == 0) write_normed(hrow, norm_w, x2 + static_cast<int64_t>(tok) * d, d, rstd, lane);
 
-    __shared__ float sh_logit[kWarpsPerBlock][64];
-    float* lg = sh_logit[threadIdx.x >> 5];
-    for (int e0 = 0; e0 < E; e0 += 8) {
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const int ne = E - e0 < 8 ? E - e0 : 8;
-        for (int c = lane * 8; c < d; c += 256) {
-            float xv[8];
-            // Re-read the just-written normalised row (same warp, after syncwarp).
-            const uint4 q = *reinterpret_cast<const uint4*>(xrow + c);
-            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+    __shared__ float lg[64];
+    for (int e = wid; e < E; e += kGateWarps) {
+        float acc = 0.f;
+    #pragma unroll 4
+    for (int c = lane * 8; c < d; c += 256) {
+            float v[8], g[8], wv[8];
+            load8(hrow + c, v);
+            load8(norm_w + c, g);
+            load8(wg + static_cast<int64_t>(e) * d + c, wv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                xv[2 * i] = bf2f(static_cast<uint16_t>(w4[i] & 0xffffu));
-                xv[2 * i + 1] = bf2f(static_cast<uint16_t>(w4[i] >> 16));
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < ne) {
-                    float wv[8];
-                    load8(wg + static_cast<int64_t>(e0 + j) * d + c, wv);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[j] = fmaf(xv[i], wv[i], acc[j]);
-                }
+            for (int i = 0; i < 8; ++i) {
+                const float xv = bf2f(f2bf(__fmul_rn(__fmul_rn(v[i], rstd), g[i])));
+                acc = fmaf(xv, wv[i], acc);
             }
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc[j] = __fadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
-            if (lane == 0 && j < ne) lg[e0 + j] = acc[j];
-        }
+        for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (lane == 0) lg[e] = acc;
     }
-    __syncwarp();
-    if (lane != 0) return;
+    __syncthreads();
+    const int warp = tok;
+    if (threadIdx.x != 0) return;
     if (logits_out != nullptr)
         for (int e = 0; e < E; ++e) logits_out[static_cast<int64_t>(warp) * E + e] = lg[e];
     // Top-k: repeated arg-max, strict '>' so ties keep the lower expert id.
@@ -244,7 +236,9 @@ __global__ void permute_scatter_kernel(const int32_t* __restrict__ idx, int64_t 
     if (xp != nullptr) {
         const uint4* src = reinterpret_cast<const uint4*>(x2 + t * d);
         uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<int64_t>(p) * d);
-        for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
+#pragma unroll 4
+    #pragma unroll 4
+    for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
     }
 }
 
@@ -261,6 +255,7 @@ __global__ void combine_kernel(const uint16_t* __restrict__ y, const int32_t* __
         p[j] = pos[t * k + j];
         w[j] = weight[t * k + j];
     }
+#pragma unroll 4
     for (int c = lane * 8; c < d; c += 256) {
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int j = 0; j < k; ++j) {
@@ -377,6 +372,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __
     if (t >= T) return;
     const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(ids[t]) * d);
     uint4* dst = reinterpret_cast<uint4*>(out + t * d);
+#pragma unroll 4
     for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
 }
 
@@ -423,7 +419,7 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
     if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 64 || k < 1 || k > 8 || k > E) return KL_EINVAL;
     if (!h || !norm_w || !wg || !x2 || !idx || !weight) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    gate_topk_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(
+    gate_topk_kernel<<<T, kGateWarps * 32, 0, stream>>>(
         h, norm_w, wg, T, d, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);
     return check_launch();
 }
@@ -519,4 +515,50 @@ extern "C" int kl_argmax_bf16(const uint16_t* logits, int64_t T, int V, int32_t*
     if (T == 0) return KL_OK;
     argmax_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(logits, T, V, out);
     return check_launch();
+}
+
+// ---------------------------------------------------------------- EP helpers --
+namespace kl {
+namespace {
+
+__global__ void map_ids_kernel(const int32_t* __restrict__ in, int64_t n, const int32_t* __restrict__ map,
+                               int32_t* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = map[in[i]];
+}
+
+__global__ void sum_rows_i32_kernel(const int32_t* __restrict__ in, int rows, int cols, int32_t* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    int32_t s = 0;
+    for (int r = 0; r < rows; ++r) s += in[static_cast<int64_t>(r) * cols + c];
+    out[c] = s;
+}
+
+__global__ void add_i64_kernel(int64_t* __restrict__ dst, const int64_t* __restrict__ src, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
+}  // namespace
+}  // namespace kl
+
+extern "C" int kl_map_ids(const int32_t* in, int64_t n, const int32_t* map, int32_t* out, cudaStream_t stream) {
+    if (n < 0 || (n > 0 && (!in || !map || !out))) return KL_EINVAL;
+    if (n == 0) return KL_OK;
+    kl::map_ids_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(in, n, map, out);
+    return kl::check_launch();
+}
+
+extern "C" int kl_sum_rows_i32(const int32_t* in, int rows, int cols, int32_t* out, cudaStream_t stream) {
+    if (rows < 0 || cols < 1 || !in || !out) return KL_EINVAL;
+    kl::sum_rows_i32_kernel<<<(cols + 127) / 128, 128, 0, stream>>>(in, rows, cols, out);
+    return kl::check_launch();
+}
+
+extern "C" int kl_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t stream) {
+    if (n < 0 || (n > 0 && (!dst || !src))) return KL_EINVAL;
+    if (n == 0) return KL_OK;
+    kl::add_i64_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(dst, src, n);
+    return kl::check_launch();
 }

@@ -32,6 +32,18 @@ _lib.kl_engine_reset_log.argtypes = [C.c_void_p]
 _lib.kl_engine_read_hidden.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 
 
+_lib.kl_ep_unique_id.argtypes = [C.c_char_p]
+_lib.kl_ep_unique_id.restype = C.c_int
+
+
+def ep_unique_id():
+    """NCCL unique id (hex) for an expert-parallel group; create on rank 0 and share."""
+    buf = C.create_string_buffer(257)
+    if _lib.kl_ep_unique_id(buf) != 0:
+        raise RuntimeError("kl_ep_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.value.decode()
+
+
 class EngineError(RuntimeError):
     pass
 
