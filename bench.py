@@ -107,7 +107,27 @@ def link_peak_gbs(torch, dev):
     return 6 * n / (s.elapsed_time(e) / 1e3) / 1e9
 
 
-def engine_config(args, rank, world):
+def share_ep_id(rank, world, make_id):
+    """Rank 0 creates the NCCL unique id for the engine's EP communicator; all
+    ranks receive it over the torch.distributed group (gloo or nccl)."""
+    import torch.distributed as dist
+    obj = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(x, world, device):
+    """Max of a host float over ranks (multi-GPU timings: slowest rank)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def engine_config(args, rank, world, ep_id=None):
     gen = 1 + args.warmup + 2 * args.steps
     cfg = {
         "model": {"preset": args.model},
@@ -119,8 +139,10 @@ def engine_config(args, rank, world):
         "prefill": False,
         "record_trace": False,
         "host_distinct_layers": args.host_distinct_layers,
-        "weight_seed": 7 + rank,
+        "weight_seed": 7 if ep_id is not None else 7 + rank,
     }
+    if ep_id is not None:
+        cfg["ep"] = {"rank": rank, "world": world, "nccl_id": ep_id}
     return cfg
 
 
@@ -173,11 +195,17 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", init_method="env://")
-    from paper_2502_06888_b200.engine import Engine
+    from paper_2502_06888_b200.engine import Engine, ep_unique_id
 
     link = link_peak_gbs(torch, dev)
     t_setup = time.perf_counter()
-    eng = Engine(engine_config(args, rank, world))
+    use_ep = (world > 1 and args.parallel == "ep") or args.ep1
+    ep_id = None
+    if use_ep:
+        ep_id = share_ep_id(rank, world, ep_unique_id) if world > 1 else ""
+    if world > 1 and not use_ep and args.host_distinct_layers == 0:
+        args.host_distinct_layers = 4  # replicas: bound pinned host memory per rank
+    eng = Engine(engine_config(args, rank, world, ep_id))
     eng.fill_kv_synthetic(args.prompt_len)
     setup_s = time.perf_counter() - t_setup
     seqs = eng.n_seqs
@@ -222,15 +250,8 @@ def run_ours(args):
     barrier()
     e2e_wall = time.perf_counter() - t1
 
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
-
-    total_ms = max_over_ranks(total_ms)
-    e2e_total_ms = max_over_ranks(max(sum(e2e_ms), e2e_wall * 1e3))
+    total_ms = max_over_ranks(total_ms, world, dev)
+    e2e_total_ms = max_over_ranks(max(sum(e2e_ms), e2e_wall * 1e3), world, dev)
     value = args.steps * seqs * world / (total_ms / 1e3)
     e2e_value = args.steps * seqs * world / (e2e_total_ms / 1e3)
 
@@ -281,7 +302,8 @@ def run_ours(args):
                 "hbm_cap_bytes": int(args.hbm_cap), "expert_slots": eng.info["expert_slots"],
                 "resident_expert_layers": eng.info["resident_expert_layers"],
                 "resident_attention_layers": eng.info["resident_attention_layers"],
-                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "parallelism": (f"ep{world} (expert shards, NCCL all-to-all)" if use_ep else
+                                f"replicas x{world}") if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (each step streams the experts of every layer)",
                 "host_distinct_layers": args.host_distinct_layers or "all",
             },
@@ -332,6 +354,9 @@ def main():
     ap.add_argument("--hbm-cap", type=float, default=24e9)
     ap.add_argument("--host-distinct-layers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="ep", choices=["ep", "replicas"],
+                    help="N>1: expert-parallel shards (default) or independent replicas")
+    ap.add_argument("--ep1", action="store_true", help="run the EP engine path even at N=1 (one shard)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
