@@ -58,6 +58,17 @@ const char* kl_error_string(int code);
  * small-M (weight-streaming) shapes; kl_gemm_workspace_bytes() is the size
  * the split heuristic would like (less -> fewer splits, never an error). */
 int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
+/* Decode shapes (M <= 256) with a workspace take the weight-streaming path:
+ * activations as the MMA's N side (rows padded to 16), weights as its M side
+ * read exactly once, one persistent CTA per SM over equal (tile, k-block)
+ * ranges; split tiles are finished by the CTA holding their last k-block,
+ * adding the fp32 partials of the others in ascending CTA order
+ * (deterministic). Its workspace holds one partial slot per CTA plus a
+ * flag page (a smaller workspace runs fewer CTAs). */
+#define KL_TUNE_STREAM_GEMM 0 /* 1 = weight-streaming path on (default), 0 = off */
+#define KL_TUNE_STREAM_NMMA 1 /* 128-row weight sub-tiles per activation tile: 1 or 2 (default) */
+/* Process-wide tuning knobs for benchmarking (not thread-safe). */
+int kl_tune(int knob, int value);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
                  int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);

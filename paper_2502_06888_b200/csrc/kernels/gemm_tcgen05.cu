@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -247,6 +248,236 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     *reinterpret_cast<uint2*>(c + static_cast<int64_t>(m) * ldc + j) = make_uint2(pack2(out[0], out[1]), pack2(out[2], out[3]));
 }
 
+// ------------------------------------------- weight-streaming (decode) GEMM --
+// Decode-shaped GEMMs (M <= 256 activation rows against a weight matrix of
+// tens to hundreds of MB) are bound by reading the weights once from HBM.
+// Layout choice ("swap AB"): the MMA's M side is the weights (128 output
+// features per UMMA, read by TMA once), its N side the activation rows
+// padded to NP (multiple of 16), so one accumulator covers every row and no
+// weight byte is read twice however many rows the expert got. NMMA weight
+// sub-tiles (1 or 2) share each activation tile, halving activation L2
+// traffic when 2; for SwiGLU the pair is (W1 rows, W3 rows) of the same 128
+// features, so gate and up land in the same TMEM lane and the epilogue needs
+// no exchange.
+//
+// Work split ("stream-K"): the (tile, k-block) space is cut into gridDim
+// contiguous, equal ranges, one persistent CTA per SM, so every SM streams
+// the same number of weight bytes (no partial last wave). A tile cut by a
+// range boundary is finished by its "owner" — the CTA holding the tile's
+// last k-block — which adds the fp32 partials of the lower-numbered CTAs
+// that hold its earlier k-blocks, in ascending CTA order (deterministic).
+// Each CTA walks its tiles last-to-first, so the partial it contributes is
+// published first and the tile it owns is finished last: owners rarely wait,
+// and they only ever wait on lower-numbered (earlier-dispatched) CTAs, which
+// guarantees forward progress.
+constexpr int kStreamThreads = 192;
+constexpr int kWRows = 128;  // weight rows per UMMA (M)
+constexpr int kWTileBytes = kWRows * BK * 2;
+
+struct StreamArgs {
+    int M;          // valid activation rows
+    int NP;         // MMA N: rows padded to a multiple of 16 (<= 256)
+    int acc_stride; // TMEM columns between the NMMA accumulators
+    int KB;         // k-blocks per tile
+    int units;      // n_tiles * KB
+    int half_rows;  // SwiGLU: first W3 row inside B
+    int stages;
+    uint16_t* c;
+    int ldc;
+    const uint16_t* r;
+    float* ws;        // [grid][NMMA][128][NP] fp32 partial slots
+    uint32_t* flags;  // [grid] publish epochs
+    uint32_t epoch;
+    uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ int range_begin(int c, int units, int G) {
+    return static_cast<int>(static_cast<int64_t>(c) * units / G);
+}
+
+template <int EPI, int NMMA>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, int a_row0,
+                   const StreamArgs p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
+    uint64_t* empty = full + p.stages;
+    uint64_t* acc_full = empty + p.stages;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int KB = p.KB;
+    const int u0 = range_begin(cta, p.units, G), u1 = range_begin(cta + 1, p.units, G);
+    const int t_hi = u1 > u0 ? (u1 - 1) / KB : 0, t_lo = u1 > u0 ? u0 / KB : 1;  // tiles walked t_hi .. t_lo
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_w);
+        tma_prefetch_desc(&tmap_x);
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
+        mbar_fence_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = l2_policy_evict_first();
+            const uint64_t pol_x = l2_policy_evict_last();
+            int it = 0;
+            for (int t = t_hi; t >= t_lo; --t) {
+                const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % p.stages;
+                    mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
+                    uint8_t* sw = smem + s * stage_bytes;
+                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+#pragma unroll
+                    for (int j = 0; j < NMMA; ++j) {
+                        const int row = EPI == kSwiGLU ? (j == 0 ? t * kWRows : p.half_rows + t * kWRows)
+                                                       : (t * NMMA + j) * kWRows;
+                        tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
+                    }
+                    tma_load_2d_hint(sw + NMMA * kWTileBytes, &tmap_x, &full[s], kb * BK, a_row0, pol_x);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16_f32(kWRows, p.NP);
+            int it = 0, seg = 0;
+            for (int t = t_hi; t >= t_lo; --t, ++seg) {
+                const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
+                mbar_wait(acc_empty, (seg & 1) ^ 1);  // epilogue drained the previous segment
+                tc_fence_after();
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % p.stages;
+                    mbar_wait(&full[s], (it / p.stages) & 1);
+                    tc_fence_after();
+                    const uint32_t sw = smem_u32(smem + s * stage_bytes);
+                    const uint32_t sx = sw + NMMA * kWTileBytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+#pragma unroll
+                        for (int j = 0; j < NMMA; ++j)
+                            tc_mma_bf16(tmem_base + j * p.acc_stride, sw128_kmajor_desc(sw + j * kWTileBytes + k * 32),
+                                        sw128_kmajor_desc(sx + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    tc_commit(&empty[s]);
+                }
+                tc_commit(acc_full);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int quarter = warp & 3;
+        const int frow = quarter * 32 + lane;  // feature row inside a 128-row sub-tile
+        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        const int cols = (p.M + 15) & ~15;  // token columns worth reading
+        int seg = 0;
+        for (int t = t_hi; t >= t_lo; --t, ++seg) {
+            const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
+            mbar_wait(acc_full, seg & 1);
+            tc_fence_after();
+            const bool has_last = kb1 == KB;
+            if (!has_last) {
+                // Contributor: publish the fp32 partial of this tile.
+                float* slot = p.ws + static_cast<int64_t>(cta) * NMMA * kWRows * p.NP;
+                for (int j = 0; j < NMMA; ++j) {
+                    float* dst = slot + (static_cast<int64_t>(j) * kWRows + frow) * p.NP;
+                    for (int col = 0; col < cols; col += 16) {
+                        float v[16];
+                        tmem_ld16(lane_addr + j * p.acc_stride + col, v);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            __stcg(reinterpret_cast<float4*>(dst + col) + i,
+                                   make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                    }
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (warp == 2 && lane == 0) st_release_gpu(p.flags + cta, p.epoch);
+            } else {
+                // Full tile, or owner of a split tile: contributors are the
+                // CTAs c_lo .. cta-1 holding k-blocks [t*KB, u0).
+                int c_lo = cta;
+                if (kb0 > 0) {
+                    c_lo = cta - 1;
+                    while (c_lo > 0 && range_begin(c_lo, p.units, G) > t * KB) --c_lo;
+                    for (int q = c_lo; q < cta; ++q)
+                        while (ld_acquire_gpu(p.flags + q) != p.epoch) {
+                        }
+                }
+                for (int col = 0; col < cols; col += 16) {
+                    float acc[NMMA][16];
+#pragma unroll
+                    for (int j = 0; j < NMMA; ++j) tmem_ld16(lane_addr + j * p.acc_stride + col, acc[j]);
+                    for (int q = c_lo; q < cta; ++q) {
+                        const float* slot = p.ws + static_cast<int64_t>(q) * NMMA * kWRows * p.NP;
+#pragma unroll
+                        for (int j = 0; j < NMMA; ++j) {
+                            const float4* src =
+                                reinterpret_cast<const float4*>(slot + (static_cast<int64_t>(j) * kWRows + frow) * p.NP + col);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 w = __ldcg(src + i);
+                                acc[j][4 * i] += w.x;
+                                acc[j][4 * i + 1] += w.y;
+                                acc[j][4 * i + 2] += w.z;
+                                acc[j][4 * i + 3] += w.w;
+                            }
+                        }
+                    }
+                    if constexpr (EPI == kSwiGLU) {
+                        uint16_t* out = p.c + static_cast<int64_t>(col) * p.ldc + t * kWRows + frow;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            if (col + i < p.M) {
+                                const float g = acc[0][i], u = acc[1][i];
+                                out[static_cast<int64_t>(i) * p.ldc] = f2bf(g / (1.0f + expf(-g)) * u);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NMMA; ++j) {
+                            const int64_t feat = static_cast<int64_t>(t * NMMA + j) * kWRows + frow;
+                            uint16_t* out = p.c + static_cast<int64_t>(col) * p.ldc + feat;
+                            const uint16_t* res = EPI == kResidual ? p.r + static_cast<int64_t>(col) * p.ldc + feat : nullptr;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                if (col + i < p.M) {
+                                    float v = acc[j][i];
+                                    if constexpr (EPI == kResidual) v += bf2f(res[static_cast<int64_t>(i) * p.ldc]);
+                                    out[static_cast<int64_t>(i) * p.ldc] = f2bf(v);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, p.tmem_cols);
+    }
+}
+
 // ------------------------------------------------------------ host side ----
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -341,12 +572,126 @@ int choose_splits(int tiles, int kb, int M, int ws_cols, int64_t ws_bytes) {
     return best;
 }
 
+// --- weight-streaming path (host) ---
+int g_stream_enabled = 1;  // kl_tune(KL_TUNE_STREAM_GEMM, ...)
+int g_stream_nmma = 2;     // kl_tune(KL_TUNE_STREAM_NMMA, ...): weight sub-tiles per activation tile
+
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = kSMs;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            return v;
+        cudaGetLastError();
+        return kSMs;
+    }();
+    return n;
+}
+
+uint32_t next_epoch() {
+    static std::atomic<uint32_t> e{0};
+    uint32_t v = ++e;
+    while (v == 0) v = ++e;
+    return v;
+}
+
+constexpr int64_t kFlagBytes = 1024;  // [<= 256 CTAs] uint32 publish epochs
+constexpr int kStreamSmemBudget = 227 * 1024 - 1024 - 256;
+
+int pow2ceil(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+int stream_np(int M) { return std::max(16, (M + 15) & ~15); }
+bool stream_eligible(int M, int N, int epilogue) {
+    if (!g_stream_enabled || M < 1 || M > 256) return false;
+    return epilogue == kSwiGLU ? (N / 2) % kWRows == 0 : N % kWRows == 0;
+}
+int stream_nmma(int N, int epilogue) {
+    if (epilogue == kSwiGLU) return 2;
+    return (g_stream_nmma == 2 && N % (2 * kWRows) == 0) ? 2 : 1;
+}
+int64_t stream_slot_bytes(int M, int nmma) { return static_cast<int64_t>(nmma) * kWRows * stream_np(M) * 4; }
+
+template <int EPI, int NMMA>
+int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
+                  int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
+                  cudaStream_t stream) {
+    StreamArgs p{};
+    p.M = M;
+    p.NP = stream_np(M);
+    p.acc_stride = pow2ceil(std::max(32, p.NP));
+    p.tmem_cols = static_cast<uint32_t>(std::max(32, NMMA * p.acc_stride));
+    p.KB = K / BK;
+    p.units = n_tiles * p.KB;
+    const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
+    p.stages = std::min(8, kStreamSmemBudget / stage_bytes);
+    if (p.stages < 2 || p.tmem_cols > 512) return KL_EUNSUPPORTED;
+    int G = std::min(sm_count(), std::max(1, p.units / 4));
+    G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
+    G = std::min(G, static_cast<int>(kFlagBytes / 4));
+    if (G < 1) return KL_EUNSUPPORTED;
+    p.half_rows = half_rows;
+    p.c = c;
+    p.ldc = ldc;
+    p.r = r;
+    p.flags = static_cast<uint32_t*>(ws);
+    p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + kFlagBytes);
+    p.epoch = next_epoch();
+    CUtensorMap mw, mx;
+    int rc = make_map(&mw, b, b_rows, K, kWRows);
+    if (rc) return rc;
+    rc = make_map(&mx, a, a_rows, K, p.NP);
+    if (rc) return rc;
+    const int smem = p.stages * stage_bytes + 1024 + 256;
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        KL_CUDA_TRY(cudaFuncSetAttribute(gemm_stream_kernel<EPI, NMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kStreamSmemBudget + 1024 + 256));
+        configured = true;
+    }
+    gemm_stream_kernel<EPI, NMMA><<<G, kStreamThreads, smem, stream>>>(mw, mx, static_cast<int>(row_offset), p);
+    return check_launch();
+}
+
+int gemm_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int N,
+                uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+    const int nmma = stream_nmma(N, epilogue);
+    if (epilogue == kSwiGLU)
+        return launch_stream<kSwiGLU, 2>(a, a_rows, row_offset, M, K, b, N, N / 2 / kWRows, N / 2, c, ldc, r, ws,
+                                         ws_bytes, stream);
+    const int n_tiles = N / (kWRows * nmma);
+    if (epilogue == kResidual)
+        return nmma == 2 ? launch_stream<kResidual, 2>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws,
+                                                       ws_bytes, stream)
+                         : launch_stream<kResidual, 1>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws,
+                                                       ws_bytes, stream);
+    return nmma == 2 ? launch_stream<kStore, 2>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws, ws_bytes,
+                                                stream)
+                     : launch_stream<kStore, 1>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws, ws_bytes,
+                                                stream);
+}
+
 }  // namespace
 }  // namespace kl
+
+extern "C" int kl_tune(int knob, int value) {
+    using namespace kl;
+    switch (knob) {
+        case KL_TUNE_STREAM_GEMM: g_stream_enabled = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_NMMA:
+            if (value != 1 && value != 2) return KL_EINVAL;
+            g_stream_nmma = value;
+            return KL_OK;
+        default: return KL_EINVAL;
+    }
+}
 
 extern "C" int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
     using namespace kl;
     if (M <= 0 || N <= 0 || K <= 0) return 0;
+    if (stream_eligible(M, N, epilogue))
+        return kFlagBytes + static_cast<int64_t>(sm_count()) * stream_slot_bytes(M, stream_nmma(N, epilogue));
     const int m_tiles = (M + BM - 1) / BM;
     const int tiles = (N / 128) * m_tiles;
     const int s = choose_splits(tiles, K / BK, M, N, INT64_MAX);
@@ -367,6 +712,12 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
     if (epilogue == kResidual && (r == nullptr || !aligned16(r))) return KL_EINVAL;
     if (epilogue == kSwiGLU && N % 256 != 0) return KL_EINVAL;
     if (workspace != nullptr && !aligned16(workspace)) return KL_EINVAL;
+    if (workspace != nullptr && stream_eligible(M, N, epilogue) &&
+        workspace_bytes >= kFlagBytes + stream_slot_bytes(M, stream_nmma(N, epilogue))) {
+        const int rc = gemm_stream(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes,
+                                   stream);
+        if (rc != KL_EUNSUPPORTED) return rc;
+    }
     const int m_tiles = (M + BM - 1) / BM;
     const int kb = K / BK;
     Launch L{a, a_rows, row_offset, M, K, b, N, 0, 0, c, ldc, r, 1, static_cast<float*>(workspace), N};

@@ -42,7 +42,16 @@ _rope = _sig("kl_rope_kv_append", [_P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _
 _dec = _sig("kl_attn_decode", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P])
 _pre = _sig("kl_attn_prefill", [_P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P])
 _fill = _sig("kl_fill_normal_bf16", [_P, _L, _U64, _F, _P])
+_tune = _sig("kl_tune", [_I, _I])
 abi_version = _sig("kl_abi_version", [])
+
+TUNE_STREAM_GEMM = 0  # weight-streaming decode GEMM path on/off
+TUNE_STREAM_NMMA = 1  # 128-row weight sub-tiles per activation tile (1 or 2)
+
+
+def tune(knob, value):
+    """Process-wide kernel tuning knob (kl_tune); for tests and benchmarks."""
+    _chk(_tune(knob, value), "kl_tune")
 device_supported = _sig("kl_device_supported", [])
 
 
@@ -82,7 +91,7 @@ def workspace_bytes(M, N, K, epilogue=0):
     return int(_gemm_ws(M, N, K, epilogue))
 
 
-def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None, split_k=True):
+def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None, split_k=True, ws_bytes=None):
     """C = A[row_offset:row_offset+m] @ B^T (bf16, fp32 accumulate) on tcgen05."""
     m = a.shape[0] - row_offset if m is None else m
     K = a.shape[1]
@@ -91,6 +100,8 @@ def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=N
     if c is None:
         c = torch.empty(m, n_out, dtype=torch.bfloat16, device=a.device)
     wsb = workspace_bytes(m, N, K, epilogue) if split_k else 0
+    if ws_bytes is not None and split_k:
+        wsb = int(ws_bytes)
     ws = workspace(wsb, a.device) if wsb else None
     _chk(_gemm(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue, _p(ws),
                wsb, _s(stream)), "kl_gemm_bf16")

@@ -89,6 +89,57 @@ def test_gemm_residual_and_row_offset(K, cuda):
     close_bf16(to_bits(c), ref)
 
 
+@pytest.mark.parametrize("nmma", [1, 2])
+@pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (16, 4096, 4096, 0), (129, 1024, 2048, 1),
+                                        (256, 2048, 1024, 2), (77, 28672 // 8, 4096, 2), (200, 384, 8192, 0)])
+def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
+    """Decode path (swap-AB, stream-K): every shape/epilogue against the
+    oracle, and bit-identical to itself across NMMA settings' reruns."""
+    rows, off = M + 40, 13
+    a = orc.normal_bf16(rows * Kd, 51, 1.0).reshape(rows, Kd)
+    b = orc.normal_bf16(N * Kd, 52, 0.03).reshape(N, Kd)
+    ad, bd = to_dev(a, cuda), to_dev(b, cuda)
+    n_out = N // 2 if epi == 2 else N
+    r = orc.normal_bf16(M * n_out, 53, 1.0).reshape(M, n_out) if epi == 1 else None
+    K.tune(K.TUNE_STREAM_NMMA, nmma)
+    try:
+        assert K.workspace_bytes(M, N, Kd, epi) > 0
+        rd = to_dev(r, cuda) if r is not None else None
+        c = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
+        c2 = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
+        torch.cuda.synchronize()
+    finally:
+        K.tune(K.TUNE_STREAM_NMMA, 2)
+    assert torch.equal(c, c2)  # deterministic split reduction
+    x = a[off:off + M]
+    if epi == 2:
+        g = orc.gemm_f32(np.ascontiguousarray(x), np.ascontiguousarray(b[:n_out])).astype(np.float64)
+        u = orc.gemm_f32(np.ascontiguousarray(x), np.ascontiguousarray(b[n_out:])).astype(np.float64)
+        ref = g / (1.0 + np.exp(-g)) * u
+    else:
+        ref = orc.gemm_f32(x, b) + (orc.bits_to_f32(r) if epi == 1 else 0)
+    close_bf16(to_bits(c), ref)
+
+
+def test_gemm_weight_streaming_small_workspace_and_off(K, cuda):
+    """A workspace for only a few CTAs still gives the right answer, and the
+    streaming path off (one-tile-per-CTA kernel) agrees within tolerance."""
+    M, N, Kd = 96, 2048, 4096
+    a = to_dev(orc.normal_bf16(M * Kd, 54, 1.0).reshape(M, Kd), cuda)
+    b = orc.normal_bf16(N * Kd, 55, 0.02).reshape(N, Kd)
+    ref = orc.gemm_f32(np.ascontiguousarray(to_bits(a)), b)
+    bd = to_dev(b, cuda)
+    small = K.gemm(a, bd, ws_bytes=1024 + 3 * 2 * 128 * 96 * 4)
+    K.tune(K.TUNE_STREAM_GEMM, 0)
+    try:
+        off = K.gemm(a, bd)
+    finally:
+        K.tune(K.TUNE_STREAM_GEMM, 1)
+    torch.cuda.synchronize()
+    close_bf16(to_bits(small), ref)
+    close_bf16(to_bits(off), ref)
+
+
 @pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048), (128, 4096, 1024),
                                    (64, 2048, 1408), (300, 512, 1792)])
 def test_expert_ffn(K, cuda, M, d, f):
