@@ -278,6 +278,7 @@ struct StreamArgs {
     int M;          // valid activation rows
     int NP;         // MMA N: rows padded to a multiple of 16 (<= 256)
     int acc_stride; // TMEM columns between the NMMA accumulators
+    int nbuf;       // TMEM accumulator sets (2 = epilogue overlaps the next segment's MMAs)
     int KB;         // k-blocks per tile
     int units;      // n_tiles * KB
     int half_rows;  // SwiGLU: first W3 row inside B
@@ -285,14 +286,55 @@ struct StreamArgs {
     uint16_t* c;
     int ldc;
     const uint16_t* r;
-    float* ws;        // [grid][NMMA][128][NP] fp32 partial slots
+    float* ws;        // [grid] partial slots, each [NMMA][NP/16][4][128] float4
     uint32_t* flags;  // [grid] publish epochs
     uint32_t epoch;
     uint32_t tmem_cols;
+    int hint;   // 1 = L2 cache-policy hints on the TMA loads
+    int pdl;    // launched with programmatic stream serialization
+    int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
 };
+
+__device__ unsigned long long g_stream_trace[256][12];  // debug & 128: per-CTA phase timestamps (ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define STREAM_TRACE(slot) \
+    do { if (p.debug & 128) g_stream_trace[blockIdx.x][slot] = gtimer(); } while (0)
 
 __device__ __forceinline__ int range_begin(int c, int units, int G) {
     return static_cast<int>(static_cast<int64_t>(c) * units / G);
+}
+
+// 1D bulk copy global -> shared (async proxy), completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+template <int EPI>
+__device__ __forceinline__ float epi_value(const float (&acc)[2][16], int j, int i) {
+    if constexpr (EPI == kSwiGLU) {
+        const float g = acc[0][i], u = acc[1][i];
+        return __fdividef(g, 1.0f + __expf(-g)) * u;
+    } else {
+        return acc[j][i];
+    }
 }
 
 template <int EPI, int NMMA>
@@ -302,17 +344,20 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
+    const int ring_bytes = p.stages * stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring_bytes);
     uint64_t* empty = full + p.stages;
-    uint64_t* acc_full = empty + p.stages;
-    uint64_t* acc_empty = acc_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    uint64_t* acc_full = empty + p.stages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;     // [2]
+    uint64_t* part_bar = acc_empty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(part_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, cta = blockIdx.x;
     const int KB = p.KB;
     const int u0 = range_begin(cta, p.units, G), u1 = range_begin(cta + 1, p.units, G);
     const int t_hi = u1 > u0 ? (u1 - 1) / KB : 0, t_lo = u1 > u0 ? u0 / KB : 1;  // tiles walked t_hi .. t_lo
+    const int buf_cols = NMMA * p.acc_stride;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_w);
@@ -321,10 +366,15 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 4);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        mbar_init(part_bar, 1);
         mbar_fence_init();
     }
+    if (threadIdx.x == 0) STREAM_TRACE(0);
+    if (p.pdl) griddep_launch_dependents();
     if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
     tc_fence_before();
     __syncthreads();
@@ -335,11 +385,30 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
         if (lane == 0) {
             const uint64_t pol_w = l2_policy_evict_first();
             const uint64_t pol_x = l2_policy_evict_last();
-            int it = 0;
+            const bool hint = p.hint != 0;
+            // Programmatic dependent launch: the weights do not depend on the
+            // previous kernel, so the first `stages` weight tiles are issued
+            // before griddepcontrol.wait; activations, outputs and the
+            // workspace are touched only after it.
+            bool waited = !p.pdl;
+            int it = 0, pending_x = 0;
+            auto load_x = [&](int s_, int kb_) {
+                uint8_t* sx = smem + s_ * stage_bytes + NMMA * kWTileBytes;
+                if (hint)
+                    tma_load_2d_hint(sx, &tmap_x, &full[s_], kb_ * BK, a_row0, pol_x);
+                else
+                    tma_load_2d(sx, &tmap_x, &full[s_], kb_ * BK, a_row0);
+            };
+            int xkb[16];  // k-block of each stage issued before the wait
             for (int t = t_hi; t >= t_lo; --t) {
                 const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % p.stages;
+                    if (!waited && it >= p.stages) {
+                        griddep_wait();
+                        waited = true;
+                        for (int i = 0; i < pending_x; ++i) load_x(i, xkb[i]);
+                    }
                     mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
                     uint8_t* sw = smem + s * stage_bytes;
                     mbar_arrive_expect_tx(&full[s], stage_bytes);
@@ -347,129 +416,211 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                     for (int j = 0; j < NMMA; ++j) {
                         const int row = EPI == kSwiGLU ? (j == 0 ? t * kWRows : p.half_rows + t * kWRows)
                                                        : (t * NMMA + j) * kWRows;
-                        tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
+                        if (hint)
+                            tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
+                        else
+                            tma_load_2d(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row);
                     }
-                    tma_load_2d_hint(sw + NMMA * kWTileBytes, &tmap_x, &full[s], kb * BK, a_row0, pol_x);
+                    if (waited) {
+                        load_x(s, kb);
+                    } else {
+                        xkb[pending_x++] = kb;
+                    }
                 }
             }
+            if (!waited) {
+                griddep_wait();
+                for (int i = 0; i < pending_x; ++i) load_x(i, xkb[i]);
+            }
         }
+        if (p.pdl) griddep_wait();  // every thread: outputs/workspace only after the previous grid
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t idesc = idesc_bf16_f32(kWRows, p.NP);
             int it = 0, seg = 0;
             for (int t = t_hi; t >= t_lo; --t, ++seg) {
                 const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
-                mbar_wait(acc_empty, (seg & 1) ^ 1);  // epilogue drained the previous segment
+                const int b = p.nbuf == 2 ? (seg & 1) : 0, use = p.nbuf == 2 ? (seg >> 1) : seg;
+                mbar_wait(&acc_empty[b], (use & 1) ^ 1);  // epilogue drained this accumulator set
                 tc_fence_after();
+                const uint32_t acc0 = tmem_base + b * buf_cols;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % p.stages;
                     mbar_wait(&full[s], (it / p.stages) & 1);
+                    if (it == 0) STREAM_TRACE(1);
                     tc_fence_after();
                     const uint32_t sw = smem_u32(smem + s * stage_bytes);
                     const uint32_t sx = sw + NMMA * kWTileBytes;
+                    if (!(p.debug & 1))
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
+                        for (int k = 0; k < BK / 16; ++k)
 #pragma unroll
-                        for (int j = 0; j < NMMA; ++j)
-                            tc_mma_bf16(tmem_base + j * p.acc_stride, sw128_kmajor_desc(sw + j * kWTileBytes + k * 32),
-                                        sw128_kmajor_desc(sx + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            for (int j = 0; j < NMMA; ++j)
+                                tc_mma_bf16(acc0 + j * p.acc_stride, sw128_kmajor_desc(sw + j * kWTileBytes + k * 32),
+                                            sw128_kmajor_desc(sx + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     tc_commit(&empty[s]);
                 }
-                tc_commit(acc_full);
+                tc_commit(&acc_full[b]);
             }
+            STREAM_TRACE(2);
         }
         __syncwarp();
     } else {
+        if (p.pdl) griddep_wait();
         const int quarter = warp & 3;
         const int frow = quarter * 32 + lane;  // feature row inside a 128-row sub-tile
-        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        const int etid = threadIdx.x - 64;     // 0..127 across the epilogue warps
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const int cols = (p.M + 15) & ~15;  // token columns worth reading
+        const int nch = p.NP / 16;
+        const int slot_f4 = NMMA * kWRows * (p.NP / 4);  // float4 per partial slot
+        auto slot4 = [&](int q) { return reinterpret_cast<float4*>(p.ws) + static_cast<int64_t>(q) * slot_f4; };
         int seg = 0;
         for (int t = t_hi; t >= t_lo; --t, ++seg) {
             const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
-            mbar_wait(acc_full, seg & 1);
+            const int b = p.nbuf == 2 ? (seg & 1) : 0, use = p.nbuf == 2 ? (seg >> 1) : seg;
+            mbar_wait(&acc_full[b], use & 1);
             tc_fence_after();
+            const uint32_t acc0 = tmem_base + lane_off + b * buf_cols;
             const bool has_last = kb1 == KB;
-            if (!has_last) {
-                // Contributor: publish the fp32 partial of this tile.
-                float* slot = p.ws + static_cast<int64_t>(cta) * NMMA * kWRows * p.NP;
+            if (p.debug & 2) {
+            } else if (!has_last) {
+                // Contributor: publish the fp32 partial of this tile. Slot
+                // layout [j][16-column chunk][float4 i][feature row] so each
+                // warp store / load is 512 contiguous bytes.
+                if (etid == 0) STREAM_TRACE(8);
+                float4* slot = slot4(cta);
                 for (int j = 0; j < NMMA; ++j) {
-                    float* dst = slot + (static_cast<int64_t>(j) * kWRows + frow) * p.NP;
-                    for (int col = 0; col < cols; col += 16) {
-                        float v[16];
-                        tmem_ld16(lane_addr + j * p.acc_stride + col, v);
+                    for (int col = 0; col < cols; col += 32) {
+                        // 32 columns per TMEM load (one wait), the second 16 only if live.
+                        float v[32];
+                        tmem_ld32(acc0 + j * p.acc_stride + col, v);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            __stcg(reinterpret_cast<float4*>(dst + col) + i,
-                                   make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                        for (int h = 0; h < 2; ++h) {
+                            if (col + 16 * h >= cols) break;
+                            float4* dst = slot + (static_cast<int64_t>(j * nch + (col >> 4) + h) * 4) * kWRows + frow;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                __stcg(dst + i * kWRows, make_float4(v[16 * h + 4 * i], v[16 * h + 4 * i + 1],
+                                                                     v[16 * h + 4 * i + 2], v[16 * h + 4 * i + 3]));
+                        }
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[b]);
                 __threadfence();
                 named_bar_sync(1, 128);
-                if (warp == 2 && lane == 0) st_release_gpu(p.flags + cta, p.epoch);
-            } else {
-                // Full tile, or owner of a split tile: contributors are the
-                // CTAs c_lo .. cta-1 holding k-blocks [t*KB, u0).
-                int c_lo = cta;
-                if (kb0 > 0) {
-                    c_lo = cta - 1;
-                    while (c_lo > 0 && range_begin(c_lo, p.units, G) > t * KB) --c_lo;
-                    for (int q = c_lo; q < cta; ++q)
-                        while (ld_acquire_gpu(p.flags + q) != p.epoch) {
-                        }
-                }
+                if (etid == 0) st_release_gpu(p.flags + cta, p.epoch);
+                if (etid == 0) STREAM_TRACE(9);
+                continue;
+            } else if (t != t_lo) {
+                // A whole tile in the middle of the range (only when a range
+                // spans more than a tile): direct, uncoalesced stores.
                 for (int col = 0; col < cols; col += 16) {
-                    float acc[NMMA][16];
+                    float acc[2][16];
 #pragma unroll
-                    for (int j = 0; j < NMMA; ++j) tmem_ld16(lane_addr + j * p.acc_stride + col, acc[j]);
-                    for (int q = c_lo; q < cta; ++q) {
-                        const float* slot = p.ws + static_cast<int64_t>(q) * NMMA * kWRows * p.NP;
+                    for (int j = 0; j < NMMA; ++j) tmem_ld16(acc0 + j * p.acc_stride + col, acc[j]);
 #pragma unroll
-                        for (int j = 0; j < NMMA; ++j) {
-                            const float4* src =
-                                reinterpret_cast<const float4*>(slot + (static_cast<int64_t>(j) * kWRows + frow) * p.NP + col);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float4 w = __ldcg(src + i);
-                                acc[j][4 * i] += w.x;
-                                acc[j][4 * i + 1] += w.y;
-                                acc[j][4 * i + 2] += w.z;
-                                acc[j][4 * i + 3] += w.w;
-                            }
-                        }
-                    }
-                    if constexpr (EPI == kSwiGLU) {
-                        uint16_t* out = p.c + static_cast<int64_t>(col) * p.ldc + t * kWRows + frow;
+                    for (int j = 0; j < (EPI == kSwiGLU ? 1 : NMMA); ++j) {
+                        const int64_t feat = static_cast<int64_t>(EPI == kSwiGLU ? t : t * NMMA + j) * kWRows + frow;
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            if (col + i < p.M) {
-                                const float g = acc[0][i], u = acc[1][i];
-                                out[static_cast<int64_t>(i) * p.ldc] = f2bf(g / (1.0f + expf(-g)) * u);
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < NMMA; ++j) {
-                            const int64_t feat = static_cast<int64_t>(t * NMMA + j) * kWRows + frow;
-                            uint16_t* out = p.c + static_cast<int64_t>(col) * p.ldc + feat;
-                            const uint16_t* res = EPI == kResidual ? p.r + static_cast<int64_t>(col) * p.ldc + feat : nullptr;
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                if (col + i < p.M) {
-                                    float v = acc[j][i];
-                                    if constexpr (EPI == kResidual) v += bf2f(res[static_cast<int64_t>(i) * p.ldc]);
-                                    out[static_cast<int64_t>(i) * p.ldc] = f2bf(v);
-                                }
-                            }
+                            if (col + i >= p.M) continue;
+                            float v = epi_value<EPI>(acc, j, i);
+                            uint16_t* o = p.c + static_cast<int64_t>(col + i) * p.ldc + feat;
+                            if constexpr (EPI == kResidual) v += bf2f(p.r[static_cast<int64_t>(col + i) * p.ldc + feat]);
+                            *o = f2bf(v);
                         }
                     }
+                }
+            } else {
+                // Last tile walked (ring idle from here on): owner fixup,
+                // then the epilogue staged through shared memory.
+                if (etid == 0) STREAM_TRACE(3);
+                if (kb0 > 0) {
+                    int c_lo = cta - 1;
+                    while (c_lo > 0 && range_begin(c_lo, p.units, G) > t * KB) --c_lo;
+                    const int slot_bytes = slot_f4 * 16;
+                    const int per_batch = max(1, ring_bytes / slot_bytes);
+                    int phase = 0;
+                    for (int q0 = c_lo; q0 < cta; q0 += per_batch, phase ^= 1) {
+                        const int nq = min(per_batch, cta - q0);
+                        if (etid == 0) {
+                            for (int q = q0; q < q0 + nq; ++q)
+                                while (ld_relaxed_gpu(p.flags + q) != p.epoch) {
+                                }
+                            fence_acq_rel_gpu();
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                            mbar_arrive_expect_tx(part_bar, static_cast<uint32_t>(nq * slot_bytes));
+                            for (int q = 0; q < nq; ++q)
+                                for (int off = 0; off < slot_bytes; off += 32768)
+                                    bulk_g2s(smem + q * slot_bytes + off,
+                                             reinterpret_cast<const uint8_t*>(slot4(q0 + q)) + off,
+                                             static_cast<uint32_t>(min(32768, slot_bytes - off)), part_bar);
+                        }
+                        if (etid == 0) STREAM_TRACE(4);
+                        mbar_wait(part_bar, phase);
+                        if (etid == 0) STREAM_TRACE(5);
+                        const float4* land = reinterpret_cast<const float4*>(smem);
+                        for (int j = 0; j < NMMA; ++j)
+                            for (int col = 0; col < cols; col += 16) {
+                                float v[16];
+                                tmem_ld16(acc0 + j * p.acc_stride + col, v);
+                                for (int q = 0; q < nq; ++q) {
+                                    const float4* src =
+                                        land + static_cast<int64_t>(q) * slot_f4 +
+                                        (static_cast<int64_t>(j * nch + (col >> 4)) * 4) * kWRows + frow;
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        const float4 w = src[i * kWRows];
+                                        v[4 * i] += w.x;
+                                        v[4 * i + 1] += w.y;
+                                        v[4 * i + 2] += w.z;
+                                        v[4 * i + 3] += w.w;
+                                    }
+                                }
+                                tmem_st16(acc0 + j * p.acc_stride + col, v);
+                            }
+                        named_bar_sync(1, 128);  // landing buffer free before the next batch
+                    }
+                }
+                if (etid == 0) STREAM_TRACE(6);
+                // Stage bf16 outputs [token][128 features] in smem, then
+                // coalesced 16-byte row stores.
+                uint16_t* stage = reinterpret_cast<uint16_t*>(smem);
+                constexpr int kOut = EPI == kSwiGLU ? 1 : NMMA;
+                for (int j = 0; j < kOut; ++j) {
+                    const int64_t feat0 = static_cast<int64_t>(EPI == kSwiGLU ? t : t * NMMA + j) * kWRows;
+                    for (int col = 0; col < cols; col += 16) {
+                        float acc[2][16];
+#pragma unroll
+                        for (int jj = 0; jj < NMMA; ++jj)
+                            if (EPI == kSwiGLU || jj == j) tmem_ld16(acc0 + jj * p.acc_stride + col, acc[jj]);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            float v = epi_value<EPI>(acc, j, i);
+                            if constexpr (EPI == kResidual)
+                                if (col + i < p.M) v += bf2f(p.r[static_cast<int64_t>(col + i) * p.ldc + feat0 + frow]);
+                            stage[(col + i) * kWRows + frow] = f2bf(v);
+                        }
+                    }
+                    named_bar_sync(1, 128);
+                    const int vec = kWRows / 8;  // 16-byte vectors per token row
+                    for (int v = etid; v < p.M * vec; v += 128) {
+                        const int row = v / vec, x = v % vec;
+                        *reinterpret_cast<uint4*>(p.c + static_cast<int64_t>(row) * p.ldc + feat0 + x * 8) =
+                            *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
+                    }
+                    named_bar_sync(1, 128);
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty);
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
         }
     }
+    if (threadIdx.x == 64) STREAM_TRACE(7);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -575,6 +726,11 @@ int choose_splits(int tiles, int kb, int M, int ws_cols, int64_t ws_bytes) {
 // --- weight-streaming path (host) ---
 int g_stream_enabled = 1;  // kl_tune(KL_TUNE_STREAM_GEMM, ...)
 int g_stream_nmma = 2;     // kl_tune(KL_TUNE_STREAM_NMMA, ...): weight sub-tiles per activation tile
+int g_stream_stages = 8;   // kl_tune(KL_TUNE_STREAM_STAGES, ...): cap on the smem ring depth
+int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/evict_last hints
+int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
+int g_stream_debug = 0;
+int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
 
 int sm_count() {
     static const int n = [] {
@@ -621,13 +777,24 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.M = M;
     p.NP = stream_np(M);
     p.acc_stride = pow2ceil(std::max(32, p.NP));
-    p.tmem_cols = static_cast<uint32_t>(std::max(32, NMMA * p.acc_stride));
+    p.nbuf = 2 * NMMA * p.acc_stride <= 512 ? 2 : 1;
+    p.tmem_cols = static_cast<uint32_t>(std::max(32, p.nbuf * NMMA * p.acc_stride));
     p.KB = K / BK;
     p.units = n_tiles * p.KB;
     const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
-    p.stages = std::min(8, kStreamSmemBudget / stage_bytes);
-    if (p.stages < 2 || p.tmem_cols > 512) return KL_EUNSUPPORTED;
-    int G = std::min(sm_count(), std::max(1, p.units / 4));
+    p.stages = std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / stage_bytes);
+    if (p.stages < 2 || p.tmem_cols * g_stream_ctas > 512) return KL_EUNSUPPORTED;
+    // The idle ring doubles as the landing buffer for one partial slot and
+    // as the bf16 output staging tile of the last segment.
+    if (p.stages * stage_bytes < std::max<int64_t>(stream_slot_bytes(M, NMMA), static_cast<int64_t>(p.NP) * kWRows * 2))
+        p.stages = static_cast<int>((std::max<int64_t>(stream_slot_bytes(M, NMMA), static_cast<int64_t>(p.NP) * kWRows * 2) +
+                                     stage_bytes - 1) / stage_bytes);
+    if (p.stages * stage_bytes > kStreamSmemBudget / g_stream_ctas) return KL_EUNSUPPORTED;
+    p.hint = g_stream_hint;
+    p.debug = g_stream_debug;
+    p.pdl = g_pdl;
+    if (p.stages > 16) p.stages = 16;
+    int G = std::min(sm_count() * g_stream_ctas, std::max(1, p.units / 4));
     G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
     G = std::min(G, static_cast<int>(kFlagBytes / 4));
     if (G < 1) return KL_EUNSUPPORTED;
@@ -639,18 +806,28 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + kFlagBytes);
     p.epoch = next_epoch();
     CUtensorMap mw, mx;
-    int rc = make_map(&mw, b, b_rows, K, kWRows);
+    int rc = (p.debug & 64) ? make_map(&mw, b, b_rows * K / BK, BK, kWRows) : make_map(&mw, b, b_rows, K, kWRows);
     if (rc) return rc;
     rc = make_map(&mx, a, a_rows, K, p.NP);
     if (rc) return rc;
-    const int smem = p.stages * stage_bytes + 1024 + 256;
+    const int smem = p.stages * stage_bytes + 1024 + 256;  // ring + alignment + barriers
     static bool configured = false;  // per template instance
     if (!configured) {
         KL_CUDA_TRY(cudaFuncSetAttribute(gemm_stream_kernel<EPI, NMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kStreamSmemBudget + 1024 + 256));
         configured = true;
     }
-    gemm_stream_kernel<EPI, NMMA><<<G, kStreamThreads, smem, stream>>>(mw, mx, static_cast<int>(row_offset), p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kStreamThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p.pdl ? 1 : 0;
+    KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_stream_kernel<EPI, NMMA>, mw, mx, static_cast<int>(row_offset), p));
     return check_launch();
 }
 
@@ -675,6 +852,13 @@ int gemm_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, in
 }  // namespace
 }  // namespace kl
 
+extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
+    const int rc = static_cast<int>(cudaMemcpyFromSymbol(host, kl::g_stream_trace, static_cast<size_t>(n_ctas) * 12 * 8));
+    static unsigned long long zero[256 * 12] = {};
+    cudaMemcpyToSymbol(kl::g_stream_trace, zero, sizeof(zero));
+    return rc;
+}
+
 extern "C" int kl_tune(int knob, int value) {
     using namespace kl;
     switch (knob) {
@@ -682,6 +866,17 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_NMMA:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_nmma = value;
+            return KL_OK;
+        case KL_TUNE_STREAM_STAGES:
+            if (value < 2 || value > 16) return KL_EINVAL;
+            g_stream_stages = value;
+            return KL_OK;
+        case KL_TUNE_STREAM_HINT: g_stream_hint = value != 0; return KL_OK;
+        case 99: g_stream_debug = value; return KL_OK;
+        case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_CTAS_PER_SM:
+            if (value != 1 && value != 2) return KL_EINVAL;
+            g_stream_ctas = value;
             return KL_OK;
         default: return KL_EINVAL;
     }

@@ -47,6 +47,10 @@ abi_version = _sig("kl_abi_version", [])
 
 TUNE_STREAM_GEMM = 0  # weight-streaming decode GEMM path on/off
 TUNE_STREAM_NMMA = 1  # 128-row weight sub-tiles per activation tile (1 or 2)
+TUNE_STREAM_STAGES = 2
+TUNE_STREAM_HINT = 3
+TUNE_STREAM_CTAS_PER_SM = 4
+TUNE_PDL = 5
 
 
 def tune(knob, value):

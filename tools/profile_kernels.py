@@ -20,12 +20,45 @@ bs, n = 64, 8
 T = bs * n
 
 
+TRACE = False
+
+
+def dump_trace(label):
+    """Per-CTA phase timestamps of the last weight-streaming GEMM launch."""
+    if not TRACE:
+        return
+    import ctypes
+    import numpy as np
+    buf = (ctypes.c_ulonglong * (256 * 12))()
+    K._lib.kl_stream_trace(buf, 256)
+    a = np.array(buf, dtype=np.float64).reshape(256, 12)[:148]
+    t0 = a[:, 0].min()
+    rel = (a - t0) / 1e3
+    rel[a == 0] = np.nan
+    names = ["start", "mma0", "mma_end", "epi_last", "flags_ok", "landed", "sums_done", "end", "contrib0",
+             "published"]
+    print(f"trace {label} (us from first CTA start)")
+    for i, nm in enumerate(names):
+        col = rel[:, i]
+        if np.all(np.isnan(col)):
+            continue
+        print(f"  {nm:10s} med {np.nanmedian(col):7.2f}  min {np.nanmin(col):7.2f}  max {np.nanmax(col):7.2f}")
+
+
 def timed(fn, iters, stream):
+    if TRACE:
+        import ctypes
+        buf = (ctypes.c_ulonglong * (256 * 12))()
+        K._lib.kl_stream_trace(buf, 256)  # read + clear
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     for _ in range(3):
         fn(0)
     torch.cuda.synchronize()
+    if TRACE:
+        import ctypes
+        buf = (ctypes.c_ulonglong * (256 * 12))()
+        K._lib.kl_stream_trace(buf, 256)  # clear: the trace shows the last timed launch only
     s.record(stream)
     for i in range(iters):
         fn(i)
@@ -40,7 +73,23 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--rows", type=int, default=128)
     ap.add_argument("--json", default="")
+    ap.add_argument("--nmma", type=int, default=2, help="weight sub-tiles per activation tile (stream GEMM)")
+    ap.add_argument("--no-stream", action="store_true", help="disable the weight-streaming decode GEMM path")
+    ap.add_argument("--stages", type=int, default=8)
+    ap.add_argument("--hint", type=int, default=1)
+    ap.add_argument("--ctas", type=int, default=1)
+    ap.add_argument("--debug", type=int, default=0)
+    ap.add_argument("--pdl", type=int, default=1)
     args = ap.parse_args()
+    K.tune(99, args.debug)
+    K.tune(K.TUNE_PDL, args.pdl)
+    global TRACE
+    TRACE = bool(args.debug & 128)
+    K.tune(K.TUNE_STREAM_STAGES, args.stages)
+    K.tune(K.TUNE_STREAM_HINT, args.hint)
+    K.tune(K.TUNE_STREAM_CTAS_PER_SM, args.ctas)
+    K.tune(K.TUNE_STREAM_NMMA, args.nmma)
+    K.tune(K.TUNE_STREAM_GEMM, 0 if args.no_stream else 1)
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream()
     res = {}
@@ -65,12 +114,14 @@ def main():
             w = ws[i % E]
             K.gemm(xp, w[: 2 * f * d].view(2 * f, d), c=h, epilogue=2, row_offset=0, m=M)
         t = timed(g1, args.iters, st)
+        dump_trace("gemm_swiglu")
         res["gemm_swiglu"] = {"M": M, "us": t * 1e6, "GBs": (2 * d * f * 2) / t / 1e9}
 
         def g2(i):
             w = ws[i % E]
             K.gemm(h, w[2 * f * d:].view(d, f), c=y[:M], m=M)
         t = timed(g2, args.iters, st)
+        dump_trace("gemm_down")
         res["gemm_down"] = {"M": M, "us": t * 1e6, "GBs": (d * f * 2) / t / 1e9}
         del ws
     if not args.only or args.only == "attn":
