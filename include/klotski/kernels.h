@@ -65,8 +65,8 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
  * adding the fp32 partials of the others in ascending CTA order
  * (deterministic). Its workspace holds one partial slot per CTA plus a
  * flag page (a smaller workspace runs fewer CTAs). */
-#define KL_TUNE_STREAM_GEMM 0 /* 1 = weight-streaming path on (default), 0 = off */
-#define KL_TUNE_STREAM_NMMA 1 /* 128-row weight sub-tiles per activation tile: 1 or 2 (default) */
+#define KL_TUNE_STREAM_GEMM 0 /* 1 = weight-streaming path for >= 40 MB of weights or M > 128 (default), 2 = always, 0 = off */
+#define KL_TUNE_STREAM_NMMA 1 /* 128-row weight sub-tiles per activation tile: 1 (default) or 2 */
 #define KL_TUNE_STREAM_STAGES 2 /* cap on the smem pipeline depth (2..16, default 8) */
 #define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints */
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */

@@ -56,7 +56,7 @@ std::uint64_t tensor_seed(std::uint64_t base, int kind, int layer, int expert) {
                            static_cast<std::uint64_t>(expert + 1));
 }
 
-constexpr byte_count kGemmWorkspace = 32LL << 20;  // split-K partials for decode-shaped GEMMs
+constexpr byte_count kGemmWorkspace = 40LL << 20;  // split-K partials for decode-shaped GEMMs
 constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKindHead = 5;
 
 }  // namespace
@@ -278,7 +278,9 @@ void Engine::plan_memory() {
                                        kl_gemm_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1),
                                        kl_gemm_workspace_bytes(mi, D_.V, D_.d, 0)});
         }
-        gemm_ws_bytes_ = std::min<int64_t>(gemm_ws_bytes_, kGemmWorkspace);
+        // A smaller workspace only means fewer CTAs in the weight-streaming
+        // GEMMs; keep it a small fraction of tight HBM caps.
+        gemm_ws_bytes_ = std::min<int64_t>({gemm_ws_bytes_, kGemmWorkspace, std::max<int64_t>(256LL << 10, cfg_.hbm_cap / 256)});
         add(gemm_ws_bytes_);
         add(5 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/ids/next/last, counts/offsets
         add(seqs * D_.d * 2 + seqs * D_.V * 2);                                  // last_h, head logits

@@ -21,3 +21,18 @@ extern "C" const char* kl_error_string(int code) {
         default: return code > 0 ? cudaGetErrorString(static_cast<cudaError_t>(code)) : "unknown error";
     }
 }
+
+// Benchmarking aid: one thread spins until *flag (host-mapped) becomes
+// non-zero, so work queued behind it starts without host launch latency.
+namespace {
+__global__ void spin_flag_kernel(const volatile int* flag) {
+    while (*flag == 0) {
+    }
+}
+}  // namespace
+
+extern "C" int kl_debug_spin_flag(const int* flag, cudaStream_t stream) {
+    if (flag == nullptr) return KL_EINVAL;
+    spin_flag_kernel<<<1, 1, 0, stream>>>(flag);
+    return kl::check_launch();
+}

@@ -725,7 +725,7 @@ int choose_splits(int tiles, int kb, int M, int ws_cols, int64_t ws_bytes) {
 
 // --- weight-streaming path (host) ---
 int g_stream_enabled = 1;  // kl_tune(KL_TUNE_STREAM_GEMM, ...)
-int g_stream_nmma = 2;     // kl_tune(KL_TUNE_STREAM_NMMA, ...): weight sub-tiles per activation tile
+int g_stream_nmma = 1;     // kl_tune(KL_TUNE_STREAM_NMMA, ...): weight sub-tiles per activation tile
 int g_stream_stages = 8;   // kl_tune(KL_TUNE_STREAM_STAGES, ...): cap on the smem ring depth
 int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/evict_last hints
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
@@ -759,15 +759,26 @@ int pow2ceil(int v) {
     return p;
 }
 int stream_np(int M) { return std::max(16, (M + 15) & ~15); }
-bool stream_eligible(int M, int N, int epilogue) {
+bool stream_eligible(int M, int N, int K, int epilogue) {
     if (!g_stream_enabled || M < 1 || M > 256) return false;
-    return epilogue == kSwiGLU ? (N / 2) % kWRows == 0 : N % kWRows == 0;
+    if (!(epilogue == kSwiGLU ? (N / 2) % kWRows == 0 : N % kWRows == 0)) return false;
+    // Below ~40 MB of weights the persistent kernel's ramp and split fixup
+    // outweigh its balance; the one-tile-per-CTA kernel wins there unless
+    // the rows need two of its 128-row tiles (each re-reading the weights).
+    return M > 128 || static_cast<int64_t>(N) * K * 2 >= (40LL << 20) || g_stream_enabled == 2;
 }
 int stream_nmma(int N, int epilogue) {
     if (epilogue == kSwiGLU) return 2;
     return (g_stream_nmma == 2 && N % (2 * kWRows) == 0) ? 2 : 1;
 }
 int64_t stream_slot_bytes(int M, int nmma) { return static_cast<int64_t>(nmma) * kWRows * stream_np(M) * 4; }
+// Persistent grid: one CTA per SM (x g_stream_ctas), at least 4 k-blocks each.
+int stream_grid(int N, int K, int epilogue) {
+    const int nmma = stream_nmma(N, epilogue);
+    const int n_tiles = epilogue == kSwiGLU ? N / 2 / kWRows : N / (kWRows * nmma);
+    const int units = n_tiles * (K / BK);
+    return std::max(1, std::min(sm_count() * g_stream_ctas, units / 4));
+}
 
 template <int EPI, int NMMA>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
@@ -794,7 +805,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
     if (p.stages > 16) p.stages = 16;
-    int G = std::min(sm_count() * g_stream_ctas, std::max(1, p.units / 4));
+    int G = std::max(1, std::min(sm_count() * g_stream_ctas, p.units / 4));
     G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
     G = std::min(G, static_cast<int>(kFlagBytes / 4));
     if (G < 1) return KL_EUNSUPPORTED;
@@ -862,7 +873,7 @@ extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
 extern "C" int kl_tune(int knob, int value) {
     using namespace kl;
     switch (knob) {
-        case KL_TUNE_STREAM_GEMM: g_stream_enabled = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_GEMM: g_stream_enabled = value; return KL_OK;
         case KL_TUNE_STREAM_NMMA:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_nmma = value;
@@ -885,8 +896,8 @@ extern "C" int kl_tune(int knob, int value) {
 extern "C" int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
     using namespace kl;
     if (M <= 0 || N <= 0 || K <= 0) return 0;
-    if (stream_eligible(M, N, epilogue))
-        return kFlagBytes + static_cast<int64_t>(sm_count()) * stream_slot_bytes(M, stream_nmma(N, epilogue));
+    if (stream_eligible(M, N, K, epilogue))
+        return kFlagBytes + static_cast<int64_t>(stream_grid(N, K, epilogue)) * stream_slot_bytes(M, stream_nmma(N, epilogue));
     const int m_tiles = (M + BM - 1) / BM;
     const int tiles = (N / 128) * m_tiles;
     const int s = choose_splits(tiles, K / BK, M, N, INT64_MAX);
@@ -907,7 +918,7 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
     if (epilogue == kResidual && (r == nullptr || !aligned16(r))) return KL_EINVAL;
     if (epilogue == kSwiGLU && N % 256 != 0) return KL_EINVAL;
     if (workspace != nullptr && !aligned16(workspace)) return KL_EINVAL;
-    if (workspace != nullptr && stream_eligible(M, N, epilogue) &&
+    if (workspace != nullptr && stream_eligible(M, N, K, epilogue) &&
         workspace_bytes >= kFlagBytes + stream_slot_bytes(M, stream_nmma(N, epilogue))) {
         const int rc = gemm_stream(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes,
                                    stream);

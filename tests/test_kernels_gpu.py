@@ -102,6 +102,7 @@ def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
     n_out = N // 2 if epi == 2 else N
     r = orc.normal_bf16(M * n_out, 53, 1.0).reshape(M, n_out) if epi == 1 else None
     K.tune(K.TUNE_STREAM_NMMA, nmma)
+    K.tune(K.TUNE_STREAM_GEMM, 2)  # force the streaming path at these small shapes
     try:
         assert K.workspace_bytes(M, N, Kd, epi) > 0
         rd = to_dev(r, cuda) if r is not None else None
@@ -109,7 +110,8 @@ def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
         c2 = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
         torch.cuda.synchronize()
     finally:
-        K.tune(K.TUNE_STREAM_NMMA, 2)
+        K.tune(K.TUNE_STREAM_NMMA, 1)
+        K.tune(K.TUNE_STREAM_GEMM, 1)
     assert torch.equal(c, c2)  # deterministic split reduction
     x = a[off:off + M]
     if epi == 2:
@@ -129,7 +131,11 @@ def test_gemm_weight_streaming_small_workspace_and_off(K, cuda):
     b = orc.normal_bf16(N * Kd, 55, 0.02).reshape(N, Kd)
     ref = orc.gemm_f32(np.ascontiguousarray(to_bits(a)), b)
     bd = to_dev(b, cuda)
-    small = K.gemm(a, bd, ws_bytes=1024 + 3 * 2 * 128 * 96 * 4)
+    K.tune(K.TUNE_STREAM_GEMM, 2)
+    try:
+        small = K.gemm(a, bd, ws_bytes=1024 + 3 * 2 * 128 * 96 * 4)
+    finally:
+        K.tune(K.TUNE_STREAM_GEMM, 1)
     K.tune(K.TUNE_STREAM_GEMM, 0)
     try:
         off = K.gemm(a, bd)

@@ -45,7 +45,36 @@ def dump_trace(label):
         print(f"  {nm:10s} med {np.nanmedian(col):7.2f}  min {np.nanmin(col):7.2f}  max {np.nanmax(col):7.2f}")
 
 
+GAP_MS = 0.0
+
+
 def timed(fn, iters, stream):
+    if GAP_MS > 0:
+        # Idle gaps between launches (as inside the link-bound decode step):
+        # per-launch event times, median.
+        # The stream is gated by a spin kernel on a host flag, so the timed
+        # launch is already queued when the GPU wakes up (no host latency).
+        import ctypes
+        import time
+        flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        for _ in range(3):
+            fn(0)
+        ts = []
+        for i in range(iters):
+            torch.cuda.synchronize()
+            flag[0] = 0
+            K._lib.kl_debug_spin_flag(ctypes.c_void_p(flag.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn(i)
+            b.record(stream)
+            time.sleep(GAP_MS / 1e3)
+            flag[0] = 1
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        return ts[len(ts) // 2] * 1e-3
     if TRACE:
         import ctypes
         buf = (ctypes.c_ulonglong * (256 * 12))()
@@ -73,17 +102,20 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--rows", type=int, default=128)
     ap.add_argument("--json", default="")
-    ap.add_argument("--nmma", type=int, default=2, help="weight sub-tiles per activation tile (stream GEMM)")
+    ap.add_argument("--nmma", type=int, default=1, help="weight sub-tiles per activation tile (stream GEMM)")
     ap.add_argument("--no-stream", action="store_true", help="disable the weight-streaming decode GEMM path")
     ap.add_argument("--stages", type=int, default=8)
     ap.add_argument("--hint", type=int, default=1)
     ap.add_argument("--ctas", type=int, default=1)
     ap.add_argument("--debug", type=int, default=0)
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
+    ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
     args = ap.parse_args()
     K.tune(99, args.debug)
     K.tune(K.TUNE_PDL, args.pdl)
-    global TRACE
+    global TRACE, GAP_MS
+    GAP_MS = args.gap_ms
     TRACE = bool(args.debug & 128)
     K.tune(K.TUNE_STREAM_STAGES, args.stages)
     K.tune(K.TUNE_STREAM_HINT, args.hint)
@@ -92,6 +124,14 @@ def main():
     K.tune(K.TUNE_STREAM_GEMM, 0 if args.no_stream else 1)
     dev = torch.device("cuda:0")
     st = torch.cuda.current_stream()
+    if args.h2d:
+        # Background H2D traffic like the link-bound decode step's expert streaming.
+        hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        hdst = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            for _ in range(200):
+                hdst.copy_(hsrc, non_blocking=True)
     res = {}
     bf = torch.bfloat16
     # Expert FFN: 8 distinct experts (2.8 GB) so weights stream from HBM, not L2.
@@ -131,6 +171,12 @@ def main():
         qkv = torch.empty(bs, width, dtype=bf, device=dev)
         t = timed(lambda i: K.gemm(x, wqkv[i % 4], c=qkv), args.iters, st)
         res["gemm_qkv_M64"] = {"us": t * 1e6, "GBs": width * d * 2 / t / 1e9}
+        wo = [torch.randn(d, Hq * hd, dtype=bf, device=dev) * 0.02 for _ in range(4)]
+        ao = torch.randn(bs, Hq * hd, dtype=bf, device=dev)
+        hres = torch.randn(bs, d, dtype=bf, device=dev)
+        t = timed(lambda i: K.gemm(ao, wo[i % 4], c=hres, residual=hres, epilogue=1), args.iters, st)
+        dump_trace("o_proj")
+        res["gemm_oproj_M64"] = {"us": t * 1e6, "GBs": d * Hq * hd * 2 / t / 1e9}
         cap = 260
         kc = torch.randn(T * cap * Hkv * hd, dtype=bf, device=dev)
         vc = torch.randn_like(kc)
