@@ -173,6 +173,17 @@ int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, cons
                    const uint16_t* v_cache, int cap, int sink, float scale, uint16_t* out,
                    cudaStream_t stream);
 
+/* Split-KV decode attention (same semantics as kl_attn_decode): one CTA per
+ * (token, 16-slot chunk) stages the chunk's K and V rows with bulk async
+ * copies, then a merge kernel folds the chunks in fixed order. workspace >=
+ * kl_attn_decode_workspace_bytes(T, Hq, hd, cap) (fp32 partials); with a
+ * smaller/NULL workspace it runs kl_attn_decode. */
+int64_t kl_attn_decode_workspace_bytes(int64_t T, int Hq, int hd, int cap);
+int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
+                      int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache,
+                      const uint16_t* v_cache, int cap, int sink, float scale, uint16_t* out,
+                      void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+
 /* Prefill (chunk) attention: T = n_seq * L query rows laid out [seq][L]; keys
  * and values read from the same qkv rows (post-rope), causal with the same
  * sink + window retention mask as decode (window = cap - sink). hd in {64, 128}. */

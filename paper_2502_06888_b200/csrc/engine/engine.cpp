@@ -278,6 +278,10 @@ void Engine::plan_memory() {
                                        kl_gemm_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1),
                                        kl_gemm_workspace_bytes(mi, D_.V, D_.d, 0)});
         }
+        // Decode attention partials (split-KV) share the same scratch.
+        gemm_ws_bytes_ = std::max(gemm_ws_bytes_,
+                                  kl_attn_decode_workspace_bytes(w.batch_size, D_.Hq, D_.hd,
+                                                                 cfg_.retention.retained(w.prompt_len + w.gen_len)));
         // A smaller workspace only means fewer CTAs in the weight-streaming
         // GEMMs; keep it a small fraction of tight HBM caps.
         gemm_ws_bytes_ = std::min<int64_t>({gemm_ws_bytes_, kGemmWorkspace, std::max<int64_t>(256LL << 10, cfg_.hbm_cap / 256)});

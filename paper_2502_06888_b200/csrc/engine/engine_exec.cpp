@@ -387,8 +387,9 @@ void Engine::exec_attention(const StreamOp& op) {
         kl_check(kl_attn_prefill(qkv_, cfg_.workload.batch_size, cfg_.workload.prompt_len, D_.Hq, D_.Hkv, D_.hd,
                                  kv_cap_, kv_sink_, scale, ao_, cs), "prefill attention");
     else
-        kl_check(kl_attn_decode(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
-                                kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, cs), "decode attention");
+        kl_check(kl_attn_decode_ws(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
+                                   kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
+                 "decode attention");
     kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs), "o proj");
 }
 

@@ -207,6 +207,215 @@ attn_decode_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32
     }
 }
 
+// Split-KV decode ("flash-decoding"), the HBM-bound path: one CTA per
+// (token, chunk of kDecChunk retained slots). The chunk's K and V rows of
+// every KV head are contiguous in the cache ([seq][slot][Hkv][hd]), so one
+// thread stages them with two 1D bulk copies (cp.async.bulk, full memory-
+// level parallelism, no per-thread address math); scores start as soon as K
+// lands while V is still in flight. Warps map to KV heads: lane = slot for
+// q.k (rotated 16-byte reads, conflict-free), lane = head dims for p.V.
+// Each CTA writes the chunk's unnormalised output with its running max and
+// sum; attn_merge_kernel folds the chunks (fixed chunk order).
+// Algorithmic bytes per (token, layer): retained * Hkv*hd*2 * 2.
+constexpr int kDecChunk = 16;
+constexpr int kDecThreads = 128;
+constexpr int kKPad = 8;  // bf16 padding per staged K row: rows land 16 B apart in the banks
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kDecThreads)
+attn_decode_split_kernel(const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
+                         const int32_t* __restrict__ seq, int Hq, int Hkv, const uint16_t* __restrict__ kc,
+                         const uint16_t* __restrict__ vc, int cap, float scale, float* __restrict__ part_o,
+                         float* __restrict__ part_ml, int n_chunks) {
+    constexpr int V8 = HD / 8;  // 16-byte vectors per head row
+    extern __shared__ __align__(128) uint8_t dsm[];
+    const int t = blockIdx.x, c = blockIdx.y;
+    const int G = Hq / Hkv;
+    const int row = Hkv * HD;        // elements per cache slot row (all KV heads)
+    const int krow = row + kKPad;    // staged K row stride (padded)
+    uint16_t* Ks = reinterpret_cast<uint16_t*>(dsm);
+    uint16_t* Vs = Ks + kDecChunk * krow;
+    float* qs = reinterpret_cast<float*>(Vs + kDecChunk * row);  // [Hq][HD], pre-scaled
+    float* S = qs + Hq * HD;                                     // [Hq][kDecChunk]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(S + Hq * kDecChunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = min(pos[t] + 1, cap);
+    const int j0 = c * kDecChunk;
+    const int cnt = min(kDecChunk, n - j0);
+    float* po = part_o + (static_cast<int64_t>(t) * n_chunks + c) * Hq * HD;
+    float* pml = part_ml + (static_cast<int64_t>(t) * n_chunks + c) * Hq * 2;
+    if (cnt <= 0) {
+        for (int h = threadIdx.x; h < Hq; h += blockDim.x) {
+            pml[2 * h] = -INFINITY;
+            pml[2 * h + 1] = 0.f;
+        }
+        return;
+    }
+    const int64_t base = (static_cast<int64_t>(seq[t]) * cap + j0) * row;
+    const uint32_t row_bytes = static_cast<uint32_t>(row) * 2;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
+        mbar_arrive_expect_tx(&bars[0], row_bytes * cnt);
+        for (int j = 0; j < cnt; ++j) bulk_load(Ks + j * krow, kc + base + static_cast<int64_t>(j) * row, row_bytes, &bars[0]);
+        mbar_arrive_expect_tx(&bars[1], row_bytes * cnt);
+        bulk_load(Vs, vc + base, row_bytes * cnt, &bars[1]);
+    }
+    const uint16_t* qp = q + static_cast<int64_t>(t) * q_stride;
+    for (int i = threadIdx.x; i < Hq * HD / 8; i += blockDim.x) {
+        float v[8];
+        const uint4 w = *reinterpret_cast<const uint4*>(qp + i * 8);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[2 * k] = bf2f(static_cast<uint16_t>(ws[k] & 0xffffu)) * scale;
+            v[2 * k + 1] = bf2f(static_cast<uint16_t>(ws[k] >> 16)) * scale;
+        }
+        *reinterpret_cast<float4*>(qs + i * 8) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(qs + i * 8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    __syncthreads();  // q staged; barrier inits visible
+    mbar_wait(&bars[0], 0);
+
+    // Scores: thread = (kv head h, slot j); every lane of a warp reads the
+    // same q element (broadcast) and its own padded K row (no conflicts).
+    for (int pr = threadIdx.x; pr < Hkv * kDecChunk; pr += blockDim.x) {
+        const int h = pr / kDecChunk, j = pr % kDecChunk;
+        if (j >= cnt) continue;
+        const uint16_t* kr = Ks + j * krow + h * HD;
+        float acc[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) acc[g] = 0.f;
+#pragma unroll 4
+        for (int x = 0; x < V8; ++x) {
+            const uint4 w = *reinterpret_cast<const uint4*>(kr + x * 8);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            float kv[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                kv[2 * k] = bf2f(static_cast<uint16_t>(ws[k] & 0xffffu));
+                kv[2 * k + 1] = bf2f(static_cast<uint16_t>(ws[k] >> 16));
+            }
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g < G) {
+                    const float* qq = qs + (h * G + g) * HD + x * 8;
+                    const float4 q0 = *reinterpret_cast<const float4*>(qq);
+                    const float4 q1 = *reinterpret_cast<const float4*>(qq + 4);
+                    acc[g] = fmaf(q0.x, kv[0], acc[g]);
+                    acc[g] = fmaf(q0.y, kv[1], acc[g]);
+                    acc[g] = fmaf(q0.z, kv[2], acc[g]);
+                    acc[g] = fmaf(q0.w, kv[3], acc[g]);
+                    acc[g] = fmaf(q1.x, kv[4], acc[g]);
+                    acc[g] = fmaf(q1.y, kv[5], acc[g]);
+                    acc[g] = fmaf(q1.z, kv[6], acc[g]);
+                    acc[g] = fmaf(q1.w, kv[7], acc[g]);
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (g < G) S[(h * G + g) * kDecChunk + j] = acc[g];
+    }
+    __syncthreads();
+
+    // Chunk softmax per q head: a half-warp per head, lane = slot.
+    {
+        const int half = lane >> 4, sl = lane & 15;
+        for (int hq = warp * 2 + half; hq < Hq; hq += kDecThreads / 16) {
+            const float sv = sl < cnt ? S[hq * kDecChunk + sl] : -INFINITY;
+            float m = sv;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const float e = sl < cnt ? __expf(sv - m) : 0.f;
+            float l = e;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+            S[hq * kDecChunk + sl] = e;
+            if (sl == 0) {
+                pml[2 * hq] = m;
+                pml[2 * hq + 1] = l;
+            }
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bars[1], 0);
+
+    // p.V: warp = kv head, lane owns HD/32 dims, G q heads.
+    constexpr int PER = HD / 32;
+    for (int h = warp; h < Hkv; h += kDecThreads / 32) {
+        float o[8][PER];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int i = 0; i < PER; ++i) o[g][i] = 0.f;
+        for (int j = 0; j < cnt; ++j) {
+            const uint16_t* vr = Vs + j * row + h * HD + lane * PER;
+            float vv[PER];
+            if constexpr (PER == 4) {
+                const uint2 w = *reinterpret_cast<const uint2*>(vr);
+                vv[0] = bf2f(static_cast<uint16_t>(w.x & 0xffffu));
+                vv[1] = bf2f(static_cast<uint16_t>(w.x >> 16));
+                vv[2] = bf2f(static_cast<uint16_t>(w.y & 0xffffu));
+                vv[3] = bf2f(static_cast<uint16_t>(w.y >> 16));
+            } else {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(vr);
+                vv[0] = bf2f(static_cast<uint16_t>(w & 0xffffu));
+                vv[1] = bf2f(static_cast<uint16_t>(w >> 16));
+            }
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g < G) {
+                    const float pj = S[(h * G + g) * kDecChunk + j];
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) o[g][i] = fmaf(pj, vv[i], o[g][i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g < G) {
+                float* dst = po + (h * G + g) * HD + lane * PER;
+                if constexpr (PER == 4)
+                    *reinterpret_cast<float4*>(dst) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+                else
+                    *reinterpret_cast<float2*>(dst) = make_float2(o[g][0], o[g][1]);
+            }
+        }
+    }
+}
+
+// Fold the chunk partials of one (token, q head): fixed chunk order.
+template <int HD>
+__global__ void attn_merge_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml, int Hq,
+                                  int n_chunks, uint16_t* __restrict__ out) {
+    const int t = blockIdx.x, hq = blockIdx.y, d = threadIdx.x;
+    const float* ml = part_ml + static_cast<int64_t>(t) * n_chunks * Hq * 2 + hq * 2;
+    const float* po = part_o + static_cast<int64_t>(t) * n_chunks * Hq * HD + static_cast<int64_t>(hq) * HD + d;
+    float M = -INFINITY;
+#pragma unroll 8
+    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, ml[c * Hq * 2]);
+    // Fixed-order fold; unrolled so the independent loads are in flight together.
+    float L = 0.f, acc = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < n_chunks; ++c) {
+        const float m = ml[c * Hq * 2], l = ml[c * Hq * 2 + 1];
+        const float o = po[static_cast<int64_t>(c) * Hq * HD];
+        const float w = m == -INFINITY ? 0.f : __expf(m - M);
+        L = fmaf(l, w, L);
+        acc = fmaf(o, w, acc);
+    }
+    out[(static_cast<int64_t>(t) * Hq + hq) * HD + d] = f2bf(acc / L);
+}
+
 // Prefill: one warp per (query row, q head); keys from the same chunk's qkv
 // rows; causal with sink + sliding-window retention; online softmax.
 template <int HD>
@@ -290,6 +499,42 @@ extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<dim3(static_cast<unsigned>(T), Hkv), kAttnWarps * 32, smem, stream>>>(q, q_stride, pos, seq, Hq, Hkv,
                                                                                k_cache, v_cache, cap, sink, scale, out);
+    return check_launch();
+}
+
+extern "C" int64_t kl_attn_decode_workspace_bytes(int64_t T, int Hq, int hd, int cap) {
+    if (T <= 0 || Hq <= 0 || hd <= 0 || cap <= 0) return 0;
+    const int64_t chunks = (cap + kDecChunk - 1) / kDecChunk;
+    return T * chunks * Hq * (static_cast<int64_t>(hd) + 2) * 4;
+}
+
+extern "C" int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
+                                 int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache,
+                                 int cap, int sink, float scale, uint16_t* out, void* workspace,
+                                 int64_t workspace_bytes, cudaStream_t stream) {
+    if (hd != 128 && hd != 64) return KL_EUNSUPPORTED;
+    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || !q || !pos || !seq || !out) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int G = Hq / Hkv;
+    if (G > 8) return KL_EUNSUPPORTED;
+    const int64_t need = kl_attn_decode_workspace_bytes(T, Hq, hd, cap);
+    const size_t smem = static_cast<size_t>(kDecChunk) * (Hkv * hd + kKPad) * 2 +
+                        static_cast<size_t>(kDecChunk) * Hkv * hd * 2 + static_cast<size_t>(Hq) * hd * 4 +
+                        static_cast<size_t>(Hq) * kDecChunk * 4 + 16;
+    if (workspace == nullptr || workspace_bytes < need || smem > 200 * 1024 || q_stride % 8 != 0 ||
+
+        (reinterpret_cast<uintptr_t>(k_cache) & 15) || (reinterpret_cast<uintptr_t>(v_cache) & 15))
+        return kl_attn_decode(q, q_stride, pos, seq, T, Hq, Hkv, hd, k_cache, v_cache, cap, sink, scale, out, stream);
+    const int n_chunks = (cap + kDecChunk - 1) / kDecChunk;
+    float* part_ml = static_cast<float*>(workspace);
+    float* part_o = part_ml + T * n_chunks * Hq * 2;
+    auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;
+    KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<dim3(static_cast<unsigned>(T), n_chunks), kDecThreads, smem, stream>>>(
+        q, q_stride, pos, seq, Hq, Hkv, k_cache, v_cache, cap, scale, part_o, part_ml, n_chunks);
+    KL_CUDA_TRY(cudaGetLastError());
+    auto merge = hd == 128 ? attn_merge_kernel<128> : attn_merge_kernel<64>;
+    merge<<<dim3(static_cast<unsigned>(T), Hq), hd, 0, stream>>>(part_o, part_ml, Hq, n_chunks, out);
     return check_launch();
 }
 

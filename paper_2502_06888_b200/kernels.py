@@ -40,6 +40,8 @@ _pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
 _rms = _sig("kl_rmsnorm", [_P, _P, _L, _I, _F, _P, _P])
 _rope = _sig("kl_rope_kv_append", [_P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _I, _I, _P])
 _dec = _sig("kl_attn_decode", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P])
+_dec_ws_bytes = _sig("kl_attn_decode_workspace_bytes", [_L, _I, _I, _I], C.c_int64)
+_dec_ws = _sig("kl_attn_decode_ws", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _L, _P])
 _pre = _sig("kl_attn_prefill", [_P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P])
 _fill = _sig("kl_fill_normal_bf16", [_P, _L, _U64, _F, _P])
 _tune = _sig("kl_tune", [_I, _I])
@@ -188,6 +190,16 @@ def attn_decode(q, q_stride, pos, seq, Hq, Hkv, hd, k_cache, v_cache, cap, sink,
     T = pos.shape[0]
     _chk(_dec(_p(q), q_stride, _p(pos), _p(seq), T, Hq, Hkv, hd, _p(k_cache), _p(v_cache), cap, sink, scale,
               _p(out), _s(stream)), "kl_attn_decode")
+    return out
+
+
+def attn_decode_split(q, q_stride, pos, seq, Hq, Hkv, hd, k_cache, v_cache, cap, sink, scale, out, stream=None):
+    """Split-KV decode attention (kl_attn_decode_ws) with a cached workspace."""
+    T = pos.shape[0]
+    wsb = int(_dec_ws_bytes(T, Hq, hd, cap))
+    ws = workspace(wsb, q.device)
+    _chk(_dec_ws(_p(q), q_stride, _p(pos), _p(seq), T, Hq, Hkv, hd, _p(k_cache), _p(v_cache), cap, sink, scale,
+                 _p(out), _p(ws), wsb, _s(stream)), "kl_attn_decode_ws")
     return out
 
 

@@ -188,6 +188,11 @@ def main():
             K.attn_decode(qkv, width, pos, seq + (i % n) * bs, Hq, Hkv, hd, kc, vc, cap, 4, hd ** -0.5, out)
         t = timed(att, args.iters, st)
         res["attn_decode_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+
+        def att2(i):
+            K.attn_decode_split(qkv, width, pos, seq + (i % n) * bs, Hq, Hkv, hd, kc, vc, cap, 4, hd ** -0.5, out)
+        t = timed(att2, args.iters, st)
+        res["attn_decode_split_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
     if not args.only or args.only == "route":
         h = torch.randn(T, d, dtype=bf, device=dev)
         nw = torch.ones(d, dtype=bf, device=dev)
