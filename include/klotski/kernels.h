@@ -71,6 +71,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints */
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */
 #define KL_TUNE_PDL 5 /* 1 = weight-streaming GEMMs use programmatic dependent launch (default) */
+#define KL_TUNE_PREFILL_TC 6 /* 1 = tcgen05 prefill attention (default), 0 = CUDA-core fallback */
 /* Process-wide tuning knobs for benchmarking (not thread-safe). */
 int kl_tune(int knob, int value);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
@@ -186,7 +187,10 @@ int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, c
 
 /* Prefill (chunk) attention: T = n_seq * L query rows laid out [seq][L]; keys
  * and values read from the same qkv rows (post-rope), causal with the same
- * sink + window retention mask as decode (window = cap - sink). hd in {64, 128}. */
+ * sink + window retention mask as decode (window = cap - sink). hd in {64, 128}.
+ * On tcgen05 when 128 % (Hq/Hkv) == 0: the GQA group's query heads share one
+ * 128-row MMA tile; S = QK^T and O = PV accumulate in TMEM (two-pass softmax,
+ * P staged as bf16 in shared memory). */
 int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap,
                     int sink, float scale, uint16_t* out, cudaStream_t stream);
 

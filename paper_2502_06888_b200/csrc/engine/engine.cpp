@@ -258,7 +258,7 @@ void Engine::plan_memory() {
         add(2LL * D_.V * D_.d * 2);
         add(2 * t_max_ * D_.d * 2);                                              // h, x2
         add(tb_max_ * (D_.d + D_.qkv_width() + D_.Hq * D_.hd) * 2);              // xa, qkv, ao
-        add(4 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
+        add(5 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
         add(2 * Rx * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
         add(kl_permute_workspace_bytes(Rx, D_.E));

@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "tma_host.cuh"
 
 namespace kl {
 namespace {
@@ -416,6 +417,217 @@ __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float*
     out[(static_cast<int64_t>(t) * Hq + hq) * HD + d] = f2bf(acc / L);
 }
 
+// ------------------------------------------------ prefill on tcgen05 -------
+// One CTA per (128/G query positions of one sequence, one KV head): the G
+// query heads of the GQA group are stacked into the 128 MMA rows, so every
+// K/V tile is shared by the whole group. Keys come in 128-row blocks that
+// cover the causal sink + sliding window of the tile. Two passes, so the
+// output needs no rescaling in TMEM:
+//   pass 1: S = Q K^T (TMEM) per block -> row max and sum (thread = row);
+//   pass 2: S again -> P = exp(S - max) / sum as bf16 into a 128B-swizzled
+//           smem tile (the MMA's A operand) -> O += P V with V read
+//           MN-major straight from its TMA tile (no transpose pass).
+// Roofline: tensor-bound; FLOPs per (row, head, retained key) = 4 * hd.
+constexpr int kPfThreads = 128;
+constexpr int kPfKeys = 128;  // keys per block (MMA N for S, K for P.V)
+
+// UMMA smem descriptor, MN-major operand in 128B-swizzled TMA tiles: 64
+// elements (128 B) contiguous along MN, 8-row atoms of 1024 B along K;
+// LBO = byte distance between 64-element MN chunks, SBO = 1024.
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kPfThreads, 1)
+attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_kv,
+                       int L, int Hq, int Hkv, int sink, int window, float scale, uint16_t* __restrict__ out) {
+    constexpr int NCH = HD / 64;                  // 64-wide swizzle chunks along hd
+    constexpr int kChunk = 128 * 128;             // bytes of a [128 rows x 64] bf16 tile
+    extern __shared__ uint8_t dsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Qs = sm;                       // NCH x [128 rows x 128 B]
+    uint8_t* Ks = Qs + NCH * kChunk;        // NCH x [128 keys x 128 B]
+    uint8_t* Vs = Ks + NCH * kChunk;        // NCH x [128 keys x 128 B]
+    uint8_t* Ps = Vs + NCH * kChunk;        // 2 x [128 rows x 128 B]  (keys 0-63, 64-127)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + 2 * kChunk);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+    uint64_t* tma_bar = &bars[0];
+    uint64_t* mma_bar = &bars[1];
+
+    const int G = Hq / Hkv;
+    const int P = 128 / G;  // query positions per tile
+    const int tile = blockIdx.x, kvh = blockIdx.y, sq = blockIdx.z;
+    const int i0 = tile * P;
+    const int64_t row0 = static_cast<int64_t>(sq) * L;
+    const int r = threadIdx.x;  // MMA row = TMEM lane
+    const int warp = r >> 5;
+    const int g = r / P, i = i0 + r % P;
+
+    if (r == 0) {
+        tma_prefetch_desc(&tmap_q);
+        tma_prefetch_desc(&tmap_kv);
+        mbar_init(tma_bar, 1);
+        mbar_init(mma_bar, 1);
+        mbar_fence_init();
+    }
+    if (warp == 0) tmem_alloc(tslot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tS = tmem, tO = tmem + 128;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+
+    // Key blocks: [lo, hi] covering the window of the tile, plus block 0 for the sink.
+    const int last = min(i0 + P - 1, L - 1);
+    const int b_lo = max(0, i0 - window + 1) / kPfKeys, b_hi = last / kPfKeys;
+    const bool sink_block = sink > 0 && b_lo > 0;
+    const int nblk = (b_hi - b_lo + 1) + (sink_block ? 1 : 0);
+    auto block_of = [&](int n) { return sink_block ? (n == 0 ? 0 : b_lo + n - 1) : b_lo + n; };
+
+    uint32_t tma_phase = 0, mma_phase = 0;
+    const uint32_t idesc_s = idesc_bf16_f32(128, kPfKeys);
+    const uint32_t idesc_o = idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
+
+    if (r == 0) {
+        mbar_arrive_expect_tx(tma_bar, NCH * kChunk);
+        for (int gg = 0; gg < G; ++gg)
+            for (int c = 0; c < NCH; ++c)
+                tma_load_2d(Qs + c * kChunk + gg * P * 128, &tmap_q, tma_bar, (kvh * G + gg) * HD + c * 64,
+                            static_cast<int>(row0 + i0));
+    }
+    auto issue_s = [&](int b, bool with_v) {
+        // (thread 0) K (and V) block b -> smem, then S = Q K^T.
+        const int krow = static_cast<int>(row0 + b * kPfKeys);
+        mbar_arrive_expect_tx(tma_bar, (with_v ? 2 : 1) * NCH * kChunk);
+        for (int c = 0; c < NCH; ++c) {
+            tma_load_2d(Ks + c * kChunk, &tmap_kv, tma_bar, (Hq + kvh) * HD + c * 64, krow);
+            if (with_v) tma_load_2d(Vs + c * kChunk, &tmap_kv, tma_bar, (Hq + Hkv + kvh) * HD + c * 64, krow);
+        }
+        mbar_wait(tma_bar, tma_phase);
+        tma_phase ^= 1;
+        tc_fence_after();
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                tc_mma_bf16(tS, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
+                            sw128_kmajor_desc(smem_u32(Ks + c * kChunk) + k * 32), idesc_s, (c | k) != 0);
+        tc_commit(mma_bar);
+    };
+    auto valid = [&](int j) { return j <= i && j < L && (j < sink || j > i - window); };
+
+    // Pass 1: row max and sum over the retained keys.
+    float m = -INFINITY, l = 0.f;
+    for (int n = 0; n < nblk; ++n) {
+        const int b = block_of(n);
+        if (r == 0) {
+            if (n == 0) {
+                mbar_wait(tma_bar, tma_phase);  // Q landed
+                tma_phase ^= 1;
+            }
+            issue_s(b, false);
+        }
+        mbar_wait(mma_bar, mma_phase);
+        mma_phase ^= 1;
+        __syncwarp();
+        tc_fence_after();
+        for (int c0 = 0; c0 < kPfKeys; c0 += 32) {
+            float v[32];
+            tmem_ld32(tS + lane_off + c0, v);
+            float bm = m;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+                v[x] = valid(b * kPfKeys + c0 + x) ? v[x] * scale : -INFINITY;
+                bm = fmaxf(bm, v[x]);
+            }
+            if (bm != -INFINITY) {  // (no divergent exit: the TMEM loads are warp-collective)
+                float sum = 0.f;
+#pragma unroll
+                for (int x = 0; x < 32; ++x) sum += __expf(v[x] - bm);
+                l = (m == -INFINITY ? 0.f : l * __expf(m - bm)) + sum;
+                m = bm;
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // S consumed, K buffer free
+    }
+    const float inv_l = 1.0f / l;
+
+    // Pass 2: P = softmax row (bf16, swizzled A tile), O += P V.
+    for (int n = 0; n < nblk; ++n) {
+        const int b = block_of(n);
+        if (r == 0) issue_s(b, true);
+        mbar_wait(mma_bar, mma_phase);
+        mma_phase ^= 1;
+        __syncwarp();
+        tc_fence_after();
+        for (int c0 = 0; c0 < kPfKeys; c0 += 32) {
+            float v[32];
+            tmem_ld32(tS + lane_off + c0, v);
+            uint8_t* prow = Ps + (c0 / 64) * kChunk + r * 128;
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h2 = 0; h2 < 4; ++h2) {
+                    const int x0 = q8 * 8 + h2 * 2;
+                    const int j = b * kPfKeys + c0 + x0;
+                    const float p0 = valid(j) ? __expf(v[x0] * scale - m) * inv_l : 0.f;
+                    const float p1 = valid(j + 1) ? __expf(v[x0 + 1] * scale - m) * inv_l : 0.f;
+                    w[h2] = pack2(p0, p1);
+                }
+                const int unit = ((c0 % 64) / 8 + q8) ^ (r & 7);  // 128B swizzle: 16-byte unit ^ row%8
+                *reinterpret_cast<uint4*>(prow + unit * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();
+        if (r == 0) {
+            tc_fence_after();
+            for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    tc_mma_bf16(tO, sw128_kmajor_desc(smem_u32(Ps + kc * kChunk) + k * 32),
+                                sw128_mnmajor_desc(smem_u32(Vs) + (kc * 64 + k * 16) * 128, kChunk), idesc_o,
+                                (n > 0 || kc > 0 || k > 0) ? 1u : 0u);
+            tc_commit(mma_bar);
+        }
+        mbar_wait(mma_bar, mma_phase);  // P.V done: P, V, S reusable
+        mma_phase ^= 1;
+        __syncwarp();
+        tc_fence_after();
+        __syncthreads();
+    }
+
+    // Epilogue: O row -> out[(seq, i)][(kvh*G + g)*HD + d].
+    uint16_t* orow = out + (row0 + i) * static_cast<int64_t>(Hq) * HD + static_cast<int64_t>(kvh * G + g) * HD;
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+        float v[32];
+        tmem_ld32(tO + lane_off + c0, v);  // warp-collective: every lane, stores predicated
+        if (i < L) {
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8)
+                *reinterpret_cast<uint4*>(orow + c0 + q8 * 8) =
+                    make_uint4(pack2(v[q8 * 8], v[q8 * 8 + 1]), pack2(v[q8 * 8 + 2], v[q8 * 8 + 3]),
+                               pack2(v[q8 * 8 + 4], v[q8 * 8 + 5]), pack2(v[q8 * 8 + 6], v[q8 * 8 + 7]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
 // Prefill: one warp per (query row, q head); keys from the same chunk's qkv
 // rows; causal with sink + sliding-window retention; online softmax.
 template <int HD>
@@ -468,6 +680,10 @@ __global__ void attn_prefill_kernel(const uint16_t* __restrict__ qkv, int n_seq,
 }  // namespace kl
 
 using namespace kl;
+
+namespace kl {
+int g_prefill_tc = 1;  // kl_tune(KL_TUNE_PREFILL_TC, ...)
+}
 
 extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int hd, const int32_t* pos,
                                  const int32_t* seq, float rope_theta, uint16_t* k_cache, uint16_t* v_cache, int cap,
@@ -544,6 +760,22 @@ extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, in
     if (n_seq < 0 || L < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || !qkv || !out) return KL_EINVAL;
     const int64_t warps = static_cast<int64_t>(n_seq) * L * Hq;
     if (warps == 0) return KL_OK;
+    const int G = Hq / Hkv;
+    const int width = (Hq + 2 * Hkv) * hd;
+    if (g_prefill_tc && 128 % G == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && width % 8 == 0) {
+        CUtensorMap mq, mkv;
+        int rc = make_map(&mq, qkv, static_cast<int64_t>(n_seq) * L, width, 128 / G);
+        if (rc) return rc;
+        rc = make_map(&mkv, qkv, static_cast<int64_t>(n_seq) * L, width, kPfKeys);
+        if (rc) return rc;
+        const int nch = hd / 64;
+        const int smem = 3 * nch * 128 * 128 + 2 * 128 * 128 + 1024 + 64;
+        auto kern = hd == 128 ? attn_prefill_tc_kernel<128> : attn_prefill_tc_kernel<64>;
+        KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const dim3 grid((L + 128 / G - 1) / (128 / G), Hkv, n_seq);
+        kern<<<grid, kPfThreads, smem, stream>>>(mq, mkv, L, Hq, Hkv, sink, cap - sink, scale, out);
+        return check_launch();
+    }
     auto kern = hd == 128 ? attn_prefill_kernel<128> : attn_prefill_kernel<64>;
     kern<<<static_cast<int>((warps + 7) / 8), 256, 0, stream>>>(qkv, n_seq, L, Hq, Hkv, cap, sink, scale, out);
     return check_launch();

@@ -25,6 +25,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tma_host.cuh"
 
 namespace kl {
 namespace {
@@ -631,37 +632,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
 
 // ------------------------------------------------------------ host side ----
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encoder() {
-    static EncodeFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
-    });
-    return fn;
-}
-
-// Row-major bf16 matrix [rows, cols] viewed by TMA in boxes of [box_rows, 64].
-int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
-    EncodeFn enc = encoder();
-    if (enc == nullptr) return KL_ENODEV;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return res == CUDA_SUCCESS ? 0 : KL_EINVAL;
-}
-
 struct Launch {
     const uint16_t* a;
     int64_t a_rows, row_offset;
@@ -870,6 +840,10 @@ extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
     return rc;
 }
 
+namespace kl {
+extern int g_prefill_tc;
+}
+
 extern "C" int kl_tune(int knob, int value) {
     using namespace kl;
     switch (knob) {
@@ -885,6 +859,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_HINT: g_stream_hint = value != 0; return KL_OK;
         case 99: g_stream_debug = value; return KL_OK;
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
+        case KL_TUNE_PREFILL_TC: g_prefill_tc = value != 0; return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_ctas = value;

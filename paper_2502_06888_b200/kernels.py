@@ -53,6 +53,7 @@ TUNE_STREAM_STAGES = 2
 TUNE_STREAM_HINT = 3
 TUNE_STREAM_CTAS_PER_SM = 4
 TUNE_PDL = 5
+TUNE_PREFILL_TC = 6
 
 
 def tune(knob, value):

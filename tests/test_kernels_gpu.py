@@ -319,13 +319,22 @@ def test_decode_attention_split_kv(K, cuda, Hq, Hkv, hd, cap, p):
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 
 
-def test_prefill_attention_window(K, cuda):
-    n_seq, L, Hq, Hkv, hd, cap, sink = 3, 40, 4, 1, 128, 24, 4
+@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("n_seq,L,Hq,Hkv,hd,cap,sink", [(3, 40, 4, 1, 128, 24, 4), (2, 512, 32, 8, 128, 260, 4),
+                                                       (2, 300, 8, 8, 64, 100, 0), (1, 200, 16, 2, 128, 1000, 4)])
+def test_prefill_attention_window(K, cuda, tc, n_seq, L, Hq, Hkv, hd, cap, sink):
+    """Prefill attention (tcgen05 two-pass kernel, and the CUDA-core fallback)
+    against the oracle: causal + sink + sliding window, GQA/MHA, hd 64/128,
+    ragged tiles (L not a multiple of the tile), window longer than L."""
     width = (Hq + 2 * Hkv) * hd
     qkv = orc.normal_bf16(n_seq * L * width, 9, 1.0).reshape(n_seq * L, width)
     out = torch.empty(n_seq * L, Hq * hd, dtype=torch.bfloat16, device=cuda)
-    K.attn_prefill(to_dev(qkv, cuda), n_seq, L, Hq, Hkv, hd, cap, sink, hd ** -0.5, out)
-    torch.cuda.synchronize()
+    K.tune(K.TUNE_PREFILL_TC, tc)
+    try:
+        K.attn_prefill(to_dev(qkv, cuda), n_seq, L, Hq, Hkv, hd, cap, sink, hd ** -0.5, out)
+        torch.cuda.synchronize()
+    finally:
+        K.tune(K.TUNE_PREFILL_TC, 1)
     ref = orc.attn_prefill(qkv, n_seq, L, Hq, Hkv, hd, cap, sink, hd ** -0.5)
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 

@@ -138,13 +138,14 @@ def main():
     if not args.only or args.only == "ffn":
         M = args.rows
         ws = [torch.randn(3 * d * f, dtype=bf, device=dev) * 0.02 for _ in range(E)]
-        xp = torch.randn(T * k, d, dtype=bf, device=dev)
-        y = torch.empty(T * k, d, dtype=bf, device=dev)
+        R = max(T * k, M)
+        xp = torch.randn(R, d, dtype=bf, device=dev)
+        y = torch.empty(R, d, dtype=bf, device=dev)
         h = torch.empty(max(M, 1), f, dtype=bf, device=dev)
 
         def ffn(i):
             w = ws[i % E]
-            K.expert_ffn(xp, (i % E) * M % (T * k - M + 1), M, w[: 2 * f * d].view(2 * f, d),
+            K.expert_ffn(xp, (i % E) * M % (R - M + 1), M, w[: 2 * f * d].view(2 * f, d),
                          w[2 * f * d:].view(d, f), y, h)
         t = timed(ffn, args.iters, st)
         byt = 3 * d * f * 2 + M * (2 * d * 2 + 2 * f * 2)
