@@ -33,7 +33,7 @@ CORE     := $(PKG)/_core$(PY_EXT)
 PARITY   := $(PKG)/libparity.so
 ORACLE   := oracle/liboracle.so
 
-all: $(LIB) $(PARITY) $(ORACLE)
+all: $(LIB) $(CORE) $(PARITY) $(ORACLE)
 
 build/host/%.o: $(CSRC)/host/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)

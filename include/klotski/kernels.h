@@ -74,6 +74,13 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_PREFILL_TC 6 /* 1 = tcgen05 prefill attention (default), 0 = CUDA-core fallback */
 /* Process-wide tuning knobs for benchmarking (not thread-safe). */
 int kl_tune(int knob, int value);
+/* Benchmarking aids: per-CTA phase timestamps (ns, globaltimer) of the last
+ * weight-streaming GEMM launched with the trace debug bit (12 per CTA; the
+ * buffer is cleared after the read), and a 1-thread kernel that holds
+ * `stream` until the host-mapped *flag becomes non-zero (launch-latency-free
+ * timing of the work queued behind it). */
+int kl_stream_trace(unsigned long long* host, int n_ctas);
+int kl_debug_spin_flag(const int* flag, cudaStream_t stream);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
                  int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
