@@ -96,6 +96,34 @@ int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row_offset, in
                   int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
                   uint16_t* y, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
+/* ---- 4-bit expert streaming ----
+ * Q4T layout: the reference's HQQ format (quant.cpp:197-252: 4-bit codes,
+ * groups of 64 along K, fp16 scale and zero, w = scale * (code - zero))
+ * with the groups of each 128-row x 64-column tile stored as one contiguous
+ * 4608-byte chunk [128 x 32 B nibble codes | 128 fp16 scales | 128 fp16
+ * zeros], chunks ordered (row tile, k-block). A permutation of the
+ * reference's QuantizedTensor groups: same codes / scales / zeros.
+ * rows % 128 == 0, K % 64 == 0. */
+int64_t kl_q4_bytes(int64_t rows, int64_t K);
+/* Min-max fit per group (moesim::fit_minmax, mirrored bit-exactly). */
+int kl_quantize_q4(const uint16_t* w, int64_t rows, int64_t K, uint8_t* out, cudaStream_t stream);
+/* out = bf16(scale * (code - zero)) (fp32 ops; equals the reference's
+ * dequantize() rounded to bf16). */
+int kl_dequantize_q4(const uint8_t* q, int64_t rows, int64_t K, uint16_t* w, cudaStream_t stream);
+/* Weight-streaming GEMM with the dequantisation fused into the producer:
+ * packed tiles bulk-copied to shared memory, expanded to 128B-swizzled bf16
+ * by the (otherwise idle) epilogue warps, consumed by tcgen05.mma. Same
+ * semantics / epilogues as kl_gemm_bf16 with B = dequantised weights;
+ * M <= 256 (larger M: kl_dequantize_q4 + kl_gemm_bf16); workspace required. */
+int64_t kl_gemm_q4_workspace_bytes(int M, int N, int K, int epilogue);
+int kl_gemm_q4(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint8_t* bq,
+               int N, uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace,
+               int64_t workspace_bytes, cudaStream_t stream);
+/* Expert FFN over Q4T weights: w13q = Q4T of [W1; W3] (2f x d), w2q = Q4T of W2 (d x f). */
+int kl_expert_ffn_q4(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
+                     int f, const uint8_t* w13q, const uint8_t* w2q, uint16_t* h_scratch,
+                     uint16_t* y, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+
 /* ---- routing ----
  * Fused RMSNorm + router + top-k for T tokens (one warp per token):
  *   x2[t]   = bf16(h[t] * rsqrt(mean(h[t]^2) + eps) * norm_w)      (stored)

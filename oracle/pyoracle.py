@@ -136,3 +136,70 @@ def attn_prefill(qkv, n_seq, L, Hq, Hkv, hd, cap, sink, scale):
     out = np.empty((n_seq * L, Hq * hd), np.uint16)
     _lib.orc_attn_prefill(_p(qkv), n_seq, L, Hq, Hkv, hd, cap, sink, scale, _p(out))
     return out
+
+
+# ---- 4-bit expert format (Q4T), restated from the reference quant.cpp ----
+# fit_minmax (quant.cpp, QuantConfig{4, 64}): s = (hi - lo) / 15 in fp32,
+# scale = fp16(s), zero = fp16(-lo / s); lo == hi -> (fp16(1), fp16(-lo)).
+# code_of: clamp(round_half_away(double(w) / scale + zero), 0, 15).
+# value_of: scale * (code - zero). Groups of 64 along K; Q4T stores the
+# groups of each 128-row x 64-column tile as [128 x 32 B codes (element 2i in
+# the low nibble of byte i) | 128 fp16 scales | 128 fp16 zeros].
+Q4_CHUNK = 128 * 32 + 128 * 4
+
+
+def q4_fit_minmax(groups_f32):
+    """groups [n, 64] float32 -> (scale f16 [n], zero f16 [n])."""
+    lo = groups_f32.min(axis=1)
+    hi = groups_f32.max(axis=1)
+    s = ((hi - lo).astype(np.float32) / np.float32(15.0)).astype(np.float32)
+    same = lo == hi
+    with np.errstate(divide="ignore", invalid="ignore"):
+        z = (-lo / np.where(same, np.float32(1.0), s)).astype(np.float32)
+    scale = np.where(same, np.float16(1.0), s.astype(np.float16))
+    zero = np.where(same, (-lo).astype(np.float16), z.astype(np.float16))
+    return scale.astype(np.float16), zero.astype(np.float16)
+
+
+def q4_codes(groups_f32, scale, zero):
+    x = groups_f32.astype(np.float64) / scale.astype(np.float64)[:, None] + zero.astype(np.float64)[:, None]
+    q = np.floor(x + 0.5)  # std::round (half away from zero) for x >= -0.5; clamped below anyway
+    return np.clip(q, 0, 15).astype(np.uint8)
+
+
+def q4_quantize_tiled(w_bits):
+    """bf16 bits [rows, K] -> Q4T bytes (min-max fit), the oracle of kl_quantize_q4."""
+    rows, K = w_bits.shape
+    KB = K // 64
+    g = bits_to_f32(np.ascontiguousarray(w_bits)).reshape(rows, KB, 64)
+    scale, zero = q4_fit_minmax(g.reshape(-1, 64))
+    codes = q4_codes(g.reshape(-1, 64), scale, zero).reshape(rows, KB, 64)
+    scale = scale.reshape(rows, KB)
+    zero = zero.reshape(rows, KB)
+    out = np.zeros(rows // 128 * KB * Q4_CHUNK, np.uint8)
+    packed = (codes[:, :, 0::2] | (codes[:, :, 1::2] << 4)).astype(np.uint8)  # [rows, KB, 32]
+    for rt in range(rows // 128):
+        for kb in range(KB):
+            base = (rt * KB + kb) * Q4_CHUNK
+            blk = slice(rt * 128, rt * 128 + 128)
+            out[base:base + 4096] = packed[blk, kb, :].reshape(-1)
+            out[base + 4096:base + 4352] = np.ascontiguousarray(scale[blk, kb]).view(np.uint8)
+            out[base + 4352:base + 4608] = np.ascontiguousarray(zero[blk, kb]).view(np.uint8)
+    return out
+
+
+def q4_dequantize_tiled(q, rows, K):
+    """Q4T -> float32 [rows, K] (value_of in fp32: one rounding of the exact product)."""
+    KB = K // 64
+    out = np.empty((rows, K), np.float32)
+    for rt in range(rows // 128):
+        for kb in range(KB):
+            base = (rt * KB + kb) * Q4_CHUNK
+            codes = q[base:base + 4096].reshape(128, 32)
+            c = np.empty((128, 64), np.float32)
+            c[:, 0::2] = codes & 15
+            c[:, 1::2] = codes >> 4
+            sc = np.ascontiguousarray(q[base + 4096:base + 4352]).view(np.float16).astype(np.float32)
+            zr = np.ascontiguousarray(q[base + 4352:base + 4608]).view(np.float16).astype(np.float32)
+            out[rt * 128:rt * 128 + 128, kb * 64:kb * 64 + 64] = (sc[:, None] * (c - zr[:, None])).astype(np.float32)
+    return out

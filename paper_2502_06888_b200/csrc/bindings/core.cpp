@@ -154,6 +154,28 @@ PYBIND11_MODULE(_core, m) {
         .def_readwrite("group_size", &QuantConfig::group_size)
         .def_readwrite("zero_scale_group_size", &QuantConfig::zero_scale_group_size);
     m.def("quantized_bytes", &quantized_bytes);
+    m.def("fit_minmax",
+          [](py::array_t<float, py::array::c_style | py::array::forcecast> g, int bits) {
+              const QuantParams p = fit_minmax(std::span<const float>(g.data(), static_cast<size_t>(g.size())), bits);
+              return py::make_tuple(p.scale, p.zero);
+          },
+          py::arg("group"), py::arg("bits") = 4);
+    m.def("dequantize",
+          [](py::array_t<std::uint8_t, py::array::c_style> packed, py::array_t<std::uint16_t, py::array::c_style> scales,
+             py::array_t<std::uint16_t, py::array::c_style> zeros, std::size_t n_elements, int bits, int group) {
+              QuantizedTensor q;
+              q.cfg.bits = bits;
+              q.cfg.group_size = group;
+              q.n_elements = n_elements;
+              q.packed.assign(packed.data(), packed.data() + packed.size());
+              q.scales_f16.assign(scales.data(), scales.data() + scales.size());
+              q.zeros_f16.assign(zeros.data(), zeros.data() + zeros.size());
+              const std::vector<float> v = dequantize(q);
+              return py::array_t<float>(static_cast<py::ssize_t>(v.size()), v.data());
+          },
+          py::arg("packed"), py::arg("scales_f16"), py::arg("zeros_f16"), py::arg("n_elements"), py::arg("bits") = 4,
+          py::arg("group_size") = 64,
+          "moesim::dequantize of a QuantizedTensor (flat little-endian code stream, per-group fp16 params)");
 
     py::class_<ActivationTrace>(m, "ActivationTrace")
         .def_readonly("n_steps", &ActivationTrace::n_steps)

@@ -294,7 +294,14 @@ struct StreamArgs {
     int hint;   // 1 = L2 cache-policy hints on the TMA loads
     int pdl;    // launched with programmatic stream serialization
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
+    const uint8_t* q4;  // Q4 variant: weights in the tiled 4-bit layout (kQ4Chunk bytes per 128x64 tile)
 };
+
+// 4-bit weights ("Q4T", the reference's HQQ format, quant.cpp:197-252, with
+// its groups of 64 laid out per 128-row x 64-column tile): per tile 128 rows
+// x 32 bytes of little-endian nibble codes, then 128 fp16 scales, then 128
+// fp16 zeros; w = scale * (code - zero). Tiles ordered (row tile, k-block).
+constexpr int kQ4Chunk = kWRows * 32 + kWRows * 2 * 2;  // 4608 bytes per 8192 weights
 
 __device__ unsigned long long g_stream_trace[256][12];  // debug & 128: per-CTA phase timestamps (ns)
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -338,7 +345,7 @@ __device__ __forceinline__ float epi_value(const float (&acc)[2][16], int j, int
     }
 }
 
-template <int EPI, int NMMA>
+template <int EPI, int NMMA, bool Q4>
 __global__ void __launch_bounds__(kStreamThreads, 1)
 gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x, int a_row0,
                    const StreamArgs p) {
@@ -346,12 +353,15 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
     const int ring_bytes = p.stages * stage_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring_bytes);
+    constexpr int kRawStage = NMMA * kQ4Chunk;
+    uint8_t* raw = smem + ring_bytes;  // Q4: packed tiles land here, dequantised into the ring
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + (Q4 ? p.stages * kRawStage : 0));
     uint64_t* empty = full + p.stages;
     uint64_t* acc_full = empty + p.stages;  // [2]
     uint64_t* acc_empty = acc_full + 2;     // [2]
     uint64_t* part_bar = acc_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(part_bar + 1);
+    uint64_t* raw_full = part_bar + 1;  // [stages] (Q4)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_full + p.stages);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -364,8 +374,9 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
         tma_prefetch_desc(&tmap_w);
         tma_prefetch_desc(&tmap_x);
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], Q4 ? 5 : 1);  // Q4: + one arrival per dequantising warp
             mbar_init(&empty[s], 1);
+            if (Q4) mbar_init(&raw_full[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -412,15 +423,20 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                     }
                     mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
                     uint8_t* sw = smem + s * stage_bytes;
-                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    mbar_arrive_expect_tx(&full[s], Q4 ? p.NP * BK * 2 : stage_bytes);
+                    if constexpr (Q4) mbar_arrive_expect_tx(&raw_full[s], kRawStage);
 #pragma unroll
                     for (int j = 0; j < NMMA; ++j) {
                         const int row = EPI == kSwiGLU ? (j == 0 ? t * kWRows : p.half_rows + t * kWRows)
                                                        : (t * NMMA + j) * kWRows;
-                        if (hint)
+                        if constexpr (Q4) {
+                            const uint8_t* src = p.q4 + (static_cast<int64_t>(row / kWRows) * KB + kb) * kQ4Chunk;
+                            bulk_g2s(raw + s * kRawStage + j * kQ4Chunk, src, kQ4Chunk, &raw_full[s]);
+                        } else if (hint) {
                             tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
-                        else
+                        } else {
                             tma_load_2d(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row);
+                        }
                     }
                     if (waited) {
                         load_x(s, kb);
@@ -476,10 +492,43 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
         const int nch = p.NP / 16;
         const int slot_f4 = NMMA * kWRows * (p.NP / 4);  // float4 per partial slot
         auto slot4 = [&](int q) { return reinterpret_cast<float4*>(p.ws) + static_cast<int64_t>(q) * slot_f4; };
-        int seg = 0;
+        int seg = 0, dq_it = 0;
         for (int t = t_hi; t >= t_lo; --t, ++seg) {
             const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
             const int b = p.nbuf == 2 ? (seg & 1) : 0, use = p.nbuf == 2 ? (seg >> 1) : seg;
+            if constexpr (Q4) {
+                // Dequantise this segment's stages into the bf16 ring (thread = weight row),
+                // written in the 128B-swizzled K-major layout the MMA descriptors expect.
+                for (int kb = kb0; kb < kb1; ++kb, ++dq_it) {
+                    const int s = dq_it % p.stages;
+                    mbar_wait(&raw_full[s], (dq_it / p.stages) & 1);
+#pragma unroll
+                    for (int j = 0; j < NMMA; ++j) {
+                        const uint8_t* rc = raw + s * kRawStage + j * kQ4Chunk;
+                        const uint4 c0 = *reinterpret_cast<const uint4*>(rc + frow * 32);
+                        const uint4 c1 = *reinterpret_cast<const uint4*>(rc + frow * 32 + 16);
+                        const float sc = __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(rc + kWRows * 32 + frow * 2)));
+                        const float zr = __half2float(
+                            __ushort_as_half(*reinterpret_cast<const uint16_t*>(rc + kWRows * 32 + kWRows * 2 + frow * 2)));
+                        const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                        uint8_t* wrow = smem + s * stage_bytes + j * kWTileBytes + frow * 128;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float lo = __fmul_rn(sc, __fsub_rn(static_cast<float>((cw[u] >> (8 * e)) & 15u), zr));
+                                const float hi = __fmul_rn(sc, __fsub_rn(static_cast<float>((cw[u] >> (8 * e + 4)) & 15u), zr));
+                                pk[e] = pack2(lo, hi);
+                            }
+                            *reinterpret_cast<uint4*>(wrow + ((u ^ (frow & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[s]);
+                }
+            }
             mbar_wait(&acc_full[b], use & 1);
             tc_fence_after();
             const uint32_t acc0 = tmem_base + lane_off + b * buf_cols;
@@ -542,6 +591,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 if (kb0 > 0) {
                     int c_lo = cta - 1;
                     while (c_lo > 0 && range_begin(c_lo, p.units, G) > t * KB) --c_lo;
+                    if (slot_f4 * 16 <= ring_bytes) {
                     const int slot_bytes = slot_f4 * 16;
                     const int per_batch = max(1, ring_bytes / slot_bytes);
                     int phase = 0;
@@ -585,6 +635,63 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                             }
                         named_bar_sync(1, 128);  // landing buffer free before the next batch
                     }
+                                    } else {
+                    // Contributors' partials land in the idle ring in 8 KB units
+                    // (one accumulator x 16 columns each), as many per batch as fit,
+                    // ordered (accumulator, column chunk, contributor): each
+                    // element adds its partials in ascending CTA order with one
+                    // TMEM load/store per run of units on the same columns.
+                    constexpr int kUnitF4 = 4 * kWRows;
+                    constexpr int kUnitBytes = kUnitF4 * 16;
+                    const int nu = cols / 16, nq = cta - c_lo;
+                    const int total = NMMA * nu * nq;
+                    const int per_batch = max(1, ring_bytes / kUnitBytes);
+                    if (etid == 0) {
+                        for (int q = c_lo; q < cta; ++q)
+                            while (ld_relaxed_gpu(p.flags + q) != p.epoch) {
+                            }
+                        fence_acq_rel_gpu();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    int phase = 0;
+                    for (int w0 = 0; w0 < total; w0 += per_batch, phase ^= 1) {
+                        const int nw = min(per_batch, total - w0);
+                        if (etid == 0) {
+                            mbar_arrive_expect_tx(part_bar, static_cast<uint32_t>(nw * kUnitBytes));
+                            for (int w = w0; w < w0 + nw; ++w) {
+                                const int jc = w / nq, q = c_lo + w % nq;
+                                bulk_g2s(smem + (w - w0) * kUnitBytes, slot4(q) + static_cast<int64_t>((jc / nu) * nch + jc % nu) * kUnitF4,
+                                         kUnitBytes, part_bar);
+                            }
+                        }
+                        if (etid == 0) STREAM_TRACE(4);
+                        mbar_wait(part_bar, phase);
+                        if (etid == 0) STREAM_TRACE(5);
+                        const float4* land = reinterpret_cast<const float4*>(smem);
+                        float v[16];
+                        int cur = -1;
+                        for (int w = w0; w < w0 + nw; ++w) {
+                            const int jc = w / nq;
+                            const uint32_t taddr = acc0 + (jc / nu) * p.acc_stride + (jc % nu) * 16;
+                            if (jc != cur) {
+                                if (cur >= 0) tmem_st16(acc0 + (cur / nu) * p.acc_stride + (cur % nu) * 16, v);
+                                tmem_ld16(taddr, v);
+                                cur = jc;
+                            }
+                            const float4* src = land + static_cast<int64_t>(w - w0) * kUnitF4 + frow;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 x4 = src[i * kWRows];
+                                v[4 * i] += x4.x;
+                                v[4 * i + 1] += x4.y;
+                                v[4 * i + 2] += x4.z;
+                                v[4 * i + 3] += x4.w;
+                            }
+                        }
+                        tmem_st16(acc0 + (cur / nu) * p.acc_stride + (cur % nu) * 16, v);
+                        named_bar_sync(1, 128);  // landing buffer free before the next batch
+                    }
+                                    }
                 }
                 if (etid == 0) STREAM_TRACE(6);
                 // Stage bf16 outputs [token][128 features] in smem, then
@@ -721,7 +828,7 @@ uint32_t next_epoch() {
 }
 
 constexpr int64_t kFlagBytes = 1024;  // [<= 256 CTAs] uint32 publish epochs
-constexpr int kStreamSmemBudget = 227 * 1024 - 1024 - 256;
+constexpr int kStreamSmemBudget = 227 * 1024 - 2048;  // + 1 KB alignment + 1 KB barriers
 
 int pow2ceil(int v) {
     int p = 1;
@@ -750,10 +857,10 @@ int stream_grid(int N, int K, int epilogue) {
     return std::max(1, std::min(sm_count() * g_stream_ctas, units / 4));
 }
 
-template <int EPI, int NMMA>
+template <int EPI, int NMMA, bool Q4 = false>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
                   int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, const uint8_t* q4 = nullptr) {
     StreamArgs p{};
     p.M = M;
     p.NP = stream_np(M);
@@ -763,14 +870,12 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.KB = K / BK;
     p.units = n_tiles * p.KB;
     const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
-    p.stages = std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / stage_bytes);
+    const int per_stage = stage_bytes + (Q4 ? NMMA * kQ4Chunk : 0);
+    p.stages = std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / per_stage);
     if (p.stages < 2 || p.tmem_cols * g_stream_ctas > 512) return KL_EUNSUPPORTED;
-    // The idle ring doubles as the landing buffer for one partial slot and
-    // as the bf16 output staging tile of the last segment.
-    if (p.stages * stage_bytes < std::max<int64_t>(stream_slot_bytes(M, NMMA), static_cast<int64_t>(p.NP) * kWRows * 2))
-        p.stages = static_cast<int>((std::max<int64_t>(stream_slot_bytes(M, NMMA), static_cast<int64_t>(p.NP) * kWRows * 2) +
-                                     stage_bytes - 1) / stage_bytes);
-    if (p.stages * stage_bytes > kStreamSmemBudget / g_stream_ctas) return KL_EUNSUPPORTED;
+    // The idle ring doubles as the landing buffer of split partials (8 KB
+    // units) and as the bf16 output staging tile of the last segment.
+    if (p.stages * stage_bytes < p.NP * kWRows * 2) return KL_EUNSUPPORTED;
     p.hint = g_stream_hint;
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
@@ -786,16 +891,19 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.flags = static_cast<uint32_t*>(ws);
     p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + kFlagBytes);
     p.epoch = next_epoch();
+    p.q4 = q4;
     CUtensorMap mw, mx;
-    int rc = (p.debug & 64) ? make_map(&mw, b, b_rows * K / BK, BK, kWRows) : make_map(&mw, b, b_rows, K, kWRows);
+    int rc = make_map(&mx, a, a_rows, K, p.NP);
     if (rc) return rc;
-    rc = make_map(&mx, a, a_rows, K, p.NP);
-    if (rc) return rc;
-    const int smem = p.stages * stage_bytes + 1024 + 256;  // ring + alignment + barriers
+    if (Q4)
+        mw = mx;  // unused: the Q4 variant bulk-copies packed tiles
+    else if ((rc = make_map(&mw, b, b_rows, K, kWRows)))
+        return rc;
+    const int smem = p.stages * per_stage + 1024 + 1024;  // rings + alignment + barriers
     static bool configured = false;  // per template instance
     if (!configured) {
-        KL_CUDA_TRY(cudaFuncSetAttribute(gemm_stream_kernel<EPI, NMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kStreamSmemBudget + 1024 + 256));
+        KL_CUDA_TRY(cudaFuncSetAttribute(gemm_stream_kernel<EPI, NMMA, Q4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kStreamSmemBudget + 2048));
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -808,7 +916,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = p.pdl ? 1 : 0;
-    KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_stream_kernel<EPI, NMMA>, mw, mx, static_cast<int>(row_offset), p));
+    KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_stream_kernel<EPI, NMMA, Q4>, mw, mx, static_cast<int>(row_offset), p));
     return check_launch();
 }
 
@@ -934,6 +1042,51 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
     }
     L.n_tiles = N / 64;
     return epilogue == kResidual ? launch<64, kResidual, false, 6>(L, stream) : launch<64, kStore, false, 6>(L, stream);
+}
+
+extern "C" int kl_gemm_q4(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint8_t* bq,
+                          int N, uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace,
+                          int64_t workspace_bytes, cudaStream_t stream) {
+    using namespace kl;
+    if (M < 0 || K <= 0 || N <= 0 || a == nullptr || bq == nullptr || c == nullptr) return KL_EINVAL;
+    if (M == 0) return KL_OK;
+    if (M > 256) return KL_EUNSUPPORTED;  // large M: kl_dequantize_q4 + kl_gemm_bf16
+    if (K % BK != 0 || N % kWRows != 0 || (epilogue == kSwiGLU && (N / 2) % kWRows != 0) || ldc % 8 != 0)
+        return KL_EINVAL;
+    if (epilogue < 0 || epilogue > 2 || (epilogue == kResidual && r == nullptr)) return KL_EINVAL;
+    if (row_offset < 0 || row_offset + M > a_rows || workspace == nullptr ||
+        workspace_bytes < kFlagBytes + stream_slot_bytes(M, epilogue == kSwiGLU ? 2 : 1))
+        return KL_EINVAL;
+    // NMMA = 1 for plain GEMMs (fewest split contributors), the gate/up pair for SwiGLU.
+    if (epilogue == kSwiGLU)
+        return launch_stream<kSwiGLU, 2, true>(a, a_rows, row_offset, M, K, nullptr, N, N / 2 / kWRows, N / 2, c, ldc,
+                                               r, workspace, workspace_bytes, stream, bq);
+    if (epilogue == kResidual)
+        return launch_stream<kResidual, 1, true>(a, a_rows, row_offset, M, K, nullptr, N, N / kWRows, 0, c, ldc, r,
+                                                 workspace, workspace_bytes, stream, bq);
+    return launch_stream<kStore, 1, true>(a, a_rows, row_offset, M, K, nullptr, N, N / kWRows, 0, c, ldc, r, workspace,
+                                          workspace_bytes, stream, bq);
+}
+
+extern "C" int64_t kl_gemm_q4_workspace_bytes(int M, int N, int K, int epilogue) {
+    using namespace kl;
+    if (M <= 0 || M > 256 || N <= 0 || K <= 0) return 0;
+    const int nmma = epilogue == kSwiGLU ? 2 : 1;
+    const int n_tiles = epilogue == kSwiGLU ? N / 2 / kWRows : N / kWRows;
+    const int G = std::max(1, std::min(sm_count(), n_tiles * (K / BK) / 4));
+    return kFlagBytes + static_cast<int64_t>(G) * stream_slot_bytes(M, nmma);
+}
+
+extern "C" int kl_expert_ffn_q4(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d, int f,
+                                const uint8_t* w13q, const uint8_t* w2q, uint16_t* h_scratch, uint16_t* y,
+                                void* workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    if (M == 0) return KL_OK;
+    if (y == nullptr || h_scratch == nullptr) return KL_EINVAL;
+    int rc = kl_gemm_q4(xp, rows_total, row_offset, M, d, w13q, 2 * f, h_scratch, f, nullptr, 2, workspace,
+                        workspace_bytes, stream);
+    if (rc) return rc;
+    return kl_gemm_q4(h_scratch, M, 0, M, f, w2q, d, y + row_offset * d, d, nullptr, 0, workspace, workspace_bytes,
+                      stream);
 }
 
 extern "C" int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d, int f,

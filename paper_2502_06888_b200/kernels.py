@@ -45,6 +45,12 @@ _dec_ws = _sig("kl_attn_decode_ws", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I,
 _pre = _sig("kl_attn_prefill", [_P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P])
 _fill = _sig("kl_fill_normal_bf16", [_P, _L, _U64, _F, _P])
 _tune = _sig("kl_tune", [_I, _I])
+_q4_bytes = _sig("kl_q4_bytes", [_L, _L], C.c_int64)
+_q4_quant = _sig("kl_quantize_q4", [_P, _L, _L, _P, _P])
+_q4_dequant = _sig("kl_dequantize_q4", [_P, _L, _L, _P, _P])
+_q4_ws = _sig("kl_gemm_q4_workspace_bytes", [_I, _I, _I, _I], C.c_int64)
+_q4_gemm = _sig("kl_gemm_q4", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P, _L, _P])
+_q4_ffn = _sig("kl_expert_ffn_q4", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P, _L, _P])
 abi_version = _sig("kl_abi_version", [])
 
 TUNE_STREAM_GEMM = 0  # weight-streaming decode GEMM path on/off
@@ -122,6 +128,45 @@ def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None, split_k=Tr
     ws = workspace(wsb, xp.device) if wsb else None
     _chk(_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _p(ws), wsb,
               _s(stream)), "kl_expert_ffn")
+
+
+def q4_bytes(rows, K):
+    return int(_q4_bytes(rows, K))
+
+
+def quantize_q4(w, stream=None):
+    """bf16 [rows, K] -> Q4T bytes (uint8 tensor), min-max fit per group of 64."""
+    rows, K = w.shape
+    out = torch.empty(q4_bytes(rows, K), dtype=torch.uint8, device=w.device)
+    _chk(_q4_quant(_p(w), rows, K, _p(out), _s(stream)), "kl_quantize_q4")
+    return out
+
+
+def dequantize_q4(q, rows, K, stream=None):
+    out = torch.empty(rows, K, dtype=torch.bfloat16, device=q.device)
+    _chk(_q4_dequant(_p(q), rows, K, _p(out), _s(stream)), "kl_dequantize_q4")
+    return out
+
+
+def gemm_q4(a, bq, N, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None):
+    """C = A[row_offset:row_offset+m] @ dequant(Bq)^T with the dequant fused into the GEMM producer."""
+    m = a.shape[0] - row_offset if m is None else m
+    K = a.shape[1]
+    n_out = N // 2 if epilogue == 2 else N
+    if c is None:
+        c = torch.empty(m, n_out, dtype=torch.bfloat16, device=a.device)
+    wsb = int(_q4_ws(m, N, K, epilogue))
+    ws = workspace(wsb, a.device)
+    _chk(_q4_gemm(_p(a), a.shape[0], row_offset, m, K, _p(bq), N, _p(c), c.stride(0), _p(residual), epilogue, _p(ws),
+                  wsb, _s(stream)), "kl_gemm_q4")
+    return c
+
+
+def expert_ffn_q4(xp, row_offset, m, w13q, w2q, d, f, y, h_scratch, stream=None):
+    wsb = max(int(_q4_ws(m, 2 * f, d, 2)), int(_q4_ws(m, d, f, 0)))
+    ws = workspace(wsb, xp.device)
+    _chk(_q4_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13q), _p(w2q), _p(h_scratch), _p(y), _p(ws), wsb,
+                 _s(stream)), "kl_expert_ffn_q4")
 
 
 def gate_topk(h, norm_w, wg, k, eps=1e-5, score_mode=0, x2=None, logits=None, hist=None, first_pos=None,

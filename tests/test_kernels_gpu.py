@@ -346,3 +346,66 @@ def test_fill_normal_matches_oracle(K, cuda):
     # Irwin-Hall stream with exact fp32 arithmetic: bit-identical to the CPU.
     assert np.array_equal(to_bits(t), orc.normal_bf16(t.numel(), 1234, 0.02))
     assert abs(orc.bits_to_f32(to_bits(t)).std() - 0.02) < 1e-3
+
+
+# ---- 4-bit expert streaming (Q4T) ----
+def test_q4_quantize_dequantize_bit_exact(K, cuda):
+    rows, Kd = 256, 448
+    w = orc.normal_bf16(rows * Kd, 81, 0.02).reshape(rows, Kd)
+    w[5, :64] = w[5, 0]  # constant group
+    q = K.quantize_q4(to_dev(w, cuda))
+    torch.cuda.synchronize()
+    ref = orc.q4_quantize_tiled(w)
+    assert np.array_equal(q.cpu().numpy(), ref)
+    deq = K.dequantize_q4(q, rows, Kd)
+    torch.cuda.synchronize()
+    ref_deq = orc.bf16_bits(orc.q4_dequantize_tiled(ref, rows, Kd))
+    assert np.array_equal(to_bits(deq), ref_deq)
+
+
+@pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (64, 6144, 4096, 0), (130, 1024, 2048, 1),
+                                        (200, 3584, 1024, 2), (256, 512, 8192, 0)])
+def test_gemm_q4_fused_dequant(K, cuda, M, N, Kd, epi):
+    """Dequant fused into the weight-streaming GEMM's producer equals a GEMM
+    on the dequantised weights (within the GEMM tolerance), deterministic."""
+    rows, off = M + 24, 9
+    a = orc.normal_bf16(rows * Kd, 82, 1.0).reshape(rows, Kd)
+    w = orc.normal_bf16(N * Kd, 83, 0.03).reshape(N, Kd)
+    qd = K.quantize_q4(to_dev(w, cuda))
+    torch.cuda.synchronize()
+    wd = orc.bf16_bits(orc.q4_dequantize_tiled(qd.cpu().numpy(), N, Kd))
+    n_out = N // 2 if epi == 2 else N
+    r = orc.normal_bf16(M * n_out, 84, 1.0).reshape(M, n_out) if epi == 1 else None
+    rd = to_dev(r, cuda) if r is not None else None
+    ad = to_dev(a, cuda)
+    c = K.gemm_q4(ad, qd, N, residual=rd, epilogue=epi, row_offset=off, m=M)
+    c2 = K.gemm_q4(ad, qd, N, residual=rd, epilogue=epi, row_offset=off, m=M)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)
+    x = np.ascontiguousarray(a[off:off + M])
+    if epi == 2:
+        g = orc.gemm_f32(x, np.ascontiguousarray(wd[:n_out])).astype(np.float64)
+        u = orc.gemm_f32(x, np.ascontiguousarray(wd[n_out:])).astype(np.float64)
+        ref = g / (1.0 + np.exp(-g)) * u
+    else:
+        ref = orc.gemm_f32(x, wd) + (orc.bits_to_f32(r) if epi == 1 else 0)
+    close_bf16(to_bits(c), ref)
+
+
+def test_expert_ffn_q4(K, cuda):
+    M, d, f = 150, 1024, 2048
+    rows, off = M + 30, 11
+    x = orc.normal_bf16(rows * d, 85, 1.0).reshape(rows, d)
+    w13 = orc.normal_bf16(2 * f * d, 86, 0.03).reshape(2 * f, d)
+    w2 = orc.normal_bf16(d * f, 87, 0.03).reshape(d, f)
+    q13 = K.quantize_q4(to_dev(w13, cuda))
+    q2 = K.quantize_q4(to_dev(w2, cuda))
+    y = torch.zeros(rows, d, dtype=torch.bfloat16, device=cuda)
+    h = torch.empty(M, f, dtype=torch.bfloat16, device=cuda)
+    K.expert_ffn_q4(to_dev(x, cuda), off, M, q13, q2, d, f, y, h)
+    torch.cuda.synchronize()
+    d13 = orc.bf16_bits(orc.q4_dequantize_tiled(q13.cpu().numpy(), 2 * f, d))
+    d2 = orc.bf16_bits(orc.q4_dequantize_tiled(q2.cpu().numpy(), d, f))
+    ref = orc.bits_to_f32(orc.expert_ffn(np.ascontiguousarray(x[off:off + M]), d13, d2))
+    close_bf16(to_bits(y)[off:off + M], ref)
+    assert not to_bits(y)[:off].any() and not to_bits(y)[off + M:].any()
