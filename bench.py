@@ -143,7 +143,96 @@ def engine_config(args, rank, world, ep_id=None):
     }
     if ep_id is not None:
         cfg["ep"] = {"rank": rank, "world": world, "nccl_id": ep_id}
+    if getattr(args, "quant_bits", 0):
+        cfg["quant"] = {"bits": args.quant_bits}
     return cfg
+
+
+def measured_tflops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops", 1590.0), "measured"
+    except (OSError, ValueError):
+        return 1590.0, "fallback"
+
+
+def prefill_variant(args, link):
+    """BASELINE configs[2]: prefill of a batch group (bs 8 x n 8 x 512-token
+    prompts = 32,768 tokens) through all layers under the same HBM cap, experts
+    streamed; one warm-up pass then one timed pass. Reports prefill tokens/s,
+    the pipeline bubble fraction and the expert GEMMs' tensor-pipe rate
+    (FLOPs / measured compute time) against the bf16 peak."""
+    from paper_2502_06888_b200.engine import Engine
+    import numpy as np
+    bs, n, P = 8, 8, args.prompt_len
+    cfg = {"model": {"preset": args.model},
+           "workload": {"batch_size": bs, "n_batches": n, "prompt_len": P, "gen_len": 2},
+           "hbm_cap_bytes": int(args.hbm_cap),
+           "kv_retention": {"mode": "streaming", "sink_tokens": 4, "window_tokens": 256},
+           "routing": "gate", "prefill": True, "record_trace": False, "host_distinct_layers": 4}
+    eng = Engine(cfg)
+    prompt = np.random.default_rng(0).integers(0, eng.info["dims"]["V"], eng.n_seqs * P, dtype=np.int32)
+    eng.step(0, prompt)
+    eng.reset_log()
+    _, ms = eng.step(0, prompt)
+    m = eng.report("metrics")
+    D = eng.info["dims"]
+    flops = 2.0 * 3 * D["d"] * D["f"] * m["expert_rows"]
+    t_exp = m["compute_ps_by_kind"]["expert"] * 1e-12
+    peak, kind = measured_tflops()
+    tf = flops / t_exp / 1e12 if t_exp > 0 else 0.0
+    out = {"config": f"{args.model} prefill, batch {bs} x n={n} x {P} tokens, HBM cap {args.hbm_cap:.3g} B",
+           "value": eng.n_seqs * P / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+           "bubble_fraction": m["bubble_fraction"], "bubbles_ps": m["bubbles_ps"],
+           "compute_ms_by_kind": {k: v / 1e9 for k, v in m["compute_ps_by_kind"].items()},
+           "h2d_gb_per_step": m["h2d_bytes"] / 1e9, "h2d_frac_of_link_peak": m["h2d_gbs_busy"] / link,
+           "expert_gemm_tflops": tf, "tensor_peak_tflops": peak, "tensor_peak_kind": kind,
+           "expert_gemm_tensor_frac": tf / peak,
+           "resident_expert_layers": eng.info["resident_expert_layers"]}
+    eng.close()
+    return out
+
+
+def q4_variant(args, link):
+    """Same decode workload with 4-bit streamed experts/attention (Q4T, the
+    reference's QuantConfig{4, 64}): the link moves 0.28125x
+    the bytes and the dequantisation runs inside the GEMM producer. A second
+    engine after the bf16 one is closed; reported beside the headline."""
+    from paper_2502_06888_b200.engine import Engine
+    a = argparse.Namespace(**vars(args))
+    a.quant_bits = 4
+    t0 = time.perf_counter()
+    eng = Engine(engine_config(a, 0, 1))
+    eng.fill_kv_synthetic(args.prompt_len)
+    setup = time.perf_counter() - t0
+    step = 1
+    for _ in range(args.warmup):
+        eng.step(step, None, want_next=False)
+        step += 1
+    eng.reset_log()
+    ms = []
+    for _ in range(args.steps):
+        _, t = eng.step(step, None, want_next=False)
+        ms.append(t)
+        step += 1
+    m = eng.report("metrics")
+    seqs = eng.n_seqs
+    n_ops = max(m["expert_ops"], 1)
+    D = eng.info["dims"]
+    out = {
+        "value": args.steps * seqs / (sum(ms) / 1e3), "unit": "tokens/s", "ms_per_step": sum(ms) / args.steps,
+        "quant": "Q4T 4-bit, group 64, fp16 scale/zero (reference QuantConfig{4,64})",
+        "expert_stream_bytes": eng.info["expert_stream_bytes"],
+        "h2d_gb_per_step": m["h2d_bytes"] / args.steps / 1e9, "h2d_gbs_link_busy": m["h2d_gbs_busy"],
+        "h2d_frac_of_link_peak": m["h2d_gbs_busy"] / link, "bubble_fraction": m["bubble_fraction"],
+        "resident_expert_layers": eng.info["resident_expert_layers"],
+        "expert_ffn_us_per_op": m["compute_ps_by_kind"]["expert"] / n_ops / 1e6,
+        "expert_ffn_q4_bytes_per_op": eng.info["expert_stream_bytes"] + m["expert_rows"] / n_ops * (2 * D["d"] * 2 + 2 * D["f"] * 2),
+        "setup_s": setup,
+    }
+    eng.close()
+    return out
 
 
 def cpu_baseline(args, warmup=0, repeats=1):
@@ -270,6 +359,23 @@ def run_ours(args):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_op")
 
+    info = dict(eng.info)
+    n_batches = eng.n_batches
+    eng.close()
+    eng = None
+    prefill = None
+    if world == 1 and not args.no_prefill:
+        try:
+            prefill = prefill_variant(args, link)
+        except Exception as ex:  # reported, not fatal
+            prefill = {"error": str(ex)[:300]}
+    q4 = None
+    if world == 1 and not args.no_q4:
+        try:
+            q4 = q4_variant(args, link)
+        except Exception as ex:  # reported, not fatal
+            q4 = {"error": str(ex)[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -295,13 +401,13 @@ def run_ours(args):
             "data": "synthetic (random-init bf16 weights of the Mixtral-8x7B architecture, random token ids, "
                     "synthetic prefilled KV of 512 positions)",
             "config": {
-                "workload": f"{args.model} bf16 decode, batch {args.batch_size} x n={eng.n_batches}, "
+                "workload": f"{args.model} bf16 decode, batch {args.batch_size} x n={n_batches}, "
                             f"HBM cap {args.hbm_cap:.3g} B, experts streamed from pinned host",
-                "model": args.model, "batch_size": args.batch_size, "n_batches": eng.n_batches,
+                "model": args.model, "batch_size": args.batch_size, "n_batches": n_batches,
                 "prompt_len": args.prompt_len, "kv_retention": "streaming sink 4 + window 256",
-                "hbm_cap_bytes": int(args.hbm_cap), "expert_slots": eng.info["expert_slots"],
-                "resident_expert_layers": eng.info["resident_expert_layers"],
-                "resident_attention_layers": eng.info["resident_attention_layers"],
+                "hbm_cap_bytes": int(args.hbm_cap), "expert_slots": info["expert_slots"],
+                "resident_expert_layers": info["resident_expert_layers"],
+                "resident_attention_layers": info["resident_attention_layers"],
                 "parallelism": (f"ep{world} (expert shards, NCCL all-to-all)" if use_ep else
                                 f"replicas x{world}") if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (each step streams the experts of every layer)",
@@ -333,9 +439,10 @@ def run_ours(args):
             },
             "setup_s": setup_s,
             "wall_s_timed": wall,
+            "q4": q4,
+            "prefill": prefill,
         }
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
@@ -354,6 +461,9 @@ def main():
     ap.add_argument("--hbm-cap", type=float, default=24e9)
     ap.add_argument("--host-distinct-layers", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-q4", action="store_true", help="skip the 4-bit streamed-expert variant")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the prefill (configs[2]) measurement")
+    ap.add_argument("--quant-bits", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicas"],
                     help="N>1: expert-parallel shards (default) or independent replicas")
     ap.add_argument("--ep1", action="store_true", help="run the EP engine path even at N=1 (one shard)")

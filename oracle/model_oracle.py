@@ -33,8 +33,16 @@ def tensor_seed(base, kind, layer, expert):
     return mix64(base, ((kind << 48) ^ (layer << 16) ^ (expert + 1)) & M64)
 
 
+def q4_roundtrip(w_bits):
+    """bf16 weights as the engine streams them in Q4T mode: quantised on the
+    GPU (kl_quantize_q4 = pyoracle.q4_quantize_tiled, bit-exact) and expanded
+    back to bf16 by the fused-dequant GEMM (= q4_dequantize_tiled)."""
+    rows, K = w_bits.shape
+    return orc.bf16_bits(orc.q4_dequantize_tiled(orc.q4_quantize_tiled(w_bits), rows, K))
+
+
 class TinyModel:
-    def __init__(self, dims, weight_seed=7):
+    def __init__(self, dims, weight_seed=7, q4_expert_layers=(), q4_attention_layers=()):
         self.D = D = dims
         self.seed = weight_seed
         d, f, E = D["d"], D["f"], D["E"]
@@ -49,10 +57,16 @@ class TinyModel:
             experts = []
             for e in range(E):
                 w = orc.normal_bf16(3 * d * f, tensor_seed(weight_seed, KIND_EXPERT, l, e), 0.02)
-                experts.append((w[: 2 * f * d].reshape(2 * f, d), w[2 * f * d:].reshape(d, f)))
+                w13, w2 = w[: 2 * f * d].reshape(2 * f, d), w[2 * f * d:].reshape(d, f)
+                if l in q4_expert_layers:
+                    w13, w2 = q4_roundtrip(w13), q4_roundtrip(w2)
+                experts.append((w13, w2))
+            wqkv, wo = a[: self.qkvw * d].reshape(self.qkvw, d), a[self.qkvw * d:].reshape(d, D["Hq"] * D["hd"])
+            if l in q4_attention_layers:
+                wqkv, wo = q4_roundtrip(wqkv), q4_roundtrip(wo)
             self.layers.append({
-                "wqkv": a[: self.qkvw * d].reshape(self.qkvw, d),
-                "wo": a[self.qkvw * d:].reshape(d, D["Hq"] * D["hd"]),
+                "wqkv": wqkv,
+                "wo": wo,
                 "wg": orc.normal_bf16(E * d, tensor_seed(weight_seed, KIND_GATE, l, 0), 0.02).reshape(E, d),
                 "experts": experts,
             })

@@ -129,6 +129,15 @@ EngineConfig parse_config(const std::string& text) {
         if (j.value("routing", "gate") != "gate") throw ConfigError("engine EP: routing must come from the gate");
     }
     c.prefill = j.value("prefill", true);
+    if (j.contains("quant") && !j["quant"].is_null()) {
+        moesim::QuantConfig q;
+        q.bits = j["quant"].value("bits", 4);
+        q.group_size = j["quant"].value("group_size", 64);
+        if (q.bits != 4 || q.group_size != 64)
+            throw ConfigError("engine: only 4-bit, group-64 expert streaming (Q4T) is executed");
+        c.quant = q;
+        if (c.ep) throw ConfigError("engine: quantised streaming is not combined with expert parallelism yet");
+    }
     D.qkv_width();
     if (D.d % 256 || D.hd % 2 || D.Hq % D.Hkv || D.k > D.E || D.k > 8 || D.E > 64)
         throw ConfigError("engine: unsupported model dimensions");
@@ -237,7 +246,12 @@ void Engine::plan_memory() {
     table0_ = build_table(wt, spec_g_);
     const TraceStats stats = compute_trace_stats(wt, D_.k);
 
-    int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, std::nullopt,
+    // Streamed tensors travel as Q4T when quantised (= the planner's
+    // quantized_bytes, model_cost.cpp on_wire); resident ones stay bf16.
+    expert_slot_bytes_ = cfg_.quant ? kl_q4_bytes(2LL * D_.f, D_.d) + kl_q4_bytes(D_.d, D_.f) : spec_.expert_bytes;
+    attn_slot_bytes_ = cfg_.quant ? kl_q4_bytes(D_.qkv_width(), D_.d) + kl_q4_bytes(D_.d, static_cast<int64_t>(D_.Hq) * D_.hd)
+                                  : spec_.attention_bytes;
+    int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, cfg_.quant,
                                                            ExpertLoadModel::measured, cfg_.retention)
                                                      .n_batches;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -251,9 +265,10 @@ void Engine::plan_memory() {
         const int64_t chunk = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1));
         byte_count ws = 0;
         auto add = [&](byte_count b) { ws += ((b + 1023) / 1024) * 1024; };
-        add(2 * spec_.attention_bytes);
+        add(2 * attn_slot_bytes_);
+        if (cfg_.quant) add(std::max(spec_.expert_bytes, spec_.attention_bytes));  // bf16 staging / dequant scratch
         add(2 * spec_.gate_bytes);
-        for (int s = 0; s < slots_; ++s) add(spec_.expert_bytes);
+        for (int s = 0; s < slots_; ++s) add(expert_slot_bytes_);
         add(static_cast<byte_count>(D_.L) * 2 * D_.d * 2 + D_.d * 2);
         add(2LL * D_.V * D_.d * 2);
         add(2 * t_max_ * D_.d * 2);                                              // h, x2
@@ -277,6 +292,11 @@ void Engine::plan_memory() {
                                        kl_gemm_workspace_bytes(mi, D_.qkv_width(), D_.d, 0),
                                        kl_gemm_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1),
                                        kl_gemm_workspace_bytes(mi, D_.V, D_.d, 0)});
+            if (cfg_.quant)
+                gemm_ws_bytes_ = std::max({gemm_ws_bytes_, kl_gemm_q4_workspace_bytes(mi, 2 * D_.f, D_.d, 2),
+                                           kl_gemm_q4_workspace_bytes(mi, D_.d, D_.f, 0),
+                                           kl_gemm_q4_workspace_bytes(mi, D_.qkv_width(), D_.d, 0),
+                                           kl_gemm_q4_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1)});
         }
         // Decode attention partials (split-KV) share the same scratch.
         gemm_ws_bytes_ = std::max(gemm_ws_bytes_,
@@ -294,7 +314,7 @@ void Engine::plan_memory() {
         ws_bytes_ = ws;
         PlacementConfig pc;
         pc.working_set_override = ws;
-        plan_ = make_plan(spec_, profile_, w, stats, std::nullopt, ExpertLoadModel::measured, cfg_.retention, n, pc);
+        plan_ = make_plan(spec_, profile_, w, stats, cfg_.quant, ExpertLoadModel::measured, cfg_.retention, n, pc);
         if (plan_.n_batches == n) break;
         n = plan_.n_batches;  // KV-capped: resize scratch for the capped n
     }
@@ -318,14 +338,17 @@ void Engine::allocate_device() {
     auto bf = [&](int64_t elems) { return static_cast<uint16_t*>(take(elems * 2)); };
     auto i32 = [&](int64_t elems) { return static_cast<int32_t*>(take(elems * 4)); };
 
-    attn_slot_ = {bf(D_.attention_elems()), bf(D_.attention_elems())};
+    if (plan_.cost.expert_transfer_bytes != expert_slot_bytes_ || plan_.cost.attention_transfer_bytes != attn_slot_bytes_)
+        throw AccountingError("engine: streamed tensor bytes disagree with the plan's transfer bytes");
+    attn_slot_ = {bf(attn_slot_bytes_ / 2), bf(attn_slot_bytes_ / 2)};
+    if (cfg_.quant) wscratch_ = bf(std::max(D_.expert_elems(), D_.attention_elems()));
     gate_slot_ = {bf(D_.gate_elems()), bf(D_.gate_elems())};
     attn_slot_busy_.assign(2, 0);
     gate_slot_busy_.assign(2, 0);
     attn_slot_release_.assign(2, nullptr);
     gate_slot_release_.assign(2, nullptr);
     pool_.ptr.clear();
-    for (int s = 0; s < slots_; ++s) pool_.ptr.push_back(bf(D_.expert_elems()));
+    for (int s = 0; s < slots_; ++s) pool_.ptr.push_back(bf(expert_slot_bytes_ / 2));
     pool_.release.assign(slots_, nullptr);
     pool_.has_release.assign(slots_, 0);
     pool_.free_fifo.clear();
@@ -426,7 +449,7 @@ void Engine::allocate_host() {
                                                 : static_cast<int>(streamed.size());
     std::vector<void*> blocks(R, nullptr);
     std::vector<cudaError_t> errs(R, cudaSuccess);
-    const byte_count layer_bytes = spec_.expert_bytes * E;
+    const byte_count layer_bytes = expert_slot_bytes_ * E;
     {
         // Pinning is CPU-bound page work: spread it over host threads.
         std::vector<std::thread> th;
@@ -445,7 +468,7 @@ void Engine::allocate_host() {
     for (size_t s = 0; s < streamed.size(); ++s) {
         char* base = static_cast<char*>(blocks[s % R]);
         for (int e = 0; e < E; ++e)
-            host_expert_[streamed[s] * E + e] = reinterpret_cast<uint16_t*>(base + spec_.expert_bytes * e);
+            host_expert_[streamed[s] * E + e] = reinterpret_cast<uint16_t*>(base + expert_slot_bytes_ * e);
     }
     auto pinned = [&](byte_count bytes) {
         void* p = nullptr;
@@ -455,7 +478,7 @@ void Engine::allocate_host() {
     };
     for (int l = 0; l < L; ++l) {
         if (plan_.placement.attention_tier[l] != Tier::vram)
-            host_attn_[l] = static_cast<uint16_t*>(pinned(spec_.attention_bytes));
+            host_attn_[l] = static_cast<uint16_t*>(pinned(attn_slot_bytes_));
         host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
     }
     const int n = plan_.n_batches;
@@ -481,8 +504,25 @@ void Engine::init_weights() {
              "init embed");
     kl_check(kl_fill_normal_bf16(head_, static_cast<int64_t>(D_.V) * D_.d, tensor_seed(ws, kKindHead, 0, 0), sd, st),
              "init head");
-    // Staging for host-resident tensors: a slot large enough for either kind.
-    uint16_t* stage = D_.expert_elems() >= D_.attention_elems() ? pool_.ptr[0] : attn_slot_[0];
+    // Staging for host-resident tensors: a slot large enough for either kind
+    // (bf16), or the bf16 scratch + a pool slot for the Q4T bytes.
+    uint16_t* stage = cfg_.quant ? wscratch_
+                                 : (D_.expert_elems() >= D_.attention_elems() ? pool_.ptr[0] : attn_slot_[0]);
+    uint8_t* qstage = reinterpret_cast<uint8_t*>(pool_.ptr[0]);
+    // bf16 stage -> host copy in the streamed format.
+    auto to_host = [&](void* host, bool expert) {
+        if (!cfg_.quant) {
+            cuda_check(cudaMemcpyAsync(host, stage, expert ? spec_.expert_bytes : spec_.attention_bytes,
+                                       cudaMemcpyDeviceToHost, st), "d2h");
+            return;
+        }
+        const int64_t r0 = expert ? 2LL * D_.f : D_.qkv_width(), k0 = D_.d;
+        const int64_t r1 = D_.d, k1 = expert ? D_.f : static_cast<int64_t>(D_.Hq) * D_.hd;
+        kl_check(kl_quantize_q4(stage, r0, k0, qstage, st), "quantize");
+        kl_check(kl_quantize_q4(stage + r0 * k0, r1, k1, qstage + kl_q4_bytes(r0, k0), st), "quantize");
+        cuda_check(cudaMemcpyAsync(host, qstage, expert ? expert_slot_bytes_ : attn_slot_bytes_, cudaMemcpyDeviceToHost, st),
+                   "d2h");
+    };
     std::vector<char> host_done(host_blocks_.size(), 0);
     for (int l = 0; l < D_.L; ++l) {
         for (int e = 0; e < El_; ++e) {
@@ -491,8 +531,14 @@ void Engine::init_weights() {
             const std::uint64_t seed = tensor_seed(ws, kKindExpert, l, ep_ ? e * G_ + rank_ : e);
             if (uint16_t* r = res_expert_[l * El_ + e]) {
                 kl_check(kl_fill_normal_bf16(r, D_.expert_elems(), seed, sd, st), "init expert");
-                if (uint16_t* h = host_expert_[l * El_ + e])
-                    cuda_check(cudaMemcpyAsync(h, r, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+                if (uint16_t* h = host_expert_[l * El_ + e]) {
+                    if (cfg_.quant) {
+                        cuda_check(cudaMemcpyAsync(stage, r, spec_.expert_bytes, cudaMemcpyDeviceToDevice, st), "d2d");
+                        to_host(h, true);
+                    } else {
+                        cuda_check(cudaMemcpyAsync(h, r, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+                    }
+                }
             } else if (uint16_t* h = host_expert_[l * El_ + e]) {
                 // Aliased host layers are filled once, by their first user.
                 bool first = true;
@@ -500,7 +546,7 @@ void Engine::init_weights() {
                     if (host_expert_[l2 * El_ + e] == h) first = false;
                 if (!first) continue;
                 kl_check(kl_fill_normal_bf16(stage, D_.expert_elems(), seed, sd, st), "init expert");
-                cuda_check(cudaMemcpyAsync(h, stage, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+                to_host(h, true);
             }
         }
         const std::uint64_t aseed = tensor_seed(ws, kKindAttn, l, 0);
@@ -508,7 +554,7 @@ void Engine::init_weights() {
             kl_check(kl_fill_normal_bf16(res_attn_[l], D_.attention_elems(), aseed, sd, st), "init attn");
         } else {
             kl_check(kl_fill_normal_bf16(stage, D_.attention_elems(), aseed, sd, st), "init attn");
-            cuda_check(cudaMemcpyAsync(host_attn_[l], stage, spec_.attention_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+            to_host(host_attn_[l], false);
         }
         kl_check(kl_fill_normal_bf16(stage, D_.gate_elems(), tensor_seed(ws, kKindGate, l, 0), sd, st), "init gate");
         cuda_check(cudaMemcpyAsync(host_gate_[l], stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
@@ -559,9 +605,21 @@ std::string Engine::describe() const {
         attn_res += plan_.placement.attention_tier[l] == Tier::vram;
     }
     j["resident_expert_layers"] = resident;
+    {
+        std::vector<int> et, at;
+        for (int l = 0; l < D_.L; ++l) {
+            et.push_back(plan_.placement.expert_tier[l] == Tier::vram ? 1 : 0);
+            at.push_back(plan_.placement.attention_tier[l] == Tier::vram ? 1 : 0);
+        }
+        j["expert_resident"] = et;
+        j["attention_resident"] = at;
+    }
     j["resident_attention_layers"] = attn_res;
     j["expert_bytes"] = spec_.expert_bytes;
     j["attention_bytes"] = spec_.attention_bytes;
+    j["expert_stream_bytes"] = expert_slot_bytes_;
+    j["attention_stream_bytes"] = attn_slot_bytes_;
+    j["quant_bits"] = cfg_.quant ? cfg_.quant->bits : 16;
     j["gate_bytes"] = spec_.gate_bytes;
     j["host_pinned_blocks"] = host_blocks_.size();
     // Everything needed to rebuild the same plan/schedule with the reference.

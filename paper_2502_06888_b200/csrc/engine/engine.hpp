@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../host/emitter.hpp"
+#include "moesim/quant.hpp"
 #include "moesim/experiment.hpp"
 #include "moesim/simulator.hpp"
 
@@ -69,6 +70,7 @@ struct EngineConfig {
     bool ep = false;                // expert-parallel engine (also for world 1)
     std::string ep_nccl_id;         // 256 hex chars of ncclUniqueId (world > 1)
     bool prefill = true;
+    std::optional<moesim::QuantConfig> quant;  // 4-bit streamed experts / attention (Q4T)
 };
 
 EngineConfig parse_config(const std::string& json_text);
@@ -162,7 +164,10 @@ class Engine {
 
     // host (pinned) store
     std::vector<void*> host_blocks_;
-    std::vector<uint16_t*> host_expert_;  // [L*E] (null when resident)
+    std::vector<uint16_t*> host_expert_;  // [L*E] (null when resident); Q4T bytes when quantised
+    byte_count expert_slot_bytes_ = 0;    // bytes of a streamed expert (bf16, or Q4T = plan.cost.expert_transfer_bytes)
+    byte_count attn_slot_bytes_ = 0;      // bytes of streamed attention weights (bf16 or Q4T)
+    uint16_t* wscratch_ = nullptr;        // Q4: bf16 staging / dequantised weights for M > 256
     std::vector<uint16_t*> host_attn_;    // [L]
     std::vector<uint16_t*> host_gate_;    // [L]
     int32_t* host_report_ = nullptr;

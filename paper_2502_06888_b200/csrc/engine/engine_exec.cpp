@@ -275,7 +275,7 @@ void Engine::exec(std::int32_t id) {
                 const int s = pick2(attn_slot_busy_);
                 wait_release(attn_slot_release_[s]);
                 cuda_check(cudaEventRecord(op_start_[id], st), "record");
-                cuda_check(cudaMemcpyAsync(attn_slot_[s], host_attn_[op.layer], spec_.attention_bytes,
+                cuda_check(cudaMemcpyAsync(attn_slot_[s], host_attn_[op.layer], attn_slot_bytes_,
                                            cudaMemcpyHostToDevice, st), "h2d attention");
                 attn_slot_of_[op.layer] = s;
             } else if (op.cls == TensorClass::gate) {
@@ -299,7 +299,7 @@ void Engine::exec(std::int32_t id) {
                 cuda_check(cudaMemcpyAsync(gate_slot_[s], host_gate_[op.layer], spec_.gate_bytes,
                                            cudaMemcpyHostToDevice, st), "h2d gate");
                 for (size_t e = 0; e < E; ++e) {
-                    cuda_check(cudaMemcpyAsync(pool_.ptr[slots[e]], host_expert_[op.layer * E + e], spec_.expert_bytes,
+                    cuda_check(cudaMemcpyAsync(pool_.ptr[slots[e]], host_expert_[op.layer * E + e], expert_slot_bytes_,
                                                cudaMemcpyHostToDevice, st), "h2d moe");
                     expert_slot_of_[{op.layer, static_cast<int>(e)}] = slots[e];
                 }
@@ -312,7 +312,7 @@ void Engine::exec(std::int32_t id) {
             const int s = pool_.acquire();
             if (pool_.has_release[s]) wait_release(pool_.release[s]);
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
-            cuda_check(cudaMemcpyAsync(pool_.ptr[s], host_expert_[op.layer * E + op.expert], spec_.expert_bytes,
+            cuda_check(cudaMemcpyAsync(pool_.ptr[s], host_expert_[op.layer * E + op.expert], expert_slot_bytes_,
                                        cudaMemcpyHostToDevice, st), "h2d expert");
             expert_slot_of_[{op.layer, op.expert}] = s;
             break;
@@ -373,12 +373,29 @@ void Engine::exec_attention(const StreamOp& op) {
     const int tpb = tokens_per_batch(step);
     const int64_t row0 = static_cast<int64_t>(b) * tpb;
     const uint16_t* w = res_attn_[l] ? res_attn_[l] : attn_slot_[attn_slot_of_.at(l)];
+    // Streamed attention weights arrive as Q4T when quantised: fused-dequant
+    // GEMMs for decode-sized batches, dequantise-then-bf16 for prefill.
+    const bool q4 = cfg_.quant && res_attn_[l] == nullptr;
+    const int64_t wo_k = static_cast<int64_t>(D_.Hq) * D_.hd;
+    const uint8_t* q4qkv = reinterpret_cast<const uint8_t*>(w);
+    const uint8_t* q4o = q4qkv + kl_q4_bytes(D_.qkv_width(), D_.d);
+    if (q4 && tpb > 256) {
+        kl_check(kl_dequantize_q4(q4qkv, D_.qkv_width(), D_.d, wscratch_, cs), "dequant qkv");
+        kl_check(kl_dequantize_q4(q4o, D_.d, wo_k, wscratch_ + static_cast<int64_t>(D_.qkv_width()) * D_.d, cs),
+                 "dequant o");
+        w = wscratch_;
+    }
+    const bool fused = q4 && tpb <= 256;
     const uint16_t* wqkv = w;
     const uint16_t* wo = w + static_cast<int64_t>(D_.qkv_width()) * D_.d;
     uint16_t* hb = h_ + row0 * D_.d;
     kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
-    kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
-                          gemm_ws_bytes_, cs), "qkv");
+    if (fused)
+        kl_check(kl_gemm_q4(xa_, tpb, 0, tpb, D_.d, q4qkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
+                            gemm_ws_bytes_, cs), "qkv q4");
+    else
+        kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
+                              gemm_ws_bytes_, cs), "qkv");
     const float scale = 1.0f / std::sqrt(static_cast<float>(D_.hd));
     const int last = step == 0 ? cfg_.workload.prompt_len - 1 : -1;
     kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, tok_seq_ + row0, D_.theta, kc_[l],
@@ -390,7 +407,12 @@ void Engine::exec_attention(const StreamOp& op) {
         kl_check(kl_attn_decode_ws(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
                                    kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
                  "decode attention");
-    kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs), "o proj");
+    if (fused)
+        kl_check(kl_gemm_q4(ao_, tpb, 0, tpb, D_.Hq * D_.hd, q4o, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),
+                 "o proj q4");
+    else
+        kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),
+                 "o proj");
 }
 
 void Engine::exec_gate(const StreamOp& op) {
@@ -506,11 +528,23 @@ void Engine::exec_expert(const StreamOp& op) {
     const int64_t M = op.token_count;
     const int64_t row0 = row_offset_[e] + (op.batch >= 0 ? batch_prefix_[op.batch][e] : 0);
     const uint16_t* w = expert_weights(l, e);
+    const bool q4 = cfg_.quant && res_expert_[static_cast<size_t>(l) * El_ + e] == nullptr;
+    const uint8_t* q13 = reinterpret_cast<const uint8_t*>(w);
+    const uint8_t* q2 = q13 + kl_q4_bytes(2LL * D_.f, D_.d);
+    if (q4 && M > 256) {  // prefill-sized: expand once, then the compute-bound bf16 GEMMs
+        kl_check(kl_dequantize_q4(q13, 2LL * D_.f, D_.d, wscratch_, cs), "dequant w13");
+        kl_check(kl_dequantize_q4(q2, D_.d, D_.f, wscratch_ + 2LL * D_.f * D_.d, cs), "dequant w2");
+        w = wscratch_;
+    }
     const uint16_t* w2 = w + 2LL * D_.f * D_.d;
     for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
-        kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
-                               gemm_ws_bytes_, cs), "expert ffn");
+        if (q4 && M <= 256)
+            kl_check(kl_expert_ffn_q4(xp_, block_rows_, row0 + c, m, D_.d, D_.f, q13, q2, hs_, y_, gemm_ws_,
+                                      gemm_ws_bytes_, cs), "expert ffn q4");
+        else
+            kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
+                                   gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
     if (--exec_expert_left_ == 0 && !ep_) {

@@ -66,4 +66,6 @@ def request_for_engine(info, cfg):
         "window_tokens": info["window_tokens"],
         "simulate": False,
     }
+    if cfg.get("quant"):
+        req["quant"] = True
     return req

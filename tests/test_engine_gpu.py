@@ -33,15 +33,18 @@ def make(cfg):
     return Engine(cfg)
 
 
-@pytest.mark.parametrize("cap,variant,skew", [
-    (90_000_000, "klotski", {"kind": "zipf", "s": 1.5}),
-    (63_000_000, "klotski", {"kind": "markov", "s": 1.5, "p": 0.8}),
-    (200_000_000, "klotski", {"kind": "zipf", "s": 1.2}),
-    (90_000_000, "strawman_no_reorder", {"kind": "zipf", "s": 1.5}),
-    (140_000_000, "multibatch_full_prefetch", {"kind": "uniform"}),
+@pytest.mark.parametrize("cap,variant,skew,quant", [
+    (90_000_000, "klotski", {"kind": "zipf", "s": 1.5}, False),
+    (40_000_000, "klotski", {"kind": "zipf", "s": 1.5}, True),
+    (63_000_000, "klotski", {"kind": "markov", "s": 1.5, "p": 0.8}, False),
+    (200_000_000, "klotski", {"kind": "zipf", "s": 1.2}, False),
+    (90_000_000, "strawman_no_reorder", {"kind": "zipf", "s": 1.5}, False),
+    (140_000_000, "multibatch_full_prefetch", {"kind": "uniform"}, False),
 ])
-def test_replay_op_log_equals_reference_schedule(cuda, cap, variant, skew):
+def test_replay_op_log_equals_reference_schedule(cuda, cap, variant, skew, quant):
     cfg = dict(TINY, hbm_cap_bytes=cap, variant=variant, routing="replay", skew=skew, trace_seed=3)
+    if quant:  # payloads = quantized_bytes (planner + schedule with QuantConfig{4, 64})
+        cfg["quant"] = {"bits": 4}
     eng = make(cfg)
     run_all_steps(eng, cfg)
     got = eng.report("schedule")["text"]
@@ -86,7 +89,8 @@ def _trace_offset(step, layer, nb, bs, prompt, L, k):
     return L * nb * tpb0 * k + ((step - 1) * L + layer) * nb * bs * k
 
 
-def test_teacher_forced_layers_match_cpu_oracle(cuda):
+@pytest.mark.parametrize("quant", [False, True])
+def test_teacher_forced_layers_match_cpu_oracle(cuda, quant):
     """Hidden states within tolerance of the CPU oracle, layer by layer.
 
     Each layer is recomputed on the CPU from the GPU's own input hidden state
@@ -98,6 +102,8 @@ def test_teacher_forced_layers_match_cpu_oracle(cuda):
     from oracle.model_oracle import TinyModel
     from tests import oracle_lib as orc
     cfg = dict(TINY, routing="gate", record_hidden=True)
+    if quant:  # 4-bit streamed experts / attention (Q4T), resident layers stay bf16
+        cfg["quant"] = {"bits": 4}
     eng = make(cfg)
     outs = []
     rng = np.random.default_rng(1)
@@ -112,7 +118,11 @@ def test_teacher_forced_layers_match_cpu_oracle(cuda):
     info = eng.info
     eng.close()
     D = dict(L=4, d=512, f=1792, Hq=8, Hkv=2, hd=64, E=8, k=2, V=1024, theta=1e6, eps=1e-5)
-    model = TinyModel(D)
+    q4e = {l for l, r in enumerate(info["expert_resident"]) if quant and not r}
+    q4a = {l for l, r in enumerate(info["attention_resident"]) if quant and not r}
+    if quant:
+        assert q4e, "the cap should force streamed (quantised) expert layers"
+    model = TinyModel(D, q4_expert_layers=q4e, q4_attention_layers=q4a)
     kv = model.new_kv(nb * bs, info["kv_cap_tokens"])
     sink = info["kv_sink"]
     assert len(dumps) == G * D["L"]
