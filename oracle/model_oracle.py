@@ -64,11 +64,19 @@ class TinyModel:
             wqkv, wo = a[: self.qkvw * d].reshape(self.qkvw, d), a[self.qkvw * d:].reshape(d, D["Hq"] * D["hd"])
             if l in q4_attention_layers:
                 wqkv, wo = q4_roundtrip(wqkv), q4_roundtrip(wo)
+            fs = D.get("n_shared", 0) * D.get("f_shared", 0)
+            g = orc.normal_bf16(E * d + 3 * d * fs, tensor_seed(weight_seed, KIND_GATE, l, 0), 0.02)
+            shared = None
+            if fs:  # router tensor = [router E x d | W13s (2 fs x d) | W2s (d x fs)] (engine gate slot)
+                w13s = g[E * d: E * d + 2 * fs * d].reshape(2 * fs, d)
+                w2s = g[E * d + 2 * fs * d:].reshape(d, fs)
+                shared = (w13s, w2s)
             self.layers.append({
                 "wqkv": wqkv,
                 "wo": wo,
-                "wg": orc.normal_bf16(E * d, tensor_seed(weight_seed, KIND_GATE, l, 0), 0.02).reshape(E, d),
+                "wg": np.ascontiguousarray(g[: E * d]).reshape(E, d),
                 "experts": experts,
+                "shared": shared,
             })
 
     def new_kv(self, n_seqs, cap):
@@ -108,6 +116,14 @@ class TinyModel:
             sel = np.take_along_axis(logits, idx, 1)
             p = np.exp(sel - sel[:, :1])
             w = (p / p.sum(1, keepdims=True)).astype(np.float32)
+        if W["shared"] is not None:
+            # h += shared SwiGLU FFN(x2): bf16 hidden, fp32 down projection + residual, one rounding.
+            w13s, w2s = W["shared"]
+            fs = w2s.shape[1]
+            g = orc.gemm_f32(x2, np.ascontiguousarray(w13s[:fs])).astype(np.float64)
+            u = orc.gemm_f32(x2, np.ascontiguousarray(w13s[fs:])).astype(np.float64)
+            hs = orc.bf16_bits((g / (1.0 + np.exp(-g)) * u).astype(np.float32))
+            h = orc.bf16_bits(orc.gemm_f32(hs, w2s) + orc.bits_to_f32(h))
         counts, offsets, pos_r, row_token = orc.permute(idx, D["E"])
         xp = np.ascontiguousarray(x2[row_token])
         y = np.empty_like(xp)

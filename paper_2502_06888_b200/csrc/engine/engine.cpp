@@ -43,6 +43,8 @@ Dims preset_dims(const std::string& p) {
         // Fine-grained routed experts (64, top-6, softmax-over-all scores);
         // MLA is replaced by GQA attention of the same width.
         d = Dims{26, 2048, 1408, 16, 16, 128, 64, 6, 102400, 1e4f, 1e-6f, 1};
+        d.n_shared = 2;
+        d.f_shared = 1408;
     } else if (p == "tiny") {
         d = Dims{4, 512, 1792, 8, 2, 64, 8, 2, 1024, 1e6f, 1e-5f, 0};
     } else {
@@ -80,6 +82,10 @@ EngineConfig parse_config(const std::string& text) {
     D.theta = m.value("rope_theta", D.theta);
     D.eps = m.value("norm_eps", D.eps);
     D.score_mode = m.value("score_mode", D.score_mode);
+    D.n_shared = m.value("n_shared", D.n_shared);
+    D.f_shared = m.value("f_shared", D.f_shared);
+    if (D.n_shared < 0 || (D.n_shared > 0 && (D.fs() % 128 != 0 || D.f_shared <= 0)))
+        throw ConfigError("engine: shared experts need n_shared * f_shared to be a multiple of 128");
     const json w = j.value("workload", json::object());
     c.workload.batch_size = w.value("batch_size", 4);
     c.workload.n_batches = w.value("n_batches", 4);
@@ -276,6 +282,7 @@ void Engine::plan_memory() {
         add(5 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
         add(2 * Rx * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
+        if (D_.fs() > 0) add(chunk * D_.fs() * 2);                               // shared-expert hidden
         add(kl_permute_workspace_bytes(Rx, D_.E));
         if (ep_) {  // exchange buffers, labels, counts, co-activation delta
             add(r_recv_max_ * D_.d * 2 * 2 + R * D_.d * 2);
@@ -292,6 +299,9 @@ void Engine::plan_memory() {
                                        kl_gemm_workspace_bytes(mi, D_.qkv_width(), D_.d, 0),
                                        kl_gemm_workspace_bytes(mi, D_.d, D_.Hq * D_.hd, 1),
                                        kl_gemm_workspace_bytes(mi, D_.V, D_.d, 0)});
+            if (D_.fs() > 0)
+                gemm_ws_bytes_ = std::max({gemm_ws_bytes_, kl_gemm_workspace_bytes(mi, 2 * D_.fs(), D_.d, 2),
+                                           kl_gemm_workspace_bytes(mi, D_.d, D_.fs(), 1)});
             if (cfg_.quant)
                 gemm_ws_bytes_ = std::max({gemm_ws_bytes_, kl_gemm_q4_workspace_bytes(mi, 2 * D_.f, D_.d, 2),
                                            kl_gemm_q4_workspace_bytes(mi, D_.d, D_.f, 0),
@@ -379,6 +389,7 @@ void Engine::allocate_device() {
     xp_ = bf(Rx * D_.d);
     y_ = bf(Rx * D_.d);
     hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
+    if (D_.fs() > 0) hshared_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.fs());
     perm_ws_ = take(kl_permute_workspace_bytes(Rx, D_.E));
     gemm_ws_ = gemm_ws_bytes_ > 0 ? take(gemm_ws_bytes_) : nullptr;
     tok_pos_ = i32(t_max_);
@@ -621,6 +632,7 @@ std::string Engine::describe() const {
     j["attention_stream_bytes"] = attn_slot_bytes_;
     j["quant_bits"] = cfg_.quant ? cfg_.quant->bits : 16;
     j["gate_bytes"] = spec_.gate_bytes;
+    j["shared_experts"] = {{"n", D_.n_shared}, {"f", D_.f_shared}};
     j["host_pinned_blocks"] = host_blocks_.size();
     // Everything needed to rebuild the same plan/schedule with the reference.
     j["spec"] = {{"n_layers", spec_.n_layers}, {"n_experts", spec_.n_experts_per_layer}, {"top_k", spec_.top_k},

@@ -25,6 +25,7 @@
 #include <map>
 #include <memory>
 #include <optional>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -41,10 +42,18 @@ struct Dims {
     int L = 4, d = 512, f = 1792, Hq = 8, Hkv = 2, hd = 64, E = 8, k = 2, V = 1024;
     float theta = 1e6f, eps = 1e-5f;
     int score_mode = 0;
+    // Shared (always-active) experts, e.g. DeepSeek-V2-Lite's 2 x 1408. They
+    // are one SwiGLU FFN of intermediate n_shared * f_shared on every token,
+    // streamed with the router as the dense part of the MoE layer (an
+    // additive extension: the reference ModelSpec has no such field, so they
+    // are accounted in gate_bytes).
+    int n_shared = 0, f_shared = 0;
+    int fs() const { return n_shared * f_shared; }
+    byte_count shared_elems() const { return 3LL * d * fs(); }
     int qkv_width() const { return (Hq + 2 * Hkv) * hd; }
     byte_count expert_elems() const { return 3LL * d * f; }
     byte_count attention_elems() const { return static_cast<byte_count>(qkv_width()) * d + static_cast<byte_count>(d) * Hq * hd; }
-    byte_count gate_elems() const { return static_cast<byte_count>(E) * d; }
+    byte_count gate_elems() const { return static_cast<byte_count>(E) * d + shared_elems(); }
 };
 
 struct EngineConfig {
@@ -150,6 +159,8 @@ class Engine {
     std::vector<uint16_t*> kc_, vc_;     // [L]
     uint16_t *h_ = nullptr, *x2_ = nullptr, *xa_ = nullptr, *qkv_ = nullptr, *ao_ = nullptr;
     uint16_t *xp_ = nullptr, *y_ = nullptr, *hs_ = nullptr, *last_h_ = nullptr, *head_logits_ = nullptr;
+    uint16_t* hshared_ = nullptr;  // shared-expert SwiGLU output, [chunk rows][fs]
+    void shared_experts(int layer, int64_t T);
     int32_t *idx_[2] = {nullptr, nullptr}, *forced_ = nullptr, *pos_ = nullptr, *row_token_ = nullptr;
     int32_t *counts_ = nullptr, *offsets_ = nullptr, *tok_pos_ = nullptr, *tok_seq_ = nullptr;
     int32_t *ids_ = nullptr, *next_ids_ = nullptr, *last_rows_ = nullptr;
@@ -189,6 +200,7 @@ class Engine {
 
     // per-block execution state
     int cur_step_ = -1;
+    std::set<int> executed_steps_;
     int idx_cur_ = 0;
     std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot
     std::map<int, int> attn_slot_of_;                      // layer -> attention slot

@@ -95,6 +95,7 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     if (step < 0 || step >= cfg_.workload.gen_len) throw RangeError("engine: step outside the batch group");
     if (step == 0 && !cfg_.prefill) throw ConfigError("engine: built without prefill support (prefill=false)");
     cur_step_ = step;
+    executed_steps_.insert(step);
     const int n = plan_.n_batches, bs = cfg_.workload.batch_size;
     const int tpb = tokens_per_batch(step);
     const int64_t T = static_cast<int64_t>(n) * tpb;
@@ -462,6 +463,7 @@ void Engine::after_layer_gates(int step, int layer) {
     int32_t* prev = idx_[idx_cur_ ^ 1];
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
+    shared_experts(layer, T);
     launches_ += 2;  // rank + scan + scatter kernels
     int64_t* scores = reinterpret_cast<int64_t*>(report_ + 2LL * n * D_.E + 16 - ((2LL * n * D_.E) % 16));
     int64_t* marg_copy = scores + D_.E;
@@ -476,6 +478,24 @@ void Engine::after_layer_gates(int step, int layer) {
     if (cfg_.record_trace)
         cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, cs), "d2h idx");
     idx_cur_ ^= 1;  // this layer's ids become "prev" for the next layer
+}
+
+// Shared experts (always active): h += FFN_shared(x2) on every token of the
+// group, from the router tensor's slot ([router E x d | W13s (2 fs x d) |
+// W2s (d x fs)]); the combine then adds the routed experts on top.
+void Engine::shared_experts(int layer, int64_t T) {
+    if (D_.fs() <= 0) return;
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const uint16_t* g = gate_slot_[gate_slot_of_.at(layer)];
+    const uint16_t* w13 = g + static_cast<int64_t>(D_.E) * D_.d;
+    const uint16_t* w2 = w13 + 2LL * D_.fs() * D_.d;
+    for (int64_t c = 0; c < T; c += cfg_.ffn_chunk_rows) {
+        const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, T - c));
+        kl_check(kl_gemm_bf16(x2_, T, c, m, D_.d, w13, 2 * D_.fs(), hshared_, D_.fs(), nullptr, 2, gemm_ws_,
+                              gemm_ws_bytes_, cs), "shared w13");
+        kl_check(kl_gemm_bf16(hshared_, m, 0, m, D_.fs(), w2, D_.d, h_ + c * D_.d, D_.d, h_ + c * D_.d, 1, gemm_ws_,
+                              gemm_ws_bytes_, cs), "shared w2");
+    }
 }
 
 detail::BlockRouting Engine::read_routing(int step, int layer) {
@@ -692,7 +712,22 @@ std::string Engine::report(const std::string& what) {
             j["skipped"] = "expert-parallel shard";
         } else {
             const ValidationReport rep = validate_schedule(s, cfg_.replay ? replay_trace_ : recorded_, plan_);
-            j["violations"] = rep.violations;
+            // A run that skipped steps (e.g. decode without the prefill step)
+            // is checked on the steps it executed: findings are tagged
+            // "(step,layer)" by the reference validator.
+            json v = json::array();
+            int skipped = 0;
+            for (const std::string& msg : rep.violations) {
+                int st = -1;
+                if (!msg.empty() && msg[0] == '(') st = std::atoi(msg.c_str() + 1);
+                if (st >= 0 && !executed_steps_.count(st)) {
+                    ++skipped;
+                    continue;
+                }
+                v.push_back(msg);
+            }
+            j["violations"] = v;
+            if (skipped) j["unexecuted_step_findings"] = skipped;
         }
     } else if (what == "hidden") {
         json arr = json::array();

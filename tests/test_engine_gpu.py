@@ -89,8 +89,8 @@ def _trace_offset(step, layer, nb, bs, prompt, L, k):
     return L * nb * tpb0 * k + ((step - 1) * L + layer) * nb * bs * k
 
 
-@pytest.mark.parametrize("quant", [False, True])
-def test_teacher_forced_layers_match_cpu_oracle(cuda, quant):
+@pytest.mark.parametrize("quant,shared", [(False, 0), (True, 0), (False, 2)])
+def test_teacher_forced_layers_match_cpu_oracle(cuda, quant, shared):
     """Hidden states within tolerance of the CPU oracle, layer by layer.
 
     Each layer is recomputed on the CPU from the GPU's own input hidden state
@@ -104,6 +104,8 @@ def test_teacher_forced_layers_match_cpu_oracle(cuda, quant):
     cfg = dict(TINY, routing="gate", record_hidden=True)
     if quant:  # 4-bit streamed experts / attention (Q4T), resident layers stay bf16
         cfg["quant"] = {"bits": 4}
+    if shared:  # DeepSeek-style always-active shared experts (2 x 256), streamed with the router
+        cfg["model"] = {"preset": "tiny", "n_shared": shared, "f_shared": 256}
     eng = make(cfg)
     outs = []
     rng = np.random.default_rng(1)
@@ -117,7 +119,8 @@ def test_teacher_forced_layers_match_cpu_oracle(cuda, quant):
     sel = np.array(eng.report("trace")["sel"], np.int32)
     info = eng.info
     eng.close()
-    D = dict(L=4, d=512, f=1792, Hq=8, Hkv=2, hd=64, E=8, k=2, V=1024, theta=1e6, eps=1e-5)
+    D = dict(L=4, d=512, f=1792, Hq=8, Hkv=2, hd=64, E=8, k=2, V=1024, theta=1e6, eps=1e-5,
+             n_shared=shared, f_shared=256 if shared else 0)
     q4e = {l for l, r in enumerate(info["expert_resident"]) if quant and not r}
     q4a = {l for l, r in enumerate(info["attention_resident"]) if quant and not r}
     if quant:
