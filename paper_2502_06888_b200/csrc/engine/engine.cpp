@@ -58,7 +58,8 @@ std::uint64_t tensor_seed(std::uint64_t base, int kind, int layer, int expert) {
                            static_cast<std::uint64_t>(expert + 1));
 }
 
-constexpr byte_count kGemmWorkspace = 40LL << 20;  // split-K partials for decode-shaped GEMMs
+constexpr byte_count kGemmWorkspace = 40LL << 20;
+constexpr int kKvSlots = 3;  // device KV slots when the KV tier is DRAM  // split-K partials for decode-shaped GEMMs
 constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKindHead = 5;
 
 }  // namespace
@@ -260,7 +261,10 @@ void Engine::plan_memory() {
     int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, cfg_.quant,
                                                            ExpertLoadModel::measured, cfg_.retention)
                                                      .n_batches;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // KV offload (KV tier = DRAM): the cache of one (layer, batch) lives in a
+    // device slot only between its load and its store; kKvSlots slots.
+    bool kv_off = false;
+    for (int attempt = 0; attempt < 4; ++attempt) {
         const int64_t seqs = static_cast<int64_t>(w.batch_size) * n;
         t_max_ = seqs * (cfg_.prefill ? w.prompt_len : 1);
         tb_max_ = static_cast<int64_t>(w.batch_size) * (cfg_.prefill ? w.prompt_len : 1);
@@ -316,26 +320,33 @@ void Engine::plan_memory() {
         // GEMMs; keep it a small fraction of tight HBM caps.
         gemm_ws_bytes_ = std::min<int64_t>({gemm_ws_bytes_, kGemmWorkspace, std::max<int64_t>(256LL << 10, cfg_.hbm_cap / 256)});
         add(gemm_ws_bytes_);
-        add(5 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/ids/next/last, counts/offsets
+        add(6 * t_max_ * 4 + 2 * (D_.E + 1) * 4);                                // pos/seq/seq_local/ids/next/last, counts/offsets
         add(seqs * D_.d * 2 + seqs * D_.V * 2);                                  // last_h, head logits
         add(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64);                           // report
         add((static_cast<byte_count>(std::max(D_.L - 1, 0)) * D_.E * D_.E + D_.E) * 8);
         add(64 * 1024);
+        if (kv_off)
+            add(static_cast<byte_count>(kKvSlots) * w.batch_size *
+                cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
         ws_bytes_ = ws;
         PlacementConfig pc;
         pc.working_set_override = ws;
         plan_ = make_plan(spec_, profile_, w, stats, cfg_.quant, ExpertLoadModel::measured, cfg_.retention, n, pc);
-        if (plan_.n_batches == n) break;
+        const bool off_now = plan_.placement.kv_tier == Tier::dram;
+        if (plan_.n_batches == n && off_now == kv_off) break;
         n = plan_.n_batches;  // KV-capped: resize scratch for the capped n
+        kv_off = off_now;     // KV slots join the working set
     }
-    if (plan_.placement.kv_tier != Tier::vram)
-        throw ConfigError("engine: KV cache does not fit the HBM cap (KV offload streams are not executed by this "
-                          "engine yet); use kv_retention streaming or a smaller batch group");
+    kv_offload_ = plan_.placement.kv_tier == Tier::dram;
+    if (kv_offload_ && ep_) throw ConfigError("engine: KV offload is not combined with expert parallelism yet");
     if (plan_.placement.cpu_window_L > 0 || plan_.placement.any_disk())
         throw ConfigError("engine: disk-tier placement (staging window) is not executed by this engine");
     kv_cap_ = plan_.placement.kv_retained_tokens;
     kv_sink_ = cfg_.retention.mode == KvRetentionPolicy::Mode::streaming ? std::min(cfg_.retention.sink_tokens, kv_cap_ - 1) : 0;
-    kv_bytes_layer_ = static_cast<byte_count>(cfg_.workload.batch_size) * plan_.n_batches * kv_cap_ * spec_.kv_bytes_per_token;
+    kv_bytes_layer_ = kv_offload_ ? 0
+                                  : static_cast<byte_count>(cfg_.workload.batch_size) * plan_.n_batches * kv_cap_ *
+                                        spec_.kv_bytes_per_token;
+    kv_slot_bytes_ = static_cast<byte_count>(cfg_.workload.batch_size) * kv_cap_ * spec_.kv_bytes_per_token;
 }
 
 void Engine::allocate_device() {
@@ -394,6 +405,7 @@ void Engine::allocate_device() {
     gemm_ws_ = gemm_ws_bytes_ > 0 ? take(gemm_ws_bytes_) : nullptr;
     tok_pos_ = i32(t_max_);
     tok_seq_ = i32(t_max_);
+    tok_seq_local_ = i32(t_max_);
     ids_ = i32(t_max_);
     next_ids_ = i32(t_max_);
     last_rows_ = i32(t_max_);
@@ -428,9 +440,21 @@ void Engine::allocate_device() {
     // KV caches and resident layers (planner's decisions).
     kc_.assign(D_.L, nullptr);
     vc_.assign(D_.L, nullptr);
-    for (int l = 0; l < D_.L; ++l) {
-        kc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
-        vc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
+    if (kv_offload_) {
+        // Device KV slots of one (layer, batch) each: [bs][cap][Hkv][hd] K and V.
+        kv_slot_k_.clear();
+        kv_slot_v_.clear();
+        for (int s = 0; s < kKvSlots; ++s) {
+            kv_slot_k_.push_back(static_cast<uint16_t*>(take(kv_slot_bytes_ / 2)));
+            kv_slot_v_.push_back(static_cast<uint16_t*>(take(kv_slot_bytes_ / 2)));
+        }
+        kv_slot_release_.assign(kKvSlots, nullptr);
+        kv_slot_next_ = 0;
+    } else {
+        for (int l = 0; l < D_.L; ++l) {
+            kc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
+            vc_[l] = static_cast<uint16_t*>(take(kv_bytes_layer_ / 2));
+        }
     }
     res_expert_.assign(static_cast<size_t>(D_.L) * El_, nullptr);
     res_attn_.assign(D_.L, nullptr);
@@ -493,11 +517,16 @@ void Engine::allocate_host() {
         host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
     }
     const int n = plan_.n_batches;
+    if (kv_offload_) {
+        // Pinned host KV per (layer, batch): [bs][cap][Hkv][hd] K then V.
+        host_kv_.assign(static_cast<size_t>(L) * n, nullptr);
+        for (size_t i = 0; i < host_kv_.size(); ++i) host_kv_[i] = static_cast<uint16_t*>(pinned(kv_slot_bytes_));
+    }
     host_report_ = static_cast<int32_t*>(pinned(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + D_.E * 4 + 128));
     if (ep_) host_recv_ids_ = static_cast<int32_t*>(pinned(std::max<int64_t>(r_recv_max_, 1) * 4));
     host_idx_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
     host_forced_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));
-    host_tokens_ = static_cast<int32_t*>(pinned(4 * t_max_ * 4));
+    host_tokens_ = static_cast<int32_t*>(pinned(5 * t_max_ * 4));
 }
 
 void Engine::init_weights() {
@@ -588,6 +617,22 @@ void Engine::fill_kv_synthetic(int positions, std::uint64_t seed) {
     const int64_t per_seq = static_cast<int64_t>(kv_cap_) * D_.Hkv * D_.hd;
     const int64_t seqs = static_cast<int64_t>(cfg_.workload.batch_size) * plan_.n_batches;
     const int filled = std::min(positions, kv_cap_);
+    if (kv_offload_) {
+        for (int l = 0; l < D_.L; ++l)
+            for (int b = 0; b < plan_.n_batches; ++b) {
+                const int64_t half = kv_slot_bytes_ / 2 / 2;  // elements of K (or V)
+                kl_check(kl_fill_normal_bf16(kv_slot_k_[0], half, mix64(seed, 2 * (l * plan_.n_batches + b)), 1.0f, st),
+                         "kv fill");
+                kl_check(kl_fill_normal_bf16(kv_slot_v_[0], half, mix64(seed, 2 * (l * plan_.n_batches + b) + 1), 1.0f,
+                                             st), "kv fill");
+                uint16_t* h = host_kv_[static_cast<size_t>(l) * plan_.n_batches + b];
+                cuda_check(cudaMemcpyAsync(h, kv_slot_k_[0], kv_slot_bytes_ / 2, cudaMemcpyDeviceToHost, st), "kv d2h");
+                cuda_check(cudaMemcpyAsync(h + half, kv_slot_v_[0], kv_slot_bytes_ / 2, cudaMemcpyDeviceToHost, st), "kv d2h");
+            }
+        cuda_check(cudaStreamSynchronize(st), "kv fill sync");
+        kv_filled_positions_ = filled;
+        return;
+    }
     for (int l = 0; l < D_.L; ++l) {
         // Whole-cache fill (unused slots are never read: attention reads
         // min(pos+1, cap) slots).
@@ -610,6 +655,8 @@ std::string Engine::describe() const {
     j["kv_cap_tokens"] = kv_cap_;
     j["kv_sink"] = kv_sink_;
     j["kv_bytes_per_layer"] = kv_bytes_layer_;
+    j["kv_offload"] = kv_offload_;
+    j["kv_slot_bytes"] = kv_slot_bytes_;
     int resident = 0, attn_res = 0;
     for (int l = 0; l < D_.L; ++l) {
         resident += plan_.placement.expert_tier[l] == Tier::vram;

@@ -200,6 +200,17 @@ class Engine {
 
     // per-block execution state
     int cur_step_ = -1;
+    // KV offload (KV tier = DRAM, reference load_cache / store_cache ops).
+    bool kv_offload_ = false;
+    byte_count kv_slot_bytes_ = 0;                 // one (layer, batch): K + V
+    std::vector<uint16_t*> host_kv_;               // [L * n] pinned, K then V
+    std::vector<uint16_t*> kv_slot_k_, kv_slot_v_; // device slots
+    std::vector<cudaEvent_t> kv_slot_release_;     // after the slot's store
+    int kv_slot_next_ = 0;
+    std::map<std::pair<int, int>, int> kv_slot_of_;  // (layer, batch) -> slot
+    int32_t* tok_seq_local_ = nullptr;             // row -> sequence within its batch
+    int kv_filled_positions_ = 0;
+    int acquire_kv_slot(cudaStream_t st);
     std::set<int> executed_steps_;
     int idx_cur_ = 0;
     std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot

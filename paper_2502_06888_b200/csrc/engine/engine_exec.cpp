@@ -65,6 +65,15 @@ const uint16_t* Engine::expert_weights(int layer, int e) const {
     return pool_.ptr[it->second];
 }
 
+int Engine::acquire_kv_slot(cudaStream_t st) {
+    const int s = kv_slot_next_;
+    kv_slot_next_ = (kv_slot_next_ + 1) % static_cast<int>(kv_slot_k_.size());
+    for (const auto& [key, slot] : kv_slot_of_)
+        if (slot == s) throw AccountingError("engine: KV slot reused before its store (raise kKvSlots)");
+    if (kv_slot_release_[s] != nullptr) cuda_check(cudaStreamWaitEvent(st, kv_slot_release_[s], 0), "kv slot wait");
+    return s;
+}
+
 PrefetchDecision Engine::decide(int /*step*/, int layer) const {
     PrefetchDecision d;
     d.layer = layer;
@@ -114,13 +123,17 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     int32_t* hp = host_tokens_;
     int32_t* hs = host_tokens_ + t_max_;
     int32_t* hl = host_tokens_ + 2 * t_max_;
+    int32_t* hsl = host_tokens_ + 4 * t_max_;
     for (int64_t r = 0; r < T; ++r) {
         const int64_t b = r / tpb, within = r % tpb;
         const int64_t sq = step == 0 ? within / cfg_.workload.prompt_len : within;
         hp[r] = step == 0 ? static_cast<int32_t>(within % cfg_.workload.prompt_len)
                           : cfg_.workload.prompt_len + step - 1;
         hs[r] = static_cast<int32_t>(b * bs + sq);
+        hsl[r] = static_cast<int32_t>(sq);
     }
+    if (kv_offload_)
+        cuda_check(cudaMemcpyAsync(tok_seq_local_, hsl, T * 4, cudaMemcpyHostToDevice, cs), "h2d seq local");
     for (int64_t s = 0; s < seqs; ++s) {
         // Row of each sequence's last token this step (greedy head input).
         const int64_t b = s / bs, i = s % bs;
@@ -213,6 +226,8 @@ void Engine::collect_step_times() {
     std::fill(pool_.has_release.begin(), pool_.has_release.end(), 0);
     std::fill(attn_slot_release_.begin(), attn_slot_release_.end(), nullptr);
     std::fill(gate_slot_release_.begin(), gate_slot_release_.end(), nullptr);
+    std::fill(kv_slot_release_.begin(), kv_slot_release_.end(), nullptr);
+    if (!kv_slot_of_.empty()) throw AccountingError("engine: KV slot still mapped at the end of a step");
 }
 
 // Enqueue every emitted-but-not-executed op. Cold computes of a reorder
@@ -350,6 +365,50 @@ void Engine::exec(std::int32_t id) {
             }
             break;
         }
+        case OpKind::load_cache: {
+            // Retained KV history of one (layer, batch) from pinned host into a
+            // free device slot (load_kv, schedule.cpp:255-268): rows
+            // [0, history) of every sequence, one 2D copy each for K and V.
+            const int slot = acquire_kv_slot(st);
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            const int history = plan_.placement.kv_retention.retained(cfg_.workload.prompt_len + op.step - 1);
+            const size_t row = static_cast<size_t>(D_.Hkv) * D_.hd * 2, pitch = row * kv_cap_;
+            const uint16_t* h = host_kv_[static_cast<size_t>(op.layer) * plan_.n_batches + op.batch];
+            const size_t half = kv_slot_bytes_ / 4;  // elements of K
+            cuda_check(cudaMemcpy2DAsync(kv_slot_k_[slot], pitch, h, pitch, row * history, cfg_.workload.batch_size,
+                                         cudaMemcpyHostToDevice, st), "h2d kv");
+            cuda_check(cudaMemcpy2DAsync(kv_slot_v_[slot], pitch, h + half, pitch, row * history,
+                                         cfg_.workload.batch_size, cudaMemcpyHostToDevice, st), "h2d kv");
+            kv_slot_of_[{op.layer, op.batch}] = slot;
+            break;
+        }
+        case OpKind::store_cache: {
+            // This step's new K/V rows back to host (store_kv, schedule.cpp:270-288);
+            // the slot is free once the copy has read it.
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            const auto it = kv_slot_of_.find({op.layer, op.batch});
+            if (it == kv_slot_of_.end()) throw AccountingError("engine: KV store without a device slot");
+            const int slot = it->second;
+            const size_t row = static_cast<size_t>(D_.Hkv) * D_.hd * 2, pitch = row * kv_cap_;
+            uint16_t* h = host_kv_[static_cast<size_t>(op.layer) * plan_.n_batches + op.batch];
+            const size_t half = kv_slot_bytes_ / 4;
+            size_t first = 0, rows = 0;
+            if (op.step == 0) {
+                rows = static_cast<size_t>(std::min(cfg_.workload.prompt_len, kv_cap_));
+            } else {
+                const int p = cfg_.workload.prompt_len + op.step - 1;
+                first = static_cast<size_t>(p < kv_sink_ ? p : kv_sink_ + (p - kv_sink_) % (kv_cap_ - kv_sink_));
+                rows = 1;
+            }
+            const size_t off = first * row / 2;
+            cuda_check(cudaMemcpy2DAsync(h + off, pitch, kv_slot_k_[slot] + off, pitch, row * rows,
+                                         cfg_.workload.batch_size, cudaMemcpyDeviceToHost, st), "d2h kv");
+            cuda_check(cudaMemcpy2DAsync(h + half + off, pitch, kv_slot_v_[slot] + off, pitch, row * rows,
+                                         cfg_.workload.batch_size, cudaMemcpyDeviceToHost, st), "d2h kv");
+            kv_slot_release_[slot] = op_end_[id];
+            kv_slot_of_.erase(it);
+            break;
+        }
         case OpKind::compute_attention:
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
             exec_attention(op);
@@ -399,14 +458,28 @@ void Engine::exec_attention(const StreamOp& op) {
                               gemm_ws_bytes_, cs), "qkv");
     const float scale = 1.0f / std::sqrt(static_cast<float>(D_.hd));
     const int last = step == 0 ? cfg_.workload.prompt_len - 1 : -1;
-    kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, tok_seq_ + row0, D_.theta, kc_[l],
-                               vc_[l], kv_cap_, kv_sink_, last, cs), "rope/kv");
+    uint16_t* kc = kc_[l];
+    uint16_t* vc = vc_[l];
+    const int32_t* seq_idx = tok_seq_ + row0;
+    if (kv_offload_) {
+        // The batch's KV slot (loaded by load_cache; a fresh one for prefill).
+        auto it = kv_slot_of_.find({l, b});
+        if (it == kv_slot_of_.end()) {
+            if (step != 0) throw AccountingError("engine: decode attention without a loaded KV slot");
+            it = kv_slot_of_.emplace(std::make_pair(l, b), acquire_kv_slot(cs)).first;
+        }
+        kc = kv_slot_k_[it->second];
+        vc = kv_slot_v_[it->second];
+        seq_idx = tok_seq_local_ + row0;
+    }
+    kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, seq_idx, D_.theta, kc, vc, kv_cap_,
+                               kv_sink_, last, cs), "rope/kv");
     if (step == 0)
         kl_check(kl_attn_prefill(qkv_, cfg_.workload.batch_size, cfg_.workload.prompt_len, D_.Hq, D_.Hkv, D_.hd,
                                  kv_cap_, kv_sink_, scale, ao_, cs), "prefill attention");
     else
-        kl_check(kl_attn_decode_ws(qkv_, D_.qkv_width(), tok_pos_ + row0, tok_seq_ + row0, tpb, D_.Hq, D_.Hkv, D_.hd,
-                                   kc_[l], vc_[l], kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
+        kl_check(kl_attn_decode_ws(qkv_, D_.qkv_width(), tok_pos_ + row0, seq_idx, tpb, D_.Hq, D_.Hkv, D_.hd,
+                                   kc, vc, kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
                  "decode attention");
     if (fused)
         kl_check(kl_gemm_q4(ao_, tpb, 0, tpb, D_.Hq * D_.hd, q4o, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),

@@ -172,3 +172,59 @@ def test_expert_parallel_world1_is_bit_identical(cuda, cap):
     assert all(np.array_equal(x, y) for x, y in zip(oa, ob))
     assert len(ha) == len(hb) and all(x == y for x, y in zip(ha, hb))
     assert m["tokens_generated"] > 0
+
+
+def _kv_offload_cfg(routing, **extra):
+    """TINY-shaped group whose KV cache cannot stay in HBM: the largest cap
+    (1 MB steps down from 140 MB) at which the planner puts the KV tier in DRAM."""
+    base = dict(TINY, workload={"batch_size": 16, "n_batches": 4, "prompt_len": 64, "gen_len": 4}, routing=routing,
+                **extra)
+    for cap in range(140_000_000, 100_000_000, -1_000_000):
+        cfg = dict(base, hbm_cap_bytes=cap)
+        try:
+            eng = make(cfg)
+        except Exception:
+            continue
+        if eng.info["kv_offload"]:
+            return cfg, eng
+        eng.close()
+    pytest.skip("no cap puts the KV tier in DRAM for this shape")
+
+
+def test_kv_offload_replay_op_log_equals_reference_schedule(cuda):
+    """KV tier = DRAM: load_cache / store_cache ops (schedule.cpp:255-288) are
+    executed as pinned-host <-> KV-slot copies on the cache streams; the
+    executed op log equals the reference schedule and validates."""
+    cfg, eng = _kv_offload_cfg("replay", skew={"kind": "zipf", "s": 1.5}, trace_seed=3)
+    run_all_steps(eng, cfg)
+    got = eng.report("schedule")["text"]
+    assert "load_cache" in got and "store_cache" in got
+    ref = parity.ref()(parity.request_for_engine(eng.info, cfg))
+    assert "error" not in ref, ref
+    assert got == ref["schedule_text"]
+    assert eng.report("validate")["violations"] == []
+    eng.close()
+
+
+def test_kv_offload_matches_resident_kv(cuda):
+    """Decode with the KV cache streamed through host memory gives the same
+    tokens and hidden states as the same group with KV resident in HBM."""
+    cfg, eng = _kv_offload_cfg("gate", record_hidden=True)
+    rng = np.random.default_rng(4)
+    w = cfg["workload"]
+    prompt = rng.integers(0, 1024, eng.n_seqs * w["prompt_len"], dtype=np.int32)
+    outs = [eng.step(0, prompt)[0]] + [eng.step(s)[0] for s in range(1, w["gen_len"])]
+    dumps = eng.report("hidden")["dumps"]
+    assert eng.report("validate")["violations"] == []
+    n = eng.n_batches
+    eng.close()
+    ref_cfg = dict(cfg, hbm_cap_bytes=400_000_000, workload=dict(w, n_batches=n))
+    ref = make(ref_cfg)
+    assert not ref.info["kv_offload"]
+    outs2 = [ref.step(0, prompt)[0]] + [ref.step(s)[0] for s in range(1, w["gen_len"])]
+    dumps2 = ref.report("hidden")["dumps"]
+    ref.close()
+    for a, b in zip(outs, outs2):
+        assert np.array_equal(a, b)
+    for a, b in zip(dumps, dumps2):
+        assert np.array_equal(np.array(a), np.array(b))

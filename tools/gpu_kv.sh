@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_engine_gpu.py -m gpu -x -q -k "kv_offload" 2>&1 | tail -25
