@@ -808,6 +808,7 @@ int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
+int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
 
 int sm_count() {
     static const int n = [] {
@@ -881,6 +882,8 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.pdl = g_pdl;
     if (p.stages > 16) p.stages = 16;
     int G = std::max(1, std::min(sm_count() * g_stream_ctas, p.units / 4));
+    if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
+        G = n_tiles;  // one whole tile per CTA: no split partials, the rest of the SMs idle
     G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
     G = std::min(G, static_cast<int>(kFlagBytes / 4));
     if (G < 1) return KL_EUNSUPPORTED;
@@ -968,6 +971,7 @@ extern "C" int kl_tune(int knob, int value) {
         case 99: g_stream_debug = value; return KL_OK;
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
         case KL_TUNE_PREFILL_TC: g_prefill_tc = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_ctas = value;

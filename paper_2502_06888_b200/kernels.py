@@ -60,6 +60,7 @@ TUNE_STREAM_HINT = 3
 TUNE_STREAM_CTAS_PER_SM = 4
 TUNE_PDL = 5
 TUNE_PREFILL_TC = 6
+TUNE_STREAM_WHOLE_TILES = 7
 
 
 def tune(knob, value):

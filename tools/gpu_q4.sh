@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python tools/deepseek_run.py --bs 32 --cap 24e9 --steps 3 > gpurun_out/deepseek.json 2> gpurun_out/deepseek.err; cat gpurun_out/deepseek.json; tail -3 gpurun_out/deepseek.err
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
+timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep compute_
