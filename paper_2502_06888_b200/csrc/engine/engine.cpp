@@ -7,6 +7,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -165,6 +166,7 @@ void ExpertSlotPool::release_after(int slot, cudaEvent_t ev) {
 }
 
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
+    diag_ = std::getenv("KL_ENGINE_DIAG") != nullptr;
     spec_.name = cfg_.name;
     spec_.n_layers = D_.L;
     spec_.n_experts_per_layer = D_.E;

@@ -121,6 +121,8 @@ class Engine {
     void exec_attention(const moesim::StreamOp& op);
     void exec_gate(const moesim::StreamOp& op);
     void exec_expert(const moesim::StreamOp& op);
+    void combine_block(int step);
+    int combine_step_ = -1;
     void after_layer_gates(int step, int layer);
     moesim::detail::BlockRouting read_routing(int step, int layer);
     moesim::PrefetchDecision decide(int step, int layer) const;
@@ -212,6 +214,15 @@ class Engine {
     int kv_filled_positions_ = 0;
     int acquire_kv_slot(cudaStream_t st);
     std::set<int> executed_steps_;
+    // Diagnostics (KL_ENGINE_DIAG=1): events around each expert op's FFN kernels.
+    struct DiagEvent {
+        std::int32_t op;
+        cudaEvent_t before, after;
+    };
+    bool diag_ = false;
+    std::int32_t next_exec_diag_ = 0;
+    std::vector<DiagEvent> diag_events_;
+    std::vector<std::array<float, 3>> diag_rows_;
     int idx_cur_ = 0;
     std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot
     std::map<int, int> attn_slot_of_;                      // layer -> attention slot

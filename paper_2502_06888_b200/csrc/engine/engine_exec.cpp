@@ -219,6 +219,15 @@ void Engine::collect_step_times() {
         ev.bytes = ops[id].payload_bytes;
         ev.tokens = ops[id].token_count;
     }
+    for (const auto& de : diag_events_) {
+        float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+        cuda_check(cudaEventElapsedTime(&a, op_start_[de.op], de.before), "diag");
+        cuda_check(cudaEventElapsedTime(&b, de.before, de.after), "diag");
+        cuda_check(cudaEventElapsedTime(&c, de.after, op_end_[de.op]), "diag");
+        (void)d;
+        diag_rows_.push_back({a * 1e3f, b * 1e3f, c * 1e3f});
+    }
+    diag_events_.clear();
     timed_from_ = next_exec_;
     // Everything this step enqueued has completed: events and release
     // markers can be recycled.
@@ -419,12 +428,17 @@ void Engine::exec(std::int32_t id) {
             break;
         case OpKind::compute_expert:
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            next_exec_diag_ = id;
             exec_expert(op);
             break;
         default:
             throw ConfigError(std::string("engine: op kind ") + op_kind_name(op.kind) + " is not executed on B200 yet");
     }
     cuda_check(cudaEventRecord(op_end_[id], st), "record");
+    if (combine_step_ >= 0) {
+        combine_block(combine_step_);
+        combine_step_ = -1;
+    }
 }
 
 void Engine::exec_attention(const StreamOp& op) {
@@ -630,6 +644,12 @@ void Engine::exec_expert(const StreamOp& op) {
         w = wscratch_;
     }
     const uint16_t* w2 = w + 2LL * D_.f * D_.d;
+    cudaEvent_t d0 = nullptr, d1 = nullptr;
+    if (diag_) {
+        d0 = event();
+        d1 = event();
+        cuda_check(cudaEventRecord(d0, cs), "diag");
+    }
     for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
         if (q4 && M <= 256)
@@ -640,16 +660,25 @@ void Engine::exec_expert(const StreamOp& op) {
                                    gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
-    if (--exec_expert_left_ == 0 && !ep_) {
-        // Every routed row of the block is computed: weighted combine + residual.
-        const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(op.step);
-        kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
-        if (cfg_.record_hidden) {
-            std::vector<uint16_t> dump(static_cast<size_t>(T) * D_.d);
-            cuda_check(cudaMemcpyAsync(dump.data(), h_, dump.size() * 2, cudaMemcpyDeviceToHost, cs), "dump");
-            cuda_check(cudaStreamSynchronize(cs), "dump sync");
-            hidden_dumps_.push_back(std::move(dump));
-        }
+    if (diag_) {
+        cuda_check(cudaEventRecord(d1, cs), "diag");
+        diag_events_.push_back({static_cast<std::int32_t>(next_exec_diag_), d0, d1});
+    }
+    // The block's last expert op: the combine follows right after the op's
+    // end event (so compute_expert events bracket the FFN kernels only).
+    if (--exec_expert_left_ == 0 && !ep_) combine_step_ = op.step;
+}
+
+void Engine::combine_block(int step) {
+    // Every routed row of the block is computed: weighted combine + residual.
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(step);
+    kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
+    if (cfg_.record_hidden) {
+        std::vector<uint16_t> dump(static_cast<size_t>(T) * D_.d);
+        cuda_check(cudaMemcpyAsync(dump.data(), h_, dump.size() * 2, cudaMemcpyDeviceToHost, cs), "dump");
+        cuda_check(cudaStreamSynchronize(cs), "dump sync");
+        hidden_dumps_.push_back(std::move(dump));
     }
 }
 
@@ -669,6 +698,7 @@ void Engine::reset_log() {
     launches_ = 0;
     step_ms_.clear();
     hidden_dumps_.clear();
+    diag_rows_.clear();
 }
 
 std::string Engine::report(const std::string& what) {
@@ -802,6 +832,9 @@ std::string Engine::report(const std::string& what) {
             j["violations"] = v;
             if (skipped) j["unexecuted_step_findings"] = skipped;
         }
+    } else if (what == "diag") {
+        // Expert-op breakdown (KL_ENGINE_DIAG=1): [start -> FFN launch, FFN kernels, FFN -> end] in us.
+        j["expert_op_us"] = diag_rows_;
     } else if (what == "hidden") {
         json arr = json::array();
         for (const auto& dmp : hidden_dumps_) arr.push_back(dmp);

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
-timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep compute_
+KL_ENGINE_DIAG=1 timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_|breakdown"

@@ -48,6 +48,11 @@ def main():
             sel = [d for d, t in ex if lo < t <= hi]
             if sel:
                 print(f"  rows ({lo},{hi}]: n={len(sel)} mean {np.mean(sel):.1f} us")
+    diag = eng.report("diag").get("expert_op_us", [])
+    if diag:
+        a = np.array(diag)
+        print("expert op breakdown (us): start->FFN %.1f  FFN kernels %.1f  FFN->end %.1f  (n=%d)" % (
+            *a.mean(0), len(a)))
     eng.close()
 
 
