@@ -145,6 +145,121 @@ gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ no
     }
 }
 
+// Latency-optimised router: one warp per token, the row held in registers
+// (NC = d/256 16-byte chunks per lane, loaded once), every expert's router row
+// loaded with independent vector loads. Same arithmetic order as
+// gate_topk_kernel (and oracle/numerics.c): lane l owns chunks c = 8l + 256j,
+// fmaf in element order, xor butterfly 16..1 with round-to-nearest adds.
+template <int NC>
+__global__ void __launch_bounds__(128)
+gate_topk_warp_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ norm_w,
+                      const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
+                      uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
+                      float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    constexpr int d = NC * 256;
+    __shared__ float lg_all[4][64];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tok = blockIdx.x * 4 + wid;
+    if (tok >= T) return;
+    const uint16_t* hrow = h + static_cast<int64_t>(tok) * d;
+    uint4 hv[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) hv[j] = __ldg(reinterpret_cast<const uint4*>(hrow + lane * 8 + 256 * j));
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const uint32_t w4[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = bf2f(static_cast<uint16_t>(w4[i] & 0xffffu)), b = bf2f(static_cast<uint16_t>(w4[i] >> 16));
+            ss = fmaf(a, a, ss);
+            ss = fmaf(b, b, ss);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    const float rstd = rsqrtf(ss / static_cast<float>(d) + eps);
+    // Normalised row (bf16, as stored in x2) kept packed in registers.
+    uint32_t xv[NC][4];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(norm_w + lane * 8 + 256 * j));
+        const uint32_t hw[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+        const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = __fmul_rn(__fmul_rn(bf2f(static_cast<uint16_t>(hw[i] & 0xffffu)), rstd),
+                                      bf2f(static_cast<uint16_t>(gw[i] & 0xffffu)));
+            const float b = __fmul_rn(__fmul_rn(bf2f(static_cast<uint16_t>(hw[i] >> 16)), rstd),
+                                      bf2f(static_cast<uint16_t>(gw[i] >> 16)));
+            xv[j][i] = pack2(a, b);
+        }
+        *reinterpret_cast<uint4*>(x2 + static_cast<int64_t>(tok) * d + lane * 8 + 256 * j) =
+            make_uint4(xv[j][0], xv[j][1], xv[j][2], xv[j][3]);
+    }
+    float* lg = lg_all[wid];
+    for (int e = 0; e < E; ++e) {
+        const uint16_t* wr = wg + static_cast<int64_t>(e) * d + lane * 8;
+        uint4 wv[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + 256 * j));
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            const uint32_t ww[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc = fmaf(bf2f(static_cast<uint16_t>(xv[j][i] & 0xffffu)), bf2f(static_cast<uint16_t>(ww[i] & 0xffffu)), acc);
+                acc = fmaf(bf2f(static_cast<uint16_t>(xv[j][i] >> 16)), bf2f(static_cast<uint16_t>(ww[i] >> 16)), acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (lane == 0) lg[e] = acc;
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    if (logits_out != nullptr)
+        for (int e = 0; e < E; ++e) logits_out[static_cast<int64_t>(tok) * E + e] = lg[e];
+    uint64_t taken = 0;
+    int sel[8];
+    float val[8];
+    for (int j = 0; j < k; ++j) {
+        int best = -1;
+        float bv = 0.f;
+        for (int e = 0; e < E; ++e) {
+            if ((taken >> e) & 1ull) continue;
+            if (best < 0 || lg[e] > bv) {
+                best = e;
+                bv = lg[e];
+            }
+        }
+        taken |= 1ull << best;
+        sel[j] = best;
+        val[j] = bv;
+    }
+    float wsum = 0.f;
+    float pr[8];
+    if (score_mode == 0) {
+        for (int j = 0; j < k; ++j) {
+            pr[j] = expf(val[j] - val[0]);
+            wsum += pr[j];
+        }
+    } else {
+        float mx = lg[0];
+        for (int e = 1; e < E; ++e) mx = fmaxf(mx, lg[e]);
+        for (int e = 0; e < E; ++e) wsum += expf(lg[e] - mx);
+        for (int j = 0; j < k; ++j) pr[j] = expf(val[j] - mx);
+    }
+    for (int j = 0; j < k; ++j) {
+        const int64_t r = static_cast<int64_t>(tok) * k + j;
+        idx[r] = sel[j];
+        weight[r] = pr[j] / wsum;
+        if (hist != nullptr) atomicAdd(&hist[sel[j]], 1);
+        if (first_pos != nullptr) atomicMin(&first_pos[sel[j]], static_cast<int32_t>(r));
+    }
+}
+
 __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int64_t T, int d,
                                float eps, uint16_t* __restrict__ out) {
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -419,6 +534,21 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
     if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 64 || k < 1 || k > 8 || k > E) return KL_EINVAL;
     if (!h || !norm_w || !wg || !x2 || !idx || !weight) return KL_EINVAL;
     if (T == 0) return KL_OK;
+    const unsigned blocks = static_cast<unsigned>((T + 3) / 4);
+#define KL_GATE_WARP(NC)                                                                                          \
+    case NC:                                                                                                      \
+        gate_topk_warp_kernel<NC><<<blocks, 128, 0, stream>>>(h, norm_w, wg, T, E, k, eps, score_mode, x2, logits, \
+                                                              idx, weight, hist, first_pos);                      \
+        return check_launch();
+    switch (d / 256) {
+        KL_GATE_WARP(2)
+        KL_GATE_WARP(4)
+        KL_GATE_WARP(8)
+        KL_GATE_WARP(16)
+        KL_GATE_WARP(24)
+        default: break;
+    }
+#undef KL_GATE_WARP
     gate_topk_kernel<<<T, kGateWarps * 32, 0, stream>>>(
         h, norm_w, wg, T, d, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);
     return check_launch();
