@@ -63,8 +63,21 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int n_tile = blockIdx.x;
-    const int m_tile = blockIdx.y;
+    // Grouped raster: CTAs launched together cover a block of kGroupM
+    // m-tiles x a few n-tiles (m fastest), so both the activation and the
+    // weight tiles of a wave are reused from L2 instead of re-streaming the
+    // whole weight matrix once per row of m-tiles.
+    int n_tile = blockIdx.x, m_tile = blockIdx.y;
+    if (gridDim.y > 1) {
+        constexpr int kGroupM = 16;
+        const int lin = blockIdx.y * gridDim.x + blockIdx.x;
+        const int per_group = kGroupM * gridDim.x;
+        const int first_m = lin / per_group * kGroupM;
+        const int group_m = min(kGroupM, static_cast<int>(gridDim.y) - first_m);
+        const int within = lin % per_group;
+        m_tile = first_m + within % group_m;
+        n_tile = within / group_m;
+    }
     const int split = blockIdx.z;
     const int kb0 = split * kb_per_split;
     const int num_kb = kb_per_split;

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_kernels_gpu.py -m gpu -x -q -k "gate" 2>&1 | tail -2
-timeout 120 python tools/profile_kernels.py --only route --iters 30 --gap-ms 0.05 2>&1 | grep -A1 "gate_topk\|permute\|combine" | grep -E "gate|perm|comb|us"
-timeout 120 python tools/profile_kernels.py --only route --iters 30 2>&1 | grep -A1 "gate_topk" | grep -E "us"
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 900 python tools/prefill_run.py --bs 8 --n 8 --reps 1 2>&1 | tail -1 | cut -c1-600
