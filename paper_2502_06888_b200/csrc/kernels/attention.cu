@@ -428,7 +428,8 @@ __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float*
 //           smem tile (the MMA's A operand) -> O += P V with V read
 //           MN-major straight from its TMA tile (no transpose pass).
 // Roofline: tensor-bound; FLOPs per (row, head, retained key) = 4 * hd.
-constexpr int kPfThreads = 128;
+constexpr int kPfThreads = 256;  // two warps per TMEM lane quarter, each owning half the key columns
+constexpr int kPfParts = kPfThreads / 128;
 constexpr int kPfKeys = 128;  // keys per block (MMA N for S, K for P.V)
 
 // UMMA smem descriptor, MN-major operand in 128B-swizzled TMA tiles: 64
@@ -450,31 +451,35 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
                        int L, int Hq, int Hkv, int sink, int window, float scale, uint16_t* __restrict__ out) {
     constexpr int NCH = HD / 64;                  // 64-wide swizzle chunks along hd
     constexpr int kChunk = 128 * 128;             // bytes of a [128 rows x 64] bf16 tile
+    constexpr int kBlk = NCH * kChunk;            // one K (or V) block of 128 keys
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* Qs = sm;                       // NCH x [128 rows x 128 B]
-    uint8_t* Ks = Qs + NCH * kChunk;        // NCH x [128 keys x 128 B]
-    uint8_t* Vs = Ks + NCH * kChunk;        // NCH x [128 keys x 128 B]
-    uint8_t* Ps = Vs + NCH * kChunk;        // 2 x [128 rows x 128 B]  (keys 0-63, 64-127)
+    uint8_t* Kb = Qs + kBlk;                // 2 buffers: K blocks, prefetched one ahead
+    uint8_t* Vb = Kb + 2 * kBlk;            // 2 buffers: V blocks
+    uint8_t* Ps = Vb + 2 * kBlk;            // 2 x [128 rows x 128 B]  (keys 0-63, 64-127)
     uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + 2 * kChunk);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
-    uint64_t* tma_bar = &bars[0];
-    uint64_t* mma_bar = &bars[1];
+    uint64_t* q_bar = &bars[0];
+    uint64_t* k_bar = &bars[1];             // [2]
+    uint64_t* v_bar = &bars[3];             // [2]
+    uint64_t* mma_bar = &bars[5];
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
 
     const int G = Hq / Hkv;
     const int P = 128 / G;  // query positions per tile
     const int tile = blockIdx.x, kvh = blockIdx.y, sq = blockIdx.z;
     const int i0 = tile * P;
     const int64_t row0 = static_cast<int64_t>(sq) * L;
-    const int r = threadIdx.x;  // MMA row = TMEM lane
-    const int warp = r >> 5;
+    const int r = threadIdx.x & 127;  // MMA row = TMEM lane
+    const int half = threadIdx.x >> 7; // column part: keys [64*half, +64), O columns [HD/2*half, +HD/2)
+    const int warp = threadIdx.x >> 5;
     const int g = r / P, i = i0 + r % P;
+    float* stats = reinterpret_cast<float*>(tslot + 4);  // [parts][2][128] (m, l)
 
-    if (r == 0) {
+    if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_q);
         tma_prefetch_desc(&tmap_kv);
-        mbar_init(tma_bar, 1);
-        mbar_init(mma_bar, 1);
+        for (int x = 0; x < 6; ++x) mbar_init(&bars[x], 1);
         mbar_fence_init();
     }
     if (warp == 0) tmem_alloc(tslot, 256);
@@ -483,7 +488,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t tS = tmem, tO = tmem + 128;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
     // Key blocks: [lo, hi] covering the window of the tile, plus block 0 for the sink.
     const int last = min(i0 + P - 1, L - 1);
@@ -492,60 +497,85 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     const int nblk = (b_hi - b_lo + 1) + (sink_block ? 1 : 0);
     auto block_of = [&](int n) { return sink_block ? (n == 0 ? 0 : b_lo + n - 1) : b_lo + n; };
 
-    uint32_t tma_phase = 0, mma_phase = 0;
     const uint32_t idesc_s = idesc_bf16_f32(128, kPfKeys);
     const uint32_t idesc_o = idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
 
-    if (r == 0) {
-        mbar_arrive_expect_tx(tma_bar, NCH * kChunk);
+    // K loads form one sequence over both passes (index ki: pass 1 blocks
+    // 0..nblk-1, then pass 2 again), V loads one over pass 2; each ring is two
+    // buffers deep and issued one use ahead, so TMA latency hides behind the
+    // previous block's MMA + softmax.
+    const int k_total = 2 * nblk;
+    auto load_k = [&](int ki) {  // thread 0
+        const int bb = ki & 1;
+        const int krow = static_cast<int>(row0 + block_of(ki % nblk) * kPfKeys);
+        mbar_arrive_expect_tx(&k_bar[bb], kBlk);
+        for (int c = 0; c < NCH; ++c)
+            tma_load_2d(Kb + bb * kBlk + c * kChunk, &tmap_kv, &k_bar[bb], (Hq + kvh) * HD + c * 64, krow);
+    };
+    auto load_v = [&](int vi) {
+        const int bb = vi & 1;
+        const int krow = static_cast<int>(row0 + block_of(vi) * kPfKeys);
+        mbar_arrive_expect_tx(&v_bar[bb], kBlk);
+        for (int c = 0; c < NCH; ++c)
+            tma_load_2d(Vb + bb * kBlk + c * kChunk, &tmap_kv, &v_bar[bb], (Hq + Hkv + kvh) * HD + c * 64, krow);
+    };
+    const bool leader = threadIdx.x == 0;
+    if (leader) {
+        mbar_arrive_expect_tx(q_bar, NCH * kChunk);
         for (int gg = 0; gg < G; ++gg)
             for (int c = 0; c < NCH; ++c)
-                tma_load_2d(Qs + c * kChunk + gg * P * 128, &tmap_q, tma_bar, (kvh * G + gg) * HD + c * 64,
+                tma_load_2d(Qs + c * kChunk + gg * P * 128, &tmap_q, q_bar, (kvh * G + gg) * HD + c * 64,
                             static_cast<int>(row0 + i0));
+        load_k(0);
+        if (k_total > 1) load_k(1);
+        load_v(0);
+        if (nblk > 1) load_v(1);
     }
-    auto issue_s = [&](int b, bool with_v) {
-        // (thread 0) K (and V) block b -> smem, then S = Q K^T.
-        const int krow = static_cast<int>(row0 + b * kPfKeys);
-        mbar_arrive_expect_tx(tma_bar, (with_v ? 2 : 1) * NCH * kChunk);
-        for (int c = 0; c < NCH; ++c) {
-            tma_load_2d(Ks + c * kChunk, &tmap_kv, tma_bar, (Hq + kvh) * HD + c * 64, krow);
-            if (with_v) tma_load_2d(Vs + c * kChunk, &tmap_kv, tma_bar, (Hq + Hkv + kvh) * HD + c * 64, krow);
-        }
-        mbar_wait(tma_bar, tma_phase);
-        tma_phase ^= 1;
+    uint32_t mma_phase = 0;
+    auto mma_s = [&](int ki) {  // thread 0: S = Q K^T for K load ki
+        const int bb = ki & 1;
+        mbar_wait(&k_bar[bb], (ki >> 1) & 1);
         tc_fence_after();
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 tc_mma_bf16(tS, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
-                            sw128_kmajor_desc(smem_u32(Ks + c * kChunk) + k * 32), idesc_s, (c | k) != 0);
+                            sw128_kmajor_desc(smem_u32(Kb + bb * kBlk + c * kChunk) + k * 32), idesc_s, (c | k) != 0);
         tc_commit(mma_bar);
     };
     auto valid = [&](int j) { return j <= i && j < L && (j < sink || j > i - window); };
+    // A 32-key chunk is entirely retained for this row when its first key is
+    // inside the window and its last is causal and in range.
+    auto all_valid = [&](int j0) { return j0 > i - window && j0 + 31 <= i && j0 + 31 < L; };
 
-    // Pass 1: row max and sum over the retained keys.
+    // Pass 1: row max and sum over the retained keys (each half its columns).
     float m = -INFINITY, l = 0.f;
+    if (leader) mbar_wait(q_bar, 0);
     for (int n = 0; n < nblk; ++n) {
         const int b = block_of(n);
-        if (r == 0) {
-            if (n == 0) {
-                mbar_wait(tma_bar, tma_phase);  // Q landed
-                tma_phase ^= 1;
-            }
-            issue_s(b, false);
-        }
+        if (leader) mma_s(n);
         mbar_wait(mma_bar, mma_phase);
         mma_phase ^= 1;
         __syncwarp();
         tc_fence_after();
-        for (int c0 = 0; c0 < kPfKeys; c0 += 32) {
+        if (leader && n + 2 < k_total) load_k(n + 2);  // its buffer's MMA has completed
+        for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
             float bm = m;
+            const int j0 = b * kPfKeys + c0;
+            if (all_valid(j0)) {
 #pragma unroll
-            for (int x = 0; x < 32; ++x) {
-                v[x] = valid(b * kPfKeys + c0 + x) ? v[x] * scale : -INFINITY;
-                bm = fmaxf(bm, v[x]);
+                for (int x = 0; x < 32; ++x) {
+                    v[x] *= scale;
+                    bm = fmaxf(bm, v[x]);
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 32; ++x) {
+                    v[x] = valid(j0 + x) ? v[x] * scale : -INFINITY;
+                    bm = fmaxf(bm, v[x]);
+                }
             }
             if (bm != -INFINITY) {  // (no divergent exit: the TMEM loads are warp-collective)
                 float sum = 0.f;
@@ -556,31 +586,52 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
             }
         }
         tc_fence_before();
-        __syncthreads();  // S consumed, K buffer free
+        __syncthreads();  // S consumed
+    }
+    // Combine the two column halves' running (max, sum) per row.
+    stats[(half * 2 + 0) * 128 + r] = m;
+    stats[(half * 2 + 1) * 128 + r] = l;
+    __syncthreads();
+    {
+        float mm = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < kPfParts; ++q) mm = fmaxf(mm, stats[(q * 2) * 128 + r]);
+        float ll = 0.f;
+#pragma unroll
+        for (int q = 0; q < kPfParts; ++q) {
+            const float mq = stats[(q * 2) * 128 + r];
+            if (mq != -INFINITY) ll += stats[(q * 2 + 1) * 128 + r] * __expf(mq - mm);
+        }
+        m = mm;
+        l = ll;
     }
     const float inv_l = 1.0f / l;
 
     // Pass 2: P = softmax row (bf16, swizzled A tile), O += P V.
     for (int n = 0; n < nblk; ++n) {
         const int b = block_of(n);
-        if (r == 0) issue_s(b, true);
+        const int ki = nblk + n;
+        if (leader) mma_s(ki);
         mbar_wait(mma_bar, mma_phase);
         mma_phase ^= 1;
         __syncwarp();
         tc_fence_after();
-        for (int c0 = 0; c0 < kPfKeys; c0 += 32) {
+        if (leader && ki + 2 < k_total) load_k(ki + 2);
+        for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
             uint8_t* prow = Ps + (c0 / 64) * kChunk + r * 128;
+            const int j0 = b * kPfKeys + c0;
+            const bool full = all_valid(j0);
 #pragma unroll
             for (int q8 = 0; q8 < 4; ++q8) {
                 uint32_t w[4];
 #pragma unroll
                 for (int h2 = 0; h2 < 4; ++h2) {
                     const int x0 = q8 * 8 + h2 * 2;
-                    const int j = b * kPfKeys + c0 + x0;
-                    const float p0 = valid(j) ? __expf(v[x0] * scale - m) * inv_l : 0.f;
-                    const float p1 = valid(j + 1) ? __expf(v[x0 + 1] * scale - m) * inv_l : 0.f;
+                    const int j = j0 + x0;
+                    const float p0 = (full || valid(j)) ? __expf(v[x0] * scale - m) * inv_l : 0.f;
+                    const float p1 = (full || valid(j + 1)) ? __expf(v[x0 + 1] * scale - m) * inv_l : 0.f;
                     w[h2] = pack2(p0, p1);
                 }
                 const int unit = ((c0 % 64) / 8 + q8) ^ (r & 7);  // 128B swizzle: 16-byte unit ^ row%8
@@ -590,26 +641,29 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         __syncthreads();
-        if (r == 0) {
+        if (leader) {
             tc_fence_after();
+            const int vb = n & 1;
+            mbar_wait(&v_bar[vb], (n >> 1) & 1);
             for (int kc = 0; kc < 2; ++kc)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     tc_mma_bf16(tO, sw128_kmajor_desc(smem_u32(Ps + kc * kChunk) + k * 32),
-                                sw128_mnmajor_desc(smem_u32(Vs) + (kc * 64 + k * 16) * 128, kChunk), idesc_o,
+                                sw128_mnmajor_desc(smem_u32(Vb + vb * kBlk) + (kc * 64 + k * 16) * 128, kChunk), idesc_o,
                                 (n > 0 || kc > 0 || k > 0) ? 1u : 0u);
             tc_commit(mma_bar);
         }
-        mbar_wait(mma_bar, mma_phase);  // P.V done: P, V, S reusable
+        mbar_wait(mma_bar, mma_phase);  // P.V done: P and this V buffer reusable
         mma_phase ^= 1;
         __syncwarp();
         tc_fence_after();
+        if (leader && n + 2 < nblk) load_v(n + 2);
         __syncthreads();
     }
 
     // Epilogue: O row -> out[(seq, i)][(kvh*G + g)*HD + d].
     uint16_t* orow = out + (row0 + i) * static_cast<int64_t>(Hq) * HD + static_cast<int64_t>(kvh * G + g) * HD;
-    for (int c0 = 0; c0 < HD; c0 += 32) {
+    for (int c0 = half * (HD / kPfParts); c0 < (half + 1) * (HD / kPfParts); c0 += 32) {
         float v[32];
         tmem_ld32(tO + lane_off + c0, v);  // warp-collective: every lane, stores predicated
         if (i < L) {
@@ -769,7 +823,7 @@ extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, in
         rc = make_map(&mkv, qkv, static_cast<int64_t>(n_seq) * L, width, kPfKeys);
         if (rc) return rc;
         const int nch = hd / 64;
-        const int smem = 3 * nch * 128 * 128 + 2 * 128 * 128 + 1024 + 64;
+        const int smem = 5 * nch * 128 * 128 + 2 * 128 * 128 + 1024 + 128 + 4096;  // Q, 2 K, 2 V, P, stats
         auto kern = hd == 128 ? attn_prefill_tc_kernel<128> : attn_prefill_tc_kernel<64>;
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         const dim3 grid((L + 128 / G - 1) / (128 / G), Hkv, n_seq);
