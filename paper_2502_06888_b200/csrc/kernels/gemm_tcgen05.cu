@@ -216,6 +216,178 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     }
 }
 
+// Persistent form of the compute-bound (prefill) GEMM: one CTA per SM walks
+// its tiles (stride gridDim.x over the grouped raster order), the TMA ring
+// runs continuously across tiles, and two TMEM accumulators alternate so a
+// tile's epilogue (SwiGLU / residual / store) overlaps the next tile's MMAs.
+template <int BN, int EPI, bool PAIRED, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_persistent_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                        int a_row0, int M, int num_kb, int b_half_rows, int n_tiles, int m_tiles,
+                        uint16_t* __restrict__ c, int ldc, const uint16_t* __restrict__ r) {
+    using C = Cfg<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    constexpr uint32_t kCols = 2 * BN;    // two accumulators
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int total = n_tiles * m_tiles;
+    auto tile_of = [&](int lin, int& n_tile, int& m_tile) {
+        constexpr int kGroupM = 16;
+        const int per_group = kGroupM * n_tiles;
+        const int first_m = lin / per_group * kGroupM;
+        const int group_m = min(kGroupM, m_tiles - first_m);
+        const int within = lin % per_group;
+        m_tile = first_m + within % group_m;
+        n_tile = within / group_m;
+    };
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_a);
+        tma_prefetch_desc(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int lin = blockIdx.x; lin < total; lin += gridDim.x) {
+                int n_tile, m_tile;
+                tile_of(lin, n_tile, m_tile);
+                const int a_row = a_row0 + m_tile * BM;
+                for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* sa = smem + s * C::kStageBytes;
+                    uint8_t* sb = sa + C::kABytes;
+                    mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+                    tma_load_2d(sa, &tmap_a, &full[s], kb * BK, a_row);
+                    if constexpr (PAIRED) {
+                        tma_load_2d(sb, &tmap_b, &full[s], kb * BK, n_tile * (BN / 2));
+                        tma_load_2d(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], kb * BK, b_half_rows + n_tile * (BN / 2));
+                    } else {
+                        tma_load_2d(sb, &tmap_b, &full[s], kb * BK, n_tile * BN);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+            int it = 0, lt = 0;
+            for (int lin = blockIdx.x; lin < total; lin += gridDim.x, ++lt) {
+                const int b = lt & 1;
+                mbar_wait(&acc_empty[b], ((lt >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t acc = tmem_base + b * BN;
+                for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
+                    const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc_mma_bf16(acc, sw128_kmajor_desc(sa + k * 32), sw128_kmajor_desc(sb + k * 32), idesc,
+                                    (kb | k) != 0);
+                    tc_commit(&empty[s]);
+                }
+                tc_commit(&acc_full[b]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int quarter = warp & 3;
+        int lt = 0;
+        for (int lin = blockIdx.x; lin < total; lin += gridDim.x, ++lt) {
+            int n_tile, m_tile;
+            tile_of(lin, n_tile, m_tile);
+            const int b = lt & 1;
+            mbar_wait(&acc_full[b], (lt >> 1) & 1);
+            tc_fence_after();
+            const int row = m_tile * BM + quarter * 32 + lane;
+            const uint32_t lane_addr = tmem_base + b * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+            const bool live = row < M;
+            if constexpr (EPI == kSwiGLU) {
+                constexpr int HALF = BN / 2;
+                uint16_t* out = c + static_cast<int64_t>(row) * ldc + n_tile * HALF;
+#pragma unroll 1
+                for (int col = 0; col < HALF; col += 16) {
+                    float g[16], u[16];
+                    tmem_ld16(lane_addr + col, g);
+                    tmem_ld16(lane_addr + HALF + col, u);
+                    if (live) {
+                        uint32_t packed[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float a0 = g[2 * i] / (1.0f + expf(-g[2 * i])) * u[2 * i];
+                            const float a1 = g[2 * i + 1] / (1.0f + expf(-g[2 * i + 1])) * u[2 * i + 1];
+                            packed[i] = pack2(a0, a1);
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(out + col);
+                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+                    }
+                }
+            } else {
+                uint16_t* out = c + static_cast<int64_t>(row) * ldc + n_tile * BN;
+                const uint16_t* res = EPI == kResidual ? r + static_cast<int64_t>(row) * ldc + n_tile * BN : nullptr;
+#pragma unroll 1
+                for (int col = 0; col < BN; col += 16) {
+                    float v[16];
+                    tmem_ld16(lane_addr + col, v);
+                    if (live) {
+                        if constexpr (EPI == kResidual) {
+                            const uint4* rp = reinterpret_cast<const uint4*>(res + col);
+                            const uint4 r0 = rp[0], r1 = rp[1];
+                            const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                v[2 * i] += bf2f(static_cast<uint16_t>(rw[i] & 0xffffu));
+                                v[2 * i + 1] += bf2f(static_cast<uint16_t>(rw[i] >> 16));
+                            }
+                        }
+                        uint32_t packed[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) packed[i] = pack2(v[2 * i], v[2 * i + 1]);
+                        uint4* dst = reinterpret_cast<uint4*>(out + col);
+                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kCols);
+    }
+}
+
 // Sum the K-split partials in split order (deterministic) and apply the
 // epilogue. Each thread produces 4 consecutive output columns of one row.
 template <int EPI>
@@ -788,6 +960,31 @@ int launch(const Launch& L, cudaStream_t stream) {
     return check_launch();
 }
 
+int g_persistent = 1;  // kl_tune(KL_TUNE_GEMM_PERSISTENT, ...)
+int sm_count();
+
+template <int BN, int EPI, bool PAIRED, int STAGES>
+int launch_persistent(const Launch& L, cudaStream_t stream) {
+    using C = Cfg<BN, STAGES>;
+    CUtensorMap ma, mb;
+    int rc = make_map(&ma, L.a, L.a_rows, L.K, BM);
+    if (rc) return rc;
+    rc = make_map(&mb, L.b, L.b_rows, L.K, PAIRED ? BN / 2 : BN);
+    if (rc) return rc;
+    static bool configured = false;
+    if (!configured) {
+        KL_CUDA_TRY(cudaFuncSetAttribute(gemm_persistent_tcgen05<BN, EPI, PAIRED, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes + 64));
+        configured = true;
+    }
+    const int m_tiles = (L.M + BM - 1) / BM;
+    const int total = L.n_tiles * m_tiles;
+    const int grid = std::min(total, sm_count());
+    gemm_persistent_tcgen05<BN, EPI, PAIRED, STAGES><<<grid, kThreads, C::kSmemBytes + 64, stream>>>(
+        ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK, L.b_half_rows, L.n_tiles, m_tiles, L.c, L.ldc, L.r);
+    return check_launch();
+}
+
 template <int EPI>
 int reduce(const Launch& L, int n_out, int pair_bn, cudaStream_t stream) {
     const int64_t threads = static_cast<int64_t>(L.M) * (n_out / 4);
@@ -985,6 +1182,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
         case KL_TUNE_PREFILL_TC: g_prefill_tc = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
+        case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_ctas = value;
@@ -1046,14 +1244,20 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
         if (epilogue == kResidual) return launch<128, kResidual, false, 3>(L, stream);
         return launch<128, kStore, false, 3>(L, stream);
     }
-    // Compute-bound regime (prefill / large M): 256-wide tiles, deep pipeline.
+    // Compute-bound regime (prefill / large M): 256-wide tiles, deep pipeline;
+    // persistent with double-buffered accumulators once there are more tiles
+    // than SMs.
+    const bool persist = g_persistent && static_cast<int64_t>(N / 256) * m_tiles > sm_count();
     if (epilogue == kSwiGLU) {
         L.n_tiles = N / 256;
         L.b_half_rows = N / 2;
-        return launch<256, kSwiGLU, true, 4>(L, stream);
+        return persist ? launch_persistent<256, kSwiGLU, true, 4>(L, stream) : launch<256, kSwiGLU, true, 4>(L, stream);
     }
     if (N % 256 == 0) {
         L.n_tiles = N / 256;
+        if (persist)
+            return epilogue == kResidual ? launch_persistent<256, kResidual, false, 4>(L, stream)
+                                         : launch_persistent<256, kStore, false, 4>(L, stream);
         return epilogue == kResidual ? launch<256, kResidual, false, 4>(L, stream)
                                      : launch<256, kStore, false, 4>(L, stream);
     }

@@ -61,6 +61,7 @@ TUNE_STREAM_CTAS_PER_SM = 4
 TUNE_PDL = 5
 TUNE_PREFILL_TC = 6
 TUNE_STREAM_WHOLE_TILES = 7
+TUNE_GEMM_PERSISTENT = 8
 
 
 def tune(knob, value):

@@ -409,3 +409,32 @@ def test_expert_ffn_q4(K, cuda):
     ref = orc.bits_to_f32(orc.expert_ffn(np.ascontiguousarray(x[off:off + M]), d13, d2))
     close_bf16(to_bits(y)[off:off + M], ref)
     assert not to_bits(y)[:off].any() and not to_bits(y)[off + M:].any()
+
+
+@pytest.mark.parametrize("M,N,Kd,epi", [(2048, 4096, 512, 0), (2600, 2560, 256, 1), (2048, 4096, 512, 2),
+                                        (1100, 7168, 1024, 2)])
+def test_gemm_persistent_large_m(K, cuda, M, N, Kd, epi):
+    """Compute-bound (prefill) GEMMs with more tiles than SMs take the
+    persistent kernel (grouped raster, double-buffered TMEM accumulators):
+    store / residual / SwiGLU against the oracle, and equal to the
+    one-tile-per-CTA kernel's result within the GEMM tolerance."""
+    a = orc.normal_bf16(M * Kd, 101, 1.0).reshape(M, Kd)
+    b = orc.normal_bf16(N * Kd, 102, 0.03).reshape(N, Kd)
+    n_out = N // 2 if epi == 2 else N
+    r = orc.normal_bf16(M * n_out, 103, 1.0).reshape(M, n_out) if epi == 1 else None
+    ad, bd = to_dev(a, cuda), to_dev(b, cuda)
+    c = K.gemm(ad, bd, residual=to_dev(r, cuda) if r is not None else None, epilogue=epi)
+    K.tune(K.TUNE_GEMM_PERSISTENT, 0)
+    try:
+        c2 = K.gemm(ad, bd, residual=to_dev(r, cuda) if r is not None else None, epilogue=epi)
+    finally:
+        K.tune(K.TUNE_GEMM_PERSISTENT, 1)
+    torch.cuda.synchronize()
+    if epi == 2:
+        g = orc.gemm_f32(a, np.ascontiguousarray(b[:n_out])).astype(np.float64)
+        u = orc.gemm_f32(a, np.ascontiguousarray(b[n_out:])).astype(np.float64)
+        ref = g / (1.0 + np.exp(-g)) * u
+    else:
+        ref = orc.gemm_f32(a, b) + (orc.bits_to_f32(r) if epi == 1 else 0)
+    close_bf16(to_bits(c), ref)
+    assert torch.equal(c, c2)  # same per-tile arithmetic, different schedule
