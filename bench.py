@@ -194,14 +194,14 @@ def measured_tflops():
 
 
 def prefill_variant(args, link):
-    """BASELINE configs[2]: prefill of a batch group (bs 16 x n 8 x 512-token
-    prompts = 65,536 tokens) through all layers under the same HBM cap, experts
+    """BASELINE configs[2]: prefill of a batch group (bs 32 x n 8 x 512-token
+    prompts = 131,072 tokens) through all layers under the same HBM cap, experts
     streamed; one warm-up pass then one timed pass. Reports prefill tokens/s,
     the pipeline bubble fraction and the expert GEMMs' tensor-pipe rate
     (FLOPs / measured compute time) against the bf16 peak."""
     from paper_2502_06888_b200.engine import Engine
     import numpy as np
-    bs, n, P = 16, 8, args.prompt_len
+    bs, n, P = 32, 8, args.prompt_len
     cfg = {"model": {"preset": args.model},
            "workload": {"batch_size": bs, "n_batches": n, "prompt_len": P, "gen_len": 2},
            "hbm_cap_bytes": int(args.hbm_cap),
