@@ -832,6 +832,20 @@ std::string Engine::report(const std::string& what) {
             j["violations"] = v;
             if (skipped) j["unexecuted_step_findings"] = skipped;
         }
+    } else if (what == "ledger") {
+        // Reference memory accounting (MemoryLedger, placement.cpp:257-292)
+        // replayed on the measured timeline of the executed window; VRAM
+        // capacity = this engine's HBM cap, not enforced (audit).
+        std::array<byte_count, 4> caps{cfg_.hbm_cap, cfg_.host_dram, INT64_MAX / 4, INT64_MAX / 4};
+        MemoryLedger ledger(caps, false);
+        const std::int64_t carried = detail::replay_ledger_on_timeline(s, tl, plan_, ledger);
+        j["vram_high_water"] = ledger.high_water(Tier::vram);
+        j["vram_capacity"] = cfg_.hbm_cap;
+        j["within_capacity"] = ledger.high_water(Tier::vram) <= cfg_.hbm_cap;
+        j["dram_high_water"] = ledger.high_water(Tier::dram);
+        j["carried_in_frees"] = carried;
+        j["arena_bytes_used"] = arena_used_;
+        j["memory_csv"] = memory_timeline_csv(ledger);
     } else if (what == "diag") {
         // Expert-op breakdown (KL_ENGINE_DIAG=1): [start -> FFN launch, FFN kernels, FFN -> end] in us.
         j["expert_op_us"] = diag_rows_;

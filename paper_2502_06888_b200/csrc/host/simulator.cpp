@@ -263,6 +263,55 @@ class Sim {
 
 namespace detail {
 
+std::int64_t replay_ledger_on_timeline(const Schedule& schedule, std::span<const SimEvent> timeline,
+                                       const PipelinePlan& plan, MemoryLedger& ledger) {
+    struct Eff {
+        duration_ps time;
+        bool is_alloc;
+        Tier tier;
+        byte_count bytes;
+        std::int64_t seq;
+        const std::string* tag;
+    };
+    std::vector<Eff> effs;
+    std::int64_t seq = 0;
+    for (const SimEvent& ev : timeline) {
+        const StreamOp& op = schedule.ops[ev.op_id];
+        for (const LedgerEffect& e : op.ledger)
+            effs.push_back({e.when == LedgerEffect::When::at_start ? ev.start : ev.end, e.is_alloc, e.tier, e.bytes,
+                            seq++, &e.tag});
+    }
+    const ModelSpec& m = plan.model;
+    ledger.alloc(plan.placement.activation_tier,
+                 m.kv_bytes_per_token * static_cast<byte_count>(schedule.batch_size) * schedule.n_batches, "activations",
+                 0);
+    for (int j = 0; j < plan.placement.n_layers; ++j) {
+        if (plan.placement.expert_tier[j] == Tier::vram)
+            ledger.alloc(Tier::vram, m.expert_bytes * m.n_experts_per_layer, "res:e:" + std::to_string(j), 0);
+        if (plan.placement.gate_tier[j] == Tier::vram)
+            ledger.alloc(Tier::vram, m.gate_bytes, "res:g:" + std::to_string(j), 0);
+        if (plan.placement.attention_tier[j] == Tier::vram)
+            ledger.alloc(Tier::vram, m.attention_bytes, "res:a:" + std::to_string(j), 0);
+    }
+    std::stable_sort(effs.begin(), effs.end(), [](const Eff& a, const Eff& b) {
+        if (a.time != b.time) return a.time < b.time;
+        if (a.is_alloc != b.is_alloc) return !a.is_alloc;
+        return a.seq < b.seq;
+    });
+    std::int64_t carried = 0;
+    for (const Eff& e : effs) {
+        if (e.is_alloc) {
+            if (ledger.live(*e.tag)) ledger.free(*e.tag, e.time);  // re-allocation of a carried-in tag
+            ledger.alloc(e.tier, e.bytes, *e.tag, e.time);
+        } else if (ledger.live(*e.tag)) {
+            ledger.free(*e.tag, e.time);
+        } else {
+            ++carried;
+        }
+    }
+    return carried;
+}
+
 void finalize_metrics(const Schedule& schedule, std::span<const SimEvent> timeline,
                       byte_count peak_vram, RunMetrics& m) {
     m = RunMetrics{};

@@ -52,6 +52,15 @@ def test_replay_op_log_equals_reference_schedule(cuda, cap, variant, skew, quant
     assert "error" not in ref, ref
     assert got == ref["schedule_text"]
     assert eng.report("validate")["violations"] == []
+    # The reference's memory accounting replayed on the measured timeline:
+    # the bounded slot pool keeps it within the HBM cap.
+    # (Quantised runs keep Q4T bytes in HBM, while the reference ledger books
+    # streamed experts at their native size, so only the bf16 runs compare.)
+    led = eng.report("ledger")
+    assert led["carried_in_frees"] == 0
+    if not quant:
+        assert led["within_capacity"], (led["vram_high_water"], led["vram_capacity"])
+    assert led["memory_csv"].startswith("time")
     m = eng.report("metrics")
     assert 0.0 <= m["bubble_fraction"] < 1.0
     assert m["tokens_generated"] == eng.n_seqs * cfg["workload"]["gen_len"]
