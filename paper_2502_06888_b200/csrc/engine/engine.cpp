@@ -6,7 +6,10 @@
 //   op semantics    Builder::emit_* (schedule.cpp:155-372)
 #include "engine.hpp"
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <cerrno>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -122,6 +125,7 @@ EngineConfig parse_config(const std::string& text) {
     c.warmup_seed = j.value("warmup_seed", c.warmup_seed);
     c.weight_seed = j.value("weight_seed", c.weight_seed);
     c.host_distinct_layers = j.value("host_distinct_layers", 0);
+    c.disk_dir = j.value("disk_dir", std::string());
     c.expert_slots = j.value("expert_slots", 0);
     c.ffn_chunk_rows = j.value("ffn_chunk_rows", 4096);
     c.record_trace = j.value("record_trace", true);
@@ -230,6 +234,7 @@ Engine::~Engine() {
     for (cudaEvent_t e : pool_.release) (void)e;
     if (arena_) cudaFree(arena_);
     for (void* p : host_blocks_) cudaFreeHost(p);
+    if (disk_fd_ >= 0) ::close(disk_fd_);
 }
 
 void* Engine::take(byte_count bytes) {
@@ -341,8 +346,8 @@ void Engine::plan_memory() {
     }
     kv_offload_ = plan_.placement.kv_tier == Tier::dram;
     if (kv_offload_ && ep_) throw ConfigError("engine: KV offload is not combined with expert parallelism yet");
-    if (plan_.placement.cpu_window_L > 0 || plan_.placement.any_disk())
-        throw ConfigError("engine: disk-tier placement (staging window) is not executed by this engine");
+    if (plan_.placement.any_disk() && ep_)
+        throw ConfigError("engine: disk-tier placement is not combined with expert parallelism yet");
     kv_cap_ = plan_.placement.kv_retained_tokens;
     kv_sink_ = cfg_.retention.mode == KvRetentionPolicy::Mode::streaming ? std::min(cfg_.retention.sink_tokens, kv_cap_ - 1) : 0;
     kv_bytes_layer_ = kv_offload_ ? 0
@@ -481,7 +486,8 @@ void Engine::allocate_host() {
     const bool whole_layer = cfg_.variant == Variant::multibatch_full_prefetch;
     std::vector<int> streamed;
     for (int l = 0; l < L; ++l)
-        if (plan_.placement.expert_tier[l] != Tier::vram || whole_layer) streamed.push_back(l);
+        if ((plan_.placement.expert_tier[l] != Tier::vram || whole_layer) && plan_.placement.expert_tier[l] != Tier::disk)
+            streamed.push_back(l);
     const int R = cfg_.host_distinct_layers > 0 ? std::min<int>(cfg_.host_distinct_layers, streamed.size())
                                                 : static_cast<int>(streamed.size());
     std::vector<void*> blocks(R, nullptr);
@@ -514,9 +520,23 @@ void Engine::allocate_host() {
         return p;
     };
     for (int l = 0; l < L; ++l) {
-        if (plan_.placement.attention_tier[l] != Tier::vram)
+        if (plan_.placement.attention_tier[l] == Tier::dram)
             host_attn_[l] = static_cast<uint16_t*>(pinned(attn_slot_bytes_));
-        host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
+        if (plan_.placement.gate_tier[l] != Tier::disk) host_gate_[l] = static_cast<uint16_t*>(pinned(spec_.gate_bytes));
+    }
+    // Disk tier: the staging window's pinned slots and the backing file.
+    window_slot_of_.assign(L, -1);
+    window_slot_.clear();
+    window_free_.clear();
+    if (plan_.placement.any_disk()) {
+        const int wl = std::max(1, plan_.placement.cpu_window_L);
+        for (int s = 0; s < wl; ++s) {
+            window_slot_.push_back(static_cast<char*>(pinned(plan_.placement.per_layer_disk_bytes_max)));
+            window_free_.push_back(s);
+        }
+        bounce_bytes_ = std::max({expert_slot_bytes_, attn_slot_bytes_, spec_.gate_bytes});
+        for (auto& b : bounce_) b = static_cast<char*>(pinned(bounce_bytes_));
+        open_disk_store();
     }
     const int n = plan_.n_batches;
     if (kv_offload_) {
@@ -567,6 +587,16 @@ void Engine::init_weights() {
     };
     std::vector<char> host_done(host_blocks_.size(), 0);
     for (int l = 0; l < D_.L; ++l) {
+        // Disk-tier parts of the layer are assembled in window slot 0 (no
+        // stage op has run yet) and written to the layer's file region.
+        const bool on_disk = disk_fd_ >= 0 && disk_bytes(l) > 0;
+        auto disk_part = [&](TensorClass cls, byte_count extra) {
+            return reinterpret_cast<uint16_t*>(window_slot_[0] + disk_part_offset(l, cls) + extra);
+        };
+        const bool exp_disk = plan_.placement.expert_tier[l] == Tier::disk;
+        uint16_t* attn_dst = plan_.placement.attention_tier[l] == Tier::disk ? disk_part(TensorClass::attention, 0)
+                                                                              : host_attn_[l];
+        uint16_t* gate_dst = plan_.placement.gate_tier[l] == Tier::disk ? disk_part(TensorClass::gate, 0) : host_gate_[l];
         for (int e = 0; e < El_; ++e) {
             // Seeds follow the GLOBAL expert id so every EP shard holds the
             // same weights the single-GPU engine would.
@@ -581,6 +611,9 @@ void Engine::init_weights() {
                         cuda_check(cudaMemcpyAsync(h, r, spec_.expert_bytes, cudaMemcpyDeviceToHost, st), "d2h");
                     }
                 }
+            } else if (exp_disk) {
+                kl_check(kl_fill_normal_bf16(stage, D_.expert_elems(), seed, sd, st), "init expert");
+                to_host(disk_part(TensorClass::expert, expert_slot_bytes_ * e), true);
             } else if (uint16_t* h = host_expert_[l * El_ + e]) {
                 // Aliased host layers are filled once, by their first user.
                 bool first = true;
@@ -596,10 +629,22 @@ void Engine::init_weights() {
             kl_check(kl_fill_normal_bf16(res_attn_[l], D_.attention_elems(), aseed, sd, st), "init attn");
         } else {
             kl_check(kl_fill_normal_bf16(stage, D_.attention_elems(), aseed, sd, st), "init attn");
-            to_host(host_attn_[l], false);
+            to_host(attn_dst, false);
         }
         kl_check(kl_fill_normal_bf16(stage, D_.gate_elems(), tensor_seed(ws, kKindGate, l, 0), sd, st), "init gate");
-        cuda_check(cudaMemcpyAsync(host_gate_[l], stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+        cuda_check(cudaMemcpyAsync(gate_dst, stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+        if (on_disk) {
+            cuda_check(cudaStreamSynchronize(st), "init sync");
+            const char* src = window_slot_[0];
+            int64_t left = disk_bytes(l), off = disk_off_[l];
+            while (left > 0) {
+                const ssize_t w = ::pwrite(disk_fd_, src, static_cast<size_t>(left), off);
+                if (w <= 0) throw std::runtime_error(std::string("engine: disk store write: ") + std::strerror(errno));
+                src += w;
+                off += w;
+                left -= w;
+            }
+        }
     }
     // Correlation table (warm-up) and marginal to HBM.
     if (D_.L > 1)
@@ -683,6 +728,14 @@ std::string Engine::describe() const {
     j["gate_bytes"] = spec_.gate_bytes;
     j["shared_experts"] = {{"n", D_.n_shared}, {"f", D_.f_shared}};
     j["host_pinned_blocks"] = host_blocks_.size();
+    {
+        std::vector<int> dl;
+        for (int l = 0; l < D_.L; ++l) dl.push_back(plan_.placement.disk_bytes_of_layer(l, spec_, cfg_.quant) > 0 ? 1 : 0);
+        j["disk_layers"] = dl;
+        j["cpu_window_L"] = plan_.placement.cpu_window_L;
+        j["disk_store_bytes"] = disk_bytes_total_;
+        j["window_slot_bytes"] = plan_.placement.per_layer_disk_bytes_max;
+    }
     // Everything needed to rebuild the same plan/schedule with the reference.
     j["spec"] = {{"n_layers", spec_.n_layers}, {"n_experts", spec_.n_experts_per_layer}, {"top_k", spec_.top_k},
                  {"expert_bytes", spec_.expert_bytes}, {"attention_bytes", spec_.attention_bytes},

@@ -20,6 +20,7 @@
 #include <cuda_runtime_api.h>
 
 #include <array>
+#include <atomic>
 #include <cstdint>
 #include <deque>
 #include <map>
@@ -80,6 +81,7 @@ struct EngineConfig {
     std::string ep_nccl_id;         // 256 hex chars of ncclUniqueId (world > 1)
     bool prefill = true;
     std::optional<moesim::QuantConfig> quant;  // 4-bit streamed experts / attention (Q4T)
+    std::string disk_dir;           // disk-tier store directory (default $TMPDIR, else /tmp)
 };
 
 EngineConfig parse_config(const std::string& json_text);
@@ -183,6 +185,38 @@ class Engine {
     uint16_t* wscratch_ = nullptr;        // Q4: bf16 staging / dequantised weights for M > 256
     std::vector<uint16_t*> host_attn_;    // [L]
     std::vector<uint16_t*> host_gate_;    // [L]
+
+    // Disk tier + DRAM staging window (placement.cpp window_advance,
+    // schedule.cpp advance_window / stage_prologue): disk-resident tensors of
+    // a layer live in one unlinked file region [experts | gate | attention]
+    // (only the disk-tier parts, in streamed format); window_stage ops read a
+    // layer's region into one of cpu_window_L pinned window slots with pread
+    // from a host function on the cpu_stage stream, and that layer's H2D
+    // loads take their source from the slot.
+    struct StageJob {
+        Engine* eng;
+        char* dst;
+        int64_t off, bytes;
+    };
+    int disk_fd_ = -1;
+    std::vector<int64_t> disk_off_;       // [L] file offset of the layer's region
+    std::vector<char*> window_slot_;      // [cpu_window_L] pinned, per_layer_disk_bytes_max each
+    std::vector<int> window_slot_of_;     // [L] slot holding the layer (emission order), -1 none
+    std::deque<int> window_free_;
+    std::array<char*, 2> bounce_{};       // per load stream: direct reads of unstaged disk tensors
+    byte_count bounce_bytes_ = 0;
+    std::deque<StageJob> stage_jobs_;     // stable addresses for in-flight host functions
+    std::atomic<int> stage_errno_{0};
+    std::atomic<int64_t> disk_bytes_read_{0};
+    int64_t disk_bytes_total_ = 0, direct_reads_ = 0, direct_bytes_ = 0;
+    byte_count disk_bytes(int layer) const;
+    byte_count disk_part_offset(int layer, moesim::TensorClass cls) const;
+    // Host source of a streamed tensor for an H2D load enqueued on `st`.
+    const void* load_src(moesim::TensorClass cls, int layer, int e, cudaStream_t st);
+    void enqueue_disk_read(char* dst, int64_t off, int64_t bytes, cudaStream_t st);
+    void open_disk_store();
+    void stage_read(const StageJob& job);
+    static void CUDART_CB stage_host_fn(void* job);
     int32_t* host_report_ = nullptr;
     int32_t* host_idx_ = nullptr;
     int32_t* host_tokens_ = nullptr;

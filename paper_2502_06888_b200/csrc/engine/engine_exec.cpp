@@ -237,6 +237,9 @@ void Engine::collect_step_times() {
     std::fill(gate_slot_release_.begin(), gate_slot_release_.end(), nullptr);
     std::fill(kv_slot_release_.begin(), kv_slot_release_.end(), nullptr);
     if (!kv_slot_of_.empty()) throw AccountingError("engine: KV slot still mapped at the end of a step");
+    stage_jobs_.clear();
+    if (const int e = stage_errno_.exchange(0))
+        throw std::runtime_error(std::string("engine: disk staging read failed: ") + std::strerror(e));
 }
 
 // Enqueue every emitted-but-not-executed op. Cold computes of a reorder
@@ -300,14 +303,14 @@ void Engine::exec(std::int32_t id) {
                 const int s = pick2(attn_slot_busy_);
                 wait_release(attn_slot_release_[s]);
                 cuda_check(cudaEventRecord(op_start_[id], st), "record");
-                cuda_check(cudaMemcpyAsync(attn_slot_[s], host_attn_[op.layer], attn_slot_bytes_,
+                cuda_check(cudaMemcpyAsync(attn_slot_[s], load_src(TensorClass::attention, op.layer, 0, st), attn_slot_bytes_,
                                            cudaMemcpyHostToDevice, st), "h2d attention");
                 attn_slot_of_[op.layer] = s;
             } else if (op.cls == TensorClass::gate) {
                 const int s = pick2(gate_slot_busy_);
                 wait_release(gate_slot_release_[s]);
                 cuda_check(cudaEventRecord(op_start_[id], st), "record");
-                cuda_check(cudaMemcpyAsync(gate_slot_[s], host_gate_[op.layer], spec_.gate_bytes,
+                cuda_check(cudaMemcpyAsync(gate_slot_[s], load_src(TensorClass::gate, op.layer, 0, st), spec_.gate_bytes,
                                            cudaMemcpyHostToDevice, st), "h2d gate");
                 gate_slot_of_[op.layer] = s;
             } else {
@@ -321,10 +324,10 @@ void Engine::exec(std::int32_t id) {
                     slots.push_back(x);
                 }
                 cuda_check(cudaEventRecord(op_start_[id], st), "record");
-                cuda_check(cudaMemcpyAsync(gate_slot_[s], host_gate_[op.layer], spec_.gate_bytes,
+                cuda_check(cudaMemcpyAsync(gate_slot_[s], load_src(TensorClass::gate, op.layer, 0, st), spec_.gate_bytes,
                                            cudaMemcpyHostToDevice, st), "h2d gate");
                 for (size_t e = 0; e < E; ++e) {
-                    cuda_check(cudaMemcpyAsync(pool_.ptr[slots[e]], host_expert_[op.layer * E + e], expert_slot_bytes_,
+                    cuda_check(cudaMemcpyAsync(pool_.ptr[slots[e]], load_src(TensorClass::expert, op.layer, static_cast<int>(e), st), expert_slot_bytes_,
                                                cudaMemcpyHostToDevice, st), "h2d moe");
                     expert_slot_of_[{op.layer, static_cast<int>(e)}] = slots[e];
                 }
@@ -337,7 +340,7 @@ void Engine::exec(std::int32_t id) {
             const int s = pool_.acquire();
             if (pool_.has_release[s]) wait_release(pool_.release[s]);
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
-            cuda_check(cudaMemcpyAsync(pool_.ptr[s], host_expert_[op.layer * E + op.expert], expert_slot_bytes_,
+            cuda_check(cudaMemcpyAsync(pool_.ptr[s], load_src(TensorClass::expert, op.layer, op.expert, st), expert_slot_bytes_,
                                        cudaMemcpyHostToDevice, st), "h2d expert");
             expert_slot_of_[{op.layer, op.expert}] = s;
             break;
@@ -416,6 +419,26 @@ void Engine::exec(std::int32_t id) {
                                          cfg_.workload.batch_size, cudaMemcpyDeviceToHost, st), "d2h kv");
             kv_slot_release_[slot] = op_end_[id];
             kv_slot_of_.erase(it);
+            break;
+        }
+        case OpKind::window_stage: {
+            // Evict op.batch's window slot (its loads of this pass are the
+            // op's deps), then read the staged layer's disk region into a
+            // free slot on the cpu_stage stream (schedule.cpp:374-426).
+            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            const int evict = op.batch;
+            if (evict >= 0 && window_slot_of_[evict] >= 0) {
+                window_free_.push_back(window_slot_of_[evict]);
+                window_slot_of_[evict] = -1;
+            }
+            if (disk_bytes(op.layer) > 0) {
+                if (window_free_.empty()) throw AccountingError("engine: DRAM staging window has no free slot");
+                if (window_slot_of_[op.layer] >= 0) throw AccountingError("engine: layer staged twice");
+                const int slot = window_free_.front();
+                window_free_.pop_front();
+                window_slot_of_[op.layer] = slot;
+                enqueue_disk_read(window_slot_[slot], disk_off_[op.layer], disk_bytes(op.layer), st);
+            }
             break;
         }
         case OpKind::compute_attention:
@@ -782,6 +805,22 @@ std::string Engine::report(const std::string& what) {
         j["h2d_gbs_makespan"] = m.makespan > 0 ? h2d / (m.makespan * 1e-12) / 1e9 : 0.0;
         j["expert_loads"] = n_expert_loads;
         j["expert_load_busy_ps"] = expert_busy;
+        {
+            int64_t n_stage = 0, stage_bytes = 0;
+            duration_ps stage_busy = 0;
+            for (const SimEvent& e : tl)
+                if (s.ops[e.op_id].kind == OpKind::window_stage) {
+                    ++n_stage;
+                    stage_bytes += e.bytes;
+                    stage_busy += e.end - e.start;
+                }
+            j["window_stages"] = n_stage;
+            j["disk_stage_bytes"] = stage_bytes;
+            j["disk_bytes_read"] = disk_bytes_read_.load();
+            j["disk_direct_reads"] = direct_reads_;
+            j["disk_direct_bytes"] = direct_bytes_;
+            j["disk_gbs_busy"] = stage_busy > 0 ? stage_bytes / (stage_busy * 1e-12) / 1e9 : 0.0;
+        }
         j["launches"] = launches_;
         int64_t n_expert_ops = 0, expert_rows = 0;
         for (const SimEvent& e : tl)

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_engine_gpu.py -m gpu -x -q 2>&1 | tail -15
+timeout 600 python -m pytest tests/test_engine_gpu.py -m gpu -q -k "disk" 2>&1 | tail -25
