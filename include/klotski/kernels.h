@@ -72,6 +72,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */
 #define KL_TUNE_PDL 5 /* 1 = weight-streaming GEMMs use programmatic dependent launch (default) */
 #define KL_TUNE_PREFILL_TC 6 /* 1 = tcgen05 prefill attention (default), 0 = CUDA-core fallback */
+#define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */
 /* Process-wide tuning knobs for benchmarking (not thread-safe). */
@@ -221,6 +222,15 @@ int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, c
                       int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache,
                       const uint16_t* v_cache, int cap, int sink, float scale, uint16_t* out,
                       void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+/* Same, with the cache extent: k_cache / v_cache hold cache_seqs sequences of
+ * cap slots (rows = cache_seqs * cap). With the extent known the persistent
+ * tensor-core kernel runs (3D TMA boxes of 16 slots, mma.sync scores and
+ * p.V, fixed-order segment merge); cache_seqs = 0 selects the per-chunk
+ * CUDA-core kernel, which kl_attn_decode_ws always uses. */
+int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq, int64_t T, int Hq,
+                       int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache, int64_t cache_seqs, int cap,
+                       int sink, float scale, uint16_t* out, void* workspace, int64_t workspace_bytes,
+                       cudaStream_t stream);
 
 /* Prefill (chunk) attention: T = n_seq * L query rows laid out [seq][L]; keys
  * and values read from the same qkv rows (post-rope), causal with the same

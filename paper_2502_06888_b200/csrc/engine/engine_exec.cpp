@@ -515,8 +515,9 @@ void Engine::exec_attention(const StreamOp& op) {
         kl_check(kl_attn_prefill(qkv_, cfg_.workload.batch_size, cfg_.workload.prompt_len, D_.Hq, D_.Hkv, D_.hd,
                                  kv_cap_, kv_sink_, scale, ao_, cs), "prefill attention");
     else
-        kl_check(kl_attn_decode_ws(qkv_, D_.qkv_width(), tok_pos_ + row0, seq_idx, tpb, D_.Hq, D_.Hkv, D_.hd,
-                                   kc, vc, kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
+        kl_check(kl_attn_decode_ws2(qkv_, D_.qkv_width(), tok_pos_ + row0, seq_idx, tpb, D_.Hq, D_.Hkv, D_.hd, kc, vc,
+                                    static_cast<int64_t>(cfg_.workload.batch_size) * (kv_offload_ ? 1 : plan_.n_batches),
+                                    kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
                  "decode attention");
     if (fused)
         kl_check(kl_gemm_q4(ao_, tpb, 0, tpb, D_.Hq * D_.hd, q4o, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),

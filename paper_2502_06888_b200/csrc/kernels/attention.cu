@@ -9,6 +9,7 @@
 // Decode attention is HBM-bound (K and V of the retained slots are read once
 // per (token, kv head); query heads of one GQA group share the reads through
 // L1): algorithmic bytes per (sequence, layer) = retained * Hkv*hd*2 * 2.
+#include <atomic>
 #include <cstdint>
 
 #include "common.cuh"
@@ -409,12 +410,402 @@ __global__ void attn_merge_kernel(const float* __restrict__ part_o, const float*
 #pragma unroll 8
     for (int c = 0; c < n_chunks; ++c) {
         const float m = ml[c * Hq * 2], l = ml[c * Hq * 2 + 1];
+        if (m == -INFINITY) continue;  // empty chunk: its part_o was never written
         const float o = po[static_cast<int64_t>(c) * Hq * HD];
-        const float w = m == -INFINITY ? 0.f : __expf(m - M);
+        const float w = __expf(m - M);
         L = fmaf(l, w, L);
         acc = fmaf(o, w, acc);
     }
     out[(static_cast<int64_t>(t) * Hq + hq) * HD + d] = f2bf(acc / L);
+}
+
+// ------------------------------------------ decode on mma.sync + TMA ring --
+// Persistent split-KV decode. Work items are (token, KV-head group, chunk of
+// kDmSlots retained slots), flattened token-major; CTA c owns the contiguous
+// item range [c*I/C, (c+1)*I/C), so every SM streams the same number of K/V
+// bytes. One producer thread stages each item's K and V with ONE 3D TMA load
+// each (box = 16 slots x the group's HG*hd columns, 128B-swizzled with the
+// slot as the swizzle row so ldmatrix over 8 slots is conflict-free; large
+// copies are what reach HBM peak) plus, at the start of a segment, the
+// token's q slice (1D bulk copy) into a kDmStages-deep ring. One consumer
+// warp per KV head runs the item on the tensor cores (legacy HMMA m16n8k16):
+// S = Q K^T with the G query heads of the GQA group as MMA rows, an online
+// softmax on the accumulator fragments (the C fragment of S is the A
+// fragment of P), O += P V with V through ldmatrix.trans. At the end of each
+// (token, head group) segment the warp writes its unnormalised O with the
+// running max (log2 domain) and sum; attn_merge_seg_kernel folds a token's
+// segments in fixed chunk order.
+// Algorithmic bytes per (token, layer): retained * Hkv*hd*2 * 2.
+constexpr int kDmSlots = 16;
+constexpr int kDmStages = 3;
+constexpr int kDmMaxHG = 8;  // consumer warps (KV heads) per CTA
+constexpr int kDmMaxG = 4;   // q heads folded per merge pass
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D += A B, m16n8k16, bf16 in, fp32 accumulate. A rows 8-15 are zero here.
+__device__ __forceinline__ void hmma(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    return static_cast<uint32_t>(f2bf(lo)) | (static_cast<uint32_t>(f2bf(hi)) << 16);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// Byte offset of (slot j, column col) in a staged box: 128-byte lines
+// ordered (64-column chunk, slot), 16-byte units XOR-swizzled by slot % 8.
+__device__ __forceinline__ uint32_t dm_off(int j, int col) {
+    return static_cast<uint32_t>((((col >> 6) * kDmSlots + j) << 7) + ((((col >> 3) & 7) ^ (j & 7)) << 4));
+}
+
+// Fold the segment partials of the G q heads of one KV head of one token,
+// in chunk order, with one warp. Lanes own chunks: the (max, sum) entries of
+// all G heads load together; the segment starts ("live" chunks, max != -inf)
+// are the same for every head, so each live chunk's G partial rows are
+// gathered with independent loads before accumulating. Reads go through L2
+// (ld.global.cg): the partials were written by other CTAs of this launch.
+// ml: entry of (chunk 0, head 0), GH float2 per chunk; po: partial row of
+// (chunk 0, head 0), HD floats per head; op: output row of head 0.
+template <int HD>
+__device__ __noinline__ void merge_heads_block(const float2* ml, const float* po, int G, int GH, int nv, uint16_t* op,
+                                               int lane) {
+    constexpr int PER = HD / 32;
+    float M[kDmMaxG], L[kDmMaxG], acc[kDmMaxG][PER];
+#pragma unroll
+    for (int g = 0; g < kDmMaxG; ++g) {
+        M[g] = -INFINITY;
+        L[g] = 0.f;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
+    }
+    for (int k0 = 0; k0 < nv; k0 += 32) {
+        const int k = k0 + lane;
+#pragma unroll
+        for (int g = 0; g < kDmMaxG; ++g)
+            if (g < G && k < nv) M[g] = fmaxf(M[g], __ldcg(ml + static_cast<int64_t>(k) * GH + g).x);
+    }
+#pragma unroll
+    for (int g = 0; g < kDmMaxG; ++g)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M[g] = fmaxf(M[g], __shfl_xor_sync(0xffffffffu, M[g], o));
+    for (int k0 = 0; k0 < nv; k0 += 32) {
+        const int k = k0 + lane;
+        float2 e[kDmMaxG];
+#pragma unroll
+        for (int g = 0; g < kDmMaxG; ++g)
+            e[g] = g < G && k < nv ? __ldcg(ml + static_cast<int64_t>(k) * GH + g) : make_float2(-INFINITY, 0.f);
+        float w[kDmMaxG];
+#pragma unroll
+        for (int g = 0; g < kDmMaxG; ++g) {
+            w[g] = e[g].x == -INFINITY ? 0.f : exp2f(e[g].x - M[g]);
+            L[g] = fmaf(e[g].y, w[g], L[g]);
+        }
+        unsigned live = __ballot_sync(0xffffffffu, e[0].x != -INFINITY);
+        while (live) {
+            const int src = __ffs(live) - 1;
+            live &= live - 1;
+            const float* p = po + static_cast<int64_t>(k0 + src) * GH * HD + lane * PER;
+            float v[kDmMaxG][PER];
+#pragma unroll
+            for (int g = 0; g < kDmMaxG; ++g) {
+                if (g >= G) continue;
+                if constexpr (PER == 4) {
+                    const float4 x = __ldcg(reinterpret_cast<const float4*>(p + g * HD));
+                    v[g][0] = x.x; v[g][1] = x.y; v[g][2] = x.z; v[g][3] = x.w;
+                } else {
+                    const float2 x = __ldcg(reinterpret_cast<const float2*>(p + g * HD));
+                    v[g][0] = x.x; v[g][1] = x.y;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < kDmMaxG; ++g) {
+                if (g >= G) continue;
+                const float wg = __shfl_sync(0xffffffffu, w[g], src);
+#pragma unroll
+                for (int i = 0; i < PER; ++i) acc[g][i] = fmaf(v[g][i], wg, acc[g][i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kDmMaxG; ++g) {
+        if (g >= G) continue;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L[g] += __shfl_xor_sync(0xffffffffu, L[g], o);
+        const float inv = 1.f / L[g];
+        uint16_t* o = op + static_cast<int64_t>(g) * HD + lane * PER;
+        if constexpr (PER == 4)
+            *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(acc[g][0] * inv, acc[g][1] * inv),
+                                                      pack_bf16(acc[g][2] * inv, acc[g][3] * inv));
+        else
+            *reinterpret_cast<uint32_t*>(o) = pack_bf16(acc[g][0] * inv, acc[g][1] * inv);
+    }
+}
+
+// Up to kDmMaxG heads per pass (register arrays stay small); out of line so
+// the rare merge does not raise the main loop's register pressure.
+template <int HD>
+__device__ __forceinline__ void merge_heads_warp(const float2* ml, const float* po, int G, int GH, int nv,
+                                                 uint16_t* op, int lane) {
+    for (int gb = 0; gb < G; gb += kDmMaxG)
+        merge_heads_block<HD>(ml + gb, po + static_cast<int64_t>(gb) * HD, min(kDmMaxG, G - gb), GH, nv,
+                              op + static_cast<int64_t>(gb) * HD, lane);
+}
+
+template <int HD>
+__global__ void __launch_bounds__((kDmMaxHG + 1) * 32)
+attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                       const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
+                       const int32_t* __restrict__ seq, int Hq, int Hkv, int HG, int cap, float scale_log2,
+                       float* part_o, float* part_ml, int n_chunks, int64_t n_items, uint16_t* __restrict__ out,
+                       unsigned long long* counters, uint32_t tag, int mode) {
+    const int G = Hq / Hkv, HGn = Hkv / HG;
+    const uint32_t box_bytes = kDmSlots * HG * HD * 2;
+    const int qelems = HG * G * HD;
+    const uint32_t stage_bytes = (2 * box_bytes + qelems * 2 + 1023) & ~1023u;
+    extern __shared__ uint8_t dsm_raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(kDmStages) * stage_bytes);
+    uint64_t* empty = full + kDmStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * n_items / gridDim.x;
+    const int64_t i1 = static_cast<int64_t>(blockIdx.x + 1) * n_items / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kDmStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], HG);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == HG) {  // producer
+        if (lane != 0) return;
+        tma_prefetch_desc(&tmap_k);
+        tma_prefetch_desc(&tmap_v);
+        int64_t it = 0;
+        // (token, group, chunk) of i0, then advanced incrementally; pos/seq
+        // are read once per (token, group) segment.
+        int k = static_cast<int>(i0 % n_chunks), hg = static_cast<int>((i0 / n_chunks) % HGn);
+        int t = static_cast<int>(i0 / n_chunks / HGn);
+        int n = min(pos[t] + 1, cap), row_t = seq[t] * cap;
+        for (int64_t i = i0; i < i1; ++i, ++k) {
+            if (k == n_chunks) {
+                k = 0;
+                if (++hg == HGn) {
+                    hg = 0;
+                    ++t;
+                    n = min(pos[t] + 1, cap);
+                    row_t = seq[t] * cap;
+                }
+            }
+            const int j0 = k * kDmSlots;
+            if (n - j0 <= 0) continue;
+            const bool seg_first = i == i0 || k == 0;
+            const int s = static_cast<int>(it % kDmStages);
+            if (it >= kDmStages) mbar_wait(&empty[s], static_cast<uint32_t>((it / kDmStages + 1) & 1));
+            uint8_t* st = ring + static_cast<size_t>(s) * stage_bytes;
+            mbar_arrive_expect_tx(&full[s], 2 * box_bytes + (seg_first ? qelems * 2u : 0u));
+            const int row = row_t + j0, chunk = hg * HG * HD / 64;
+            tma_load_3d(st, &tmap_k, &full[s], 0, row, chunk);
+            tma_load_3d(st + box_bytes, &tmap_v, &full[s], 0, row, chunk);
+            if (seg_first)
+                bulk_load(st + 2 * box_bytes, q + static_cast<int64_t>(t) * q_stride + static_cast<int64_t>(hg) * HG * G * HD,
+                          qelems * 2u, &full[s]);
+            ++it;
+        }
+        return;
+    }
+
+    // Consumer warp = KV head `warp` of the group. Fragment roles: row g =
+    // lane/4 is the query head within the GQA group (valid for g < G),
+    // c4 = lane%4 picks the column pair.
+    const int h = warp, g = lane >> 2, c4 = lane & 3;
+    constexpr int KS = HD / 16, NT = HD / 8;
+    uint32_t qa[KS][2];
+    float o[NT][4];
+    float m_run = -INFINITY, l_run = 0.f;
+    bool seg_valid = false;
+    int64_t seg_item = 0;
+    int64_t it = 0;
+    int k = static_cast<int>(i0 % n_chunks), hg = static_cast<int>((i0 / n_chunks) % HGn);
+    int t = static_cast<int>(i0 / n_chunks / HGn);
+    int n = min(pos[t] + 1, cap);
+    for (int64_t i = i0; i < i1; ++i, ++k) {
+        if (k == n_chunks) {
+            k = 0;
+            if (++hg == HGn) {
+                hg = 0;
+                n = min(pos[++t] + 1, cap);
+            }
+        }
+        const int j0 = k * kDmSlots;
+        const int cnt = min(kDmSlots, n - j0);
+        const bool seg_first = i == i0 || k == 0;
+        const bool seg_last = i == i1 - 1 || k == n_chunks - 1;
+        if (seg_first) {
+            seg_valid = cnt > 0;
+            seg_item = i;
+        }
+        if (cnt > 0) {
+            const int s = static_cast<int>(it % kDmStages);
+            mbar_wait(&full[s], static_cast<uint32_t>((it / kDmStages) & 1));
+            uint8_t* Kb = ring + static_cast<size_t>(s) * stage_bytes;
+            uint8_t* Vb = Kb + box_bytes;
+            if (mode >= 2) {  // load-only timing probe
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                ++it;
+                continue;
+            }
+            if (seg_first) {
+                const uint16_t* Qs = reinterpret_cast<const uint16_t*>(Kb + 2 * box_bytes) + (h * G + g) * HD + 2 * c4;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    qa[ks][0] = g < G ? *reinterpret_cast<const uint32_t*>(Qs + ks * 16) : 0u;
+                    qa[ks][1] = g < G ? *reinterpret_cast<const uint32_t*>(Qs + ks * 16 + 8) : 0u;
+                }
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+                m_run = -INFINITY;
+                l_run = 0.f;
+            }
+            if (cnt < kDmSlots) {
+                // Ragged chunk: rows past the retained count may be unwritten
+                // cache memory; zero this head's V rows there (p = 0 must not
+                // meet a NaN).
+                constexpr int LINES = HD / 64;
+                const int units = (kDmSlots - cnt) * LINES * 8;
+                for (int u = lane; u < units; u += 32) {
+                    const int j = cnt + u / (LINES * 8), line = (u / 8) % LINES, w = u & 7;
+                    *reinterpret_cast<uint4*>(Vb + (((h * LINES + line) * kDmSlots + j) << 7) + (w << 4)) =
+                        make_uint4(0u, 0u, 0u, 0u);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+            }
+            // S = Q K^T over the chunk's 16 slots (two n-tiles of 8 slots).
+            const uint32_t kb = smem_u32(Kb), vb = smem_u32(Vb);
+            float sc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+                const int j = nt * 8 + (lane & 7);
+#pragma unroll
+                for (int kp = 0; kp < HD / 32; ++kp) {
+                    uint32_t r0, r1, r2, r3;
+                    ldsm_x4(kb + dm_off(j, h * HD + kp * 32 + (lane >> 3) * 8), r0, r1, r2, r3);
+                    hmma(sc[nt], qa[2 * kp][0], qa[2 * kp][1], r0, r1);
+                    hmma(sc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], r2, r3);
+                }
+            }
+            // Online softmax on row g: this lane holds slots 2c4, 2c4+1, 8+2c4, 9+2c4.
+            float x[4] = {sc[0][0], sc[0][1], sc[1][0], sc[1][1]};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int slot = (e >> 1) * 8 + 2 * c4 + (e & 1);
+                x[e] = slot < cnt ? x[e] * scale_log2 : -INFINITY;
+            }
+            float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m_run, mx);
+            const float m_use = m_new == -INFINITY ? 0.f : m_new;
+            const float alpha = exp2f(m_run - m_use);
+            float p[4], rs = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                p[e] = exp2f(x[e] - m_use);
+                rs += p[e];
+            }
+            rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+            rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+            l_run = l_run * alpha + rs;
+            m_run = m_new;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                o[nt][0] *= alpha;
+                o[nt][1] *= alpha;
+            }
+            const uint32_t pa0 = pack_bf16(p[0], p[1]), pa2 = pack_bf16(p[2], p[3]);
+            // O += P V: V^T fragments through ldmatrix.trans, 16 dims per x4.
+            const int jv = ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+            for (int dp = 0; dp < HD / 16; ++dp) {
+                uint32_t r0, r1, r2, r3;
+                ldsm_x4_t(vb + dm_off(jv, h * HD + dp * 16 + (lane >> 4) * 8), r0, r1, r2, r3);
+                hmma(o[2 * dp], pa0, pa2, r0, r1);
+                hmma(o[2 * dp + 1], pa0, pa2, r2, r3);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            ++it;
+            if (!seg_first && c4 == 0 && g < G) {  // not a segment start: nothing to fold here
+                part_ml[(i * (HG * G) + h * G + g) * 2] = -INFINITY;
+                part_ml[(i * (HG * G) + h * G + g) * 2 + 1] = 0.f;
+            }
+        }
+        if (!seg_last) continue;
+        if (seg_valid && g < G) {
+            const int hq_local = h * G + g;
+            float* po = part_o + (seg_item * (HG * G) + hq_local) * HD + 2 * c4;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) *reinterpret_cast<float2*>(po + nt * 8) = make_float2(o[nt][0], o[nt][1]);
+            if (c4 == 0) {
+                part_ml[(seg_item * (HG * G) + hq_local) * 2] = m_run;
+                part_ml[(seg_item * (HG * G) + hq_local) * 2 + 1] = l_run;
+            }
+        }
+        // Count this segment for its (token, KV head); the warp completing
+        // the count folds the token's G q heads of this KV head (no merge
+        // launch, no CTA-wide sync). The counter word is (tag << 32 | count):
+        // a word left by any other use of the workspace never carries this
+        // call's tag (a NaN pattern).
+        __syncwarp();  // the lanes' partial writes are ordered before lane 0's release below
+        const int64_t base = (static_cast<int64_t>(t) * HGn + hg) * n_chunks;
+        unsigned last = 0;
+        if (lane == 0) {
+            const int64_t C = gridDim.x;
+            auto cta_of = [&](int64_t x) { return ((x + 1) * C + n_items - 1) / n_items - 1; };
+            const unsigned need = static_cast<unsigned>(cta_of(base + n_chunks - 1) - cta_of(base) + 1);
+            unsigned long long* cp = counters + (static_cast<int64_t>(t) * Hkv + hg * HG + h);
+            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(cp), nxt;
+            for (;;) {
+                nxt = static_cast<uint32_t>(cur >> 32) == tag ? cur + 1 : (static_cast<unsigned long long>(tag) << 32) | 1ull;
+                unsigned long long prev;
+                // acq_rel at gpu scope: releases this warp's partials, and the
+                // completing warp acquires every other contributor's.
+                asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;"
+                             : "=l"(prev) : "l"(cp), "l"(cur), "l"(nxt) : "memory");
+                if (prev == cur) break;
+                cur = prev;
+            }
+            last = static_cast<unsigned>(nxt & 0xffffffffull) == need;
+            if (last) *reinterpret_cast<volatile unsigned long long*>(cp) = 0ull;
+        }
+        if (__shfl_sync(0xffffffffu, last, 0)) {
+            const int GH = HG * G;
+            merge_heads_warp<HD>(reinterpret_cast<const float2*>(part_ml) + base * GH + h * G,
+                                 part_o + (base * GH + h * G) * HD, G, GH, (n + kDmSlots - 1) / kDmSlots,
+                                 out + (static_cast<int64_t>(t) * Hq + hg * GH + h * G) * HD, lane);
+        }
+    }
 }
 
 // ------------------------------------------------ prefill on tcgen05 -------
@@ -737,6 +1128,18 @@ using namespace kl;
 
 namespace kl {
 int g_prefill_tc = 1;  // kl_tune(KL_TUNE_PREFILL_TC, ...)
+int g_decode_mma = 1;  // kl_tune(KL_TUNE_DECODE_MMA, ...)
+
+static int attn_sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            return v;
+        cudaGetLastError();
+        return 148;
+    }();
+    return n;
+}
 }
 
 extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int hd, const int32_t* pos,
@@ -775,15 +1178,34 @@ extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t
 extern "C" int64_t kl_attn_decode_workspace_bytes(int64_t T, int Hq, int hd, int cap) {
     if (T <= 0 || Hq <= 0 || hd <= 0 || cap <= 0) return 0;
     const int64_t chunks = (cap + kDecChunk - 1) / kDecChunk;
-    return T * chunks * Hq * (static_cast<int64_t>(hd) + 2) * 4;
+    // fp32 partials (max, sum, o) per (token, chunk, q head) + one 64-bit
+    // segment counter per (token, KV head group).
+    return T * chunks * Hq * (static_cast<int64_t>(hd) + 2) * 4 + T * Hq * 8 + 64;
 }
 
-extern "C" int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
-                                 int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache,
-                                 int cap, int sink, float scale, uint16_t* out, void* workspace,
-                                 int64_t workspace_bytes, cudaStream_t stream) {
+// 3D view of a KV cache [rows = cache_seqs * cap][Hkv * hd] for the decode
+// kernel: dims (64 columns, rows, 64-column chunks), box (64, 16 slots, the
+// group's chunks), 128B swizzle with the slot as the swizzle row.
+static int make_kv_map(CUtensorMap* map, const void* base, int64_t rows, int row_elems, int chunks_per_box) {
+    EncodeFn enc = encoder();
+    if (enc == nullptr) return KL_ENODEV;
+    const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(row_elems / 64)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_elems) * 2, 128};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kDmSlots), static_cast<cuuint32_t>(chunks_per_box)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return res == CUDA_SUCCESS ? 0 : KL_EINVAL;
+}
+
+extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
+                                  int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache,
+                                  int64_t cache_seqs, int cap, int sink, float scale, uint16_t* out, void* workspace,
+                                  int64_t workspace_bytes, cudaStream_t stream) {
     if (hd != 128 && hd != 64) return KL_EUNSUPPORTED;
-    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || !q || !pos || !seq || !out) return KL_EINVAL;
+    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || cap <= sink || cache_seqs < 0 || !q || !pos || !seq || !out)
+        return KL_EINVAL;
     if (T == 0) return KL_OK;
     const int G = Hq / Hkv;
     if (G > 8) return KL_EUNSUPPORTED;
@@ -792,12 +1214,48 @@ extern "C" int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int3
                         static_cast<size_t>(kDecChunk) * Hkv * hd * 2 + static_cast<size_t>(Hq) * hd * 4 +
                         static_cast<size_t>(Hq) * kDecChunk * 4 + 16;
     if (workspace == nullptr || workspace_bytes < need || smem > 200 * 1024 || q_stride % 8 != 0 ||
-
         (reinterpret_cast<uintptr_t>(k_cache) & 15) || (reinterpret_cast<uintptr_t>(v_cache) & 15))
         return kl_attn_decode(q, q_stride, pos, seq, T, Hq, Hkv, hd, k_cache, v_cache, cap, sink, scale, out, stream);
     const int n_chunks = (cap + kDecChunk - 1) / kDecChunk;
     float* part_ml = static_cast<float*>(workspace);
     float* part_o = part_ml + T * n_chunks * Hq * 2;
+    const int HG = std::min(Hkv, kDmMaxHG);
+    if (g_decode_mma && cache_seqs > 0 && Hkv % HG == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+        static_assert(kDmSlots == kDecChunk, "workspace layout shared with the per-chunk kernel");
+        CUtensorMap mk, mv;
+        const int64_t rows = cache_seqs * cap;
+        int rc = make_kv_map(&mk, k_cache, rows, Hkv * hd, HG * hd / 64);
+        if (rc) return rc;
+        rc = make_kv_map(&mv, v_cache, rows, Hkv * hd, HG * hd / 64);
+        if (rc) return rc;
+        const size_t stage = (static_cast<size_t>(2) * kDmSlots * HG * hd * 2 + static_cast<size_t>(HG) * G * hd * 2 + 1023) &
+                             ~static_cast<size_t>(1023);
+        const size_t msmem = kDmStages * stage + 1024 + 2 * kDmStages * 8;
+        if (msmem > 227 * 1024) return KL_EUNSUPPORTED;
+        auto kern = hd == 128 ? attn_decode_mma_kernel<128> : attn_decode_mma_kernel<64>;
+        KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+        static int occ_cache[2][kDmMaxHG + 1] = {};
+        static size_t occ_smem[2][kDmMaxHG + 1] = {};
+        const int hi = hd == 128;
+        if (occ_smem[hi][HG] != msmem) {
+            int occ = 0;
+            KL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (HG + 1) * 32, msmem));
+            occ_cache[hi][HG] = std::max(occ, 1);
+            occ_smem[hi][HG] = msmem;
+        }
+        const int64_t n_items = T * (Hkv / HG) * n_chunks;
+        const int ctas = static_cast<int>(std::min<int64_t>(n_items, static_cast<int64_t>(attn_sm_count()) * occ_cache[hi][HG]));
+        // Segment counters after the partials (8-byte aligned); tags are
+        // quiet-NaN bit patterns, distinct per call.
+        static std::atomic<uint32_t> epoch{1};
+        const uint32_t tag = 0x7FC00000u | (epoch.fetch_add(1) & 0x3FFFFFu);
+        auto* counters = reinterpret_cast<unsigned long long*>(
+            (reinterpret_cast<uintptr_t>(part_o + T * n_chunks * Hq * hd) + 7) & ~uintptr_t(7));
+        kern<<<ctas, (HG + 1) * 32, msmem, stream>>>(mk, mv, q, q_stride, pos, seq, Hq, Hkv, HG, cap,
+                                                     scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items,
+                                                     out, counters, tag, g_decode_mma);
+        return check_launch();
+    }
     auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;
     KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<dim3(static_cast<unsigned>(T), n_chunks), kDecThreads, smem, stream>>>(
@@ -806,6 +1264,16 @@ extern "C" int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int3
     auto merge = hd == 128 ? attn_merge_kernel<128> : attn_merge_kernel<64>;
     merge<<<dim3(static_cast<unsigned>(T), Hq), hd, 0, stream>>>(part_o, part_ml, Hq, n_chunks, out);
     return check_launch();
+}
+
+extern "C" int kl_attn_decode_ws(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
+                                 int64_t T, int Hq, int Hkv, int hd, const uint16_t* k_cache, const uint16_t* v_cache,
+                                 int cap, int sink, float scale, uint16_t* out, void* workspace,
+                                 int64_t workspace_bytes, cudaStream_t stream) {
+    // Cache extent unknown: the per-chunk kernel (it never reads past a
+    // sequence's retained slots).
+    return kl_attn_decode_ws2(q, q_stride, pos, seq, T, Hq, Hkv, hd, k_cache, v_cache, 0, cap, sink, scale, out,
+                              workspace, workspace_bytes, stream);
 }
 
 extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, int Hkv, int hd, int cap, int sink,

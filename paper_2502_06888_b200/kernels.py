@@ -42,6 +42,7 @@ _rope = _sig("kl_rope_kv_append", [_P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _
 _dec = _sig("kl_attn_decode", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P])
 _dec_ws_bytes = _sig("kl_attn_decode_workspace_bytes", [_L, _I, _I, _I], C.c_int64)
 _dec_ws = _sig("kl_attn_decode_ws", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _L, _P])
+_dec_ws2 = _sig("kl_attn_decode_ws2", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _L, _I, _I, _F, _P, _P, _L, _P])
 _pre = _sig("kl_attn_prefill", [_P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P])
 _fill = _sig("kl_fill_normal_bf16", [_P, _L, _U64, _F, _P])
 _tune = _sig("kl_tune", [_I, _I])
@@ -62,6 +63,7 @@ TUNE_PDL = 5
 TUNE_PREFILL_TC = 6
 TUNE_STREAM_WHOLE_TILES = 7
 TUNE_GEMM_PERSISTENT = 8
+TUNE_DECODE_MMA = 9  # persistent mma.sync split-KV decode attention (1) or per-chunk CUDA-core kernel (0)
 
 
 def tune(knob, value):
@@ -246,8 +248,9 @@ def attn_decode_split(q, q_stride, pos, seq, Hq, Hkv, hd, k_cache, v_cache, cap,
     T = pos.shape[0]
     wsb = int(_dec_ws_bytes(T, Hq, hd, cap))
     ws = workspace(wsb, q.device)
-    _chk(_dec_ws(_p(q), q_stride, _p(pos), _p(seq), T, Hq, Hkv, hd, _p(k_cache), _p(v_cache), cap, sink, scale,
-                 _p(out), _p(ws), wsb, _s(stream)), "kl_attn_decode_ws")
+    cache_seqs = k_cache.numel() // (cap * Hkv * hd)  # the cache's extent: the tensor-core kernel's TMA bounds
+    _chk(_dec_ws2(_p(q), q_stride, _p(pos), _p(seq), T, Hq, Hkv, hd, _p(k_cache), _p(v_cache), cache_seqs, cap, sink,
+                  scale, _p(out), _p(ws), wsb, _s(stream)), "kl_attn_decode_ws2")
     return out
 
 

@@ -299,22 +299,32 @@ def test_rope_append_and_decode_attention(K, cuda):
         close_bf16(to_bits(out2), orc.bits_to_f32(ref))
 
 
-@pytest.mark.parametrize("Hq,Hkv,hd,cap,p", [(32, 8, 128, 260, 600), (32, 8, 128, 260, 40), (16, 16, 64, 100, 99),
-                                             (8, 1, 128, 70, 69)])
-def test_decode_attention_split_kv(K, cuda, Hq, Hkv, hd, cap, p):
-    """Split-KV decode (bulk-staged 32-slot chunks + merge) against the oracle:
-    full ring, partially filled cache (empty chunks), MHA and MQA shapes."""
-    T, sink = 5, 4
+@pytest.mark.parametrize("mma", [1, 0])
+@pytest.mark.parametrize("T,Hq,Hkv,hd,cap,p", [(5, 32, 8, 128, 260, 600), (5, 32, 8, 128, 260, 40),
+                                               (5, 16, 16, 64, 100, 99), (5, 8, 1, 128, 70, 69),
+                                               (64, 32, 8, 128, 260, 600), (37, 32, 8, 128, 260, 200),
+                                               (300, 8, 2, 64, 40, 39)])
+def test_decode_attention_split_kv(K, cuda, mma, T, Hq, Hkv, hd, cap, p):
+    """Split-KV decode against the oracle, for the persistent mma.sync kernel
+    (mma=1: segments spanning several chunks and CTA boundaries inside a
+    token) and the per-chunk CUDA-core kernel: full ring, partially filled
+    caches (empty chunks), ragged last chunk, GQA/MHA/MQA, hd 64/128."""
+    sink = 4
     width = (Hq + 2 * Hkv) * hd
     q = orc.normal_bf16(T * width, 61, 1.0).reshape(T, width)
     kc = orc.normal_bf16(T * cap * Hkv * hd, 62, 1.0)
     vc = orc.normal_bf16(T * cap * Hkv * hd, 63, 1.0)
-    pos = np.array([p, max(p - 3, 0), p // 2, 1, p], np.int32)
-    seq = np.array([4, 3, 2, 1, 0], np.int32)
+    base = [p, max(p - 3, 0), p // 2, 1, p]
+    pos = np.array([base[i % 5] for i in range(T)], np.int32)
+    seq = np.array(list(range(T))[::-1], np.int32)
     out = torch.empty(T, Hq * hd, dtype=torch.bfloat16, device=cuda)
-    K.attn_decode_split(to_dev(q, cuda), width, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda), Hq,
-                        Hkv, hd, to_dev(kc, cuda), to_dev(vc, cuda), cap, sink, hd ** -0.5, out)
-    torch.cuda.synchronize()
+    K.tune(K.TUNE_DECODE_MMA, mma)
+    try:
+        K.attn_decode_split(to_dev(q, cuda), width, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda),
+                            Hq, Hkv, hd, to_dev(kc, cuda), to_dev(vc, cuda), cap, sink, hd ** -0.5, out)
+        torch.cuda.synchronize()
+    finally:
+        K.tune(K.TUNE_DECODE_MMA, 1)
     ref = orc.attn_decode(q, width, pos, seq, Hq, Hkv, hd, kc, vc, cap, hd ** -0.5)
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 

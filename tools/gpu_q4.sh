@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_engine_gpu.py -m gpu -q -k "disk" 2>&1 | tail -25
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3

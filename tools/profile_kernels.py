@@ -96,6 +96,28 @@ def timed(fn, iters, stream):
     return s.elapsed_time(e) / iters * 1e-3
 
 
+def timed_graph(fn, iters):
+    """Device time per call with host overhead removed: `iters` calls
+    captured once into a CUDA graph, replayed 3 times."""
+    for _ in range(3):
+        fn(0)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(iters):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / (3 * iters) * 1e-3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -194,10 +216,26 @@ def main():
         t = timed(att, args.iters, st)
         res["attn_decode_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
 
+        seqs = [seq + j * bs for j in range(n)]
+
         def att2(i):
-            K.attn_decode_split(qkv, width, pos, seq + (i % n) * bs, Hq, Hkv, hd, kc, vc, cap, 4, hd ** -0.5, out)
+            K.attn_decode_split(qkv, width, pos, seqs[i % n], Hq, Hkv, hd, kc, vc, cap, 4, hd ** -0.5, out)
         t = timed(att2, args.iters, st)
         res["attn_decode_split_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+        dump_trace("attn_decode_mma")
+        t = timed_graph(att2, 20)
+        res["attn_decode_mma_graph_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+        K.tune(K.TUNE_DECODE_MMA, 0)
+        t = timed_graph(att2, 20)
+        res["attn_decode_cudacore_graph_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+        K.tune(K.TUNE_DECODE_MMA, 1)
+        K.tune(K.TUNE_DECODE_MMA, 2)
+        t = timed(att2, args.iters, st)
+        res["attn_decode_mma_loadonly_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+        K.tune(K.TUNE_DECODE_MMA, 0)
+        t = timed(att2, args.iters, st)
+        K.tune(K.TUNE_DECODE_MMA, 1)
+        res["attn_decode_split_cudacore_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
     if not args.only or args.only == "route":
         h = torch.randn(T, d, dtype=bf, device=dev)
         nw = torch.ones(d, dtype=bf, device=dev)
