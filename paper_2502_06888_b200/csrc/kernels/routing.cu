@@ -145,6 +145,120 @@ gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ no
     }
 }
 
+// Decode-sized router (few tokens): one 256-thread block per token so the
+// token's E router rows are read by 8 warps at once. Every warp computes the
+// row's RMSNorm itself, in the same order as gate_topk_warp_kernel (so x2
+// and the logits are bit-identical to it and to the oracle), writes its
+// eighth of x2, and dot-products the experts e = warp, warp + 8, ...; thread
+// 0 then runs the same top-k / weights code.
+template <int NC>
+__global__ void __launch_bounds__(256)
+gate_topk_block_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ norm_w,
+                       const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
+                       uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
+                       float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    constexpr int d = NC * 256;
+    __shared__ float lg[64];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tok = blockIdx.x;
+    const uint16_t* hrow = h + static_cast<int64_t>(tok) * d;
+    uint4 hv[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) hv[j] = __ldg(reinterpret_cast<const uint4*>(hrow + lane * 8 + 256 * j));
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const uint32_t w4[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = bf2f(static_cast<uint16_t>(w4[i] & 0xffffu)), b = bf2f(static_cast<uint16_t>(w4[i] >> 16));
+            ss = fmaf(a, a, ss);
+            ss = fmaf(b, b, ss);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    const float rstd = rsqrtf(ss / static_cast<float>(d) + eps);
+    uint32_t xv[NC][4];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(norm_w + lane * 8 + 256 * j));
+        const uint32_t hw[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+        const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = __fmul_rn(__fmul_rn(bf2f(static_cast<uint16_t>(hw[i] & 0xffffu)), rstd),
+                                      bf2f(static_cast<uint16_t>(gw[i] & 0xffffu)));
+            const float b = __fmul_rn(__fmul_rn(bf2f(static_cast<uint16_t>(hw[i] >> 16)), rstd),
+                                      bf2f(static_cast<uint16_t>(gw[i] >> 16)));
+            xv[j][i] = pack2(a, b);
+        }
+        if ((j & 7) == wid)
+            *reinterpret_cast<uint4*>(x2 + static_cast<int64_t>(tok) * d + lane * 8 + 256 * j) =
+                make_uint4(xv[j][0], xv[j][1], xv[j][2], xv[j][3]);
+    }
+    for (int e = wid; e < E; e += 8) {
+        const uint16_t* wr = wg + static_cast<int64_t>(e) * d + lane * 8;
+        uint4 wv[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + 256 * j));
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            const uint32_t ww[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc = fmaf(bf2f(static_cast<uint16_t>(xv[j][i] & 0xffffu)), bf2f(static_cast<uint16_t>(ww[i] & 0xffffu)), acc);
+                acc = fmaf(bf2f(static_cast<uint16_t>(xv[j][i] >> 16)), bf2f(static_cast<uint16_t>(ww[i] >> 16)), acc);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (lane == 0) lg[e] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (logits_out != nullptr)
+        for (int e = 0; e < E; ++e) logits_out[static_cast<int64_t>(tok) * E + e] = lg[e];
+    uint64_t taken = 0;
+    int sel[8];
+    float val[8];
+    for (int j = 0; j < k; ++j) {
+        int best = -1;
+        float bv = 0.f;
+        for (int e = 0; e < E; ++e) {
+            if ((taken >> e) & 1ull) continue;
+            if (best < 0 || lg[e] > bv) {
+                best = e;
+                bv = lg[e];
+            }
+        }
+        taken |= 1ull << best;
+        sel[j] = best;
+        val[j] = bv;
+    }
+    float wsum = 0.f;
+    float pr[8];
+    if (score_mode == 0) {
+        for (int j = 0; j < k; ++j) {
+            pr[j] = expf(val[j] - val[0]);
+            wsum += pr[j];
+        }
+    } else {
+        float mx = lg[0];
+        for (int e = 1; e < E; ++e) mx = fmaxf(mx, lg[e]);
+        for (int e = 0; e < E; ++e) wsum += expf(lg[e] - mx);
+        for (int j = 0; j < k; ++j) pr[j] = expf(val[j] - mx);
+    }
+    for (int j = 0; j < k; ++j) {
+        const int64_t r = static_cast<int64_t>(tok) * k + j;
+        idx[r] = sel[j];
+        weight[r] = pr[j] / wsum;
+        if (hist != nullptr) atomicAdd(&hist[sel[j]], 1);
+        if (first_pos != nullptr) atomicMin(&first_pos[sel[j]], static_cast<int32_t>(r));
+    }
+}
+
 // Latency-optimised router: one warp per token, the row held in registers
 // (NC = d/256 16-byte chunks per lane, loaded once), every expert's router row
 // loaded with independent vector loads. Same arithmetic order as
@@ -267,6 +381,30 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
     if (row >= T) return;
     const float rstd = row_rstd(x + row * d, d, eps, lane);
     write_normed(x + row * d, w, out + row * d, d, rstd, lane);
+}
+
+// Few rows (decode): one 8-warp block per row; every warp computes the
+// row's rstd (same order, bit-identical) and writes every 8th 256-column
+// span, so a 64-row call spreads over 64 SMs instead of 16.
+__global__ void __launch_bounds__(256)
+rmsnorm_row_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d, float eps,
+                   uint16_t* __restrict__ out) {
+    const int64_t row = blockIdx.x;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float rstd = row_rstd(x + row * d, d, eps, lane);
+    const uint16_t* xr = x + row * d;
+    uint16_t* orow = out + row * d;
+    for (int c = wid * 256 + lane * 8; c < d; c += 8 * 256) {
+        float v[8], g[8];
+        load8(xr + c, v);
+        load8(w + c, g);
+        uint4 o;
+        o.x = pack2(__fmul_rn(__fmul_rn(v[0], rstd), g[0]), __fmul_rn(__fmul_rn(v[1], rstd), g[1]));
+        o.y = pack2(__fmul_rn(__fmul_rn(v[2], rstd), g[2]), __fmul_rn(__fmul_rn(v[3], rstd), g[3]));
+        o.z = pack2(__fmul_rn(__fmul_rn(v[4], rstd), g[4]), __fmul_rn(__fmul_rn(v[5], rstd), g[5]));
+        o.w = pack2(__fmul_rn(__fmul_rn(v[6], rstd), g[6]), __fmul_rn(__fmul_rn(v[7], rstd), g[7]));
+        *reinterpret_cast<uint4*>(orow + c) = o;
+    }
 }
 
 // ---------------------------------------------------------------- permute --
@@ -535,10 +673,17 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
     if (!h || !norm_w || !wg || !x2 || !idx || !weight) return KL_EINVAL;
     if (T == 0) return KL_OK;
     const unsigned blocks = static_cast<unsigned>((T + 3) / 4);
+    // Few tokens (decode): a block per token fills more SMs and keeps 8 router
+    // rows in flight per token; many tokens (prefill): a warp per token.
+    const bool per_block = T <= 4 * 148;
 #define KL_GATE_WARP(NC)                                                                                          \
     case NC:                                                                                                      \
-        gate_topk_warp_kernel<NC><<<blocks, 128, 0, stream>>>(h, norm_w, wg, T, E, k, eps, score_mode, x2, logits, \
-                                                              idx, weight, hist, first_pos);                      \
+        if (per_block)                                                                                            \
+            gate_topk_block_kernel<NC><<<static_cast<unsigned>(T), 256, 0, stream>>>(                             \
+                h, norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);               \
+        else                                                                                                      \
+            gate_topk_warp_kernel<NC><<<blocks, 128, 0, stream>>>(h, norm_w, wg, T, E, k, eps, score_mode, x2,     \
+                                                                  logits, idx, weight, hist, first_pos);          \
         return check_launch();
     switch (d / 256) {
         KL_GATE_WARP(2)
@@ -558,7 +703,10 @@ extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d
                           cudaStream_t stream) {
     if (T < 0 || d <= 0 || d % 256 != 0 || !x || !w || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    rmsnorm_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(x, w, T, d, eps, out);
+    if (T <= 4 * 148)
+        rmsnorm_row_kernel<<<static_cast<unsigned>(T), 256, 0, stream>>>(x, w, d, eps, out);
+    else
+        rmsnorm_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(x, w, T, d, eps, out);
     return check_launch();
 }
 

@@ -164,7 +164,7 @@ def test_expert_ffn(K, cuda, M, d, f):
 
 
 @pytest.mark.parametrize("T,d,E,k,mode", [(64, 4096, 8, 2, 0), (300, 512, 8, 2, 0), (97, 2048, 64, 6, 1),
-                                          (5, 256, 4, 4, 0)])
+                                          (5, 256, 4, 4, 0), (1000, 512, 8, 2, 0), (700, 2048, 64, 6, 1)])
 def test_gate_topk_bit_exact(K, cuda, T, d, E, k, mode):
     h = orc.normal_bf16(T * d, 41, 1.0).reshape(T, d)
     nw = orc.normal_bf16(d, 42, 0.1).reshape(d)
@@ -192,6 +192,22 @@ def test_gate_topk_bit_exact(K, cuda, T, d, E, k, mode):
     for e in range(E):
         where = np.nonzero(flat == e)[0]
         assert fp[e] == (where[0] if where.size else 2**31 - 1)
+
+
+@pytest.mark.parametrize("T,d", [(64, 4096), (1000, 512), (5, 256)])
+def test_rmsnorm_paths_agree_with_gate_x2(K, cuda, T, d):
+    """kl_rmsnorm (block-per-row kernel for few rows, warp-per-row for many)
+    is bit-identical to the router's fused normalisation and within one bf16
+    ulp of the oracle."""
+    h = orc.normal_bf16(T * d, 71, 1.0).reshape(T, d)
+    nw = orc.bf16_bits(orc.bits_to_f32(orc.normal_bf16(d, 72, 0.1)) + 1.0)
+    wg = orc.normal_bf16(8 * d, 73, 0.02).reshape(8, d)
+    out = K.rmsnorm(to_dev(h, cuda), to_dev(nw, cuda))
+    x2, _, _ = K.gate_topk(to_dev(h, cuda), to_dev(nw, cuda), to_dev(wg, cuda), 2)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_bits(out), to_bits(x2))
+    ref = orc.bits_to_f32(orc.rmsnorm(h, nw))
+    assert np.abs(orc.bits_to_f32(to_bits(out)) - ref).max() <= 2 ** -7 * np.abs(ref).max()
 
 
 def test_gate_tie_break_lower_id(K, cuda):

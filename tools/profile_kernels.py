@@ -176,6 +176,8 @@ def main():
         t = timed(ffn, args.iters, st)
         byt = 3 * d * f * 2 + M * (2 * d * 2 + 2 * f * 2)
         res["expert_ffn"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9, "TFLOPs": 6 * M * d * f / t / 1e12}
+        t = timed_graph(ffn, 16)
+        res["expert_ffn_graph"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9}
 
         def g1(i):
             w = ws[i % E]
@@ -183,6 +185,8 @@ def main():
         t = timed(g1, args.iters, st)
         dump_trace("gemm_swiglu")
         res["gemm_swiglu"] = {"M": M, "us": t * 1e6, "GBs": (2 * d * f * 2) / t / 1e9}
+        t = timed_graph(g1, 16)
+        res["gemm_swiglu_graph"] = {"M": M, "us": t * 1e6, "GBs": (2 * d * f * 2) / t / 1e9}
 
         def g2(i):
             w = ws[i % E]
@@ -190,6 +194,8 @@ def main():
         t = timed(g2, args.iters, st)
         dump_trace("gemm_down")
         res["gemm_down"] = {"M": M, "us": t * 1e6, "GBs": (d * f * 2) / t / 1e9}
+        t = timed_graph(g2, 16)
+        res["gemm_down_graph"] = {"M": M, "us": t * 1e6, "GBs": (d * f * 2) / t / 1e9}
         del ws
     if not args.only or args.only == "attn":
         width = (Hq + 2 * Hkv) * hd
