@@ -69,6 +69,65 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
     }
 }
 
+// Token-per-block RoPE + KV append: the token's cos/sin table (hd/2 entries,
+// the same powf / sincosf per element as rope_append_kernel, so results are
+// bit-identical) is computed once into shared memory and shared by all
+// Hq + Hkv rotated heads; each thread rotates two adjacent dims per step
+// with 32-bit accesses; V rows are copied with 16-byte vectors.
+constexpr int kRopeThreads = 256;
+__global__ void __launch_bounds__(kRopeThreads)
+rope_append_tok_kernel(uint16_t* __restrict__ qkv, int Hq, int Hkv, int hd, const int32_t* __restrict__ pos,
+                       const int32_t* __restrict__ seq, float theta, uint16_t* __restrict__ kc,
+                       uint16_t* __restrict__ vc, int cap, int sink, int chunk_last_pos) {
+    extern __shared__ float cs_tab[];  // [half] cos, then [half] sin
+    const int half = hd / 2;
+    const int64_t t = blockIdx.x;
+    const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * hd;
+    uint16_t* row = qkv + t * width;
+    const int p = pos[t];
+    const int slot = slot_of(p, cap, sink);
+    const bool to_cache = chunk_last_pos < 0 || p < sink || p > chunk_last_pos - (cap - sink);
+    const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot) * Hkv * hd;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const float inv = powf(theta, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
+        float sn, cs;
+        sincosf(static_cast<float>(p) * inv, &sn, &cs);
+        cs_tab[i] = cs;
+        cs_tab[half + i] = sn;
+    }
+    __syncthreads();
+    const int pairs = half / 2;  // 2 dims per thread-step
+    const int heads = Hq + Hkv;
+    for (int w = threadIdx.x; w < heads * pairs; w += blockDim.x) {
+        const int head = w / pairs, i = (w % pairs) * 2;
+        uint16_t* base = row + static_cast<int64_t>(head) * hd;
+        const uint32_t av = *reinterpret_cast<const uint32_t*>(base + i);
+        const uint32_t bv = *reinterpret_cast<const uint32_t*>(base + i + half);
+        uint16_t ra[2], rb[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const float a = bf2f(static_cast<uint16_t>(e ? av >> 16 : av & 0xffffu));
+            const float b = bf2f(static_cast<uint16_t>(e ? bv >> 16 : bv & 0xffffu));
+            const float cs = cs_tab[i + e], sn = cs_tab[half + i + e];
+            ra[e] = f2bf(a * cs - b * sn);
+            rb[e] = f2bf(b * cs + a * sn);
+        }
+        const uint32_t ro = static_cast<uint32_t>(ra[0]) | (static_cast<uint32_t>(ra[1]) << 16);
+        const uint32_t rbo = static_cast<uint32_t>(rb[0]) | (static_cast<uint32_t>(rb[1]) << 16);
+        *reinterpret_cast<uint32_t*>(base + i) = ro;
+        *reinterpret_cast<uint32_t*>(base + i + half) = rbo;
+        if (head >= Hq && to_cache) {  // rotated key -> cache
+            uint16_t* dst = kc + cache_row + static_cast<int64_t>(head - Hq) * hd;
+            *reinterpret_cast<uint32_t*>(dst + i) = ro;
+            *reinterpret_cast<uint32_t*>(dst + i + half) = rbo;
+        }
+    }
+    if (!to_cache) return;
+    const uint4* vsrc = reinterpret_cast<const uint4*>(row + static_cast<int64_t>(Hq + Hkv) * hd);
+    uint4* vdst = reinterpret_cast<uint4*>(vc + cache_row);
+    for (int w = threadIdx.x; w < Hkv * hd / 8; w += blockDim.x) vdst[w] = vsrc[w];
+}
+
 // One CTA (4 warps) per (token, kv head) covering the G query heads of the
 // GQA group, so each retained K/V row is read from HBM exactly once:
 //   1. thread-per-slot scores for all G heads (q in smem, broadcast reads);
@@ -1129,6 +1188,7 @@ using namespace kl;
 namespace kl {
 int g_prefill_tc = 1;  // kl_tune(KL_TUNE_PREFILL_TC, ...)
 int g_decode_mma = 1;  // kl_tune(KL_TUNE_DECODE_MMA, ...)
+int g_rope_tok = 1;    // kl_tune(KL_TUNE_ROPE_TOKEN_BLOCKS, ...)
 
 static int attn_sm_count() {
     static const int n = [] {
@@ -1148,6 +1208,12 @@ extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int 
     if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || hd % 2 || cap <= sink || sink < 0) return KL_EINVAL;
     if (!qkv || !pos || !seq || !k_cache || !v_cache) return KL_EINVAL;
     if (T == 0) return KL_OK;
+    if (g_rope_tok && hd % 8 == 0 && T <= 0x7fffffff &&
+        ((reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache)) & 15) == 0) {
+        rope_append_tok_kernel<<<static_cast<unsigned>(T), kRopeThreads, static_cast<size_t>(hd) * 4, stream>>>(
+            qkv, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink, chunk_last_pos);
+        return check_launch();
+    }
     const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
     rope_append_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(qkv, T, Hq, Hkv, hd, pos, seq,
                                                                                rope_theta, k_cache, v_cache, cap, sink,

@@ -1164,6 +1164,7 @@ extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
 namespace kl {
 extern int g_prefill_tc;
 extern int g_decode_mma;
+extern int g_rope_tok;
 }
 
 extern "C" int kl_tune(int knob, int value) {
@@ -1183,6 +1184,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
         case KL_TUNE_PREFILL_TC: g_prefill_tc = value != 0; return KL_OK;
         case KL_TUNE_DECODE_MMA: g_decode_mma = value; return KL_OK;
+        case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:

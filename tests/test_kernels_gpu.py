@@ -283,6 +283,33 @@ def test_coact_and_predict_exact(K, cuda, E, k, T):
     assert np.array_equal(s.cpu().numpy(), orc.predict_scores(hist, rt, E, 2))
 
 
+@pytest.mark.parametrize("T,Hq,Hkv,hd,cap,sink,last", [(4096, 32, 8, 128, 260, 4, 4095), (64, 32, 8, 128, 260, 4, -1),
+                                                        (37, 8, 2, 64, 40, 0, -1)])
+def test_rope_token_blocks_bit_identical(K, cuda, T, Hq, Hkv, hd, cap, sink, last):
+    """The block-per-token RoPE/KV append (shared cos/sin table) writes the
+    same bits as the thread-per-element kernel: rotated q/k in place, K and V
+    rows in the cache (prefill chunk with its window filter, and decode)."""
+    width = (Hq + 2 * Hkv) * hd
+    qkv = orc.normal_bf16(T * width, 81, 1.0).reshape(T, width)
+    pos = (np.arange(T) % 600).astype(np.int32) if last < 0 else np.arange(T, dtype=np.int32) % (last + 1)
+    seq = (np.arange(T) % 7).astype(np.int32) if last < 0 else np.zeros(T, np.int32)
+    outs = []
+    for tok in (1, 0):
+        q = to_dev(qkv, cuda)
+        kc = torch.zeros(8 * cap * Hkv * hd, dtype=torch.bfloat16, device=cuda)
+        vc = torch.zeros_like(kc)
+        K.tune(K.TUNE_ROPE_TOKEN_BLOCKS, tok)
+        try:
+            K.rope_kv_append(q, Hq, Hkv, hd, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda), 1e6,
+                             kc, vc, cap, sink, chunk_last_pos=last)
+            torch.cuda.synchronize()
+        finally:
+            K.tune(K.TUNE_ROPE_TOKEN_BLOCKS, 1)
+        outs.append((to_bits(q), to_bits(kc), to_bits(vc)))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_rope_append_and_decode_attention(K, cuda):
     n_seq, Hq, Hkv, hd, cap, sink = 6, 8, 2, 128, 20, 4
     width = (Hq + 2 * Hkv) * hd

@@ -1,2 +1,2 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "rope" 2>&1 | tail -2
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rope" -c 4 python tools/prefill_run.py --bs 32 --n 8 --reps 1 2>&1 | grep -E "^  void|gpu__time" | cut -c1-70 | tail -4

@@ -18,7 +18,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--hbm-cap", type=float, default=24e9)
+    ap.add_argument("--pdl", type=int, default=1)
     a = ap.parse_args()
+    from paper_2502_06888_b200 import kernels as K
+    K.tune(K.TUNE_PDL, a.pdl)
     ns = argparse.Namespace(model="mixtral-8x7b", batch_size=64, n_batches=8, prompt_len=512, hbm_cap=a.hbm_cap,
                             host_distinct_layers=4, warmup=1, steps=a.steps)
     eng = Engine(bench.engine_config(ns, 0, 1))
