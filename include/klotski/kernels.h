@@ -73,6 +73,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_PDL 5 /* 1 = weight-streaming GEMMs use programmatic dependent launch (default) */
 #define KL_TUNE_PREFILL_TC 6 /* 1 = tcgen05 prefill attention (default), 0 = CUDA-core fallback */
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
+#define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 2 (default; 3D TMA boxes, used where >= 3 stages fit) or 1 */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */

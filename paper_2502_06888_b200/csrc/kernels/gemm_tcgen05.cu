@@ -478,6 +478,7 @@ struct StreamArgs {
     uint32_t tmem_cols;
     int hint;   // 1 = L2 cache-policy hints on the TMA loads
     int pdl;    // launched with programmatic stream serialization
+    int ks;     // k-blocks per stage: 2 = one 3D TMA box covers two 64-column k-blocks (larger copies)
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
     const uint8_t* q4;  // Q4 variant: weights in the tiled 4-bit layout (kQ4Chunk bytes per 128x64 tile)
 };
@@ -499,6 +500,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ int range_begin(int c, int units, int G) {
     return static_cast<int>(static_cast<int64_t>(c) * units / G);
+}
+
+// 3D tile load: box (64 columns, rows, k-chunks) of a [rows][K] matrix viewed
+// as (64, rows, K/64); lands as k-chunk slabs of [rows][64] 128B-swizzled.
+__device__ __forceinline__ void tma_load_3d_k(void* dst, const CUtensorMap* map, uint64_t* bar, int row, int kchunk,
+                                              uint64_t policy, bool hint) {
+    if (hint)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(row), "r"(kchunk), "l"(policy)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(row), "r"(kchunk)
+            : "memory");
 }
 
 // 1D bulk copy global -> shared (async proxy), completing on `bar`.
@@ -536,7 +555,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                    const StreamArgs p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
+    const int stage_bytes = p.ks * (NMMA * kWTileBytes + p.NP * BK * 2);
+    const int wbytes = p.ks * kWTileBytes;  // one weight sub-tile's k-chunks in a stage
     const int ring_bytes = p.stages * stage_bytes;
     constexpr int kRawStage = NMMA * kQ4Chunk;
     uint8_t* raw = smem + ring_bytes;  // Q4: packed tiles land here, dequantised into the ring
@@ -590,8 +610,10 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
             bool waited = !p.pdl;
             int it = 0, pending_x = 0;
             auto load_x = [&](int s_, int kb_) {
-                uint8_t* sx = smem + s_ * stage_bytes + NMMA * kWTileBytes;
-                if (hint)
+                uint8_t* sx = smem + s_ * stage_bytes + NMMA * wbytes;
+                if (p.ks > 1)
+                    tma_load_3d_k(sx, &tmap_x, &full[s_], a_row0, kb_ * p.ks, pol_x, hint);
+                else if (hint)
                     tma_load_2d_hint(sx, &tmap_x, &full[s_], kb_ * BK, a_row0, pol_x);
                 else
                     tma_load_2d(sx, &tmap_x, &full[s_], kb_ * BK, a_row0);
@@ -617,6 +639,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                         if constexpr (Q4) {
                             const uint8_t* src = p.q4 + (static_cast<int64_t>(row / kWRows) * KB + kb) * kQ4Chunk;
                             bulk_g2s(raw + s * kRawStage + j * kQ4Chunk, src, kQ4Chunk, &raw_full[s]);
+                        } else if (p.ks > 1) {
+                            tma_load_3d_k(sw + j * wbytes, &tmap_w, &full[s], row, kb * p.ks, pol_w, hint);
                         } else if (hint) {
                             tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
                         } else {
@@ -652,14 +676,17 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                     if (it == 0) STREAM_TRACE(1);
                     tc_fence_after();
                     const uint32_t sw = smem_u32(smem + s * stage_bytes);
-                    const uint32_t sx = sw + NMMA * kWTileBytes;
+                    const uint32_t sx = sw + NMMA * wbytes;
                     if (!(p.debug & 1))
+                        for (int kk = 0; kk < p.ks; ++kk)
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)
+                            for (int k = 0; k < BK / 16; ++k)
 #pragma unroll
-                            for (int j = 0; j < NMMA; ++j)
-                                tc_mma_bf16(acc0 + j * p.acc_stride, sw128_kmajor_desc(sw + j * kWTileBytes + k * 32),
-                                            sw128_kmajor_desc(sx + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                                for (int j = 0; j < NMMA; ++j)
+                                    tc_mma_bf16(acc0 + j * p.acc_stride,
+                                                sw128_kmajor_desc(sw + j * wbytes + kk * kWTileBytes + k * 32),
+                                                sw128_kmajor_desc(sx + kk * p.NP * BK * 2 + k * 32), idesc,
+                                                (kb > kb0 || kk > 0 || k > 0) ? 1u : 0u);
                     tc_commit(&empty[s]);
                 }
                 tc_commit(&acc_full[b]);
@@ -1019,6 +1046,7 @@ int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
+int g_stream_ks = 2;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2): 2 where >= 3 stages still fit
 
 int sm_count() {
     static const int n = [] {
@@ -1078,9 +1106,19 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.acc_stride = pow2ceil(std::max(32, p.NP));
     p.nbuf = 2 * NMMA * p.acc_stride <= 512 ? 2 : 1;
     p.tmem_cols = static_cast<uint32_t>(std::max(32, p.nbuf * NMMA * p.acc_stride));
-    p.KB = K / BK;
+    // Two k-blocks per stage (one 3D TMA box each for weights and
+    // activations) when K allows: 32-64 KB copies stream HBM faster than
+    // 16 KB ones (tools/bw_probe.cu).
+    {
+        const int per_kb = NMMA * kWTileBytes + p.NP * BK * 2;
+        p.ks = (!Q4 && g_stream_ks == 2 && (K / BK) % 2 == 0 &&
+                std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / (2 * per_kb)) >= 3)
+                   ? 2
+                   : 1;  // keep >= 3 stages in flight (the SwiGLU pair's 96 KB stages would leave 2)
+    }
+    p.KB = K / BK / p.ks;
     p.units = n_tiles * p.KB;
-    const int stage_bytes = NMMA * kWTileBytes + p.NP * BK * 2;
+    const int stage_bytes = p.ks * (NMMA * kWTileBytes + p.NP * BK * 2);
     const int per_stage = stage_bytes + (Q4 ? NMMA * kQ4Chunk : 0);
     p.stages = std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / per_stage);
     if (p.stages < 2 || p.tmem_cols * g_stream_ctas > 512) return KL_EUNSUPPORTED;
@@ -1106,11 +1144,11 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     p.epoch = next_epoch();
     p.q4 = q4;
     CUtensorMap mw, mx;
-    int rc = make_map(&mx, a, a_rows, K, p.NP);
+    int rc = p.ks > 1 ? make_map_kchunks(&mx, a, a_rows, K, p.NP, p.ks) : make_map(&mx, a, a_rows, K, p.NP);
     if (rc) return rc;
     if (Q4)
         mw = mx;  // unused: the Q4 variant bulk-copies packed tiles
-    else if ((rc = make_map(&mw, b, b_rows, K, kWRows)))
+    else if ((rc = p.ks > 1 ? make_map_kchunks(&mw, b, b_rows, K, kWRows, p.ks) : make_map(&mw, b, b_rows, K, kWRows)))
         return rc;
     const int smem = p.stages * per_stage + 1024 + 1024;  // rings + alignment + barriers
     static bool configured = false;  // per template instance
@@ -1187,6 +1225,10 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
+            if (value != 1 && value != 2) return KL_EINVAL;
+            g_stream_ks = value;
+            return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_ctas = value;

@@ -47,5 +47,23 @@ inline int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
     return res == CUDA_SUCCESS ? 0 : KL_EINVAL;
 }
 
+// Row-major bf16 matrix [rows, cols] viewed as (64 columns, rows, cols / 64):
+// one box = box_rows rows x kchunks consecutive 64-column chunks, landing as
+// kchunks slabs of [box_rows][64] (each the same 128B-swizzled tile a 2D box
+// gives), so a single copy covers several k-blocks.
+inline int make_map_kchunks(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows, int kchunks) {
+    EncodeFn enc = encoder();
+    if (enc == nullptr) return KL_ENODEV;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTmaBoxK), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(cols / kTmaBoxK)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, static_cast<cuuint64_t>(kTmaBoxK) * 2};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kTmaBoxK), static_cast<cuuint32_t>(box_rows),
+                               static_cast<cuuint32_t>(kchunks)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return res == CUDA_SUCCESS ? 0 : KL_EINVAL;
+}
 
 }  // namespace kl

@@ -89,10 +89,11 @@ def test_gemm_residual_and_row_offset(K, cuda):
     close_bf16(to_bits(c), ref)
 
 
+@pytest.mark.parametrize("ks", [1, 2])
 @pytest.mark.parametrize("nmma", [1, 2])
 @pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (16, 4096, 4096, 0), (129, 1024, 2048, 1),
                                         (256, 2048, 1024, 2), (77, 28672 // 8, 4096, 2), (200, 384, 8192, 0)])
-def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
+def test_gemm_weight_streaming(K, cuda, ks, nmma, M, N, Kd, epi):
     """Decode path (swap-AB, stream-K): every shape/epilogue against the
     oracle, and bit-identical to itself across NMMA settings' reruns."""
     rows, off = M + 40, 13
@@ -103,6 +104,7 @@ def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
     r = orc.normal_bf16(M * n_out, 53, 1.0).reshape(M, n_out) if epi == 1 else None
     K.tune(K.TUNE_STREAM_NMMA, nmma)
     K.tune(K.TUNE_STREAM_GEMM, 2)  # force the streaming path at these small shapes
+    K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, ks)
     try:
         assert K.workspace_bytes(M, N, Kd, epi) > 0
         rd = to_dev(r, cuda) if r is not None else None
@@ -112,6 +114,7 @@ def test_gemm_weight_streaming(K, cuda, nmma, M, N, Kd, epi):
     finally:
         K.tune(K.TUNE_STREAM_NMMA, 1)
         K.tune(K.TUNE_STREAM_GEMM, 1)
+        K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, 2)
     assert torch.equal(c, c2)  # deterministic split reduction
     x = a[off:off + M]
     if epi == 2:

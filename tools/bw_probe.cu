@@ -114,6 +114,14 @@ int main() {
         const double gbs = time([&] { bulk_ring<<<sms * c.ctas_per_sm, 64, smem>>>(buf, bytes, c.chunk, c.piece, c.stages); });
         printf(", \"bulk_c%d_p%d_s%d_x%d\": %.0f", c.chunk, c.piece, c.stages, c.ctas_per_sm, gbs);
     }
+    // Fewer CTAs than SMs (the whole-tile SwiGLU GEMM runs 112): can each SM
+    // pull more than its 1/148 share?
+    for (int ctas : {112, 128}) {
+        const size_t smem = static_cast<size_t>(65536) * 3 + 48;
+        cudaFuncSetAttribute(bulk_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        const double gbs = time([&] { bulk_ring<<<ctas, 64, smem>>>(buf, bytes, 65536, 65536, 3); });
+        printf(", \"bulk_c65536_s3_ctas%d\": %.0f", ctas, gbs);
+    }
     // Short launches (68 MB, the decode-attention size) rotating over 4
     // buffers so L2 (126 MB) never holds the next launch's bytes.
     {

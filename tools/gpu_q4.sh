@@ -1,2 +1,6 @@
-timeout 600 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "rope" 2>&1 | tail -2
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rope" -c 4 python tools/prefill_run.py --bs 32 --n 8 --reps 1 2>&1 | grep -E "^  void|gpu__time" | cut -c1-70 | tail -4
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 300 python tools/profile_kernels.py --only ffn --iters 24 2>&1 | python -c "
+import json,sys; t=sys.stdin.read(); d=json.loads(t[t.index(\"{\"):])
+print({k: round(v[\"us\"],1) for k,v in d.items()})
+"
