@@ -150,8 +150,10 @@ def test_gemm_weight_streaming_small_workspace_and_off(K, cuda):
 
 
 @pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048), (128, 4096, 1024),
-                                   (64, 2048, 1408), (300, 512, 1792)])
+                                   (64, 2048, 1408), (300, 512, 1792), (8, 4096, 14336), (21, 4096, 14336)])
 def test_expert_ffn(K, cuda, M, d, f):
+    """Expert FFN (SwiGLU GEMM + down GEMM) against the CPU oracle, up to the
+    full Mixtral-8x7B expert (d 4096, f 14336: the weight-streaming path)."""
     rows, off = M + 50, 19
     x = orc.normal_bf16(rows * d, 31, 1.0).reshape(rows, d)
     w13 = orc.normal_bf16(2 * f * d, 32, 0.03).reshape(2 * f, d)
