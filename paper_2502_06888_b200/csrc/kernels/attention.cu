@@ -11,6 +11,7 @@
 // L1): algorithmic bytes per (sequence, layer) = retained * Hkv*hd*2 * 2.
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tma_host.cuh"
@@ -633,7 +634,7 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
                        const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
                        const int32_t* __restrict__ seq, int Hq, int Hkv, int HG, int cap, float scale_log2,
                        float* part_o, float* part_ml, int n_chunks, int64_t n_items, uint16_t* __restrict__ out,
-                       unsigned long long* counters, uint32_t tag, int mode) {
+                       unsigned long long* counters, uint32_t tag, int whole, int mode) {
     const int G = Hq / Hkv, HGn = Hkv / HG;
     const uint32_t box_bytes = kDmSlots * HG * HD * 2;
     const int qelems = HG * G * HD;
@@ -643,8 +644,13 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(kDmStages) * stage_bytes);
     uint64_t* empty = full + kDmStages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * n_items / gridDim.x;
-    const int64_t i1 = static_cast<int64_t>(blockIdx.x + 1) * n_items / gridDim.x;
+    // whole: ranges cover whole (token, group) pairs, so no segment is split
+    // across CTAs and every output is written directly.
+    const int64_t pairs = n_items / n_chunks;
+    const int64_t i0 = whole ? static_cast<int64_t>(blockIdx.x) * pairs / gridDim.x * n_chunks
+                             : static_cast<int64_t>(blockIdx.x) * n_items / gridDim.x;
+    const int64_t i1 = whole ? static_cast<int64_t>(blockIdx.x + 1) * pairs / gridDim.x * n_chunks
+                             : static_cast<int64_t>(blockIdx.x + 1) * n_items / gridDim.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kDmStages; ++s) {
             mbar_init(&full[s], 1);
@@ -821,6 +827,17 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
             }
         }
         if (!seg_last) continue;
+        if (seg_item == (static_cast<int64_t>(t) * HGn + hg) * n_chunks && k == n_chunks - 1) {
+            // The whole (token, group) ran in this warp: normalise and store.
+            if (g < G) {
+                const float inv = 1.f / l_run;
+                uint16_t* op = out + (static_cast<int64_t>(t) * Hq + (hg * HG + h) * G + g) * HD + 2 * c4;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    *reinterpret_cast<uint32_t*>(op + nt * 8) = pack_bf16(o[nt][0] * inv, o[nt][1] * inv);
+            }
+            continue;
+        }
         if (seg_valid && g < G) {
             const int hq_local = h * G + g;
             float* po = part_o + (seg_item * (HG * G) + hq_local) * HD + 2 * c4;
@@ -1285,7 +1302,19 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
     const int n_chunks = (cap + kDecChunk - 1) / kDecChunk;
     float* part_ml = static_cast<float*>(workspace);
     float* part_o = part_ml + T * n_chunks * Hq * 2;
-    const int HG = std::min(Hkv, kDmMaxHG);
+    // KV heads per CTA work item. With enough (token, head-group) pairs to
+    // fill the GPU (>= 80 % of the SMs), each CTA takes whole pairs and no
+    // token is split; otherwise the widest group and split tokens.
+    int HG = std::min(Hkv, kDmMaxHG);
+    int whole = 0;
+    for (int hg_try = HG; hg_try >= 1; hg_try /= 2) {
+        if (Hkv % hg_try) continue;
+        if (T * (Hkv / hg_try) * 5 >= static_cast<int64_t>(attn_sm_count()) * 4) {
+            HG = hg_try;
+            whole = 1;
+            break;
+        }
+    }
     if (g_decode_mma && cache_seqs > 0 && Hkv % HG == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
         static_assert(kDmSlots == kDecChunk, "workspace layout shared with the per-chunk kernel");
         CUtensorMap mk, mv;
@@ -1310,7 +1339,8 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
             occ_smem[hi][HG] = msmem;
         }
         const int64_t n_items = T * (Hkv / HG) * n_chunks;
-        const int ctas = static_cast<int>(std::min<int64_t>(n_items, static_cast<int64_t>(attn_sm_count()) * occ_cache[hi][HG]));
+        const int ctas = static_cast<int>(std::min<int64_t>(whole ? n_items / n_chunks : n_items,
+                                                            static_cast<int64_t>(attn_sm_count()) * occ_cache[hi][HG]));
         // Segment counters after the partials (8-byte aligned); tags are
         // quiet-NaN bit patterns, distinct per call.
         static std::atomic<uint32_t> epoch{1};
@@ -1319,7 +1349,7 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
             (reinterpret_cast<uintptr_t>(part_o + T * n_chunks * Hq * hd) + 7) & ~uintptr_t(7));
         kern<<<ctas, (HG + 1) * 32, msmem, stream>>>(mk, mv, q, q_stride, pos, seq, Hq, Hkv, HG, cap,
                                                      scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items,
-                                                     out, counters, tag, g_decode_mma);
+                                                     out, counters, tag, whole, g_decode_mma);
         return check_launch();
     }
     auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;
