@@ -1270,6 +1270,8 @@ extern "C" int64_t kl_attn_decode_workspace_bytes(int64_t T, int Hq, int hd, int
 // kernel: dims (64 columns, rows, 64-column chunks), box (64, 16 slots, the
 // group's chunks), 128B swizzle with the slot as the swizzle row.
 static int make_kv_map(CUtensorMap* map, const void* base, int64_t rows, int row_elems, int chunks_per_box) {
+    const MapKey key{base, rows, row_elems, -kDmSlots, -chunks_per_box};  // negative: this layout's own key space
+    if (map_cache_get(key, map)) return 0;
     EncodeFn enc = encoder();
     if (enc == nullptr) return KL_ENODEV;
     const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(row_elems / 64)};
@@ -1279,7 +1281,9 @@ static int make_kv_map(CUtensorMap* map, const void* base, int64_t rows, int row
     const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return res == CUDA_SUCCESS ? 0 : KL_EINVAL;
+    if (res != CUDA_SUCCESS) return KL_EINVAL;
+    map_cache_put(key, map);
+    return 0;
 }
 
 extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq,
