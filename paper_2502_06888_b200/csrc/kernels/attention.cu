@@ -929,8 +929,9 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     uint64_t* q_bar = &bars[0];
     uint64_t* k_bar = &bars[1];             // [2]
     uint64_t* v_bar = &bars[3];             // [2]
-    uint64_t* mma_bar = &bars[5];
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+    uint64_t* s_bar = &bars[5];             // [2] S = QK^T done, per TMEM S buffer
+    uint64_t* o_bar = &bars[7];             // O += PV done
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
 
     const int G = Hq / Hkv;
     const int P = 128 / G;  // query positions per tile
@@ -946,15 +947,17 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_q);
         tma_prefetch_desc(&tmap_kv);
-        for (int x = 0; x < 6; ++x) mbar_init(&bars[x], 1);
+        for (int x = 0; x < 8; ++x) mbar_init(&bars[x], 1);
         mbar_fence_init();
     }
-    if (warp == 0) tmem_alloc(tslot, 256);
+    if (warp == 0) tmem_alloc(tslot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t tS = tmem, tO = tmem + 128;
+    // Two S buffers (the next block's QK^T runs while this one's softmax is
+    // computed) and O.
+    const uint32_t tS0 = tmem, tO = tmem + 256;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
     // Key blocks: [lo, hi] covering the window of the tile, plus block 0 for the sink.
@@ -998,17 +1001,23 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         load_v(0);
         if (nblk > 1) load_v(1);
     }
-    uint32_t mma_phase = 0;
-    auto mma_s = [&](int ki) {  // thread 0: S = Q K^T for K load ki
+    auto mma_s = [&](int ki) {  // thread 0: S buffer ki&1 = Q K^T for K load ki
         const int bb = ki & 1;
         mbar_wait(&k_bar[bb], (ki >> 1) & 1);
         tc_fence_after();
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(tS, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
+                tc_mma_bf16(tS0 + bb * 128, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
                             sw128_kmajor_desc(smem_u32(Kb + bb * kBlk + c * kChunk) + k * 32), idesc_s, (c | k) != 0);
-        tc_commit(mma_bar);
+        tc_commit(&s_bar[bb]);
+    };
+    // S buffer b completes once per K load with that parity: load ki waits
+    // phase (ki >> 1) & 1.
+    auto wait_s = [&](int ki) {
+        mbar_wait(&s_bar[ki & 1], (ki >> 1) & 1);
+        __syncwarp();
+        tc_fence_after();
     };
     auto valid = [&](int j) { return j <= i && j < L && (j < sink || j > i - window); };
     // A 32-key chunk is entirely retained for this row when its first key is
@@ -1017,15 +1026,18 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
 
     // Pass 1: row max and sum over the retained keys (each half its columns).
     float m = -INFINITY, l = 0.f;
-    if (leader) mbar_wait(q_bar, 0);
+    if (leader) {
+        mbar_wait(q_bar, 0);
+        mma_s(0);
+    }
     for (int n = 0; n < nblk; ++n) {
         const int b = block_of(n);
-        if (leader) mma_s(n);
-        mbar_wait(mma_bar, mma_phase);
-        mma_phase ^= 1;
-        __syncwarp();
-        tc_fence_after();
+        // Next block's (or pass 2's first) QK^T into the other S buffer, ahead
+        // of this block's softmax; its K was loaded two uses back.
+        if (leader && n + 1 < k_total) mma_s(n + 1);
+        wait_s(n);
         if (leader && n + 2 < k_total) load_k(n + 2);  // its buffer's MMA has completed
+        const uint32_t tS = tS0 + (n & 1) * 128;
         for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
@@ -1053,7 +1065,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
             }
         }
         tc_fence_before();
-        __syncthreads();  // S consumed
+        __syncthreads();  // S buffer consumed
     }
     // Combine the two column halves' running (max, sum) per row.
     stats[(half * 2 + 0) * 128 + r] = m;
@@ -1074,16 +1086,24 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     }
     const float inv_l = 1.0f / l;
 
-    // Pass 2: P = softmax row (bf16, swizzled A tile), O += P V.
+    // Pass 2: P = softmax row (bf16, swizzled A tile), O += P V. The next
+    // block's QK^T is issued before this block's P is built; the P tile is
+    // rewritten only after the previous P.V completed.
+    uint32_t o_phase = 0;
     for (int n = 0; n < nblk; ++n) {
         const int b = block_of(n);
         const int ki = nblk + n;
-        if (leader) mma_s(ki);
-        mbar_wait(mma_bar, mma_phase);
-        mma_phase ^= 1;
-        __syncwarp();
-        tc_fence_after();
+        if (leader && ki + 1 < k_total) mma_s(ki + 1);
+        wait_s(ki);
         if (leader && ki + 2 < k_total) load_k(ki + 2);
+        if (n > 0) {  // P.V(n-1) done: P reusable, its V buffer free
+            mbar_wait(o_bar, o_phase);
+            o_phase ^= 1;
+            __syncwarp();
+            tc_fence_after();
+            if (leader && n + 1 < nblk) load_v(n + 1);
+        }
+        const uint32_t tS = tS0 + (ki & 1) * 128;
         for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
@@ -1118,15 +1138,12 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
                     tc_mma_bf16(tO, sw128_kmajor_desc(smem_u32(Ps + kc * kChunk) + k * 32),
                                 sw128_mnmajor_desc(smem_u32(Vb + vb * kBlk) + (kc * 64 + k * 16) * 128, kChunk), idesc_o,
                                 (n > 0 || kc > 0 || k > 0) ? 1u : 0u);
-            tc_commit(mma_bar);
+            tc_commit(o_bar);
         }
-        mbar_wait(mma_bar, mma_phase);  // P.V done: P and this V buffer reusable
-        mma_phase ^= 1;
-        __syncwarp();
-        tc_fence_after();
-        if (leader && n + 2 < nblk) load_v(n + 2);
-        __syncthreads();
     }
+    mbar_wait(o_bar, o_phase);  // last P.V done
+    __syncwarp();
+    tc_fence_after();
 
     // Epilogue: O row -> out[(seq, i)][(kvh*G + g)*HD + d].
     uint16_t* orow = out + (row0 + i) * static_cast<int64_t>(Hq) * HD + static_cast<int64_t>(kvh * G + g) * HD;
@@ -1145,7 +1162,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 

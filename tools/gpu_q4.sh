@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_expert|compute_attention|compute_gate"
+timeout 600 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "prefill" 2>&1 | tail -2
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn_prefill_tc" -c 3 python tools/prefill_run.py --bs 32 --n 8 --reps 1 2>&1 | grep -E "gpu__time" | cut -c1-70
