@@ -71,7 +71,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints */
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */
 #define KL_TUNE_PDL 5 /* 1 = weight-streaming GEMMs use programmatic dependent launch (default) */
-#define KL_TUNE_PREFILL_TC 6 /* 1 = tcgen05 prefill attention (default), 0 = CUDA-core fallback */
+#define KL_TUNE_PREFILL_TC 6 /* tcgen05 prefill attention: 2 = 64-key blocks, two CTAs per SM (default), 1 = 128-key blocks, 0 = CUDA-core fallback */
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
 #define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 2 (default; 3D TMA boxes, used where >= 3 stages fit) or 1 */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */

@@ -912,20 +912,24 @@ __device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint3
     return d;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kPfThreads, 1)
+template <int HD, int KEYS>
+__global__ void __launch_bounds__(kPfThreads)
 attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_kv,
                        int L, int Hq, int Hkv, int sink, int window, float scale, uint16_t* __restrict__ out) {
     constexpr int NCH = HD / 64;                  // 64-wide swizzle chunks along hd
-    constexpr int kChunk = 128 * 128;             // bytes of a [128 rows x 64] bf16 tile
-    constexpr int kBlk = NCH * kChunk;            // one K (or V) block of 128 keys
+    constexpr int kChunk = 128 * 128;             // bytes of a [128 rows x 64] bf16 tile (Q, P)
+    constexpr int kBlk = NCH * kChunk;            // the Q tile
+    constexpr int kvChunk = KEYS * 128;           // bytes of a [KEYS keys x 64] bf16 tile
+    constexpr int kvBlk = NCH * kvChunk;          // one K (or V) block of KEYS keys
+    constexpr int VBUF = KEYS == 64 ? 1 : 2;      // 64-key blocks: one V buffer, so 2 CTAs fit per SM
+    constexpr int PCH = KEYS / 64;                // 64-key chunks of the P tile
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* Qs = sm;                       // NCH x [128 rows x 128 B]
     uint8_t* Kb = Qs + kBlk;                // 2 buffers: K blocks, prefetched one ahead
-    uint8_t* Vb = Kb + 2 * kBlk;            // 2 buffers: V blocks
-    uint8_t* Ps = Vb + 2 * kBlk;            // 2 x [128 rows x 128 B]  (keys 0-63, 64-127)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + 2 * kChunk);
+    uint8_t* Vb = Kb + 2 * kvBlk;           // VBUF buffers: V blocks
+    uint8_t* Ps = Vb + VBUF * kvBlk;        // PCH x [128 rows x 128 B]  (keys 0-63, 64-127)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + PCH * kChunk);
     uint64_t* q_bar = &bars[0];
     uint64_t* k_bar = &bars[1];             // [2]
     uint64_t* v_bar = &bars[3];             // [2]
@@ -950,24 +954,25 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         for (int x = 0; x < 8; ++x) mbar_init(&bars[x], 1);
         mbar_fence_init();
     }
-    if (warp == 0) tmem_alloc(tslot, 512);
+    constexpr uint32_t kTmemCols = 2 * KEYS + HD <= 256 ? 256 : 512;
+    if (warp == 0) tmem_alloc(tslot, kTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     // Two S buffers (the next block's QK^T runs while this one's softmax is
     // computed) and O.
-    const uint32_t tS0 = tmem, tO = tmem + 256;
+    const uint32_t tS0 = tmem, tO = tmem + 2 * KEYS;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
 
     // Key blocks: [lo, hi] covering the window of the tile, plus block 0 for the sink.
     const int last = min(i0 + P - 1, L - 1);
-    const int b_lo = max(0, i0 - window + 1) / kPfKeys, b_hi = last / kPfKeys;
+    const int b_lo = max(0, i0 - window + 1) / KEYS, b_hi = last / KEYS;
     const bool sink_block = sink > 0 && b_lo > 0;
     const int nblk = (b_hi - b_lo + 1) + (sink_block ? 1 : 0);
     auto block_of = [&](int n) { return sink_block ? (n == 0 ? 0 : b_lo + n - 1) : b_lo + n; };
 
-    const uint32_t idesc_s = idesc_bf16_f32(128, kPfKeys);
+    const uint32_t idesc_s = idesc_bf16_f32(128, KEYS);
     const uint32_t idesc_o = idesc_bf16_f32(128, HD) | (1u << 16);  // B (V) MN-major
 
     // K loads form one sequence over both passes (index ki: pass 1 blocks
@@ -977,17 +982,17 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     const int k_total = 2 * nblk;
     auto load_k = [&](int ki) {  // thread 0
         const int bb = ki & 1;
-        const int krow = static_cast<int>(row0 + block_of(ki % nblk) * kPfKeys);
-        mbar_arrive_expect_tx(&k_bar[bb], kBlk);
+        const int krow = static_cast<int>(row0 + block_of(ki % nblk) * KEYS);
+        mbar_arrive_expect_tx(&k_bar[bb], kvBlk);
         for (int c = 0; c < NCH; ++c)
-            tma_load_2d(Kb + bb * kBlk + c * kChunk, &tmap_kv, &k_bar[bb], (Hq + kvh) * HD + c * 64, krow);
+            tma_load_2d(Kb + bb * kvBlk + c * kvChunk, &tmap_kv, &k_bar[bb], (Hq + kvh) * HD + c * 64, krow);
     };
     auto load_v = [&](int vi) {
-        const int bb = vi & 1;
-        const int krow = static_cast<int>(row0 + block_of(vi) * kPfKeys);
-        mbar_arrive_expect_tx(&v_bar[bb], kBlk);
+        const int bb = vi % VBUF;
+        const int krow = static_cast<int>(row0 + block_of(vi) * KEYS);
+        mbar_arrive_expect_tx(&v_bar[bb], kvBlk);
         for (int c = 0; c < NCH; ++c)
-            tma_load_2d(Vb + bb * kBlk + c * kChunk, &tmap_kv, &v_bar[bb], (Hq + Hkv + kvh) * HD + c * 64, krow);
+            tma_load_2d(Vb + bb * kvBlk + c * kvChunk, &tmap_kv, &v_bar[bb], (Hq + Hkv + kvh) * HD + c * 64, krow);
     };
     const bool leader = threadIdx.x == 0;
     if (leader) {
@@ -999,7 +1004,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         load_k(0);
         if (k_total > 1) load_k(1);
         load_v(0);
-        if (nblk > 1) load_v(1);
+        if (VBUF == 2 && nblk > 1) load_v(1);
     }
     auto mma_s = [&](int ki) {  // thread 0: S buffer ki&1 = Q K^T for K load ki
         const int bb = ki & 1;
@@ -1008,8 +1013,8 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(tS0 + bb * 128, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
-                            sw128_kmajor_desc(smem_u32(Kb + bb * kBlk + c * kChunk) + k * 32), idesc_s, (c | k) != 0);
+                tc_mma_bf16(tS0 + bb * KEYS, sw128_kmajor_desc(smem_u32(Qs + c * kChunk) + k * 32),
+                            sw128_kmajor_desc(smem_u32(Kb + bb * kvBlk + c * kvChunk) + k * 32), idesc_s, (c | k) != 0);
         tc_commit(&s_bar[bb]);
     };
     // S buffer b completes once per K load with that parity: load ki waits
@@ -1037,12 +1042,12 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         if (leader && n + 1 < k_total) mma_s(n + 1);
         wait_s(n);
         if (leader && n + 2 < k_total) load_k(n + 2);  // its buffer's MMA has completed
-        const uint32_t tS = tS0 + (n & 1) * 128;
-        for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
+        const uint32_t tS = tS0 + (n & 1) * KEYS;
+        for (int c0 = half * (KEYS / kPfParts); c0 < (half + 1) * (KEYS / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
             float bm = m;
-            const int j0 = b * kPfKeys + c0;
+            const int j0 = b * KEYS + c0;
             if (all_valid(j0)) {
 #pragma unroll
                 for (int x = 0; x < 32; ++x) {
@@ -1101,14 +1106,14 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
             o_phase ^= 1;
             __syncwarp();
             tc_fence_after();
-            if (leader && n + 1 < nblk) load_v(n + 1);
+            if (leader && n - 1 + VBUF < nblk) load_v(n - 1 + VBUF);
         }
-        const uint32_t tS = tS0 + (ki & 1) * 128;
-        for (int c0 = half * (kPfKeys / kPfParts); c0 < (half + 1) * (kPfKeys / kPfParts); c0 += 32) {
+        const uint32_t tS = tS0 + (ki & 1) * KEYS;
+        for (int c0 = half * (KEYS / kPfParts); c0 < (half + 1) * (KEYS / kPfParts); c0 += 32) {
             float v[32];
             tmem_ld32(tS + lane_off + c0, v);
             uint8_t* prow = Ps + (c0 / 64) * kChunk + r * 128;
-            const int j0 = b * kPfKeys + c0;
+            const int j0 = b * KEYS + c0;
             const bool full = all_valid(j0);
 #pragma unroll
             for (int q8 = 0; q8 < 4; ++q8) {
@@ -1130,14 +1135,14 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
         __syncthreads();
         if (leader) {
             tc_fence_after();
-            const int vb = n & 1;
-            mbar_wait(&v_bar[vb], (n >> 1) & 1);
-            for (int kc = 0; kc < 2; ++kc)
+            const int vb = n % VBUF;
+            mbar_wait(&v_bar[vb], (n / VBUF) & 1);
+            for (int kc = 0; kc < PCH; ++kc)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     tc_mma_bf16(tO, sw128_kmajor_desc(smem_u32(Ps + kc * kChunk) + k * 32),
-                                sw128_mnmajor_desc(smem_u32(Vb + vb * kBlk) + (kc * 64 + k * 16) * 128, kChunk), idesc_o,
-                                (n > 0 || kc > 0 || k > 0) ? 1u : 0u);
+                                sw128_mnmajor_desc(smem_u32(Vb + vb * kvBlk) + (kc * 64 + k * 16) * 128, kvChunk),
+                                idesc_o, (n > 0 || kc > 0 || k > 0) ? 1u : 0u);
             tc_commit(o_bar);
         }
     }
@@ -1162,7 +1167,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, kTmemCols);
     }
 }
 
@@ -1220,7 +1225,7 @@ __global__ void attn_prefill_kernel(const uint16_t* __restrict__ qkv, int n_seq,
 using namespace kl;
 
 namespace kl {
-int g_prefill_tc = 1;  // kl_tune(KL_TUNE_PREFILL_TC, ...)
+int g_prefill_tc = 2;  // kl_tune(KL_TUNE_PREFILL_TC, ...): 2 = 64-key blocks (default), 1 = 128-key blocks, 0 = CUDA cores
 int g_decode_mma = 1;  // kl_tune(KL_TUNE_DECODE_MMA, ...)
 int g_rope_tok = 1;    // kl_tune(KL_TUNE_ROPE_TOKEN_BLOCKS, ...)
 
@@ -1405,11 +1410,16 @@ extern "C" int kl_attn_prefill(const uint16_t* qkv, int n_seq, int L, int Hq, in
         CUtensorMap mq, mkv;
         int rc = make_map(&mq, qkv, static_cast<int64_t>(n_seq) * L, width, 128 / G);
         if (rc) return rc;
-        rc = make_map(&mkv, qkv, static_cast<int64_t>(n_seq) * L, width, kPfKeys);
+        // g_prefill_tc 2: 64-key blocks with one V buffer (two CTAs per SM).
+        const int keys = g_prefill_tc == 2 ? 64 : kPfKeys;
+        rc = make_map(&mkv, qkv, static_cast<int64_t>(n_seq) * L, width, keys);
         if (rc) return rc;
         const int nch = hd / 64;
-        const int smem = 5 * nch * 128 * 128 + 2 * 128 * 128 + 1024 + 128 + 4096;  // Q, 2 K, 2 V, P, stats
-        auto kern = hd == 128 ? attn_prefill_tc_kernel<128> : attn_prefill_tc_kernel<64>;
+        const int vbuf = keys == 64 ? 1 : 2;
+        const int smem = nch * 128 * 128 + (2 + vbuf) * nch * keys * 128 + (keys / 64) * 128 * 128 + 1024 + 128 +
+                         4096;  // Q, 2 K, V, P, alignment, barriers, stats
+        auto kern = keys == 64 ? (hd == 128 ? attn_prefill_tc_kernel<128, 64> : attn_prefill_tc_kernel<64, 64>)
+                               : (hd == 128 ? attn_prefill_tc_kernel<128, 128> : attn_prefill_tc_kernel<64, 128>);
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         const dim3 grid((L + 128 / G - 1) / (128 / G), Hkv, n_seq);
         kern<<<grid, kPfThreads, smem, stream>>>(mq, mkv, L, Hq, Hkv, sink, cap - sink, scale, out);

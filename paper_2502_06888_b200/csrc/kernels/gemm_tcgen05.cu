@@ -1220,7 +1220,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_HINT: g_stream_hint = value != 0; return KL_OK;
         case 99: g_stream_debug = value; return KL_OK;
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
-        case KL_TUNE_PREFILL_TC: g_prefill_tc = value != 0; return KL_OK;
+        case KL_TUNE_PREFILL_TC: g_prefill_tc = value; return KL_OK;
         case KL_TUNE_DECODE_MMA: g_decode_mma = value; return KL_OK;
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;

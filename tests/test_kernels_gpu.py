@@ -377,7 +377,7 @@ def test_decode_attention_split_kv(K, cuda, mma, T, Hq, Hkv, hd, cap, p):
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 
 
-@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("tc", [1, 2, 0])
 @pytest.mark.parametrize("n_seq,L,Hq,Hkv,hd,cap,sink", [(3, 40, 4, 1, 128, 24, 4), (2, 512, 32, 8, 128, 260, 4),
                                                        (2, 300, 8, 8, 64, 100, 0), (1, 200, 16, 2, 128, 1000, 4)])
 def test_prefill_attention_window(K, cuda, tc, n_seq, L, Hq, Hkv, hd, cap, sink):
@@ -392,7 +392,7 @@ def test_prefill_attention_window(K, cuda, tc, n_seq, L, Hq, Hkv, hd, cap, sink)
         K.attn_prefill(to_dev(qkv, cuda), n_seq, L, Hq, Hkv, hd, cap, sink, hd ** -0.5, out)
         torch.cuda.synchronize()
     finally:
-        K.tune(K.TUNE_PREFILL_TC, 1)
+        K.tune(K.TUNE_PREFILL_TC, 2)
     ref = orc.attn_prefill(qkv, n_seq, L, Hq, Hkv, hd, cap, sink, hd ** -0.5)
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 
