@@ -19,9 +19,12 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--hbm-cap", type=float, default=24e9)
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--trace", action="store_true", help="per-CTA phase trace of the step's last streaming GEMM")
     a = ap.parse_args()
     from paper_2502_06888_b200 import kernels as K
     K.tune(K.TUNE_PDL, a.pdl)
+    if a.trace:
+        K.tune(99, 128)
     ns = argparse.Namespace(model="mixtral-8x7b", batch_size=64, n_batches=8, prompt_len=512, hbm_cap=a.hbm_cap,
                             host_distinct_layers=4, warmup=1, steps=a.steps)
     eng = Engine(bench.engine_config(ns, 0, 1))
@@ -30,6 +33,21 @@ def main():
     eng.reset_log()
     for s in range(a.steps):
         eng.step(2 + s, None, want_next=False)
+    if a.trace:
+        import ctypes
+        buf = (ctypes.c_ulonglong * (256 * 12))()
+        K._lib.kl_stream_trace(buf, 256)
+        tr = np.array(buf, dtype=np.float64).reshape(256, 12)[:148]
+        t0 = tr[:, 0][tr[:, 0] > 0].min()
+        rel = (tr - t0) / 1e3
+        rel[tr == 0] = np.nan
+        names = ["start", "mma0", "mma_end", "epi_last", "flags_ok", "landed", "sums_done", "end", "contrib0", "published"]
+        print("in-step trace of the last streaming GEMM (us from first CTA start)")
+        for i, nm in enumerate(names):
+            col = rel[:, i]
+            if np.all(np.isnan(col)):
+                continue
+            print(f"  {nm:10s} med {np.nanmedian(col):7.2f}  min {np.nanmin(col):7.2f}  max {np.nanmax(col):7.2f}")
     tl = eng.report("timeline_csv")["text"]
     rows = list(csv.DictReader(io.StringIO(tl)))
     print("columns:", list(rows[0].keys()))
