@@ -74,6 +74,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_PREFILL_TC 6 /* tcgen05 prefill attention: 2 = 64-key blocks, two CTAs per SM (default), 1 = 128-key blocks, 0 = CUDA-core fallback */
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
 #define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 2 (default; 3D TMA boxes, used where >= 3 stages fit) or 1 */
+#define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 0 = one CTA per SM */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */

@@ -1046,6 +1046,7 @@ int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
+int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...)
 int g_stream_ks = 2;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2): 2 where >= 3 stages still fit
 
 int sm_count() {
@@ -1132,6 +1133,8 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     int G = std::max(1, std::min(sm_count() * g_stream_ctas, p.units / 4));
     if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
         G = n_tiles;  // one whole tile per CTA: no split partials, the rest of the SMs idle
+    else if (g_stream_even_split && n_tiles < G && G / n_tiles >= 2 && p.KB % (G / n_tiles) == 0)
+        G = n_tiles * (G / n_tiles);  // every tile split into the same number of equal k-ranges
     G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
     G = std::min(G, static_cast<int>(kFlagBytes / 4));
     if (G < 1) return KL_EUNSUPPORTED;
@@ -1225,6 +1228,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_EVEN_SPLIT: g_stream_even_split = value != 0; return KL_OK;
         case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
             if (value != 1 && value != 2) return KL_EINVAL;
             g_stream_ks = value;

@@ -65,6 +65,7 @@ TUNE_STREAM_WHOLE_TILES = 7
 TUNE_GEMM_PERSISTENT = 8
 TUNE_ROPE_TOKEN_BLOCKS = 11  # RoPE/KV append: block per token (1) or thread per element (0)
 TUNE_STREAM_KBLOCKS_PER_STAGE = 12  # weight-streaming GEMM k-blocks per stage (1 or 2)
+TUNE_STREAM_EVEN_SPLIT = 13  # weight-streaming GEMM: equal k-splits per tile
 TUNE_DECODE_MMA = 9  # persistent mma.sync split-KV decode attention (1) or per-chunk CUDA-core kernel (0)
 
 

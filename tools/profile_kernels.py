@@ -133,6 +133,7 @@ def main():
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--persist", type=int, default=1)
     ap.add_argument("--ks", type=int, default=2, help="stream GEMM k-blocks per stage")
+    ap.add_argument("--even", type=int, default=1, help="stream GEMM equal k-splits per tile")
     ap.add_argument("--whole", type=int, default=70, help="whole-tile grid when tiles >= pct%% of SMs")
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
     ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
@@ -142,6 +143,7 @@ def main():
     K.tune(K.TUNE_STREAM_WHOLE_TILES, args.whole)
     K.tune(K.TUNE_GEMM_PERSISTENT, args.persist)
     K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, args.ks)
+    K.tune(K.TUNE_STREAM_EVEN_SPLIT, args.even)
     global TRACE, GAP_MS
     GAP_MS = args.gap_ms
     TRACE = bool(args.debug & 128)
