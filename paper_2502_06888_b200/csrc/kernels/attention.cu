@@ -634,15 +634,15 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
                        const uint16_t* __restrict__ q, int64_t q_stride, const int32_t* __restrict__ pos,
                        const int32_t* __restrict__ seq, int Hq, int Hkv, int HG, int cap, float scale_log2,
                        float* part_o, float* part_ml, int n_chunks, int64_t n_items, uint16_t* __restrict__ out,
-                       unsigned long long* counters, uint32_t tag, int whole, int mode) {
+                       unsigned long long* counters, uint32_t tag, int whole, int nst, int mode) {
     const int G = Hq / Hkv, HGn = Hkv / HG;
     const uint32_t box_bytes = kDmSlots * HG * HD * 2;
     const int qelems = HG * G * HD;
     const uint32_t stage_bytes = (2 * box_bytes + qelems * 2 + 1023) & ~1023u;
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(kDmStages) * stage_bytes);
-    uint64_t* empty = full + kDmStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(nst) * stage_bytes);
+    uint64_t* empty = full + nst;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // whole: ranges cover whole (token, group) pairs, so no segment is split
     // across CTAs and every output is written directly.
@@ -652,7 +652,7 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
     const int64_t i1 = whole ? static_cast<int64_t>(blockIdx.x + 1) * pairs / gridDim.x * n_chunks
                              : static_cast<int64_t>(blockIdx.x + 1) * n_items / gridDim.x;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kDmStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], HG);
         }
@@ -665,6 +665,8 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
         tma_prefetch_desc(&tmap_k);
         tma_prefetch_desc(&tmap_v);
         int64_t it = 0;
+        int ps = 0;          // ring slot of the next item
+        uint32_t pph = 0;    // its fill round parity
         // (token, group, chunk) of i0, then advanced incrementally; pos/seq
         // are read once per (token, group) segment.
         int k = static_cast<int>(i0 % n_chunks), hg = static_cast<int>((i0 / n_chunks) % HGn);
@@ -683,8 +685,12 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
             const int j0 = k * kDmSlots;
             if (n - j0 <= 0) continue;
             const bool seg_first = i == i0 || k == 0;
-            const int s = static_cast<int>(it % kDmStages);
-            if (it >= kDmStages) mbar_wait(&empty[s], static_cast<uint32_t>((it / kDmStages + 1) & 1));
+            const int s = ps;
+            if (it >= nst) mbar_wait(&empty[s], pph ^ 1u);
+            if (++ps == nst) {
+                ps = 0;
+                pph ^= 1u;
+            }
             uint8_t* st = ring + static_cast<size_t>(s) * stage_bytes;
             mbar_arrive_expect_tx(&full[s], 2 * box_bytes + (seg_first ? qelems * 2u : 0u));
             const int row = row_t + j0, chunk = hg * HG * HD / 64;
@@ -708,6 +714,8 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
     float m_run = -INFINITY, l_run = 0.f;
     bool seg_valid = false;
     int64_t seg_item = 0;
+    int cs_ = 0;          // ring slot of the next item
+    uint32_t cph = 0;     // its fill round parity
     int64_t it = 0;
     int k = static_cast<int>(i0 % n_chunks), hg = static_cast<int>((i0 / n_chunks) % HGn);
     int t = static_cast<int>(i0 / n_chunks / HGn);
@@ -729,8 +737,12 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
             seg_item = i;
         }
         if (cnt > 0) {
-            const int s = static_cast<int>(it % kDmStages);
-            mbar_wait(&full[s], static_cast<uint32_t>((it / kDmStages) & 1));
+            const int s = cs_;
+            mbar_wait(&full[s], cph);
+            if (++cs_ == nst) {
+                cs_ = 0;
+                cph ^= 1u;
+            }
             uint8_t* Kb = ring + static_cast<size_t>(s) * stage_bytes;
             uint8_t* Vb = Kb + box_bytes;
             if (mode >= 2) {  // load-only timing probe
@@ -1353,6 +1365,9 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
                              ~static_cast<size_t>(1023);
         const size_t msmem = kDmStages * stage + 1024 + 2 * kDmStages * 8;
         if (msmem > 227 * 1024) return KL_EUNSUPPORTED;
+        // (A deeper ring at one CTA per SM measured the same as two CTAs with
+        // three stages each.)
+        const int nst = kDmStages;
         auto kern = hd == 128 ? attn_decode_mma_kernel<128> : attn_decode_mma_kernel<64>;
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
         static int occ_cache[2][kDmMaxHG + 1] = {};
@@ -1375,7 +1390,7 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
             (reinterpret_cast<uintptr_t>(part_o + T * n_chunks * Hq * hd) + 7) & ~uintptr_t(7));
         kern<<<ctas, (HG + 1) * 32, msmem, stream>>>(mk, mv, q, q_stride, pos, seq, Hq, Hkv, HG, cap,
                                                      scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items,
-                                                     out, counters, tag, whole, g_decode_mma);
+                                                     out, counters, tag, whole, nst, g_decode_mma);
         return check_launch();
     }
     auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;

@@ -1,3 +1,2 @@
-timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_expert|compute_attention|compute_gate"
-echo "-- no gate"
-KL_ENGINE_NO_ENQUEUE_GATE=1 timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_expert|compute_attention|compute_gate"
+timeout 600 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "decode_attention" 2>&1 | tail -1
+timeout 300 python tools/profile_kernels.py --only attn --iters 20 2>&1 | grep -A1 graph | grep -v GBs
