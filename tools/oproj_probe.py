@@ -13,7 +13,7 @@ for M in (64, 128):
     x = torch.randn(M, d, dtype=bf, device=dev)
     h = torch.randn(M, d, dtype=bf, device=dev)
     qkv = torch.empty(M, (Hq + 2 * Hkv) * hd, dtype=bf, device=dev)
-    for mode in (1, 2):
+    for mode in (0, 1, 2):
         K.tune(K.TUNE_STREAM_GEMM, mode)
         t1 = timed_graph(lambda i: K.gemm(ao, wo[i % 8], c=h, residual=h, epilogue=1), 16)
         t2 = timed_graph(lambda i: K.gemm(x, wqkv[i % 8], c=qkv), 16)
