@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "decode_attention" 2>&1 | tail -1
-timeout 300 python tools/profile_kernels.py --only attn --iters 20 2>&1 | grep -A1 graph | grep -v GBs
+timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_expert"
+KL_FFN_NO_FIRST_PDL=1 timeout 600 python tools/op_timing.py --steps 2 2>&1 | grep -E "compute_expert"
