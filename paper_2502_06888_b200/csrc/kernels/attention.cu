@@ -1259,7 +1259,9 @@ extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int 
     if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || hd % 2 || cap <= sink || sink < 0) return KL_EINVAL;
     if (!qkv || !pos || !seq || !k_cache || !v_cache) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    if (g_rope_tok && hd % 8 == 0 && T <= 0x7fffffff &&
+    // Block per token for prefill-sized calls; decode-sized calls (a few
+    // dozen tokens) spread better with a thread per element.
+    if (g_rope_tok && T >= 4 * 148 && hd % 8 == 0 && T <= 0x7fffffff &&
         ((reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache)) & 15) == 0) {
         rope_append_tok_kernel<<<static_cast<unsigned>(T), kRopeThreads, static_cast<size_t>(hd) * 4, stream>>>(
             qkv, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink, chunk_last_pos);

@@ -289,7 +289,7 @@ def test_coact_and_predict_exact(K, cuda, E, k, T):
 
 
 @pytest.mark.parametrize("T,Hq,Hkv,hd,cap,sink,last", [(4096, 32, 8, 128, 260, 4, 4095), (64, 32, 8, 128, 260, 4, -1),
-                                                        (37, 8, 2, 64, 40, 0, -1)])
+                                                        (37, 8, 2, 64, 40, 0, -1), (700, 32, 8, 128, 1000, 4, -1)])
 def test_rope_token_blocks_bit_identical(K, cuda, T, Hq, Hkv, hd, cap, sink, last):
     """The block-per-token RoPE/KV append (shared cos/sin table) writes the
     same bits as the thread-per-element kernel: rotated q/k in place, K and V
