@@ -909,6 +909,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 // Stage bf16 outputs [token][128 features] in smem, then
                 // coalesced 16-byte row stores.
                 uint16_t* stage = reinterpret_cast<uint16_t*>(smem);
+                float* stage_f = reinterpret_cast<float*>(smem);  // residual: fp32 staging, one rounding after the add
                 constexpr int kOut = EPI == kSwiGLU ? 1 : NMMA;
                 for (int j = 0; j < kOut; ++j) {
                     const int64_t feat0 = static_cast<int64_t>(EPI == kSwiGLU ? t : t * NMMA + j) * kWRows;
@@ -919,18 +920,35 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                             if (EPI == kSwiGLU || jj == j) tmem_ld16(acc0 + jj * p.acc_stride + col, acc[jj]);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            float v = epi_value<EPI>(acc, j, i);
+                            const float v = epi_value<EPI>(acc, j, i);
                             if constexpr (EPI == kResidual)
-                                if (col + i < p.M) v += bf2f(p.r[static_cast<int64_t>(col + i) * p.ldc + feat0 + frow]);
-                            stage[(col + i) * kWRows + frow] = f2bf(v);
+                                stage_f[(col + i) * kWRows + frow] = v;
+                            else
+                                stage[(col + i) * kWRows + frow] = f2bf(v);
                         }
                     }
                     named_bar_sync(1, 128);
                     const int vec = kWRows / 8;  // 16-byte vectors per token row
                     for (int v = etid; v < p.M * vec; v += 128) {
                         const int row = v / vec, x = v % vec;
-                        *reinterpret_cast<uint4*>(p.c + static_cast<int64_t>(row) * p.ldc + feat0 + x * 8) =
-                            *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
+                        uint16_t* o = p.c + static_cast<int64_t>(row) * p.ldc + feat0 + x * 8;
+                        if constexpr (EPI == kResidual) {
+                            // Residual rows read as 16-byte vectors (coalesced) here
+                            // rather than element-wise in the TMEM pass.
+                            const uint4 rv = *reinterpret_cast<const uint4*>(p.r + static_cast<int64_t>(row) * p.ldc + feat0 + x * 8);
+                            const float4 a = *reinterpret_cast<const float4*>(stage_f + row * kWRows + x * 8);
+                            const float4 b = *reinterpret_cast<const float4*>(stage_f + row * kWRows + x * 8 + 4);
+                            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+                            const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                            uint32_t ow[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                ow[e] = pack2(f[2 * e] + bf2f(static_cast<uint16_t>(rw[e] & 0xffffu)),
+                                              f[2 * e + 1] + bf2f(static_cast<uint16_t>(rw[e] >> 16)));
+                            *reinterpret_cast<uint4*>(o) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                        } else {
+                            *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
+                        }
                     }
                     named_bar_sync(1, 128);
                 }
@@ -1125,7 +1143,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     if (p.stages < 2 || p.tmem_cols * g_stream_ctas > 512) return KL_EUNSUPPORTED;
     // The idle ring doubles as the landing buffer of split partials (8 KB
     // units) and as the bf16 output staging tile of the last segment.
-    if (p.stages * stage_bytes < p.NP * kWRows * 2) return KL_EUNSUPPORTED;
+    if (p.stages * stage_bytes < p.NP * kWRows * (EPI == kResidual ? 4 : 2)) return KL_EUNSUPPORTED;
     p.hint = g_stream_hint;
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
