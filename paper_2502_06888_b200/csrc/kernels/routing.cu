@@ -389,6 +389,10 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
 __global__ void __launch_bounds__(256)
 rmsnorm_row_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d, float eps,
                    uint16_t* __restrict__ out) {
+    // The QKV GEMM that follows (launched with programmatic dependent
+    // launch) may start now and prefetch its weights; it reads this
+    // kernel's output only after griddepcontrol.wait.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t row = blockIdx.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float rstd = row_rstd(x + row * d, d, eps, lane);
