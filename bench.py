@@ -137,7 +137,7 @@ def engine_config(args, rank, world, ep_id=None):
         "kv_retention": {"mode": "streaming", "sink_tokens": 4, "window_tokens": 256},
         "routing": "gate",
         "prefill": False,
-        "record_trace": False,
+        "record_trace": True,  # the executed routing feeds the reference validator below
         "host_distinct_layers": args.host_distinct_layers,
         "weight_seed": 7 if ep_id is not None else 7 + rank,
     }
@@ -368,6 +368,11 @@ def run_ours(args):
     clk = clocks.stop()
     metrics = eng.report("metrics")
     total_ms = sum(dev_ms)
+    # The executed op log through the reference validator (validate_schedule,
+    # schedule.cpp:729-860) and the reference ledger replayed on the measured
+    # timeline (placement.cpp:257-292), both outside the timed region.
+    validation = eng.report("validate")
+    ledger = eng.report("ledger")
 
     # Timed region 2: end to end through the C-ABI with host buffers.
     rng = np.random.default_rng(rank)
@@ -491,6 +496,10 @@ def run_ours(args):
                 "hot_accuracy": metrics["hot_accuracy"],
                 "link_bound_ceiling_tok_s": seqs / (metrics["h2d_bytes"] / args.steps / (link * 1e9)),
             },
+            "validate": {"violations": len(validation["violations"]),
+                         "first": validation["violations"][:3], "skipped": validation.get("skipped"),
+                         "ledger_vram_high_water": ledger["vram_high_water"],
+                         "ledger_within_cap": ledger["within_capacity"]},
             "setup_s": setup_s,
             "wall_s_timed": wall,
             "q4": q4,

@@ -113,9 +113,14 @@ class TinyModel:
         own_idx = idx.copy()
         if forced_idx is not None:
             idx = forced_idx.astype(np.int32).reshape(idx.shape)
-            sel = np.take_along_axis(logits, idx, 1)
-            p = np.exp(sel - sel[:, :1])
-            w = (p / p.sum(1, keepdims=True)).astype(np.float32)
+            sel = np.take_along_axis(logits, idx, 1).astype(np.float32)
+            if D.get("score_mode", 0) == 0:  # Mixtral: softmax over the k selected logits
+                p = np.exp(sel - sel[:, :1])
+                w = (p / p.sum(1, keepdims=True)).astype(np.float32)
+            else:  # softmax over all E logits, weights of the selected ones (no renormalisation)
+                mx = logits.max(1, keepdims=True).astype(np.float32)
+                s = np.exp(logits.astype(np.float32) - mx).sum(1, keepdims=True)
+                w = (np.exp(sel - mx) / s).astype(np.float32)
         if W["shared"] is not None:
             # h += shared SwiGLU FFN(x2): bf16 hidden, fp32 down projection + residual, one rounding.
             w13s, w2s = W["shared"]

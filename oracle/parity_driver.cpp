@@ -21,6 +21,7 @@
 
 #include "moesim/correlation.hpp"
 #include "moesim/cost.hpp"
+#include "moesim/error.hpp"
 #include "moesim/model.hpp"
 #include "moesim/planner.hpp"
 #include "moesim/quant.hpp"
@@ -94,8 +95,41 @@ const char* dup(const std::string& s) {
     return out;
 }
 
+// 4-bit format pins (quant.cpp:120-252): fit_minmax per group and
+// dequantize of a flat QuantizedTensor, straight from the library.
+json quant_ops(const json& q) {
+    json out;
+    if (q.contains("fit")) {
+        const int bits = q.value("bits", 4);
+        json fits = json::array();
+        for (const auto& g : q["fit"]) {
+            const std::vector<float> v = g.get<std::vector<float>>();
+            const moesim::QuantParams p = moesim::fit_minmax(v, bits);
+            fits.push_back({p.scale, p.zero});
+        }
+        out["fit"] = fits;
+    }
+    if (q.contains("dequant")) {
+        const json& d = q["dequant"];
+        moesim::QuantizedTensor t;
+        t.cfg.bits = d.value("bits", 4);
+        t.cfg.group_size = d.value("group_size", 64);
+        t.n_elements = d.at("n").get<std::size_t>();
+        t.packed = d.at("packed").get<std::vector<std::uint8_t>>();
+        t.scales_f16 = d.at("scales").get<std::vector<std::uint16_t>>();
+        t.zeros_f16 = d.at("zeros").get<std::vector<std::uint16_t>>();
+        out["dequant"] = moesim::dequantize(t);
+    }
+    if (q.contains("bytes")) {
+        moesim::QuantConfig c;
+        out["bytes"] = moesim::quantized_bytes(q["bytes"].get<std::int64_t>(), c);
+    }
+    return out;
+}
+
 json request(const char* text) {
     json req = json::parse(text);
+    if (req.contains("quant_ops")) return quant_ops(req["quant_ops"]);
     const moesim::ModelSpec model = model_of(req.value("model", json::object()));
     const moesim::HardwareProfile hw = hw_of(req.value("hw", json::object()));
     const json w = req.value("workload", json::object());
@@ -134,7 +168,25 @@ json request(const char* text) {
     out["plan_text"] = plan.to_text();
     out["n_batches"] = plan.n_batches;
     cfg.n_batches = plan.n_batches;
-    moesim::ActivationTrace trace = moesim::generate_trace(model, cfg, skew, seed);
+    moesim::ActivationTrace trace;
+    if (!req.contains("recorded")) {
+        trace = moesim::generate_trace(model, cfg, skew, seed);
+    } else {
+        // Routing recorded by the B200 engine (gate mode): the schedule is
+        // rebuilt from the selections the engine actually executed. A
+        // decode-only run of S steps is a trace of S single-token steps
+        // (prompt_len 1), renumbered by step_offset when printed.
+        const json& rj = req["recorded"];
+        moesim::BatchGroupConfig tc = cfg;
+        tc.prompt_len = rj.value("prompt_len", cfg.prompt_len);
+        tc.gen_len = rj.at("gen_len").get<int>();
+        trace = moesim::generate_trace(model, tc, moesim::SkewSpec::uniform(), 0);
+        const std::vector<std::uint16_t> sel = rj.at("sel").get<std::vector<std::uint16_t>>();
+        if (sel.size() != trace.sel.size())
+            throw moesim::ConfigError("recorded trace has " + std::to_string(sel.size()) + " ids, expected " +
+                                      std::to_string(trace.sel.size()));
+        trace.sel = sel;
+    }
     out["trace_hash"] = fnv1a(trace.sel.data(), trace.sel.size());
     out["trace_size"] = trace.sel.size();
     if (req.value("want_trace", false)) out["trace"] = trace.sel;
@@ -163,10 +215,16 @@ json request(const char* text) {
         v == moesim::Variant::klotski
             ? moesim::build_klotski_schedule(plan, trace, provider, sopts)
             : moesim::build_baseline_schedule(v, plan, trace, provider, sopts);
-    out["schedule_text"] = sched.to_text();
-    out["n_ops"] = sched.ops.size();
     const moesim::ValidationReport rep = moesim::validate_schedule(sched, trace, plan);
     out["violations"] = rep.violations;
+    if (const int off = req.value("step_offset", 0); off != 0) {
+        moesim::Schedule shifted = sched;
+        for (moesim::StreamOp& op : shifted.ops) op.step = static_cast<std::int16_t>(op.step + off);
+        out["schedule_text"] = shifted.to_text();
+    } else {
+        out["schedule_text"] = sched.to_text();
+    }
+    out["n_ops"] = sched.ops.size();
 
     if (req.value("simulate", true)) {
         moesim::MemoryLedger ledger =

@@ -279,7 +279,10 @@ void Engine::plan_memory() {
         r_recv_max_ = ep_ ? static_cast<int64_t>(G_) * t_max_ * D_.k : 0;
         const int64_t Rx = std::max<int64_t>(t_max_ * D_.k, r_recv_max_);
         const int64_t R = t_max_ * D_.k;
-        const int64_t chunk = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1));
+        // One local expert can receive rows from every rank under EP, so the
+        // FFN chunk is bounded by the exchange rows, not this rank's own.
+        const int64_t chunk = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(Rx, 1));
+        const int64_t chunk_own = std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1));
         byte_count ws = 0;
         auto add = [&](byte_count b) { ws += ((b + 1023) / 1024) * 1024; };
         add(2 * attn_slot_bytes_);
@@ -293,7 +296,7 @@ void Engine::plan_memory() {
         add(5 * R * 4 + R * 4 + t_max_ * D_.E * 4);                              // idx x2, forced, pos, row_token, weight, logits
         add(2 * Rx * D_.d * 2);                                                   // xp, y
         add(chunk * D_.f * 2);                                                   // hs
-        if (D_.fs() > 0) add(chunk * D_.fs() * 2);                               // shared-expert hidden
+        if (D_.fs() > 0) add(chunk_own * D_.fs() * 2);                           // shared-expert hidden
         add(kl_permute_workspace_bytes(Rx, D_.E));
         if (ep_) {  // exchange buffers, labels, counts, co-activation delta
             add(r_recv_max_ * D_.d * 2 * 2 + R * D_.d * 2);
@@ -406,7 +409,7 @@ void Engine::allocate_device() {
     const int64_t Rx = std::max<int64_t>(R, r_recv_max_);
     xp_ = bf(Rx * D_.d);
     y_ = bf(Rx * D_.d);
-    hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.f);
+    hs_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(Rx, 1)) * D_.f);
     if (D_.fs() > 0) hshared_ = bf(std::min<int64_t>(cfg_.ffn_chunk_rows, std::max<int64_t>(R, 1)) * D_.fs());
     perm_ws_ = take(kl_permute_workspace_bytes(Rx, D_.E));
     gemm_ws_ = gemm_ws_bytes_ > 0 ? take(gemm_ws_bytes_) : nullptr;
@@ -570,6 +573,9 @@ void Engine::init_weights() {
     // (bf16), or the bf16 scratch + a pool slot for the Q4T bytes.
     uint16_t* stage = cfg_.quant ? wscratch_
                                  : (D_.expert_elems() >= D_.attention_elems() ? pool_.ptr[0] : attn_slot_[0]);
+    // The router (+ shared experts) tensor can exceed both (deepseek-v2-lite:
+    // 17.4M gate elements vs 16.8M attention): it is staged in its own slot.
+    uint16_t* gate_stage = gate_slot_[0];
     uint8_t* qstage = reinterpret_cast<uint8_t*>(pool_.ptr[0]);
     // bf16 stage -> host copy in the streamed format.
     auto to_host = [&](void* host, bool expert) {
@@ -631,8 +637,8 @@ void Engine::init_weights() {
             kl_check(kl_fill_normal_bf16(stage, D_.attention_elems(), aseed, sd, st), "init attn");
             to_host(attn_dst, false);
         }
-        kl_check(kl_fill_normal_bf16(stage, D_.gate_elems(), tensor_seed(ws, kKindGate, l, 0), sd, st), "init gate");
-        cuda_check(cudaMemcpyAsync(gate_dst, stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+        kl_check(kl_fill_normal_bf16(gate_stage, D_.gate_elems(), tensor_seed(ws, kKindGate, l, 0), sd, st), "init gate");
+        cuda_check(cudaMemcpyAsync(gate_dst, gate_stage, spec_.gate_bytes, cudaMemcpyDeviceToHost, st), "d2h");
         if (on_disk) {
             cuda_check(cudaStreamSynchronize(st), "init sync");
             const char* src = window_slot_[0];
@@ -652,6 +658,9 @@ void Engine::init_weights() {
                    "table");
     cuda_check(cudaMemcpyAsync(marginal_, table0_.marginal.data(), D_.E * 8, cudaMemcpyHostToDevice, st), "marginal");
     cuda_check(cudaMemsetAsync(h_, 0, t_max_ * D_.d * 2, st), "h");
+    // A decode step fed from the device reads the previous step's greedy ids;
+    // before any step has produced them they are token 0, never garbage.
+    cuda_check(cudaMemsetAsync(next_ids_, 0, t_max_ * 4, st), "next ids");
     cuda_check(cudaStreamSynchronize(st), "init sync");
     (void)host_done;
 }
@@ -695,6 +704,8 @@ std::string Engine::describe() const {
     j["plan_text"] = plan_.to_text();
     j["n_batches"] = plan_.n_batches;
     j["batch_size"] = cfg_.workload.batch_size;
+    j["prompt_len"] = cfg_.workload.prompt_len;
+    j["gen_len"] = cfg_.workload.gen_len;
     j["expert_slots"] = slots_;
     j["arena_used_bytes"] = arena_used_;
     j["hbm_cap_bytes"] = cfg_.hbm_cap;
@@ -749,7 +760,8 @@ std::string Engine::describe() const {
     j["sink_tokens"] = cfg_.retention.sink_tokens;
     j["window_tokens"] = cfg_.retention.window_tokens;
     j["dims"] = {{"L", D_.L}, {"d", D_.d}, {"f", D_.f}, {"Hq", D_.Hq}, {"Hkv", D_.Hkv}, {"hd", D_.hd},
-                 {"E", D_.E}, {"k", D_.k}, {"V", D_.V}};
+                 {"E", D_.E}, {"k", D_.k}, {"V", D_.V}, {"theta", D_.theta}, {"eps", D_.eps},
+                 {"score_mode", D_.score_mode}, {"n_shared", D_.n_shared}, {"f_shared", D_.f_shared}};
     return j.dump();
 }
 

@@ -16,6 +16,7 @@
 // of their previous occupant (bounded pool with backpressure).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -103,11 +104,17 @@ PrefetchDecision Engine::decide(int /*step*/, int layer) const {
 double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     if (step < 0 || step >= cfg_.workload.gen_len) throw RangeError("engine: step outside the batch group");
     if (step == 0 && !cfg_.prefill) throw ConfigError("engine: built without prefill support (prefill=false)");
-    cur_step_ = step;
-    executed_steps_.insert(step);
     const int n = plan_.n_batches, bs = cfg_.workload.batch_size;
     const int tpb = tokens_per_batch(step);
     const int64_t T = static_cast<int64_t>(n) * tpb;
+    // Host ids index the embedding table on the device: reject bad ones
+    // before anything is enqueued (the caller provides exactly T of them).
+    if (tokens_in != nullptr)
+        for (int64_t i = 0; i < T; ++i)
+            if (tokens_in[i] < 0 || tokens_in[i] >= D_.V)
+                throw RangeError("engine: token id " + std::to_string(tokens_in[i]) + " outside the vocabulary");
+    cur_step_ = step;
+    executed_steps_.insert(step);
     const int64_t seqs = static_cast<int64_t>(n) * bs;
     cudaStream_t cs = stream_of(StreamId::compute);
 
@@ -846,7 +853,17 @@ std::string Engine::report(const std::string& what) {
         j["records"] = recs;
     } else if (what == "trace") {
         j["sel"] = recorded_.sel;
-        j["text_header"] = trace_to_string(ActivationTrace{}).substr(0, 0);
+    } else if (what.rfind("trace_steps:", 0) == 0) {
+        // Executed routing of steps [a, b) only ("trace_steps:a:b"), in the
+        // reference's flat [step][layer][batch][token][k] order.
+        int a = 0, b = 0;
+        if (std::sscanf(what.c_str(), "trace_steps:%d:%d", &a, &b) != 2 || a < 0 || b <= a ||
+            b > recorded_.n_steps)
+            throw ConfigError("engine report: bad step range '" + what + "'");
+        const size_t lo = recorded_.offset(a, 0, 0, 0);
+        const size_t hi = b == recorded_.n_steps ? recorded_.sel.size() : recorded_.offset(b, 0, 0, 0);
+        j["sel"] = std::vector<uint16_t>(recorded_.sel.begin() + lo, recorded_.sel.begin() + hi);
+        j["steps"] = {a, b};
     } else if (what == "validate") {
         if (ep_) {
             // A shard's schedule covers its local experts only; the

@@ -96,7 +96,10 @@ class Engine:
         """Run one step; tokens (host int32) or None to feed back the last greedy tokens."""
         tin = None
         if tokens is not None:
-            tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+            tokens = np.ascontiguousarray(tokens, dtype=np.int32).reshape(-1)
+            want = self.n_seqs * (self.info["prompt_len"] if step == 0 else 1)
+            if tokens.size != want:
+                raise EngineError(f"step {step}: expected {want} token ids, got {tokens.size}")
             tin = tokens.ctypes.data_as(C.c_void_p)
         nxt = np.empty(self.n_seqs, np.int32) if want_next else None
         ms = C.c_double()

@@ -1,0 +1,144 @@
+"""Parity at the configurations that are actually run (BASELINE.json configs).
+
+* configs[1], the bench config itself: Mixtral-8x7B, 32 layers, bs 64 x n 8,
+  24e9-byte HBM cap, StreamingLLM KV retention, gate routing, decode-only
+  (synthetic prefilled KV). The executed op log must equal
+  moesim_ref::build_klotski_schedule rebuilt on the routing the engine
+  recorded (schedule.cpp:466-634, correlation.cpp:74-140), validate, and keep
+  the reference ledger within the cap.
+* configs[3] shapes: Mixtral-8x22B layers (d 6144, f 16384, 48/8 heads;
+  model.cpp:70-82), 2 of 56 layers, replay op log = reference.
+* configs[4] shapes: DeepSeek-V2-Lite routed experts (E 64, top-6, softmax
+  over all scores) + 2 shared experts: replay op log = reference under a
+  markov trace (many cold loads per block), and hidden states teacher-forced
+  against the CPU oracle.
+"""
+import argparse
+
+import numpy as np
+import pytest
+
+from tests import parity
+from tests.test_engine_gpu import make, run_all_steps, teacher_forced_check
+
+pytestmark = pytest.mark.gpu
+
+
+def _op_lines(text):
+    return text.split("\n", 1)[1]
+
+
+def bench_cfg(steps_total):
+    import bench
+    args = argparse.Namespace(model="mixtral-8x7b", batch_size=64, n_batches=8, prompt_len=512, hbm_cap=24e9,
+                              host_distinct_layers=0, warmup=0, steps=0, quant_bits=0)
+    cfg = bench.engine_config(args, 0, 1)
+    cfg["workload"]["gen_len"] = 1 + steps_total
+    cfg["record_trace"] = True
+    return cfg
+
+
+def test_bench_config_op_log_equals_reference_on_recorded_routing(cuda):
+    S = 2
+    cfg = bench_cfg(S)
+    eng = make(cfg)
+    info = eng.info
+    assert info["n_batches"] == 8 and info["batch_size"] == 64
+    assert info["resident_expert_layers"] < info["dims"]["L"]  # experts stream
+    eng.fill_kv_synthetic(512)
+    for s in range(1, S + 1):
+        nxt, _ = eng.step(s, None, want_next=True)
+        assert ((nxt >= 0) & (nxt < info["dims"]["V"])).all()
+    got = eng.report("schedule")["text"]
+    sel = eng.report(f"trace_steps:1:{S + 1}")["sel"]
+    assert len(sel) == S * info["dims"]["L"] * 8 * 64 * 2
+    val = eng.report("validate")
+    led = eng.report("ledger")
+    m = eng.report("metrics")
+    eng.close()
+    assert val["violations"] == [], val["violations"][:5]
+    assert led["within_capacity"] and led["carried_in_frees"] == 0, (led["vram_high_water"], led["vram_capacity"])
+    req = parity.request_for_engine(info, cfg)
+    req["recorded"] = {"prompt_len": 1, "gen_len": S, "sel": sel}
+    req["step_offset"] = 1
+    ref = parity.ref()(req)
+    assert "error" not in ref, ref
+    assert ref["plan_text"] == info["plan_text"]
+    assert ref["violations"] == []
+    assert _op_lines(got) == _op_lines(ref["schedule_text"])
+    assert m["expert_loads"] > 0 and m["tokens_generated"] == S * 512
+
+
+def test_mixtral_8x22b_replay_op_log_equals_reference(cuda):
+    """configs[3] layer shapes (2 of 56 layers), experts streamed."""
+    cfg = {"model": {"preset": "mixtral-8x22b", "n_layers": 2},
+           "workload": {"batch_size": 64, "n_batches": 2, "prompt_len": 16, "gen_len": 3},
+           "hbm_cap_bytes": 12_000_000_000, "host_distinct_layers": 2,
+           "routing": "replay", "skew": {"kind": "zipf", "s": 1.5}, "trace_seed": 5}
+    eng = make(cfg)
+    assert eng.info["dims"]["d"] == 6144 and eng.info["dims"]["f"] == 16384 and eng.info["dims"]["Hq"] == 48
+    assert eng.info["expert_bytes"] == 603_979_776  # model.cpp:70-82
+    assert eng.info["resident_expert_layers"] < 2
+    run_all_steps(eng, cfg)
+    got = eng.report("schedule")["text"]
+    ref = parity.ref()(parity.request_for_engine(eng.info, cfg))
+    assert "error" not in ref, ref
+    assert got == ref["schedule_text"]
+    assert eng.report("validate")["violations"] == []
+    assert eng.report("ledger")["within_capacity"]
+    eng.close()
+
+
+def test_mixtral_8x22b_gate_mode_deterministic_and_valid(cuda):
+    cfg = {"model": {"preset": "mixtral-8x22b", "n_layers": 2},
+           "workload": {"batch_size": 64, "n_batches": 2, "prompt_len": 16, "gen_len": 3},
+           "hbm_cap_bytes": 12_000_000_000, "host_distinct_layers": 2, "routing": "gate"}
+    outs = []
+    for _ in range(2):
+        e = make(cfg)
+        outs.append(run_all_steps(e, cfg, seed=9))
+        assert e.report("validate")["violations"] == []
+        e.close()
+    assert all(np.array_equal(a, b) for a, b in zip(outs[0], outs[1]))
+
+
+DSV2 = {"model": {"preset": "deepseek-v2-lite", "n_layers": 2, "vocab": 4096},
+        "workload": {"batch_size": 8, "n_batches": 4, "prompt_len": 8, "gen_len": 3}}
+
+
+def _dsv2_cap():
+    """Largest cap (100 MB steps down from 3 GB) that streams expert layers."""
+    for cap in range(3_000_000_000, 1_000_000_000, -100_000_000):
+        try:
+            e = make(dict(DSV2, hbm_cap_bytes=cap))
+        except Exception:
+            continue
+        streamed = e.info["resident_expert_layers"] < 2
+        e.close()
+        if streamed:
+            return cap
+    pytest.skip("no cap streams the DeepSeek expert layers")
+
+
+def test_deepseek_replay_op_log_equals_reference(cuda):
+    """E 64, top-6, 2 shared experts; markov trace: many colds per block, the
+    prefetcher's 64x64 co-activation table and cold-load ordering."""
+    cap = _dsv2_cap()
+    cfg = dict(DSV2, hbm_cap_bytes=cap, routing="replay", skew={"kind": "markov", "s": 1.5, "p": 0.8},
+               trace_seed=7)
+    eng = make(cfg)
+    assert eng.info["dims"]["E"] == 64 and eng.info["dims"]["k"] == 6 and eng.info["dims"]["n_shared"] == 2
+    run_all_steps(eng, cfg)
+    got = eng.report("schedule")["text"]
+    pf = eng.report("prefetch")["records"]
+    ref = parity.ref()(dict(parity.request_for_engine(eng.info, cfg), want_prefetch=True))
+    assert "error" not in ref, ref
+    assert got == ref["schedule_text"]
+    assert got.count("load_expert") > 20
+    assert eng.report("validate")["violations"] == []
+    assert len(pf) == cfg["workload"]["gen_len"] * 2
+    eng.close()
+
+
+def test_deepseek_teacher_forced_hidden_states(cuda):
+    teacher_forced_check(dict(DSV2, hbm_cap_bytes=_dsv2_cap()), agree_min=0.8)

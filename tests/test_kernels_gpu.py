@@ -150,10 +150,13 @@ def test_gemm_weight_streaming_small_workspace_and_off(K, cuda):
 
 
 @pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048), (128, 4096, 1024),
-                                   (64, 2048, 1408), (300, 512, 1792), (8, 4096, 14336), (21, 4096, 14336)])
+                                   (64, 2048, 1408), (300, 512, 1792), (8, 4096, 14336), (21, 4096, 14336),
+                                   (128, 4096, 14336), (8, 6144, 16384), (128, 6144, 16384)])
 def test_expert_ffn(K, cuda, M, d, f):
     """Expert FFN (SwiGLU GEMM + down GEMM) against the CPU oracle, up to the
-    full Mixtral-8x7B expert (d 4096, f 14336: the weight-streaming path)."""
+    full Mixtral-8x7B expert (d 4096, f 14336: the weight-streaming path) at
+    the bench's routed rows (M 128) and the Mixtral-8x22B expert (d 6144,
+    f 16384) at decode sizes."""
     rows, off = M + 50, 19
     x = orc.normal_bf16(rows * d, 31, 1.0).reshape(rows, d)
     w13 = orc.normal_bf16(2 * f * d, 32, 0.03).reshape(2 * f, d)
@@ -169,7 +172,8 @@ def test_expert_ffn(K, cuda, M, d, f):
 
 
 @pytest.mark.parametrize("T,d,E,k,mode", [(64, 4096, 8, 2, 0), (300, 512, 8, 2, 0), (97, 2048, 64, 6, 1),
-                                          (5, 256, 4, 4, 0), (1000, 512, 8, 2, 0), (700, 2048, 64, 6, 1)])
+                                          (5, 256, 4, 4, 0), (1000, 512, 8, 2, 0), (700, 2048, 64, 6, 1),
+                                          (64, 6144, 8, 2, 0), (512, 4096, 8, 2, 0), (64, 2048, 64, 6, 1)])
 def test_gate_topk_bit_exact(K, cuda, T, d, E, k, mode):
     h = orc.normal_bf16(T * d, 41, 1.0).reshape(T, d)
     nw = orc.normal_bf16(d, 42, 0.1).reshape(d)
@@ -293,7 +297,8 @@ def test_coact_and_predict_exact(K, cuda, E, k, T):
 def test_rope_token_blocks_bit_identical(K, cuda, T, Hq, Hkv, hd, cap, sink, last):
     """The block-per-token RoPE/KV append (shared cos/sin table) writes the
     same bits as the thread-per-element kernel: rotated q/k in place, K and V
-    rows in the cache (prefill chunk with its window filter, and decode)."""
+    rows in the cache (prefill chunk with its window filter, and decode); and
+    both agree with the CPU oracle's cache (V bit-exact, K within 1 ulp)."""
     width = (Hq + 2 * Hkv) * hd
     qkv = orc.normal_bf16(T * width, 81, 1.0).reshape(T, width)
     pos = (np.arange(T) % 600).astype(np.int32) if last < 0 else np.arange(T, dtype=np.int32) % (last + 1)
@@ -313,6 +318,16 @@ def test_rope_token_blocks_bit_identical(K, cuda, T, Hq, Hkv, hd, cap, sink, las
         outs.append((to_bits(q), to_bits(kc), to_bits(vc)))
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+    # Both against the oracle's cache: V bit-exact, K within 1 bf16 ulp.
+    kc = np.zeros(8 * cap * Hkv * hd, np.uint16)
+    vc = np.zeros_like(kc)
+    q_ref = qkv.copy()
+    orc.rope_kv_append(q_ref, Hq, Hkv, hd, pos, seq, 1e6, kc, vc, cap, sink, last)
+    _, gk, gv = outs[0]
+    assert np.array_equal(gv, vc)
+    assert np.array_equal(gk != 0, kc != 0)
+    kf, rk = orc.bits_to_f32(gk), orc.bits_to_f32(kc)
+    assert np.all(np.abs(kf - rk) <= 2 ** -7 * np.abs(rk) + 2 ** -16 * np.abs(rk).max())
 
 
 def test_rope_append_and_decode_attention(K, cuda):
@@ -337,9 +352,20 @@ def test_rope_append_and_decode_attention(K, cuda):
         torch.cuda.synchronize()
         got_q = orc.bits_to_f32(to_bits(qd))
         assert np.abs(got_q - orc.bits_to_f32(qkv)).max() <= 2e-2 * np.abs(orc.bits_to_f32(qkv)).max()
-        # Compare attention against the oracle fed the GPU's own roped q and cache.
-        ref = orc.attn_decode(to_bits(qd), width, pos, seq, Hq, Hkv, hd, to_bits(kcd), to_bits(vcd), cap, scale)
+        # The device KV cache against the oracle's own cache (not the GPU's
+        # state fed back): V rows are copies -> bit-exact; K rows are rotated
+        # (sincosf/powf on each side) -> same occupied slots, within 1 bf16 ulp.
+        gk, gv = to_bits(kcd), to_bits(vcd)
+        assert np.array_equal(gv, vc), p
+        assert np.array_equal(gk != 0, kc != 0), p
+        kf, rk = orc.bits_to_f32(gk), orc.bits_to_f32(kc)
+        assert np.all(np.abs(kf - rk) <= 2 ** -7 * np.abs(rk) + 2 ** -16 * np.abs(rk).max()), p
+        # Attention against the oracle fed the GPU's own roped q and cache
+        # (kernel arithmetic), and against the oracle's own state end to end.
+        ref = orc.attn_decode(to_bits(qd), width, pos, seq, Hq, Hkv, hd, gk, gv, cap, scale)
         close_bf16(to_bits(out), orc.bits_to_f32(ref))
+        own = orc.attn_decode(qkv, width, pos, seq, Hq, Hkv, hd, kc, vc, cap, scale)
+        close_bf16(to_bits(out), orc.bits_to_f32(own))
         out2 = torch.empty_like(out)
         K.attn_decode_split(qd, width, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda), Hq, Hkv, hd,
                             kcd, vcd, cap, sink, scale, out2)
@@ -351,7 +377,8 @@ def test_rope_append_and_decode_attention(K, cuda):
 @pytest.mark.parametrize("T,Hq,Hkv,hd,cap,p", [(5, 32, 8, 128, 260, 600), (5, 32, 8, 128, 260, 40),
                                                (5, 16, 16, 64, 100, 99), (5, 8, 1, 128, 70, 69),
                                                (64, 32, 8, 128, 260, 600), (37, 32, 8, 128, 260, 200),
-                                               (300, 8, 2, 64, 40, 39)])
+                                               (300, 8, 2, 64, 40, 39), (64, 48, 8, 128, 260, 600),
+                                               (7, 48, 8, 128, 260, 130), (32, 16, 16, 128, 260, 600)])
 def test_decode_attention_split_kv(K, cuda, mma, T, Hq, Hkv, hd, cap, p):
     """Split-KV decode against the oracle, for the persistent mma.sync kernel
     (mma=1: segments spanning several chunks and CTA boundaries inside a
