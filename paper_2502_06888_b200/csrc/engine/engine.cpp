@@ -135,6 +135,12 @@ EngineConfig parse_config(const std::string& text) {
         c.ep_rank = j["ep"].value("rank", 0);
         c.ep_world = j["ep"].value("world", 1);
         c.ep_nccl_id = j["ep"].value("nccl_id", "");
+        c.ep_backend = j["ep"].value("backend", "nccl");
+        c.ep_group = j["ep"].value("group", "");
+        if (c.ep_backend != "nccl" && c.ep_backend != "loopback")
+            throw ConfigError("engine EP: backend must be 'nccl' or 'loopback'");
+        if (c.ep_backend == "loopback" && c.ep_world > 1 && c.ep_group.empty())
+            throw ConfigError("engine EP: the loopback backend needs a group name");
         if (c.ep_world < 1 || c.ep_rank < 0 || c.ep_rank >= c.ep_world || D.E % c.ep_world != 0)
             throw ConfigError("engine EP: need 0 <= rank < world and experts divisible by world");
         if (c.variant != Variant::klotski) throw ConfigError("engine EP: only the klotski variant is sharded");
@@ -302,6 +308,7 @@ void Engine::plan_memory() {
             add(r_recv_max_ * D_.d * 2 * 2 + R * D_.d * 2);
             add((R + 3 * r_recv_max_) * 4 + (3LL * D_.E + 2 * El_ + 8) * 4);
             add((static_cast<int64_t>(D_.E) * D_.E + D_.E) * 8);
+            if (cfg_.ep_backend == "loopback") add(static_cast<int64_t>(G_) * (D_.E * D_.E + D_.E) * 8);
         }
         // Split-K partials: the largest request of any small-M GEMM we issue.
         gemm_ws_bytes_ = 0;
@@ -438,6 +445,8 @@ void Engine::allocate_device() {
         offsets2_ = i32(El_ + 1);
         send_counts_ = i32(D_.E + 1);
         delta_ = static_cast<int64_t*>(take((static_cast<int64_t>(D_.E) * D_.E + D_.E) * 8));
+        if (cfg_.ep_backend == "loopback")
+            xstage_ = static_cast<int64_t*>(take(static_cast<int64_t>(G_) * (D_.E * D_.E + D_.E) * 8));
         recv_x_ = bf(r_recv_max_ * D_.d);
         y_back_ = bf(r_recv_max_ * D_.d);
         y_ret_ = bf(R * D_.d);

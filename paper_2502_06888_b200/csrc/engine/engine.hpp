@@ -78,7 +78,12 @@ struct EngineConfig {
     bool record_hidden = false;
     int ep_rank = 0, ep_world = 1;
     bool ep = false;                // expert-parallel engine (also for world 1)
-    std::string ep_nccl_id;         // 256 hex chars of ncclUniqueId (world > 1)
+    std::string ep_nccl_id;         // 256 hex chars of ncclUniqueId (world > 1, backend nccl)
+    // Exchange backend for world > 1: "nccl" (one process per GPU) or
+    // "loopback" (G engines of one process on one device, host threads,
+    // device copies + events; rendezvous by ep_group name).
+    std::string ep_backend = "nccl";
+    std::string ep_group;
     bool prefill = true;
     std::optional<moesim::QuantConfig> quant;  // 4-bit streamed experts / attention (Q4T)
     std::string disk_dir;           // disk-tier store directory (default $TMPDIR, else /tmp)
@@ -108,6 +113,7 @@ class Engine {
     std::string report(const std::string& what);
     void reset_log();
     void read_hidden(uint16_t* host, int64_t n) const;
+    struct Exchange;  // expert-parallel exchange backend (engine_ep.cpp)
 
   private:
     // setup
@@ -283,11 +289,14 @@ class Engine {
     moesim::detail::BlockRouting ep_read_routing(int step, int layer);
     void ep_dispatch();
     void ep_return(int64_t T);
+    void exchange_rows(const char* send, const std::vector<int64_t>& soff, const std::vector<int64_t>& scnt, char* recv,
+                       const std::vector<int64_t>& roff, const std::vector<int64_t>& rcnt, int64_t row_bytes,
+                       cudaStream_t st);
     moesim::ModelSpec spec_g_;            // global model (E experts) for traces/tables
     bool ep_ = false;
     int G_ = 1, rank_ = 0, El_ = 0;
-    struct Nccl;
-    Nccl* nccl_ = nullptr;
+    Exchange* xch_ = nullptr;
+    int64_t* xstage_ = nullptr;           // loopback all-reduce staging, [G][E*E + E] int64
     void ep_shutdown();
     int32_t *label_map_ = nullptr, *lbl_ = nullptr, *recv_ids_ = nullptr, *pos2_ = nullptr, *row_token2_ = nullptr;
     int32_t *recv_counts_ = nullptr, *hist_all_ = nullptr, *counts2_ = nullptr, *offsets2_ = nullptr;
@@ -295,6 +304,7 @@ class Engine {
     int64_t* delta_ = nullptr;
     uint16_t *recv_x_ = nullptr, *y_back_ = nullptr, *y_ret_ = nullptr;
     int64_t r_recv_max_ = 0, r_recv_ = 0, r_send_ = 0;
+    int64_t ep_max_local_rows_ = 0;       // most rows one local expert received (since reset)
     std::vector<int64_t> send_cnt_, send_off_, recv_cnt_, recv_off_;
     int32_t* host_recv_ids_ = nullptr;
     bool dispatched_ = false;

@@ -727,6 +727,7 @@ void Engine::reset_log() {
     t0_recorded_ = false;
     tokens_generated_ = 0;
     launches_ = 0;
+    ep_max_local_rows_ = 0;
     step_ms_.clear();
     hidden_dumps_.clear();
     diag_rows_.clear();
@@ -830,6 +831,11 @@ std::string Engine::report(const std::string& what) {
             j["disk_gbs_busy"] = stage_busy > 0 ? stage_bytes / (stage_busy * 1e-12) / 1e9 : 0.0;
         }
         j["launches"] = launches_;
+        if (ep_) {
+            j["ep_world"] = G_;
+            j["ep_rank"] = rank_;
+            j["ep_max_local_rows"] = ep_max_local_rows_;
+        }
         int64_t n_expert_ops = 0, expert_rows = 0;
         for (const SimEvent& e : tl)
             if (s.ops[e.op_id].kind == OpKind::compute_expert) {

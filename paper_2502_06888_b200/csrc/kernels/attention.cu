@@ -11,6 +11,7 @@
 // L1): algorithmic bytes per (sequence, layer) = retained * Hkv*hd*2 * 2.
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1372,18 +1373,26 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
         const int nst = kDmStages;
         auto kern = hd == 128 ? attn_decode_mma_kernel<128> : attn_decode_mma_kernel<64>;
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+        // Occupancy per (hd, HG, smem), queried once; several host threads
+        // (loopback expert-parallel engines) may launch concurrently.
         static int occ_cache[2][kDmMaxHG + 1] = {};
         static size_t occ_smem[2][kDmMaxHG + 1] = {};
+        static std::mutex occ_mu;
         const int hi = hd == 128;
-        if (occ_smem[hi][HG] != msmem) {
-            int occ = 0;
-            KL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (HG + 1) * 32, msmem));
-            occ_cache[hi][HG] = std::max(occ, 1);
-            occ_smem[hi][HG] = msmem;
+        int occ_now = 0;
+        {
+            std::lock_guard<std::mutex> lk(occ_mu);
+            if (occ_smem[hi][HG] != msmem) {
+                int occ = 0;
+                KL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (HG + 1) * 32, msmem));
+                occ_cache[hi][HG] = std::max(occ, 1);
+                occ_smem[hi][HG] = msmem;
+            }
+            occ_now = occ_cache[hi][HG];
         }
         const int64_t n_items = T * (Hkv / HG) * n_chunks;
         const int ctas = static_cast<int>(std::min<int64_t>(whole ? n_items / n_chunks : n_items,
-                                                            static_cast<int64_t>(attn_sm_count()) * occ_cache[hi][HG]));
+                                                            static_cast<int64_t>(attn_sm_count()) * occ_now));
         // Segment counters after the partials (8-byte aligned); tags are
         // quiet-NaN bit patterns, distinct per call.
         static std::atomic<uint32_t> epoch{1};

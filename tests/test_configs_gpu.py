@@ -141,4 +141,7 @@ def test_deepseek_replay_op_log_equals_reference(cuda):
 
 
 def test_deepseek_teacher_forced_hidden_states(cuda):
-    teacher_forced_check(dict(DSV2, hbm_cap_bytes=_dsv2_cap()), agree_min=0.8)
+    # 64 router logits, top-6: the 6th/7th gap is often tiny, and the CPU's
+    # router input differs from the GPU's by the attention block's bf16
+    # rounding, so a routing mismatch is accepted only below a 1e-2 margin.
+    teacher_forced_check(dict(DSV2, hbm_cap_bytes=_dsv2_cap()), agree_min=0.8, margin_tol=1e-2)
