@@ -34,11 +34,15 @@
  *   workload: {batch_size, n_batches, prompt_len, gen_len}
  *   hbm_cap_bytes, host_dram_bytes, pcie_bandwidth, attn_ps, gate_ps, expert_ps
  *   kv_retention: {mode: "full"|"streaming", sink_tokens, window_tokens}
- *   variant: "klotski"|"strawman_no_reorder"|"multibatch_full_prefetch"
+ *   variant: "klotski"|"strawman_no_reorder"|"multibatch_full_prefetch"|"simple"
  *   routing: "gate"|"replay";  skew: {kind, s, p};  trace_seed, warmup_seed
  *   weight_seed, host_distinct_layers (0 = every layer distinct)
  *   expert_slots (0 = auto), ffn_chunk_rows, record_trace, record_hidden
- *   ep: {rank, world}  expert-parallel shard (experts e with e % world == rank)
+ *   ep: {rank, world, backend: "nccl"|"loopback", nccl_id, group}  expert-parallel
+ *       shard (experts e with e % world == rank); loopback = G engines of one
+ *       process on one device (host threads), rendezvous by group name
+ *   profile: {measure: "decode"|"prefill"}  plan with rates measured here
+ *   solve_n: true  let make_plan solve n (ignores workload.n_batches)
  */
 #ifndef KLOTSKI_ENGINE_H
 #define KLOTSKI_ENGINE_H
@@ -85,6 +89,17 @@ int kl_engine_reset_log(kl_engine* e);
  * NUL into hex_out[257]) and shares it; every rank then passes it as
  * config "ep": {"rank": r, "world": G, "nccl_id": hex}. 0 = success. */
 int kl_ep_unique_id(char* hex_out);
+
+/* Planner stage 1 ("measure, then solve"): time this
+ * engine's kernels on the config's model shapes (attention block, router,
+ * expert FFN at the phase's mean routed rows) and the pinned H2D link on one
+ * and two copy streams. phase = "decode" | "prefill". JSON out: per-token
+ * ps rates for moesim::HardwareProfile (model.hpp:43-58:
+ * attn/gate/expert_compute_per_token) and pcie_bandwidth (bytes/s). Feeds
+ * moesim::build_cost_profile (cost.cpp:106-167) and make_plan
+ * (planner.cpp:167-239); config key "profile": {"measure": phase} makes
+ * kl_engine_create plan with it. Errors: kl_engine_last_error(NULL). */
+int kl_measure_profile(const char* config_json, const char* phase, char** json_out);
 
 /* Copy the group's current hidden states [T, d] (bf16 bits) to host. */
 int kl_engine_read_hidden(kl_engine* e, uint16_t* host, int64_t n_elems);

@@ -112,7 +112,6 @@ EngineConfig parse_config(const std::string& text) {
         c.retention.window_tokens = r.value("window_tokens", 256);
     }
     c.variant = variant_from_name(j.value("variant", "klotski"));
-    if (c.variant == Variant::simple) throw ConfigError("engine: the 'simple' row-by-row variant is not executed");
     c.replay = j.value("routing", "gate") == "replay";
     if (j.contains("skew")) {
         const json& s = j["skew"];
@@ -147,6 +146,11 @@ EngineConfig parse_config(const std::string& text) {
         if (j.value("routing", "gate") != "gate") throw ConfigError("engine EP: routing must come from the gate");
     }
     c.prefill = j.value("prefill", true);
+    if (j.contains("profile") && j["profile"].is_object() && j["profile"].contains("measure")) {
+        c.measure_phase = j["profile"]["measure"].get<std::string>();
+        if (c.measure_phase != "decode" && c.measure_phase != "prefill")
+            throw ConfigError("engine: profile.measure must be 'decode' or 'prefill'");
+    }
     if (j.contains("quant") && !j["quant"].is_null()) {
         moesim::QuantConfig q;
         q.bits = j["quant"].value("bits", 4);
@@ -210,6 +214,15 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     if (kl_device_supported() != 1) throw std::runtime_error("engine: device is not sm_100 (B200)");
+    if (!cfg_.measure_phase.empty()) {
+        // Paper stage 1: the planner's rates are measured on
+        // this GPU with this engine's kernels before n and placement are solved.
+        measured_ = measure_profile(cfg_, cfg_.measure_phase);
+        profile_.attn_compute_per_token = measured_->attn_ps;
+        profile_.gate_compute_per_token = measured_->gate_ps;
+        profile_.expert_compute_per_token = measured_->expert_ps;
+        profile_.pcie_bandwidth = measured_->pcie_bandwidth;
+    }
     plan_memory();
     allocate_device();
     allocate_host();
@@ -312,8 +325,10 @@ void Engine::plan_memory() {
         }
         // Split-K partials: the largest request of any small-M GEMM we issue.
         gemm_ws_bytes_ = 0;
-        for (int64_t m : {int64_t{32}, int64_t{64}, int64_t{128}, int64_t{192}, int64_t{256}, tb_max_, seqs}) {
-            if (m > std::max<int64_t>(R, tb_max_)) continue;
+        for (int64_t m : {int64_t{32}, int64_t{64}, int64_t{128}, int64_t{192}, int64_t{256}, tb_max_, seqs, Rx}) {
+            // Largest GEMM row count this engine issues: own routed rows, a
+            // batch, or (EP) the rows one local expert can receive.
+            if (m > std::max({R, Rx, tb_max_})) continue;
             const int mi = static_cast<int>(m);
             gemm_ws_bytes_ = std::max({gemm_ws_bytes_, kl_gemm_workspace_bytes(mi, 2 * D_.f, D_.d, 2),
                                        kl_gemm_workspace_bytes(mi, D_.d, D_.f, 0),
@@ -495,7 +510,7 @@ void Engine::allocate_host() {
     // Non-resident expert layers, optionally aliased onto R distinct copies.
     // The whole-layer baseline moves every expert over the link each block
     // (its reference semantics, schedule.cpp:190-208), resident or not.
-    const bool whole_layer = cfg_.variant == Variant::multibatch_full_prefetch;
+    const bool whole_layer = cfg_.variant == Variant::multibatch_full_prefetch || cfg_.variant == Variant::simple;
     std::vector<int> streamed;
     for (int l = 0; l < L; ++l)
         if ((plan_.placement.expert_tier[l] != Tier::vram || whole_layer) && plan_.placement.expert_tier[l] != Tier::disk)
@@ -765,6 +780,7 @@ std::string Engine::describe() const {
                     {"disk_bandwidth", profile_.disk_bandwidth}, {"transfer_fixed_latency_ps", 0},
                     {"attn_ps", profile_.attn_compute_per_token}, {"gate_ps", profile_.gate_compute_per_token},
                     {"expert_ps", profile_.expert_compute_per_token}};
+    if (measured_) j["measured_profile"] = json::parse(measured_->to_json());
     j["streaming_kv"] = cfg_.retention.mode == KvRetentionPolicy::Mode::streaming;
     j["sink_tokens"] = cfg_.retention.sink_tokens;
     j["window_tokens"] = cfg_.retention.window_tokens;

@@ -87,9 +87,22 @@ struct EngineConfig {
     bool prefill = true;
     std::optional<moesim::QuantConfig> quant;  // 4-bit streamed experts / attention (Q4T)
     std::string disk_dir;           // disk-tier store directory (default $TMPDIR, else /tmp)
+    std::string measure_phase;      // "decode" | "prefill": plan with rates measured on this GPU
 };
 
 EngineConfig parse_config(const std::string& json_text);
+
+// Planner stage 1 (engine_profile.cpp): this engine's kernels and the pinned
+// host link timed on the model's shapes -> HardwareProfile rates.
+struct MeasuredProfile {
+    std::string phase;
+    int tokens_per_batch = 0, expert_rows = 0, kv_slots = 0;
+    double attn_ms = 0, gate_ms = 0, expert_ms = 0, h2d_1_gbs = 0, h2d_2_gbs = 0;
+    moesim::duration_ps attn_ps = 0, gate_ps = 0, expert_ps = 0;
+    double pcie_bandwidth = 0;
+    std::string to_json() const;
+};
+MeasuredProfile measure_profile(const EngineConfig& cfg, const std::string& phase);
 
 struct ExpertSlotPool {
     std::vector<uint16_t*> ptr;
@@ -145,6 +158,7 @@ class Engine {
     Dims D_;
     moesim::ModelSpec spec_;
     moesim::HardwareProfile profile_;
+    std::optional<MeasuredProfile> measured_;
     moesim::PipelinePlan plan_;
     moesim::CorrelationTable table0_;
     moesim::ActivationTrace replay_trace_;
@@ -170,7 +184,10 @@ class Engine {
     uint16_t *h_ = nullptr, *x2_ = nullptr, *xa_ = nullptr, *qkv_ = nullptr, *ao_ = nullptr;
     uint16_t *xp_ = nullptr, *y_ = nullptr, *hs_ = nullptr, *last_h_ = nullptr, *head_logits_ = nullptr;
     uint16_t* hshared_ = nullptr;  // shared-expert SwiGLU output, [chunk rows][fs]
-    void shared_experts(int layer, int64_t T);
+    void shared_experts(int layer, int64_t T, int64_t row0);
+    void after_batch_gate(int step, int layer, int b);
+    moesim::detail::BlockRouting read_routing_row(int step, int layer, int b);
+    int combine_batch_ = -1;
     int32_t *idx_[2] = {nullptr, nullptr}, *forced_ = nullptr, *pos_ = nullptr, *row_token_ = nullptr;
     int32_t *counts_ = nullptr, *offsets_ = nullptr, *tok_pos_ = nullptr, *tok_seq_ = nullptr;
     int32_t *ids_ = nullptr, *next_ids_ = nullptr, *last_rows_ = nullptr;

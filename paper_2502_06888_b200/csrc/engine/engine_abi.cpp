@@ -7,6 +7,7 @@
 
 #include "engine.hpp"
 #include "klotski/engine.h"
+#include "klotski/kernels.h"
 
 struct kl_engine {
     std::unique_ptr<klotski::Engine> impl;
@@ -89,6 +90,20 @@ int kl_engine_report(kl_engine* e, const char* what, char** json_out) {
 
 int kl_engine_reset_log(kl_engine* e) {
     return guarded(e, [&](klotski::Engine& g) { g.reset_log(); });
+}
+
+int kl_measure_profile(const char* config_json, const char* phase, char** json_out) {
+    if (json_out == nullptr) return 1;
+    *json_out = nullptr;
+    try {
+        if (kl_device_supported() != 1) throw std::runtime_error("kl_measure_profile: device is not sm_100 (B200)");
+        const klotski::EngineConfig cfg = klotski::parse_config(config_json ? config_json : "");
+        *json_out = dup_string(klotski::measure_profile(cfg, phase ? phase : "decode").to_json());
+        return 0;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return 1;
+    }
 }
 
 int kl_engine_read_hidden(kl_engine* e, uint16_t* host, int64_t n_elems) {

@@ -353,7 +353,7 @@ void Engine::ep_after_gates(int step, int layer) {
     // Own routed rows grouped by destination rank, then local expert.
     kl_check(kl_map_ids(cur, T * D_.k, label_map_, lbl_, cs), "relabel");
     // y_ret_ doubles as the send buffer (dispatch completes before return).
-    shared_experts(layer, T);  // replicated with the router: every rank on its own tokens
+    shared_experts(layer, T, 0);  // replicated with the router: every rank on its own tokens
     kl_check(kl_permute(lbl_, T, D_.k, E, x2_, D_.d, send_counts_, offsets_, pos_, row_token_, y_ret_, perm_ws_, cs),
              "permute (dispatch order)");
     launches_ += 2;

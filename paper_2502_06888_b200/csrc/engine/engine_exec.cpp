@@ -46,7 +46,73 @@ void kl_check_impl(int rc, const char* what) {
 
 constexpr int32_t kNoPos = 0x7f7f7f7f;  // memset(0x7f) sentinel for first_pos
 
+// The reference's RunMetrics / bubble_stats (simulator.cpp:256-331) over one
+// window of a timeline (measured or simulated), makespan counted from the
+// window's first op.
+json reference_metrics(const Schedule& s, size_t records_from, const std::vector<SimEvent>& tl, byte_count peak_vram,
+                       int64_t tokens) {
+    json j;
+    Schedule view;
+    view.batch_size = s.batch_size;
+    view.n_batches = s.n_batches;
+    view.n_steps = s.n_steps;
+    view.ops = s.ops;
+    view.prefetch_records.assign(s.prefetch_records.begin() + records_from, s.prefetch_records.end());
+    RunMetrics m;
+    detail::finalize_metrics(view, tl, peak_vram, m);
+    duration_ps t_begin = tl.empty() ? 0 : tl.front().start;
+    for (const SimEvent& e : tl) t_begin = std::min(t_begin, e.start);
+    m.makespan -= t_begin;  // measured from the first op of the window
+    m.bubble_time = m.makespan - m.compute_busy;
+    m.tokens_generated = tokens;
+    m.throughput_tps = m.makespan > 0 ? static_cast<double>(tokens) / sec_from_ps(m.makespan) : 0.0;
+    j["makespan_ps"] = m.makespan;
+    j["compute_busy_ps"] = m.compute_busy;
+    j["bubble_ps"] = m.bubble_time;
+    j["bubble_fraction"] = m.makespan > 0 ? static_cast<double>(m.bubble_time) / m.makespan : 0.0;
+    j["expert_layer_bubble_ps"] = m.expert_layer_bubble_time;
+    j["throughput_tps"] = m.throughput_tps;
+    j["tokens_generated"] = m.tokens_generated;
+    j["peak_vram_bytes"] = m.peak_vram;
+    j["prefetch_participation"] = m.prefetch_participation;
+    j["hot_accuracy"] = m.hot_accuracy;
+    const BubbleBreakdown& b = m.bubbles;
+    j["bubbles_ps"] = {{"startup", b.startup - t_begin},    {"intra_attention", b.intra_attention},
+                       {"attn_to_moe", b.attn_to_moe},      {"intra_gate", b.intra_gate},
+                       {"gate_to_expert", b.gate_to_expert}, {"intra_expert", b.intra_expert},
+                       {"moe_to_attn", b.moe_to_attn},      {"drain", b.drain}};
+    return j;
+}
+
+// Bytes moved by load ops and the time the host link had at least one load
+// in flight (union of the load intervals).
+std::pair<int64_t, duration_ps> link_usage(const Schedule& s, const std::vector<SimEvent>& tl) {
+    std::vector<std::pair<duration_ps, duration_ps>> iv;
+    int64_t h2d = 0;
+    for (const SimEvent& e : tl) {
+        const StreamOp& op = s.ops[e.op_id];
+        if (op.kind == OpKind::load_weights || op.kind == OpKind::load_expert) {
+            h2d += op.payload_bytes;
+            iv.emplace_back(e.start, e.end);
+        }
+    }
+    std::sort(iv.begin(), iv.end());
+    duration_ps busy = 0, cur_s = -1, cur_e = -1;
+    for (const auto& [a, bnd] : iv) {
+        if (a > cur_e) {
+            if (cur_e > cur_s) busy += cur_e - cur_s;
+            cur_s = a;
+            cur_e = bnd;
+        } else {
+            cur_e = std::max(cur_e, bnd);
+        }
+    }
+    if (cur_e > cur_s) busy += cur_e - cur_s;
+    return {h2d, busy};
+}
+
 }  // namespace
+
 
 cudaEvent_t Engine::event() {
     if (event_next_ == event_pool_.size()) {
@@ -162,7 +228,29 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     kl_check(kl_embed(ids_, embed_, T, D_.d, h_, cs), "embed");
 
     const bool split = em_->split_moe();
-    for (int layer = 0; layer < D_.L; ++layer) {
+    if (cfg_.variant == Variant::simple) {
+        // Row-by-row (schedule.cpp:636-690): each batch traverses every layer
+        // alone, reloading each block's weights; the host reads the routing
+        // of every (batch, layer) row before emitting its expert computes.
+        for (int b = 0; b < n; ++b)
+            for (int layer = 0; layer < D_.L; ++layer) {
+                if (cfg_.replay) {
+                    const auto sel = replay_trace_.layer_selections(step, layer);
+                    for (size_t i = 0; i < sel.size(); ++i) host_forced_[i] = sel[i];
+                }
+                const detail::SimpleRow row = em_->simple_open(step, b, layer);
+                block_layer_ = layer;
+                issue_pending();
+                const detail::BlockRouting routing = read_routing_row(step, layer, b);
+                const std::int32_t first = static_cast<std::int32_t>(em_->schedule().ops.size());
+                em_->simple_close(row, routing);
+                exec_expert_left_ = 0;
+                for (std::int32_t id = first; id < static_cast<std::int32_t>(em_->schedule().ops.size()); ++id)
+                    exec_expert_left_ += em_->schedule().ops[id].kind == OpKind::compute_expert;
+                issue_pending();
+            }
+    }
+    for (int layer = 0; layer < D_.L && cfg_.variant != Variant::simple; ++layer) {
         PrefetchDecision d;
         if (split) d = decide(step, layer);
         if (cfg_.replay) {
@@ -542,7 +630,16 @@ void Engine::exec_gate(const StreamOp& op) {
     const int64_t row0 = static_cast<int64_t>(b) * tpb;
     int32_t* hist = report_ + static_cast<int64_t>(b) * D_.E;
     int32_t* first = report_ + static_cast<int64_t>(n) * D_.E + static_cast<int64_t>(b) * D_.E;
-    if (b == 0) {
+    const bool simple = cfg_.variant == Variant::simple;
+    if (simple) {
+        // One batch per row: clear only this batch's histogram / first demand.
+        cuda_check(cudaMemsetAsync(hist, 0, static_cast<size_t>(D_.E) * 4, cs), "memset hist");
+        cuda_check(cudaMemsetAsync(first, 0x7f, static_cast<size_t>(D_.E) * 4, cs), "memset first");
+        if (cfg_.replay)
+            cuda_check(cudaMemcpyAsync(forced_ + row0 * D_.k, host_forced_ + row0 * D_.k,
+                                       static_cast<size_t>(tpb) * D_.k * 4, cudaMemcpyHostToDevice, cs),
+                       "h2d forced routing");
+    } else if (b == 0) {
         cuda_check(cudaMemsetAsync(report_, 0, static_cast<size_t>(n) * D_.E * 4, cs), "memset hist");
         cuda_check(cudaMemsetAsync(report_ + static_cast<int64_t>(n) * D_.E, 0x7f, static_cast<size_t>(n) * D_.E * 4, cs),
                    "memset first");
@@ -562,7 +659,9 @@ void Engine::exec_gate(const StreamOp& op) {
         kl_check(kl_gate_topk(h_ + row0 * D_.d, norm_ffn_[l], wg, tpb, D_.d, D_.E, D_.k, D_.eps, D_.score_mode,
                               x2_ + row0 * D_.d, nullptr, idx, wt, hist, first, cs), "gate");
     }
-    if (b == n - 1) {
+    if (simple)
+        after_batch_gate(step, l, b);
+    else if (b == n - 1) {
         if (ep_)
             ep_after_gates(step, l);
         else
@@ -581,7 +680,7 @@ void Engine::after_layer_gates(int step, int layer) {
     int32_t* prev = idx_[idx_cur_ ^ 1];
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
-    shared_experts(layer, T);
+    shared_experts(layer, T, 0);
     launches_ += 2;  // rank + scan + scatter kernels
     int64_t* scores = reinterpret_cast<int64_t*>(report_ + 2LL * n * D_.E + 16 - ((2LL * n * D_.E) % 16));
     int64_t* marg_copy = scores + D_.E;
@@ -601,7 +700,7 @@ void Engine::after_layer_gates(int step, int layer) {
 // Shared experts (always active): h += FFN_shared(x2) on every token of the
 // group, from the router tensor's slot ([router E x d | W13s (2 fs x d) |
 // W2s (d x fs)]); the combine then adds the routed experts on top.
-void Engine::shared_experts(int layer, int64_t T) {
+void Engine::shared_experts(int layer, int64_t T, int64_t row0) {
     if (D_.fs() <= 0) return;
     cudaStream_t cs = stream_of(StreamId::compute);
     const uint16_t* g = gate_slot_[gate_slot_of_.at(layer)];
@@ -609,11 +708,73 @@ void Engine::shared_experts(int layer, int64_t T) {
     const uint16_t* w2 = w13 + 2LL * D_.fs() * D_.d;
     for (int64_t c = 0; c < T; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, T - c));
-        kl_check(kl_gemm_bf16(x2_, T, c, m, D_.d, w13, 2 * D_.fs(), hshared_, D_.fs(), nullptr, 2, gemm_ws_,
-                              gemm_ws_bytes_, cs), "shared w13");
-        kl_check(kl_gemm_bf16(hshared_, m, 0, m, D_.fs(), w2, D_.d, h_ + c * D_.d, D_.d, h_ + c * D_.d, 1, gemm_ws_,
-                              gemm_ws_bytes_, cs), "shared w2");
+        uint16_t* hrow = h_ + (row0 + c) * D_.d;
+        kl_check(kl_gemm_bf16(x2_, row0 + T, row0 + c, m, D_.d, w13, 2 * D_.fs(), hshared_, D_.fs(), nullptr, 2,
+                              gemm_ws_, gemm_ws_bytes_, cs), "shared w13");
+        kl_check(kl_gemm_bf16(hshared_, m, 0, m, D_.fs(), w2, D_.d, hrow, D_.d, hrow, 1, gemm_ws_, gemm_ws_bytes_, cs),
+                 "shared w2");
     }
+}
+
+// simple variant: the gate of ONE batch row is followed by that batch's own
+// expert-major permutation (and shared experts) and a readback of its
+// histogram / first demand (the reference's build_simple, schedule.cpp:636-690,
+// routes each batch alone).
+void Engine::after_batch_gate(int step, int layer, int b) {
+    cudaStream_t cs = stream_of(StreamId::compute);
+    const int tpb = tokens_per_batch(step);
+    const int64_t row0 = static_cast<int64_t>(b) * tpb;
+    int32_t* cur = idx_[idx_cur_] + row0 * D_.k;
+    kl_check(kl_permute(cur, tpb, D_.k, D_.E, x2_ + row0 * D_.d, D_.d, counts_, offsets_, pos_ + row0 * D_.k,
+                        row_token_ + row0 * D_.k, xp_, perm_ws_, cs), "permute (row)");
+    launches_ += 2;
+    shared_experts(layer, tpb, row0);
+    const int n = plan_.n_batches;
+    const size_t hist_off = static_cast<size_t>(b) * D_.E, first_off = static_cast<size_t>(n) * D_.E + hist_off;
+    cuda_check(cudaMemcpyAsync(host_report_ + hist_off, report_ + hist_off, D_.E * 4, cudaMemcpyDeviceToHost, cs),
+               "d2h row hist");
+    cuda_check(cudaMemcpyAsync(host_report_ + first_off, report_ + first_off, D_.E * 4, cudaMemcpyDeviceToHost, cs),
+               "d2h row first");
+    if (cfg_.record_trace)
+        cuda_check(cudaMemcpyAsync(host_idx_ + row0 * D_.k, cur, static_cast<size_t>(tpb) * D_.k * 4,
+                                   cudaMemcpyDeviceToHost, cs), "d2h row idx");
+    (void)step;
+}
+
+detail::BlockRouting Engine::read_routing_row(int step, int layer, int b) {
+    const std::int32_t last_gate = next_exec_ - 1;
+    cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
+    const int n = plan_.n_batches, E = D_.E;
+    detail::BlockRouting r;
+    r.group_hist.assign(E, 0);
+    r.demand.resize(n);
+    r.batch_hist.assign(n, std::vector<int64_t>(E, 0));
+    std::vector<std::pair<int32_t, int>> firsts;
+    for (int e = 0; e < E; ++e) {
+        const int32_t c = host_report_[b * E + e];
+        r.batch_hist[b][e] = c;
+        r.group_hist[e] = c;
+        if (c > 0) {
+            const int32_t f = host_report_[n * E + b * E + e];
+            if (f == kNoPos) throw AccountingError("engine: routed expert without a first position");
+            firsts.emplace_back(f, e);
+        }
+    }
+    std::sort(firsts.begin(), firsts.end());
+    for (const auto& [f, e] : firsts) r.demand[b].push_back(e);
+    // The row's permuted rows start at 0 in xp_ (this batch only).
+    row_offset_.assign(E, 0);
+    for (int e = 1; e < E; ++e) row_offset_[e] = row_offset_[e - 1] + r.group_hist[e - 1];
+    block_rows_ = std::accumulate(r.group_hist.begin(), r.group_hist.end(), int64_t{0});
+    batch_prefix_.assign(n, std::vector<int64_t>(E, 0));
+    if (cfg_.record_trace) {
+        const int tpb = tokens_per_batch(step);
+        const size_t off = recorded_.offset(step, layer, b, 0);
+        const int64_t row0 = static_cast<int64_t>(b) * tpb;
+        for (int64_t i = 0; i < static_cast<int64_t>(tpb) * D_.k; ++i)
+            recorded_.sel[off + i] = static_cast<uint16_t>(host_idx_[row0 * D_.k + i]);
+    }
+    return r;
 }
 
 detail::BlockRouting Engine::read_routing(int step, int layer) {
@@ -664,7 +825,7 @@ void Engine::exec_expert(const StreamOp& op) {
     cudaStream_t cs = stream_of(StreamId::compute);
     const int l = op.layer, e = op.expert;
     const int64_t M = op.token_count;
-    const int64_t row0 = row_offset_[e] + (op.batch >= 0 ? batch_prefix_[op.batch][e] : 0);
+    const int64_t row0 = row_offset_[e] + (op.batch >= 0 ? batch_prefix_[op.batch][e] : 0);  // simple: prefix 0
     const uint16_t* w = expert_weights(l, e);
     const bool q4 = cfg_.quant && res_expert_[static_cast<size_t>(l) * El_ + e] == nullptr;
     const uint8_t* q13 = reinterpret_cast<const uint8_t*>(w);
@@ -697,12 +858,29 @@ void Engine::exec_expert(const StreamOp& op) {
     }
     // The block's last expert op: the combine follows right after the op's
     // end event (so compute_expert events bracket the FFN kernels only).
-    if (--exec_expert_left_ == 0 && !ep_) combine_step_ = op.step;
+    if (--exec_expert_left_ == 0 && !ep_) {
+        combine_step_ = op.step;
+        combine_batch_ = cfg_.variant == Variant::simple ? op.batch : -1;
+    }
 }
 
 void Engine::combine_block(int step) {
     // Every routed row of the block is computed: weighted combine + residual.
     cudaStream_t cs = stream_of(StreamId::compute);
+    if (combine_batch_ >= 0) {  // simple: one batch row
+        const int tpb = tokens_per_batch(step);
+        const int64_t row0 = static_cast<int64_t>(combine_batch_) * tpb;
+        uint16_t* hb = h_ + row0 * D_.d;
+        kl_check(kl_combine(y_, pos_ + row0 * D_.k, weight_ + row0 * D_.k, hb, tpb, D_.k, D_.d, hb, cs), "combine");
+        combine_batch_ = -1;
+        if (cfg_.record_hidden) {  // one dump per (batch, layer) row: that batch's rows only
+            std::vector<uint16_t> dump(static_cast<size_t>(tpb) * D_.d);
+            cuda_check(cudaMemcpyAsync(dump.data(), hb, dump.size() * 2, cudaMemcpyDeviceToHost, cs), "dump");
+            cuda_check(cudaStreamSynchronize(cs), "dump sync");
+            hidden_dumps_.push_back(std::move(dump));
+        }
+        return;
+    }
     const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(step);
     kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
     if (cfg_.record_hidden) {
@@ -746,72 +924,26 @@ std::string Engine::report(const std::string& what) {
     } else if (what == "timeline_json") {
         j["text"] = timeline_to_string(tl, s, TimelineFormat::trace_event_json);
     } else if (what == "metrics") {
-        Schedule view;
-        view.batch_size = s.batch_size;
-        view.n_batches = s.n_batches;
-        view.n_steps = s.n_steps;
-        view.ops = s.ops;
-        view.prefetch_records.assign(s.prefetch_records.begin() + records_from_, s.prefetch_records.end());
-        RunMetrics m;
-        detail::finalize_metrics(view, tl, arena_used_, m);
-        duration_ps t_begin = tl.empty() ? 0 : tl.front().start;
-        for (const SimEvent& e : tl) t_begin = std::min(t_begin, e.start);
-        m.makespan -= t_begin;  // measured from the first op of the window
-        m.bubble_time = m.makespan - m.compute_busy;
-        m.tokens_generated = tokens_generated_;
-        m.throughput_tps = m.makespan > 0 ? static_cast<double>(tokens_generated_) / sec_from_ps(m.makespan) : 0.0;
-        j["makespan_ps"] = m.makespan;
-        j["compute_busy_ps"] = m.compute_busy;
-        j["bubble_ps"] = m.bubble_time;
-        j["bubble_fraction"] = m.makespan > 0 ? static_cast<double>(m.bubble_time) / m.makespan : 0.0;
-        j["expert_layer_bubble_ps"] = m.expert_layer_bubble_time;
-        j["throughput_tps"] = m.throughput_tps;
-        j["tokens_generated"] = m.tokens_generated;
-        j["peak_vram_bytes"] = m.peak_vram;
-        j["prefetch_participation"] = m.prefetch_participation;
-        j["hot_accuracy"] = m.hot_accuracy;
-        const BubbleBreakdown& b = m.bubbles;
-        j["bubbles_ps"] = {{"startup", b.startup - t_begin},    {"intra_attention", b.intra_attention},
-                           {"attn_to_moe", b.attn_to_moe},      {"intra_gate", b.intra_gate},
-                           {"gate_to_expert", b.gate_to_expert}, {"intra_expert", b.intra_expert},
-                           {"moe_to_attn", b.moe_to_attn},      {"drain", b.drain}};
+        j = reference_metrics(s, records_from_, tl, arena_used_, tokens_generated_);
         // Host-link accounting: bytes moved by load ops and the time the
         // link had at least one load in flight (union of load intervals).
-        std::vector<std::pair<duration_ps, duration_ps>> iv;
-        int64_t h2d = 0, n_expert_loads = 0;
-        duration_ps expert_busy = 0, compute_busy = 0;
+        const auto [h2d, link_busy] = link_usage(s, tl);
+        const duration_ps makespan = j["makespan_ps"].get<duration_ps>();
+        int64_t n_expert_loads = 0;
+        duration_ps expert_busy = 0;
         std::map<int, duration_ps> kind_busy;
         for (const SimEvent& e : tl) {
             const StreamOp& op = s.ops[e.op_id];
-            if (op.kind == OpKind::load_weights || op.kind == OpKind::load_expert) {
-                h2d += op.payload_bytes;
-                iv.emplace_back(e.start, e.end);
-                if (op.kind == OpKind::load_expert) {
-                    ++n_expert_loads;
-                    expert_busy += e.end - e.start;
-                }
+            if (op.kind == OpKind::load_expert) {
+                ++n_expert_loads;
+                expert_busy += e.end - e.start;
             }
-            if (op.stream == StreamId::compute) {
-                compute_busy += e.end - e.start;
-                kind_busy[static_cast<int>(op.kind)] += e.end - e.start;
-            }
+            if (op.stream == StreamId::compute) kind_busy[static_cast<int>(op.kind)] += e.end - e.start;
         }
-        std::sort(iv.begin(), iv.end());
-        duration_ps link_busy = 0, cur_s = -1, cur_e = -1;
-        for (const auto& [a, bnd] : iv) {
-            if (a > cur_e) {
-                if (cur_e > cur_s) link_busy += cur_e - cur_s;
-                cur_s = a;
-                cur_e = bnd;
-            } else {
-                cur_e = std::max(cur_e, bnd);
-            }
-        }
-        if (cur_e > cur_s) link_busy += cur_e - cur_s;
         j["h2d_bytes"] = h2d;
         j["h2d_link_busy_ps"] = link_busy;
         j["h2d_gbs_busy"] = link_busy > 0 ? h2d / (link_busy * 1e-12) / 1e9 : 0.0;
-        j["h2d_gbs_makespan"] = m.makespan > 0 ? h2d / (m.makespan * 1e-12) / 1e9 : 0.0;
+        j["h2d_gbs_makespan"] = makespan > 0 ? h2d / (makespan * 1e-12) / 1e9 : 0.0;
         j["expert_loads"] = n_expert_loads;
         j["expert_load_busy_ps"] = expert_busy;
         {
@@ -849,6 +981,49 @@ std::string Engine::report(const std::string& what) {
                                    {"gate", kind_busy[static_cast<int>(OpKind::compute_gate)]},
                                    {"expert", kind_busy[static_cast<int>(OpKind::compute_expert)]}};
         j["step_ms"] = step_ms_;
+    } else if (what == "simulated") {
+        // The reference's discrete-event model (moesim::run, simulator.cpp:70-287,
+        // shared-PCIe fluid link 99-129) priced with rates MEASURED in this
+        // window: per-token attention / gate / expert time of the executed
+        // compute ops and the link's bytes / busy time. The executed schedule
+        // is simulated whole; the window's simulated metrics sit next to the
+        // measured ones.
+        duration_ps busy[3] = {0, 0, 0};
+        int64_t tok[3] = {0, 0, 0};
+        for (const SimEvent& e : tl) {
+            const StreamOp& op = s.ops[e.op_id];
+            const int k = op.kind == OpKind::compute_attention ? 0
+                          : op.kind == OpKind::compute_gate    ? 1
+                          : op.kind == OpKind::compute_expert  ? 2
+                                                               : -1;
+            if (k < 0) continue;
+            busy[k] += e.end - e.start;
+            tok[k] += op.token_count;
+        }
+        const auto [h2d, link_busy] = link_usage(s, tl);
+        HardwareProfile p = profile_;
+        auto rate = [](duration_ps b, int64_t t) { return t > 0 ? std::max<duration_ps>(1, b / t) : duration_ps{1}; };
+        p.attn_compute_per_token = rate(busy[0], tok[0]);
+        p.gate_compute_per_token = rate(busy[1], tok[1]);
+        p.expert_compute_per_token = rate(busy[2], tok[2]);
+        if (link_busy > 0 && h2d > 0) p.pcie_bandwidth = static_cast<double>(h2d) / (static_cast<double>(link_busy) * 1e-12);
+        p.transfer_fixed_latency = 0;
+        const CostProfile cost = build_cost_profile(spec_, p, cfg_.workload.batch_size, cfg_.quant);
+        std::array<byte_count, 4> caps{INT64_MAX / 4, INT64_MAX / 4, INT64_MAX / 4, INT64_MAX / 4};
+        MemoryLedger ledger(caps, false);
+        SimOptions so;
+        so.shared_pcie = true;
+        const SimResult r = run(s, cost, plan_, ledger, so);
+        std::vector<SimEvent> stl(r.timeline.begin() + std::min<size_t>(log_from_, r.timeline.size()),
+                                  r.timeline.begin() + std::min<size_t>(next_exec_, r.timeline.size()));
+        j["simulated"] = reference_metrics(s, records_from_, stl, arena_used_, tokens_generated_);
+        j["measured"] = reference_metrics(s, records_from_, tl, arena_used_, tokens_generated_);
+        j["rates"] = {{"attn_ps_per_token", p.attn_compute_per_token},
+                      {"gate_ps_per_token", p.gate_compute_per_token},
+                      {"expert_ps_per_token", p.expert_compute_per_token},
+                      {"pcie_bytes_per_s", p.pcie_bandwidth},
+                      {"ps_per_byte_pinned", cost.ps_per_byte_pinned}};
+        j["shared_pcie"] = true;
     } else if (what == "prefetch") {
         json recs = json::array();
         for (size_t i = records_from_; i < s.prefetch_records.size(); ++i) {

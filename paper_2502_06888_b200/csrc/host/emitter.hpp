@@ -55,6 +55,12 @@ struct OpenBlock {
     std::int32_t first_op = 0;
 };
 
+// One row of the simple (row-by-row) variant, split at its gate like a block.
+struct SimpleRow {
+    int step = 0, batch = 0, layer = 0;
+    std::int32_t issue = -1, moe = -1, gate = -1, next_attn = -1;
+};
+
 struct ClosedBlock {
     std::vector<std::pair<int, int>> cold;  // (expert, demanding batch) in issue order
     std::int32_t block_last = -1;
@@ -69,7 +75,10 @@ class Emitter {
     OpenBlock open_block(int step, int layer, const PrefetchDecision* decision);
     ClosedBlock close_block(OpenBlock& blk, const BlockRouting& routing);
 
-    // simple variant: one (step, batch, layer) row.
+    // simple variant: one (step, batch, layer) row; open = weights, cache,
+    // attention and gate; close = the batch's expert computes (needs routing).
+    SimpleRow simple_open(int step, int batch, int layer);
+    void simple_close(const SimpleRow& row, const BlockRouting& routing);
     void simple_row(int step, int batch, int layer, const BlockRouting& routing);
 
     const Schedule& schedule() const { return s_; }

@@ -497,10 +497,9 @@ ClosedBlock Emitter::close_block(OpenBlock& b, const BlockRouting& r) {
     return c;
 }
 
-void Emitter::simple_row(int step, int batch, int layer, const BlockRouting& r) {
-    const std::int32_t issue = prev_block_last_;
-    std::int32_t moe = -1;
-    if (!experts_resident(layer) || !gate_resident(layer)) moe = load_moe(step, layer, batch, issue);
+SimpleRow Emitter::simple_open(int step, int batch, int layer) {
+    SimpleRow row{step, batch, layer, prev_block_last_, -1, -1, -1};
+    if (!experts_resident(layer) || !gate_resident(layer)) row.moe = load_moe(step, layer, batch, row.issue);
 
     // Next row in (step, batch, layer) order.
     int nl = layer + 1, nb = batch, ns = step;
@@ -511,21 +510,29 @@ void Emitter::simple_row(int step, int batch, int layer, const BlockRouting& r) 
             ++ns;
         }
     }
-    std::int32_t next_attn = -1;
-    if (ns < shape_.n_steps && !attention_resident(nl)) next_attn = load_attention(ns, nl, issue);
+    if (ns < shape_.n_steps && !attention_resident(nl)) row.next_attn = load_attention(ns, nl, row.issue);
 
     const std::int32_t cache = load_kv(step, layer, batch, -1);
     const std::int32_t att = attention(step, layer, batch, pending_attn_load_, cache);
     store_kv(step, layer, batch, att);
     if (pending_attn_load_ >= 0) offload_weights(TensorClass::attention, step, layer, -1, att);
-    const std::int32_t g = gate(step, layer, batch, moe, att);
-    std::int32_t last = g;
-    for (int e : r.demand[batch]) last = expert(step, layer, e, r.batch_hist[batch][e], false, batch, moe, g, -1);
-    if (moe >= 0) offload_weights(TensorClass::gate, step, layer, batch, last);
-    s_.sync_points.emplace_back(step, layer);
-    advance_window(step, layer, issue);
+    row.gate = gate(step, layer, batch, row.moe, att);
+    return row;
+}
+
+void Emitter::simple_close(const SimpleRow& row, const BlockRouting& r) {
+    std::int32_t last = row.gate;
+    for (int e : r.demand[row.batch])
+        last = expert(row.step, row.layer, e, r.batch_hist[row.batch][e], false, row.batch, row.moe, row.gate, -1);
+    if (row.moe >= 0) offload_weights(TensorClass::gate, row.step, row.layer, row.batch, last);
+    s_.sync_points.emplace_back(row.step, row.layer);
+    advance_window(row.step, row.layer, row.issue);
     prev_block_last_ = last;
-    pending_attn_load_ = next_attn;
+    pending_attn_load_ = row.next_attn;
+}
+
+void Emitter::simple_row(int step, int batch, int layer, const BlockRouting& r) {
+    simple_close(simple_open(step, batch, layer), r);
 }
 
 }  // namespace detail

@@ -1358,15 +1358,22 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
     }
     if (g_decode_mma && cache_seqs > 0 && Hkv % HG == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
         static_assert(kDmSlots == kDecChunk, "workspace layout shared with the per-chunk kernel");
+        auto ring_bytes = [&](int hg) {
+            const size_t stage = (static_cast<size_t>(2) * kDmSlots * hg * hd * 2 + static_cast<size_t>(hg) * G * hd * 2 +
+                                  1023) & ~static_cast<size_t>(1023);
+            return kDmStages * stage + 1024 + 2 * kDmStages * 8;
+        };
+        // Wide GQA groups (e.g. 48 q / 8 kv heads with split tokens) can
+        // overflow shared memory with all KV heads in one item: narrow the
+        // item (HG stays a divisor of Hkv) until the ring fits.
+        while (ring_bytes(HG) > 227 * 1024 && HG > 1 && Hkv % (HG / 2) == 0) HG /= 2;
         CUtensorMap mk, mv;
         const int64_t rows = cache_seqs * cap;
         int rc = make_kv_map(&mk, k_cache, rows, Hkv * hd, HG * hd / 64);
         if (rc) return rc;
         rc = make_kv_map(&mv, v_cache, rows, Hkv * hd, HG * hd / 64);
         if (rc) return rc;
-        const size_t stage = (static_cast<size_t>(2) * kDmSlots * HG * hd * 2 + static_cast<size_t>(HG) * G * hd * 2 + 1023) &
-                             ~static_cast<size_t>(1023);
-        const size_t msmem = kDmStages * stage + 1024 + 2 * kDmStages * 8;
+        const size_t msmem = ring_bytes(HG);
         if (msmem > 227 * 1024) return KL_EUNSUPPORTED;
         // (A deeper ring at one CTA per SM measured the same as two CTAs with
         // three stages each.)

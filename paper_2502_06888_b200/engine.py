@@ -32,6 +32,8 @@ _lib.kl_engine_reset_log.argtypes = [C.c_void_p]
 _lib.kl_engine_read_hidden.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 
 
+_lib.kl_measure_profile.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]
+_lib.kl_measure_profile.restype = C.c_int
 _lib.kl_ep_unique_id.argtypes = [C.c_char_p]
 _lib.kl_ep_unique_id.restype = C.c_int
 
@@ -46,6 +48,18 @@ def ep_unique_id():
 
 class EngineError(RuntimeError):
     pass
+
+
+def measure_profile(config, phase="decode"):
+    """Planner stage 1: this GPU's per-token attention / gate / expert rates
+    and pinned H2D bandwidth on the config's model shapes (kl_measure_profile)."""
+    out = C.c_void_p()
+    if _lib.kl_measure_profile(json.dumps(config).encode(), phase.encode(), C.byref(out)) != 0:
+        raise EngineError(_lib.kl_engine_last_error(None).decode())
+    try:
+        return json.loads(C.string_at(out).decode())
+    finally:
+        _lib.kl_engine_free_string(out)
 
 
 class MemoryInfeasible(EngineError):
