@@ -191,11 +191,14 @@ def ffn_isolated(torch, dev, D, M, iters=20):
     return us, byts
 
 
-def measured_tflops():
+def measured_tflops(sustained=False):
+    key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p.get("bf16_tflops", 1590.0), "measured"
+        if key in p:
+            return p[key], "measured " + ("sustained" if sustained else "burst")
+        return p.get("bf16_tflops", 1590.0), "measured burst"
     except (OSError, ValueError):
         return 1590.0, "fallback"
 
@@ -223,9 +226,10 @@ def prefill_variant(args, link):
     D = eng.info["dims"]
     flops = 2.0 * 3 * D["d"] * D["f"] * m["expert_rows"]
     t_exp = m["compute_ps_by_kind"]["expert"] * 1e-12
-    peak, kind = measured_tflops()
+    peak, kind = measured_tflops(sustained=True)  # a seconds-long in-step rate: the sustained peak
     tf = flops / t_exp / 1e12 if t_exp > 0 else 0.0
-    out = {"config": f"{args.model} prefill, batch {bs} x n={n} x {P} tokens, HBM cap {args.hbm_cap:.3g} B",
+    out = {"config": f"{args.model} prefill, batch {bs} x n={n} x {P} tokens, HBM cap {args.hbm_cap:.3g} B, "
+                     "host copies of the layers aliased onto 4 distinct layers (link bytes unchanged)",
            "value": eng.n_seqs * P / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
            "bubble_fraction": m["bubble_fraction"], "bubbles_ps": m["bubbles_ps"],
            "compute_ms_by_kind": {k: v / 1e9 for k, v in m["compute_ps_by_kind"].items()},
@@ -285,24 +289,26 @@ def cpu_baseline(args, warmup=0, repeats=1):
 
 
 def run_reference(args):
+    """The reference arm: the CPU path timed on this box's host cores, whole
+    decode steps (one batch of the group through all layers per step), so
+    steps x ms_per_step is the timed wall time."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    times = []
     from oracle import cpu_port
-    D = cpu_port.mixtral_dims(args.model)
-    layer = cpu_port.LayerSample(D, args.n_batches, args.batch_size, 260)
+    sample = cpu_port.StepSample(args.model, args.batch_size, 260)
     for _ in range(args.warmup):
-        layer.decode_layer(600)
+        sample.decode_step(600)
+    times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        layer.decode_layer(600)
-        times.append((time.perf_counter() - t0) * D["L"])  # one layer sampled, x L layers
-    step_s = statistics.median(times)
-    toks = args.n_batches * args.batch_size
-    value = toks / step_s
-    sample = (f"each step: 1 of {D['L']} layers of one {args.model} decode step ({args.n_batches}x{args.batch_size} "
-              f"tokens, 260 retained KV slots), extrapolated x{D['L']}")
+        sample.decode_step(600)
+        times.append(time.perf_counter() - t0)
+    step_s = sum(times) / len(times)
+    value = sample.tokens / step_s
+    desc = (f"each step: one whole {args.model} decode step of one batch ({args.batch_size} sequences, 260 "
+            f"retained KV slots) through all {sample.D['L']} layers (layers aliased onto one layer's weights/KV); "
+            f"the group's {args.n_batches} batches are independent steps of this size")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
@@ -310,12 +316,144 @@ def run_reference(args):
         "config": {"workload": f"{args.model} decode, batch {args.batch_size} x n={args.n_batches}, CPU port",
                    "batch_size": args.batch_size, "n_batches": args.n_batches},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": sample},
+                         "sample": desc},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s_timed": sum(times),
         "note": "reference proj/ is a discrete-event simulator without numerics; its CPU path is the oracle port",
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def simulator_baseline(info, rates, args):
+    """Second CPU figure: the reference's own CPU path, the
+    discrete-event simulator of oracle/_ref (build_klotski_schedule + run,
+    shared-PCIe link) on the cfg2 workload (prompt 512 + generate 128,
+    bs 64 x n 8, 24 GB cap) priced with the rates this run measured;
+    single-threaded by design. Reports its wall time and simulated tok/s."""
+    import ctypes as C
+    lib = C.CDLL(os.path.join(ROOT, "oracle", "_ref", "libref_parity.so"))
+    lib.parity_request.argtypes = [C.c_char_p]
+    lib.parity_request.restype = C.c_void_p
+    lib.parity_free.argtypes = [C.c_void_p]
+    spec = info["spec"]
+    gen = 128
+    req = {
+        "model": {"preset": "toy", "n_layers": spec["n_layers"], "n_experts": spec["n_experts"],
+                  "top_k": spec["top_k"], "expert_bytes": spec["expert_bytes"],
+                  "attention_bytes": spec["attention_bytes"], "gate_bytes": spec["gate_bytes"],
+                  "kv_bytes_per_token": spec["kv_bytes_per_token"]},
+        "hw": dict(info["profile"], attn_ps=int(rates["attn_ps_per_token"]), gate_ps=int(rates["gate_ps_per_token"]),
+                   expert_ps=int(rates["expert_ps_per_token"]), pcie_bandwidth=float(rates["pcie_bytes_per_s"]),
+                   transfer_fixed_latency_ps=0),
+        "workload": {"batch_size": args.batch_size, "n_batches": args.n_batches, "prompt_len": args.prompt_len,
+                     "gen_len": gen},
+        "skew": {"kind": "zipf", "s": 1.5}, "seed": 1, "n": args.n_batches,
+        "working_set_override": info["working_set_bytes"], "streaming_kv": info["streaming_kv"],
+        "sink_tokens": info["sink_tokens"], "window_tokens": info["window_tokens"],
+        "simulate": True, "shared_pcie": True, "lean": True,
+    }
+    t0 = time.perf_counter()
+    ptr = lib.parity_request(json.dumps(req).encode())
+    wall = time.perf_counter() - t0
+    try:
+        out = json.loads(C.string_at(ptr).decode())
+    finally:
+        lib.parity_free(ptr)
+    if "error" in out or "run_error" in out:
+        return {"error": out.get("error") or out.get("run_error")}
+    toks = args.batch_size * args.n_batches * gen
+    mk = out["makespan"] * 1e-12
+    return {"kind": "reference", "impl": "oracle/_ref moesim::build_klotski_schedule + moesim::run (shared PCIe)",
+            "cores": 1, "nproc": os.cpu_count(), "wall_s": wall, "n_ops": out["n_ops"],
+            "value": toks / wall, "unit": "simulated tokens per wall-clock second",
+            "simulated_tok_s": out["throughput_tps"], "simulated_makespan_s": mk,
+            "simulated_bubble_fraction": out["bubble_time"] / out["makespan"] if out["makespan"] else None,
+            "sample": f"prompt {args.prompt_len} + generate {gen}, bs {args.batch_size} x n {args.n_batches}, "
+                      f"zipf(1.5) trace, rates measured in this run"}
+
+
+def decode_engine_run(cfg, warmup, steps, prompt_len):
+    """Build an engine, prefill-free decode: warm-up steps, then `steps`
+    timed steps (device events per step). Returns (engine, ms list)."""
+    from paper_2502_06888_b200.engine import Engine
+    eng = Engine(cfg)
+    eng.fill_kv_synthetic(prompt_len)
+    step = 1
+    for _ in range(warmup):
+        eng.step(step, None, want_next=False)
+        step += 1
+    eng.reset_log()
+    ms = []
+    for _ in range(steps):
+        _, t = eng.step(step, None, want_next=False)
+        ms.append(t)
+        step += 1
+    return eng, ms
+
+
+def resident_variant(args):
+    """Compute-exposed decode (the regime of one EP shard that fits HBM, where
+    north_star's <10% bubble target applies): the same decode workload with an
+    HBM budget (140e9 B) that keeps every expert and attention layer resident,
+    so nothing is streamed and the step is the kernels plus the per-layer
+    routing round trip. Reports tok/s, the reference bubble fraction and
+    breakdown on the measured timeline, and the expert FFN per op."""
+    a = argparse.Namespace(**vars(args))
+    a.hbm_cap = 140e9
+    steps = max(4, min(args.steps, 20))
+    eng, ms = decode_engine_run(engine_config(a, 0, 1), 3, steps, args.prompt_len)
+    m = eng.report("metrics")
+    val = eng.report("validate")
+    D = eng.info["dims"]
+    n_ops = max(m["expert_ops"], 1)
+    hbm_peak, _ = measured_peaks()
+    op_us = m["compute_ps_by_kind"]["expert"] / n_ops / 1e6
+    byts = m["expert_bytes"] + m["expert_rows"] / n_ops * (2 * D["d"] * 2 + 2 * D["f"] * 2)
+    out = {"config": f"{args.model} bf16 decode, batch {args.batch_size} x n={eng.n_batches}, HBM cap 1.4e11 B "
+                     "(all layers resident, nothing streamed)",
+           "value": steps * eng.n_seqs / (sum(ms) / 1e3), "unit": "tokens/s", "steps": steps,
+           "ms_per_step": sum(ms) / steps, "bubble_fraction": m["bubble_fraction"], "bubbles_ps": m["bubbles_ps"],
+           "compute_busy_ms": m["compute_busy_ps"] / 1e9, "makespan_ms": m["makespan_ps"] / 1e9,
+           "compute_ms_by_kind": {k: v / 1e9 for k, v in m["compute_ps_by_kind"].items()},
+           "resident_expert_layers": eng.info["resident_expert_layers"],
+           "resident_attention_layers": eng.info["resident_attention_layers"],
+           "h2d_gb_per_step": m["h2d_bytes"] / steps / 1e9,
+           "expert_op_us": op_us, "expert_ffn_frac_of_hbm_peak": byts / op_us / 1e3 / hbm_peak,
+           "violations": len(val["violations"]), "gpu_launches": m["launches"]}
+    eng.close()
+    return out
+
+
+def ablation_variant(args):
+    """Table-6-style ablation at the headline scale: the
+    reference's schedule variants executed by the engine on the same decode
+    workload and HBM cap (experts streamed). simple = row-by-row, one batch
+    through every layer reloading its weights (schedule.cpp:636-690);
+    multibatch_full_prefetch = whole MoE layers prefetched; strawman_no_reorder
+    = split hot/cold without the expert-major reorder; klotski = the headline.
+    Host copies of the layers are aliased onto 4 distinct layers to bound setup
+    time (link bytes per op are unchanged)."""
+    out = {}
+    for v, steps in (("multibatch_full_prefetch", 2), ("strawman_no_reorder", 2), ("simple", 1)):
+        a = argparse.Namespace(**vars(args))
+        a.host_distinct_layers = 4
+        a.steps = steps
+        cfg = engine_config(a, 0, 1)
+        cfg["variant"] = v
+        cfg["record_trace"] = False
+        try:
+            t0 = time.perf_counter()
+            eng, ms = decode_engine_run(cfg, 1, steps, args.prompt_len)
+            m = eng.report("metrics")
+            out[v] = {"value": steps * eng.n_seqs / (sum(ms) / 1e3), "unit": "tokens/s",
+                      "ms_per_step": sum(ms) / steps, "steps": steps, "bubble_fraction": m["bubble_fraction"],
+                      "h2d_gb_per_step": m["h2d_bytes"] / steps / 1e9, "h2d_gbs_link_busy": m["h2d_gbs_busy"],
+                      "wall_s": time.perf_counter() - t0}
+            eng.close()
+        except Exception as ex:  # reported, not fatal
+            out[v] = {"error": str(ex)[:300]}
+    return out
 
 
 def run_ours(args):
@@ -373,6 +511,9 @@ def run_ours(args):
     # timeline (placement.cpp:257-292), both outside the timed region.
     validation = eng.report("validate")
     ledger = eng.report("ledger")
+    # The reference simulator over the executed schedule, priced with this
+    # window's measured rates (simulator.cpp:70-287, shared PCIe 99-129).
+    simulated = eng.report("simulated")
 
     # Timed region 2: end to end through the C-ABI with host buffers.
     rng = np.random.default_rng(rank)
@@ -424,6 +565,19 @@ def run_ours(args):
         except Exception as ex:  # reported, not fatal
             q4 = {"error": str(ex)[:300]}
 
+    resident = ablation = None
+    if world == 1 and not args.no_resident:
+        try:
+            resident = resident_variant(args)
+        except Exception as ex:  # reported, not fatal
+            resident = {"error": str(ex)[:300]}
+    if world == 1 and not args.no_ablation:
+        ablation = ablation_variant(args)
+        ablation["klotski"] = {"value": value, "unit": "tokens/s", "ms_per_step": total_ms / args.steps,
+                               "steps": args.steps, "bubble_fraction": metrics["bubble_fraction"],
+                               "h2d_gb_per_step": metrics["h2d_bytes"] / args.steps / 1e9,
+                               "h2d_gbs_link_busy": metrics["h2d_gbs_busy"], "note": "the headline run"}
+
     iso = None
     try:
         M = int(round(rows / n_ops))
@@ -433,6 +587,12 @@ def run_ours(args):
     except Exception as ex:  # reported, not fatal
         iso = {"error": str(ex)[:200]}
 
+    sim_cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sim_cpu = simulator_baseline(info, simulated["rates"], args)
+        except Exception as ex:  # reported, not fatal
+            sim_cpu = {"error": str(ex)[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -500,6 +660,16 @@ def run_ours(args):
                          "first": validation["violations"][:3], "skipped": validation.get("skipped"),
                          "ledger_vram_high_water": ledger["vram_high_water"],
                          "ledger_within_cap": ledger["within_capacity"]},
+            "simulated": {"note": "reference moesim::run over the executed schedule with the rates measured in "
+                                  "this window (shared PCIe); same window as 'pipeline'",
+                          "simulated": {k: simulated["simulated"][k] for k in
+                                        ("makespan_ps", "compute_busy_ps", "bubble_fraction", "bubbles_ps")},
+                          "measured": {k: simulated["measured"][k] for k in
+                                       ("makespan_ps", "compute_busy_ps", "bubble_fraction", "bubbles_ps")},
+                          "rates": simulated["rates"]},
+            "cpu_baseline_simulator": sim_cpu,
+            "resident": resident,
+            "ablation": ablation,
             "setup_s": setup_s,
             "wall_s_timed": wall,
             "q4": q4,
@@ -526,6 +696,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-q4", action="store_true", help="skip the 4-bit streamed-expert variant")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill (configs[2]) measurement")
+    ap.add_argument("--no-resident", action="store_true", help="skip the all-resident (compute-exposed) decode")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the schedule-variant ablation")
     ap.add_argument("--quant-bits", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicas"],
                     help="N>1: expert-parallel shards (default) or independent replicas")

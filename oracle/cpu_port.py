@@ -10,8 +10,12 @@ gate, top-k), the expert-major permutation, every active expert's SwiGLU FFN
 and the weighted combine — exactly the B200 kernels' arithmetic in fp32/bf16
 on host cores with OpenMP (all threads the box gives us).
 
-Bounded sample: one full layer of one decode step at the workload's shape
-(n batches x batch_size tokens), timed, then extrapolated to all layers.
+Bounded samples: `measure` times one full layer of one decode step at the
+workload's shape (n batches x batch_size tokens) and extrapolates to all
+layers (bench.py's cpu_baseline); `StepSample` runs WHOLE decode steps of one
+batch through every layer (bench.py --impl reference), the layers aliased onto
+one layer's weights and KV (a layer's 2.8 GB of weights exceeds every CPU
+cache, so each layer streams them from DRAM either way).
 Weights/KV are synthetic bf16 from the same SplitMix64 stream family.
 """
 import os
@@ -76,6 +80,20 @@ class LayerSample:
             if hi > lo:
                 y[lo:hi] = orc.expert_ffn(np.ascontiguousarray(xp[lo:hi]), self.w13[e], self.w2[e])
         self.h = orc.combine(y, pos_r, w, self.h)
+
+
+class StepSample:
+    """Whole decode steps: one batch of `batch_size` sequences through all L
+    layers (the layers share one LayerSample's weights and KV)."""
+
+    def __init__(self, preset="mixtral-8x7b", batch_size=64, cap=260):
+        self.D = mixtral_dims(preset)
+        self.layer = LayerSample(self.D, 1, batch_size, cap)
+        self.tokens = batch_size
+
+    def decode_step(self, pos_value=600):
+        for _ in range(self.D["L"]):
+            self.layer.decode_layer(pos_value)
 
 
 def measure(preset="mixtral-8x7b", n_batches=8, batch_size=64, cap=260, repeats=1, warmup=0):

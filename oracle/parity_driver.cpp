@@ -217,11 +217,15 @@ json request(const char* text) {
             : moesim::build_baseline_schedule(v, plan, trace, provider, sopts);
     const moesim::ValidationReport rep = moesim::validate_schedule(sched, trace, plan);
     out["violations"] = rep.violations;
-    if (const int off = req.value("step_offset", 0); off != 0) {
+    // "lean": the caller times the reference path (bench.py's simulator CPU
+    // baseline) and wants neither the schedule nor the timeline text.
+    const bool lean = req.value("lean", false);
+    const int off = req.value("step_offset", 0);
+    if (!lean && off != 0) {
         moesim::Schedule shifted = sched;
         for (moesim::StreamOp& op : shifted.ops) op.step = static_cast<std::int16_t>(op.step + off);
         out["schedule_text"] = shifted.to_text();
-    } else {
+    } else if (!lean) {
         out["schedule_text"] = sched.to_text();
     }
     out["n_ops"] = sched.ops.size();
@@ -246,11 +250,13 @@ json request(const char* text) {
             const auto& b = m.bubbles;
             out["bubbles"] = {b.startup,      b.intra_attention, b.attn_to_moe, b.intra_gate,
                               b.gate_to_expert, b.intra_expert,  b.moe_to_attn, b.drain};
-            out["timeline_csv"] =
-                moesim::timeline_to_string(r.timeline, sched, moesim::TimelineFormat::csv);
-            out["timeline_json"] = moesim::timeline_to_string(
-                r.timeline, sched, moesim::TimelineFormat::trace_event_json);
-            out["memory_csv"] = moesim::memory_timeline_csv(ledger);
+            if (!lean) {
+                out["timeline_csv"] =
+                    moesim::timeline_to_string(r.timeline, sched, moesim::TimelineFormat::csv);
+                out["timeline_json"] = moesim::timeline_to_string(
+                    r.timeline, sched, moesim::TimelineFormat::trace_event_json);
+                out["memory_csv"] = moesim::memory_timeline_csv(ledger);
+            }
         } catch (const moesim::MemoryInfeasible& e) {
             out["run_error"] = std::string("MemoryInfeasible: ") + e.what();
         } catch (const std::exception& e) {
