@@ -33,6 +33,14 @@ sys.path.insert(0, ROOT)
 METRIC = "decode tokens/s (Mixtral-8x7B, capped HBM)"
 
 
+T_START = time.perf_counter()
+
+
+def log(msg):
+    """Progress on stderr (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.perf_counter() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -209,6 +217,7 @@ def prefill_variant(args, link):
     streamed; one warm-up pass then one timed pass. Reports prefill tokens/s,
     the pipeline bubble fraction and the expert GEMMs' tensor-pipe rate
     (FLOPs / measured compute time) against the bf16 peak."""
+    log('prefill_variant')
     from paper_2502_06888_b200.engine import Engine
     import numpy as np
     bs, n, P = 32, 8, args.prompt_len
@@ -246,6 +255,7 @@ def q4_variant(args, link):
     reference's QuantConfig{4, 64}): the link moves 0.28125x
     the bytes and the dequantisation runs inside the GEMM producer. A second
     engine after the bf16 one is closed; reported beside the headline."""
+    log('q4_variant')
     from paper_2502_06888_b200.engine import Engine
     a = argparse.Namespace(**vars(args))
     a.quant_bits = 4
@@ -331,6 +341,7 @@ def simulator_baseline(info, rates, args):
     shared-PCIe link) on the cfg2 workload (prompt 512 + generate 128,
     bs 64 x n 8, 24 GB cap) priced with the rates this run measured;
     single-threaded by design. Reports its wall time and simulated tok/s."""
+    log('simulator_baseline')
     import ctypes as C
     lib = C.CDLL(os.path.join(ROOT, "oracle", "_ref", "libref_parity.so"))
     lib.parity_request.argtypes = [C.c_char_p]
@@ -377,6 +388,7 @@ def decode_engine_run(cfg, warmup, steps, prompt_len):
     """Build an engine, prefill-free decode: warm-up steps, then `steps`
     timed steps (device events per step). Returns (engine, ms list)."""
     from paper_2502_06888_b200.engine import Engine
+    cfg = dict(cfg, workload=dict(cfg["workload"], gen_len=1 + warmup + steps))
     eng = Engine(cfg)
     eng.fill_kv_synthetic(prompt_len)
     step = 1
@@ -399,6 +411,7 @@ def resident_variant(args):
     so nothing is streamed and the step is the kernels plus the per-layer
     routing round trip. Reports tok/s, the reference bubble fraction and
     breakdown on the measured timeline, and the expert FFN per op."""
+    log('resident_variant')
     a = argparse.Namespace(**vars(args))
     a.hbm_cap = 140e9
     steps = max(4, min(args.steps, 20))
@@ -425,6 +438,52 @@ def resident_variant(args):
     return out
 
 
+def x22b_variant(args, link):
+    """BASELINE configs[3] at N=1: Mixtral-8x22B (56 layers, d 6144, f 16384,
+    48q/8kv heads; model.cpp:70-82, 603,979,776 B per expert) bf16 decode,
+    batch 64 x n 8, HBM capped at 40e9 B so the experts stream from pinned host
+    (the KV of 260 retained positions stays in HBM). The expert-parallel
+    streaming-scaling workload of SURVEY 8(e) on one GPU: tok/s, link
+    fraction and bubble. Host copies aliased onto 4 distinct layers (link
+    bytes unchanged) to bound pinned host memory and setup time."""
+    log('x22b_variant')
+    a = argparse.Namespace(**vars(args))
+    a.model = "mixtral-8x22b"
+    a.hbm_cap = 40e9
+    a.host_distinct_layers = 4
+    steps = 2
+    a.steps = steps
+    a.warmup = 1
+    cfg = engine_config(a, 0, 1)
+    # The planner is told the host holds every layer (282 GB of 8x22B host
+    # copies; this box's RAM is smaller, hence the aliasing): no disk tier.
+    cfg["host_dram_bytes"] = int(1e12)
+    t0 = time.perf_counter()
+    eng, ms = decode_engine_run(cfg, 1, steps, args.prompt_len)
+    m = eng.report("metrics")
+    val = eng.report("validate")
+    D = eng.info["dims"]
+    n_ops = max(m["expert_ops"], 1)
+    hbm_peak, _ = measured_peaks()
+    op_us = m["compute_ps_by_kind"]["expert"] / n_ops / 1e6
+    byts = m["expert_bytes"] + m["expert_rows"] / n_ops * (2 * D["d"] * 2 + 2 * D["f"] * 2)
+    h2d = m["h2d_bytes"] / steps
+    out = {"config": f"mixtral-8x22b bf16 decode, batch {args.batch_size} x n={eng.n_batches}, HBM cap 4e10 B, "
+                     "experts streamed from pinned host (host copies aliased onto 4 distinct layers)",
+           "value": steps * eng.n_seqs / (sum(ms) / 1e3), "unit": "tokens/s", "steps": steps,
+           "ms_per_step": sum(ms) / steps, "bubble_fraction": m["bubble_fraction"],
+           "h2d_gb_per_step": h2d / 1e9, "h2d_gbs_link_busy": m["h2d_gbs_busy"],
+           "h2d_frac_of_link_peak": m["h2d_gbs_busy"] / link,
+           "link_bound_ceiling_tok_s": eng.n_seqs / (h2d / (link * 1e9)),
+           "resident_expert_layers": eng.info["resident_expert_layers"],
+           "resident_attention_layers": eng.info["resident_attention_layers"],
+           "expert_bytes": m["expert_bytes"], "expert_op_us": op_us,
+           "expert_ffn_frac_of_hbm_peak": byts / op_us / 1e3 / hbm_peak,
+           "violations": len(val["violations"]), "wall_s": time.perf_counter() - t0}
+    eng.close()
+    return out
+
+
 def ablation_variant(args):
     """Table-6-style ablation at the headline scale: the
     reference's schedule variants executed by the engine on the same decode
@@ -434,6 +493,7 @@ def ablation_variant(args):
     = split hot/cold without the expert-major reorder; klotski = the headline.
     Host copies of the layers are aliased onto 4 distinct layers to bound setup
     time (link bytes per op are unchanged)."""
+    log('ablation_variant')
     out = {}
     for v, steps in (("multibatch_full_prefetch", 2), ("strawman_no_reorder", 2), ("simple", 1)):
         a = argparse.Namespace(**vars(args))
@@ -475,6 +535,7 @@ def run_ours(args):
         ep_id = share_ep_id(rank, world, ep_unique_id) if world > 1 else ""
     if world > 1 and not use_ep and args.host_distinct_layers == 0:
         args.host_distinct_layers = 4  # replicas: bound pinned host memory per rank
+    log('headline engine')
     eng = Engine(engine_config(args, rank, world, ep_id))
     eng.fill_kv_synthetic(args.prompt_len)
     setup_s = time.perf_counter() - t_setup
@@ -571,6 +632,12 @@ def run_ours(args):
             resident = resident_variant(args)
         except Exception as ex:  # reported, not fatal
             resident = {"error": str(ex)[:300]}
+    x22b = None
+    if world == 1 and not args.no_x22b:
+        try:
+            x22b = x22b_variant(args, link)
+        except Exception as ex:  # reported, not fatal
+            x22b = {"error": str(ex)[:300]}
     if world == 1 and not args.no_ablation:
         ablation = ablation_variant(args)
         ablation["klotski"] = {"value": value, "unit": "tokens/s", "ms_per_step": total_ms / args.steps,
@@ -670,6 +737,7 @@ def run_ours(args):
             "cpu_baseline_simulator": sim_cpu,
             "resident": resident,
             "ablation": ablation,
+            "mixtral_8x22b": x22b,
             "setup_s": setup_s,
             "wall_s_timed": wall,
             "q4": q4,
@@ -697,6 +765,7 @@ def main():
     ap.add_argument("--no-q4", action="store_true", help="skip the 4-bit streamed-expert variant")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill (configs[2]) measurement")
     ap.add_argument("--no-resident", action="store_true", help="skip the all-resident (compute-exposed) decode")
+    ap.add_argument("--no-x22b", action="store_true", help="skip the Mixtral-8x22B (configs[3]) decode")
     ap.add_argument("--no-ablation", action="store_true", help="skip the schedule-variant ablation")
     ap.add_argument("--quant-bits", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicas"],

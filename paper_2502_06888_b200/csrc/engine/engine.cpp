@@ -248,7 +248,8 @@ Engine::~Engine() {
     ep_shutdown();
     for (auto& s : streams_)
         if (s) cudaStreamDestroy(s);
-    for (cudaEvent_t e : event_pool_) cudaEventDestroy(e);
+    for (auto& pool : event_pool_)
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
     if (t0_) cudaEventDestroy(t0_);
     for (cudaEvent_t e : pool_.release) (void)e;
     if (arena_) cudaFree(arena_);

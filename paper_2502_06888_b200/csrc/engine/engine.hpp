@@ -37,6 +37,9 @@
 
 namespace klotski {
 
+// Op event pairs of the previous step collected per routing wait.
+constexpr std::int32_t kCollectPerWait = 96;
+
 using moesim::byte_count;
 
 struct Dims {
@@ -150,6 +153,8 @@ class Engine {
     cudaStream_t stream_of(moesim::StreamId s) const { return streams_[static_cast<int>(s)]; }
     cudaEvent_t event();
     void collect_step_times();
+    void collect_some(std::int32_t budget);
+    void flush_times();
     int tokens_per_batch(int step) const { return cfg_.workload.batch_size * (step == 0 ? cfg_.workload.prompt_len : 1); }
     int n_batches() const { return plan_.n_batches; }
     const uint16_t* expert_weights(int layer, int e) const;
@@ -247,8 +252,14 @@ class Engine {
 
     // streams / events
     std::array<cudaStream_t, moesim::kNumStreams> streams_{};
-    std::vector<cudaEvent_t> event_pool_;
+    // Two event pools alternate by step: the events of step N are turned into
+    // timeline entries while step N+1 runs (collect_some, in the host's
+    // routing waits), so the GPU does not idle between steps on ~2 event
+    // queries per op.
+    std::array<std::vector<cudaEvent_t>, 2> event_pool_;
+    int event_par_ = 0;
     std::size_t event_next_ = 0;
+    std::int32_t pend_from_ = 0, pend_to_ = 0;   // ops of the previous step not yet collected
     cudaEvent_t t0_ = nullptr;
     bool t0_recorded_ = false;
     std::vector<cudaEvent_t> op_start_, op_end_;     // by op id (current step window)
@@ -278,7 +289,7 @@ class Engine {
     };
     bool diag_ = false;
     std::int32_t next_exec_diag_ = 0;
-    std::vector<DiagEvent> diag_events_;
+    std::vector<DiagEvent> diag_events_, pend_diag_;
     std::vector<std::array<float, 3>> diag_rows_;
     int idx_cur_ = 0;
     std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot

@@ -14,6 +14,7 @@
 // Every op records start/end cudaEvents; cross-stream deps are
 // cudaStreamWaitEvent; expert slots are reused only after the release event
 // of their previous occupant (bounded pool with backpressure).
+#include <limits>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -115,12 +116,13 @@ std::pair<int64_t, duration_ps> link_usage(const Schedule& s, const std::vector<
 
 
 cudaEvent_t Engine::event() {
-    if (event_next_ == event_pool_.size()) {
+    auto& pool = event_pool_[event_par_];
+    if (event_next_ == pool.size()) {
         cudaEvent_t e;
         cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-        event_pool_.push_back(e);
+        pool.push_back(e);
     }
-    return event_pool_[event_next_++];
+    return pool[event_next_++];
 }
 
 const uint16_t* Engine::expert_weights(int layer, int e) const {
@@ -299,10 +301,14 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     return ms;
 }
 
-void Engine::collect_step_times() {
+// Turn up to `budget` op event pairs of the previous step into timeline
+// entries (the events completed at that step's end). Called from the host's
+// routing waits, where the host would otherwise only block.
+void Engine::collect_some(std::int32_t budget) {
     const auto& ops = em_->schedule().ops;
     if (timeline_.size() < ops.size()) timeline_.resize(ops.size());
-    for (std::int32_t id = timed_from_; id < next_exec_; ++id) {
+    for (; pend_from_ < pend_to_ && budget > 0; ++pend_from_, --budget) {
+        const std::int32_t id = pend_from_;
         float a = 0.f, b = 0.f;
         cuda_check(cudaEventElapsedTime(&a, t0_, op_start_[id]), "elapsed");
         cuda_check(cudaEventElapsedTime(&b, t0_, op_end_[id]), "elapsed");
@@ -314,19 +320,33 @@ void Engine::collect_step_times() {
         ev.bytes = ops[id].payload_bytes;
         ev.tokens = ops[id].token_count;
     }
-    for (const auto& de : diag_events_) {
-        float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+    if (pend_from_ < pend_to_) return;
+    for (const auto& de : pend_diag_) {
+        float a = 0.f, b = 0.f, c = 0.f;
         cuda_check(cudaEventElapsedTime(&a, op_start_[de.op], de.before), "diag");
         cuda_check(cudaEventElapsedTime(&b, de.before, de.after), "diag");
         cuda_check(cudaEventElapsedTime(&c, de.after, op_end_[de.op]), "diag");
-        (void)d;
         diag_rows_.push_back({a * 1e3f, b * 1e3f, c * 1e3f});
     }
+    pend_diag_.clear();
+}
+
+void Engine::flush_times() { collect_some(std::numeric_limits<std::int32_t>::max()); }
+
+// End of a synchronized step: the previous step's leftovers are collected
+// now (its event pool is about to be reused), this step's ops become the
+// pending window, and slot release markers are recycled.
+void Engine::collect_step_times() {
+    flush_times();
+    pend_from_ = timed_from_;
+    pend_to_ = next_exec_;
+    pend_diag_ = std::move(diag_events_);
     diag_events_.clear();
     timed_from_ = next_exec_;
-    // Everything this step enqueued has completed: events and release
-    // markers can be recycled.
+    event_par_ ^= 1;
     event_next_ = 0;
+    // Everything this step enqueued has completed: release markers can be
+    // recycled.
     std::fill(pool_.has_release.begin(), pool_.has_release.end(), 0);
     std::fill(attn_slot_release_.begin(), attn_slot_release_.end(), nullptr);
     std::fill(gate_slot_release_.begin(), gate_slot_release_.end(), nullptr);
@@ -444,13 +464,15 @@ void Engine::exec(std::int32_t id) {
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
             const auto it = expert_slot_of_.find({op.layer, op.expert});
             if (it == expert_slot_of_.end()) throw AccountingError("engine: offload of an unloaded expert");
-            pool_.release_after(it->second, op_end_[op.deps.front()]);
+            // The slot is free once the offload op itself has completed (the
+            // ledger frees at the offload's end), not merely its compute dep.
+            pool_.release_after(it->second, op_end_[id]);
             expert_slot_of_.erase(it);
             break;
         }
         case OpKind::offload_weights: {
             cuda_check(cudaEventRecord(op_start_[id], st), "record");
-            cudaEvent_t after = op_end_[op.deps.front()];
+            cudaEvent_t after = op_end_[id];  // recorded after the dep wait above
             if (op.cls == TensorClass::attention) {
                 const int s = attn_slot_of_.at(op.layer);
                 attn_slot_busy_[s] = 0;
@@ -743,6 +765,7 @@ void Engine::after_batch_gate(int step, int layer, int b) {
 
 detail::BlockRouting Engine::read_routing_row(int step, int layer, int b) {
     const std::int32_t last_gate = next_exec_ - 1;
+    collect_some(kCollectPerWait);
     cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
@@ -781,6 +804,7 @@ detail::BlockRouting Engine::read_routing(int step, int layer) {
     // The last op issued on the compute stream is the block's last gate;
     // its end event covers the readback copies.
     const std::int32_t last_gate = next_exec_ - 1;
+    collect_some(kCollectPerWait);
     cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
@@ -898,6 +922,7 @@ void Engine::read_hidden(uint16_t* host, int64_t n) const {
 }
 
 void Engine::reset_log() {
+    flush_times();
     // Keep the emitter (op ids keep growing); measurement restarts here.
     timed_from_ = next_exec_;
     log_from_ = next_exec_;
@@ -912,6 +937,7 @@ void Engine::reset_log() {
 }
 
 std::string Engine::report(const std::string& what) {
+    flush_times();
     const Schedule& s = em_->schedule();
     json j;
     std::vector<SimEvent> tl(timeline_.begin() + std::min<size_t>(log_from_, timeline_.size()),
