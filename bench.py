@@ -484,6 +484,85 @@ def x22b_variant(args, link):
     return out
 
 
+def sweep_variant(args, full=False):
+    """BASELINE configs[2]: Mixtral-8x7B prefill 512 + generate 128, swept over
+    the batch number n and the HBM cap through the I/O-compute planner
+    (the reference's run_sweep, experiment.cpp:342-378, on the engine).
+    Stage 1: the engine's per-token rates and the pinned link
+    are measured once (kl_measure_profile, decode phase, which dominates a
+    128-token generation); stage 2: make_plan solves n and the placement under
+    each cap with those rates (a plan_only engine reports solved_n_uncapped
+    and the KV-capped n). Each (cap, n) point then runs on the engine: the
+    prefill pass (step 0) and two decode steps, timed on the device; the
+    group's tok/s is the reference definition bs*n*gen_len / makespan
+    (simulator.cpp:264-267) with makespan = prefill + 127 x mean decode step
+    (sink 4 + window 256 retention: every decode step sees the same 260
+    positions, so the steps are alike). batch 32; host copies aliased onto 4
+    distinct layers (link bytes unchanged)."""
+    log('sweep_variant')
+    from paper_2502_06888_b200.engine import Engine, measure_profile
+    import numpy as np
+    bs, P, G = 32, args.prompt_len, 128
+    caps = (16e9, 24e9, 40e9) if full else (24e9,)
+    ns = (1, 2, 4, 8, 12, 16, 24, 32) if full else (2, 8)
+    base = {"model": {"preset": args.model},
+            "workload": {"batch_size": bs, "n_batches": 8, "prompt_len": P, "gen_len": G},
+            "kv_retention": {"mode": "streaming", "sink_tokens": 4, "window_tokens": 256},
+            "routing": "gate", "prefill": True, "record_trace": False, "host_distinct_layers": 4}
+    prof = measure_profile(dict(base, hbm_cap_bytes=int(24e9)), "decode")
+    rates = {"attn_ps": int(prof["attn_ps_per_token"]), "gate_ps": int(prof["gate_ps_per_token"]),
+             "expert_ps": int(prof["expert_ps_per_token"]), "pcie_bandwidth": float(prof["pcie_bandwidth"])}
+    out = {"config": f"{args.model} prefill {P} + generate {G}, batch {bs}, n x HBM cap grid; host copies aliased onto "
+                     "4 distinct layers (link bytes unchanged)",
+           "method": "tok/s = bs*n*128 / (prefill_ms + 127 * mean of 2 decode steps), device-timed per step",
+           "rates": rates, "caps": {}}
+    rng = np.random.default_rng(0)
+    for cap in caps:
+        key = f"{cap / 1e9:.0f}GB"
+        row = {"points": []}
+        try:
+            pe = Engine(dict(base, hbm_cap_bytes=int(cap), solve_n=True, plan_only=True, **rates))
+            row["planner_solved_n"] = pe.info["planner_solved_n"]   # solve_min_n (planner.cpp:58-116)
+            row["planner_n"] = pe.info["planner_n"]                 # after the reference KV cap
+            row["engine_n"] = pe.info["n_batches"]                  # after the engine's HBM working set
+            row["kv_capped"] = pe.info["kv_capped"]
+            pe.close()
+        except Exception as ex:  # reported, not fatal
+            row["planner_error"] = str(ex)[:200]
+        grid = sorted(set(ns) | ({row["engine_n"]} if row.get("engine_n") else set()))
+        for n in grid:
+            pt = {"n": n}
+            try:
+                cfg = dict(base, hbm_cap_bytes=int(cap), **rates)
+                cfg["workload"] = dict(base["workload"], n_batches=n)
+                eng = Engine(cfg)
+                prompt = rng.integers(0, eng.info["dims"]["V"], eng.n_seqs * P, dtype=np.int32)
+                _, pms = eng.step(0, prompt, want_next=False)
+                dms = [eng.step(s, None, want_next=False)[1] for s in (1, 2)]
+                m = eng.report("metrics")
+                dmean = sum(dms) / len(dms)
+                makespan_ms = pms + (G - 1) * dmean
+                pt.update({"tok_s": bs * n * G / (makespan_ms / 1e3), "prefill_ms": pms, "decode_ms": dmean,
+                           "decode_tok_s": bs * n / (dmean / 1e3), "bubble_fraction": m["bubble_fraction"],
+                           "resident_expert_layers": eng.info["resident_expert_layers"],
+                           "kv_offload": eng.info["kv_offload"]})
+                eng.close()
+            except Exception as ex:  # infeasible points are reported, not fatal
+                pt["error"] = str(ex)[:200]
+            row["points"].append(pt)
+        ok = [p for p in row["points"] if "tok_s" in p]
+        if ok:
+            best = max(ok, key=lambda p: p["tok_s"])
+            row["measured_best_n"] = best["n"]
+            row["measured_best_tok_s"] = best["tok_s"]
+            at = [p for p in ok if p["n"] == row.get("engine_n")]
+            if at:
+                row["solved_n_tok_s"] = at[0]["tok_s"]
+                row["solved_over_best"] = at[0]["tok_s"] / best["tok_s"]
+        out["caps"][key] = row
+    return out
+
+
 def ablation_variant(args):
     """Table-6-style ablation at the headline scale: the
     reference's schedule variants executed by the engine on the same decode
@@ -638,6 +717,12 @@ def run_ours(args):
             x22b = x22b_variant(args, link)
         except Exception as ex:  # reported, not fatal
             x22b = {"error": str(ex)[:300]}
+    sweep = None
+    if world == 1 and args.sweep != "off":
+        try:
+            sweep = sweep_variant(args, full=args.sweep == "full")
+        except Exception as ex:  # reported, not fatal
+            sweep = {"error": str(ex)[:300]}
     if world == 1 and not args.no_ablation:
         ablation = ablation_variant(args)
         ablation["klotski"] = {"value": value, "unit": "tokens/s", "ms_per_step": total_ms / args.steps,
@@ -738,6 +823,7 @@ def run_ours(args):
             "resident": resident,
             "ablation": ablation,
             "mixtral_8x22b": x22b,
+            "sweep": sweep,
             "setup_s": setup_s,
             "wall_s_timed": wall,
             "q4": q4,
@@ -766,6 +852,9 @@ def main():
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill (configs[2]) measurement")
     ap.add_argument("--no-resident", action="store_true", help="skip the all-resident (compute-exposed) decode")
     ap.add_argument("--no-x22b", action="store_true", help="skip the Mixtral-8x22B (configs[3]) decode")
+    ap.add_argument("--sweep", default="light", choices=["off", "light", "full"],
+                    help="configs[2] n x HBM-cap sweep: light = 24 GB cap, n in {2, 8, solved}; "
+                         "full = caps {16, 24, 40} GB x n in {1..32} (8 points) + solved n")
     ap.add_argument("--no-ablation", action="store_true", help="skip the schedule-variant ablation")
     ap.add_argument("--quant-bits", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicas"],

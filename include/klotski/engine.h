@@ -43,6 +43,8 @@
  *       process on one device (host threads), rendezvous by group name
  *   profile: {measure: "decode"|"prefill"}  plan with rates measured here
  *   solve_n: true  let make_plan solve n (ignores workload.n_batches)
+ *   plan_only: true  plan and stop (kl_engine_describe only: n, solved_n_uncapped,
+ *                    placement, working set; no memory is allocated, steps fail)
  */
 #ifndef KLOTSKI_ENGINE_H
 #define KLOTSKI_ENGINE_H

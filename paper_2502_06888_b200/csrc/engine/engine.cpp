@@ -99,6 +99,7 @@ EngineConfig parse_config(const std::string& text) {
     if (w.contains("n_batches")) c.n_override = c.workload.n_batches;
     if (j.contains("n_override")) c.n_override = j["n_override"].get<int>();
     if (j.value("solve_n", false)) c.n_override.reset();
+    c.plan_only = j.value("plan_only", false);
     c.hbm_cap = j.value("hbm_cap_bytes", c.hbm_cap);
     c.host_dram = j.value("host_dram_bytes", c.host_dram);
     c.pcie_bandwidth = j.value("pcie_bandwidth", c.pcie_bandwidth);
@@ -224,6 +225,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
         profile_.pcie_bandwidth = measured_->pcie_bandwidth;
     }
     plan_memory();
+    if (cfg_.plan_only) return;  // the planner's answer only: no HBM, host memory or streams
     allocate_device();
     allocate_host();
     for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
@@ -278,16 +280,54 @@ void Engine::plan_memory() {
     const ActivationTrace wt =
         generate_trace(spec_g_, warm, cfg_.skew, cfg_.warmup_seed ? cfg_.warmup_seed : cfg_.trace_seed + 1);
     table0_ = build_table(wt, spec_g_);
-    const TraceStats stats = compute_trace_stats(wt, D_.k);
+    stats_ = compute_trace_stats(wt, D_.k);
 
     // Streamed tensors travel as Q4T when quantised (= the planner's
     // quantized_bytes, model_cost.cpp on_wire); resident ones stay bf16.
     expert_slot_bytes_ = cfg_.quant ? kl_q4_bytes(2LL * D_.f, D_.d) + kl_q4_bytes(D_.d, D_.f) : spec_.expert_bytes;
     attn_slot_bytes_ = cfg_.quant ? kl_q4_bytes(D_.qkv_width(), D_.d) + kl_q4_bytes(D_.d, static_cast<int64_t>(D_.Hq) * D_.hd)
                                   : spec_.attention_bytes;
-    int n = cfg_.n_override ? *cfg_.n_override : make_plan(spec_, profile_, w, stats, cfg_.quant,
-                                                           ExpertLoadModel::measured, cfg_.retention)
-                                                     .n_batches;
+    // The reference planner's own answer (its working-set formula,
+    // placement.cpp:109-118): solved n and the KV-capped n.
+    int n = 0;
+    if (cfg_.n_override) {
+        n = *cfg_.n_override;
+    } else {
+        const PipelinePlan ref = make_plan(spec_, profile_, w, stats_, cfg_.quant, ExpertLoadModel::measured, cfg_.retention);
+        planner_solved_n_ = ref.solved_n_uncapped;
+        planner_n_ = ref.n_batches;
+        n = ref.n_batches;
+    }
+    // The engine's working set grows with n (the group's activations and
+    // routed rows live in HBM), so a solved n is further capped to the
+    // largest n whose real working set fits, the same monotone search the
+    // reference uses for its KV cap (planner.cpp:195-229).
+    if (plan_at(n)) return finish_plan();
+    if (cfg_.n_override) {
+        plan_at(n, /*rethrow=*/true);
+        return;
+    }
+    if (!plan_at(1)) plan_at(1, /*rethrow=*/true);
+    int lo = 1, hi = n - 1;
+    while (lo < hi) {
+        const int mid = lo + (hi - lo + 1) / 2;
+        if (plan_at(mid))
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    plan_at(lo, true);
+    memory_capped_n_ = lo;
+    plan_.warnings.push_back("planner n=" + std::to_string(n) + " exceeds the engine's HBM working set; capped to n=" +
+                             std::to_string(plan_.n_batches));
+    finish_plan();
+}
+
+// One planning attempt at n with the engine's working set at n (and at the
+// KV-capped n if the planner lowers it). false = MemoryInfeasible at n.
+bool Engine::plan_at(int n, bool rethrow) {
+    const BatchGroupConfig& w = cfg_.workload;
+    const TraceStats stats = stats_;
     // KV offload (KV tier = DRAM): the cache of one (layer, batch) lives in a
     // device slot only between its load and its store; kKvSlots slots.
     bool kv_off = false;
@@ -364,12 +404,21 @@ void Engine::plan_memory() {
         ws_bytes_ = ws;
         PlacementConfig pc;
         pc.working_set_override = ws;
-        plan_ = make_plan(spec_, profile_, w, stats, cfg_.quant, ExpertLoadModel::measured, cfg_.retention, n, pc);
+        try {
+            plan_ = make_plan(spec_, profile_, w, stats, cfg_.quant, ExpertLoadModel::measured, cfg_.retention, n, pc);
+        } catch (const MemoryInfeasible&) {
+            if (rethrow) throw;
+            return false;
+        }
         const bool off_now = plan_.placement.kv_tier == Tier::dram;
         if (plan_.n_batches == n && off_now == kv_off) break;
         n = plan_.n_batches;  // KV-capped: resize scratch for the capped n
         kv_off = off_now;     // KV slots join the working set
     }
+    return true;
+}
+
+void Engine::finish_plan() {
     kv_offload_ = plan_.placement.kv_tier == Tier::dram;
     if (kv_offload_ && ep_) throw ConfigError("engine: KV offload is not combined with expert parallelism yet");
     if (plan_.placement.any_disk() && ep_)
@@ -691,6 +740,7 @@ void Engine::init_weights() {
 }
 
 void Engine::fill_kv_synthetic(int positions, std::uint64_t seed) {
+    if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (no KV cache)");
     // KV content of a synthetic prefill: values for the retained slots of
     // positions [0, positions) of every sequence (post-rope keys are just
     // random vectors here; the decode kernels read them like real ones).
@@ -728,6 +778,11 @@ std::string Engine::describe() const {
     json j;
     j["plan_text"] = plan_.to_text();
     j["n_batches"] = plan_.n_batches;
+    j["solved_n_uncapped"] = plan_.solved_n_uncapped;
+    j["planner_solved_n"] = planner_solved_n_;       // reference working-set model, before the KV cap
+    j["planner_n"] = planner_n_;                     // ... after its KV cap
+    j["memory_capped_n"] = memory_capped_n_;         // 0 = the engine's working set did not cap n
+    j["kv_capped"] = plan_.kv_capped;
     j["batch_size"] = cfg_.workload.batch_size;
     j["prompt_len"] = cfg_.workload.prompt_len;
     j["gen_len"] = cfg_.workload.gen_len;

@@ -88,6 +88,7 @@ struct EngineConfig {
     std::string ep_backend = "nccl";
     std::string ep_group;
     bool prefill = true;
+    bool plan_only = false;  // stop after planning (describe() only): n, placement, working set
     std::optional<moesim::QuantConfig> quant;  // 4-bit streamed experts / attention (Q4T)
     std::string disk_dir;           // disk-tier store directory (default $TMPDIR, else /tmp)
     std::string measure_phase;      // "decode" | "prefill": plan with rates measured on this GPU
@@ -134,6 +135,10 @@ class Engine {
   private:
     // setup
     void plan_memory();
+    bool plan_at(int n, bool rethrow = false);
+    void finish_plan();
+    moesim::TraceStats stats_;
+    int planner_solved_n_ = 0, planner_n_ = 0, memory_capped_n_ = 0;
     void allocate_device();
     void allocate_host();
     void init_weights();

@@ -170,6 +170,7 @@ PrefetchDecision Engine::decide(int /*step*/, int layer) const {
 }
 
 double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
+    if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (no memory to run on)");
     if (step < 0 || step >= cfg_.workload.gen_len) throw RangeError("engine: step outside the batch group");
     if (step == 0 && !cfg_.prefill) throw ConfigError("engine: built without prefill support (prefill=false)");
     const int n = plan_.n_batches, bs = cfg_.workload.batch_size;
@@ -916,12 +917,14 @@ void Engine::combine_block(int step) {
 }
 
 void Engine::read_hidden(uint16_t* host, int64_t n) const {
+    if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (no hidden states)");
     cuda_check(cudaDeviceSynchronize(), "sync");
     cuda_check(cudaMemcpy(host, h_, static_cast<size_t>(std::min<int64_t>(n, t_max_ * D_.d)) * 2,
                           cudaMemcpyDeviceToHost), "read hidden");
 }
 
 void Engine::reset_log() {
+    if (cfg_.plan_only) return;
     flush_times();
     // Keep the emitter (op ids keep growing); measurement restarts here.
     timed_from_ = next_exec_;
@@ -937,6 +940,7 @@ void Engine::reset_log() {
 }
 
 std::string Engine::report(const std::string& what) {
+    if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (nothing executed to report)");
     flush_times();
     const Schedule& s = em_->schedule();
     json j;

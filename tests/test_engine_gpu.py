@@ -121,6 +121,36 @@ def test_measured_profile_and_simulated_report(cuda):
     eng.close()
 
 
+def test_solve_n_is_capped_by_the_engine_working_set(cuda):
+    """solve_n: make_plan's n (reference working-set formula) is lowered to
+    the largest n whose REAL engine working set fits the cap (the reference's
+    monotone feasibility search, planner.cpp:195-229); plan_only reports it
+    without allocating, and a real engine at that n builds and runs."""
+    rates = {"attn_ps": 40_000_000, "gate_ps": 1_000_000, "expert_ps": 20_000_000, "pcie_bandwidth": 5e8}
+    cfg = dict(TINY, routing="gate", solve_n=True, hbm_cap_bytes=90_000_000, **rates)
+    p = make(dict(cfg, plan_only=True))
+    info = p.info
+    p.close()
+    assert info["planner_solved_n"] >= 1 and info["planner_n"] >= 1
+    assert 1 <= info["n_batches"] <= info["planner_n"]
+    if info["memory_capped_n"]:
+        assert info["memory_capped_n"] == info["n_batches"] < info["planner_n"]
+    # n + 1 batches would not fit this engine's working set (maximality),
+    # unless the planner itself asked for no more.
+    if info["n_batches"] < info["planner_n"]:
+        from paper_2502_06888_b200.engine import MemoryInfeasible
+        bigger = dict(cfg, solve_n=False, workload=dict(TINY["workload"], n_batches=info["n_batches"] + 1))
+        with pytest.raises(MemoryInfeasible):
+            make(bigger)
+    eng = make(cfg)
+    assert eng.n_batches == info["n_batches"]
+    run_all_steps(eng, cfg)
+    assert eng.report("validate")["violations"] == []
+    eng.close()
+    with pytest.raises(Exception):
+        make(dict(cfg, plan_only=True)).step(1)
+
+
 def test_gate_mode_is_deterministic(cuda):
     cfg = dict(TINY, routing="gate", hbm_cap_bytes=63_000_000)
     a = make(cfg)
