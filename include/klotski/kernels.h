@@ -153,6 +153,9 @@ int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uint16_t* wg, 
  *   xp[pos[r], :] = x2[r / k, :]   (vectorised 16-byte copies; xp may be NULL).
  * workspace: >= kl_permute_workspace_bytes(R, E) bytes. */
 int64_t kl_permute_workspace_bytes(int64_t R, int E);
+/* Kernels one kl_permute call launches for R = T*k routed rows (1 scan-only
+ * for R = 0, 2 for a single 1024-row chunk, else 3). */
+int kl_permute_launches(int64_t R);
 int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uint16_t* x2, int d,
                int32_t* counts, int32_t* offsets, int32_t* pos, int32_t* row_token,
                uint16_t* xp, void* workspace, cudaStream_t stream);

@@ -356,7 +356,7 @@ void Engine::ep_after_gates(int step, int layer) {
     shared_experts(layer, T, 0);  // replicated with the router: every rank on its own tokens
     kl_check(kl_permute(lbl_, T, D_.k, E, x2_, D_.d, send_counts_, offsets_, pos_, row_token_, y_ret_, perm_ws_, cs),
              "permute (dispatch order)");
-    launches_ += 2;
+    launches_ += kl_permute_launches(T * D_.k) - 1;
     // Per-(destination, local expert) counts exchange.
     {
         std::vector<int64_t> off(G_), len(G_, static_cast<int64_t>(El_) * 4);
@@ -471,7 +471,7 @@ void Engine::ep_dispatch() {
     kl_check(kl_permute(recv_ids_, r_recv_, 1, El_, recv_x_, D_.d, counts2_, offsets2_, pos2_, row_token2_, xp_,
                         perm_ws_, cs),
              "permute (local experts)");
-    launches_ += 2;
+    launches_ += kl_permute_launches(r_recv_) - 1;
 }
 
 void Engine::ep_return(int64_t T) {

@@ -704,7 +704,7 @@ void Engine::after_layer_gates(int step, int layer) {
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
     shared_experts(layer, T, 0);
-    launches_ += 2;  // rank + scan + scatter kernels
+    launches_ += kl_permute_launches(T * D_.k) - 1;  // rank (+ scan) + scatter kernels
     int64_t* scores = reinterpret_cast<int64_t*>(report_ + 2LL * n * D_.E + 16 - ((2LL * n * D_.E) % 16));
     int64_t* marg_copy = scores + D_.E;
     if (layer + 1 < D_.L) {
@@ -750,7 +750,7 @@ void Engine::after_batch_gate(int step, int layer, int b) {
     int32_t* cur = idx_[idx_cur_] + row0 * D_.k;
     kl_check(kl_permute(cur, tpb, D_.k, D_.E, x2_ + row0 * D_.d, D_.d, counts_, offsets_, pos_ + row0 * D_.k,
                         row_token_ + row0 * D_.k, xp_, perm_ws_, cs), "permute (row)");
-    launches_ += 2;
+    launches_ += kl_permute_launches(static_cast<int64_t>(tpb) * D_.k) - 1;
     shared_experts(layer, tpb, row0);
     const int n = plan_.n_batches;
     const size_t hist_off = static_cast<size_t>(b) * D_.E, first_off = static_cast<size_t>(n) * D_.E + hist_off;

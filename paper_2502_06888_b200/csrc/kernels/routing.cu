@@ -418,8 +418,9 @@ constexpr int kChunk = 1024;
 
 __global__ void __launch_bounds__(kChunk)
 permute_rank_kernel(const int32_t* __restrict__ idx, int64_t R, int E, int32_t* __restrict__ chunk_counts,
-                    int32_t* __restrict__ local_rank) {
+                    int32_t* __restrict__ local_rank, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
     __shared__ int32_t warp_cnt[32][64];
+    __shared__ int32_t tot[64];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
     for (int i = threadIdx.x; i < 32 * 64; i += blockDim.x) (&warp_cnt[0][0])[i] = 0;
@@ -439,9 +440,33 @@ permute_rank_kernel(const int32_t* __restrict__ idx, int64_t R, int E, int32_t* 
             run += c;
         }
         chunk_counts[static_cast<int64_t>(blockIdx.x) * E + threadIdx.x] = run;
+        tot[threadIdx.x] = run;
     }
     __syncthreads();
     if (valid) local_rank[r] = warp_cnt[warp][e] + rank;
+    if (offsets != nullptr && threadIdx.x < 32) {
+        // Single chunk (decode-sized calls): the scan kernel's work in the
+        // same launch. Chunk base of expert e = its exclusive offset.
+        int run = 0;
+        for (int base = 0; base < E; base += 32) {
+            const int e2 = base + threadIdx.x;
+            const int v = e2 < E ? tot[e2] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (threadIdx.x >= o) incl += y;
+            }
+            if (e2 < E) {
+                const int excl = run + incl - v;
+                offsets[e2] = excl;
+                chunk_counts[e2] = excl;
+                if (counts != nullptr) counts[e2] = v;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (threadIdx.x == 0) offsets[E] = run;
+    }
 }
 
 // One thread per expert: totals, exclusive offsets, per-chunk bases.
@@ -475,66 +500,110 @@ __global__ void permute_scan_kernel(int32_t* __restrict__ chunk_counts, int64_t 
     }
 }
 
-// One warp per routed row: position, inverse map, 16-byte vector row copy.
-__global__ void permute_scatter_kernel(const int32_t* __restrict__ idx, int64_t R, int k, int E,
-                                       const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ local_rank,
-                                       const uint16_t* __restrict__ x2, int d, int32_t* __restrict__ pos,
-                                       int32_t* __restrict__ row_token, uint16_t* __restrict__ xp) {
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+// One CTA of kRowThreads per routed row: position and inverse map (thread
+// 0), then the 16-byte row copy with every load of a group issued before its
+// stores (a row is d*2 bytes: 8 KB at d = 4096, 4 x 16 B per thread), so a
+// decode-sized call keeps the whole copy in flight at once instead of one
+// warp-serial 16 B chain per row.
+constexpr int kRowThreads = 128;
+constexpr int kRowGroup = 4;  // 16-byte chunks per thread in flight
+
+__global__ void __launch_bounds__(kRowThreads)
+permute_scatter_kernel(const int32_t* __restrict__ idx, int64_t R, int k, int E,
+                       const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ local_rank,
+                       const uint16_t* __restrict__ x2, int d, int32_t* __restrict__ pos,
+                       int32_t* __restrict__ row_token, uint16_t* __restrict__ xp) {
+    const int64_t r = blockIdx.x;
     if (r >= R) return;
     const int e = idx[r];
     const int32_t p = chunk_base[(r / kChunk) * E + e] + local_rank[r];
     const int64_t t = r / k;
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         pos[r] = p;
         if (row_token != nullptr) row_token[p] = static_cast<int32_t>(t);
     }
-    if (xp != nullptr) {
-        const uint4* src = reinterpret_cast<const uint4*>(x2 + t * d);
-        uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<int64_t>(p) * d);
-#pragma unroll 4
-    #pragma unroll 4
-    for (int i = lane; i < d / 8; i += 32) dst[i] = __ldg(src + i);
+    if (xp == nullptr) return;
+    const uint4* src = reinterpret_cast<const uint4*>(x2 + t * d);
+    uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<int64_t>(p) * d);
+    const int n16 = d / 8;
+    for (int g = 0; g < n16; g += kRowThreads * kRowGroup) {
+        uint4 v[kRowGroup];
+#pragma unroll
+        for (int u = 0; u < kRowGroup; ++u) {
+            const int i = g + u * kRowThreads + threadIdx.x;
+            if (i < n16) v[u] = __ldg(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowGroup; ++u) {
+            const int i = g + u * kRowThreads + threadIdx.x;
+            if (i < n16) dst[i] = v[u];
+        }
     }
 }
 
 // ---------------------------------------------------------------- combine --
-__global__ void combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos,
-                               const float* __restrict__ weight, const uint16_t* resid, int64_t T, int k, int d,
-                               uint16_t* out) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+// out[t] = resid[t] + sum_j w[t,j] * y[pos[t,j]]  (fp32 fma in j order, one
+// rounding), one CTA of kRowThreads per token. Each thread owns up to
+// kRowGroup 8-column chunks of the row per pass and issues all of their
+// loads (residual + k gathered expert rows) before any arithmetic or store;
+// out may alias resid (the engine combines in place), which is safe because
+// a thread only stores the chunks it has already loaded.
+template <int KMAX>
+__global__ void __launch_bounds__(kRowThreads)
+combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos, const float* __restrict__ weight,
+               const uint16_t* resid, int64_t T, int k, int d, uint16_t* out) {
+    const int64_t t = blockIdx.x;
     if (t >= T) return;
-    int32_t p[8];
-    float w[8];
-    for (int j = 0; j < k; ++j) {
-        p[j] = pos[t * k + j];
-        w[j] = weight[t * k + j];
+    int32_t p[KMAX];
+    float w[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        p[j] = j < k ? pos[t * k + j] : 0;
+        w[j] = j < k ? weight[t * k + j] : 0.f;
     }
-#pragma unroll 4
-    for (int c = lane * 8; c < d; c += 256) {
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j < k; ++j) {
-            float v[8];
-            load8(y + static_cast<int64_t>(p[j]) * d + c, v);
+    const int n8 = d / 8;
+    for (int g = 0; g < n8; g += kRowThreads * kRowGroup) {
+        uint4 rq[kRowGroup];
+        uint4 yq[kRowGroup][KMAX];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[j], v[i], acc[i]);
-        }
-        float rv[8];
-        const uint4 q = *reinterpret_cast<const uint4*>(resid + t * d + c);
-        const uint32_t rw[4] = {q.x, q.y, q.z, q.w};
+        for (int u = 0; u < kRowGroup; ++u) {
+            const int i = g + u * kRowThreads + threadIdx.x;
+            if (i < n8) {
+                rq[u] = *reinterpret_cast<const uint4*>(resid + t * d + i * 8);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            rv[2 * i] = bf2f(static_cast<uint16_t>(rw[i] & 0xffffu));
-            rv[2 * i + 1] = bf2f(static_cast<uint16_t>(rw[i] >> 16));
+                for (int j = 0; j < KMAX; ++j)
+                    if (j < k) yq[u][j] = __ldg(reinterpret_cast<const uint4*>(y + static_cast<int64_t>(p[j]) * d) + i);
+            }
         }
-        uint4 o;
-        o.x = pack2(__fadd_rn(rv[0], acc[0]), __fadd_rn(rv[1], acc[1]));
-        o.y = pack2(__fadd_rn(rv[2], acc[2]), __fadd_rn(rv[3], acc[3]));
-        o.z = pack2(__fadd_rn(rv[4], acc[4]), __fadd_rn(rv[5], acc[5]));
-        o.w = pack2(__fadd_rn(rv[6], acc[6]), __fadd_rn(rv[7], acc[7]));
-        *reinterpret_cast<uint4*>(out + t * d + c) = o;
+#pragma unroll
+        for (int u = 0; u < kRowGroup; ++u) {
+            const int i = g + u * kRowThreads + threadIdx.x;
+            if (i >= n8) continue;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+                if (j >= k) break;
+                const uint32_t yw[4] = {yq[u][j].x, yq[u][j].y, yq[u][j].z, yq[u][j].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[2 * q] = fmaf(w[j], bf2f(static_cast<uint16_t>(yw[q] & 0xffffu)), acc[2 * q]);
+                    acc[2 * q + 1] = fmaf(w[j], bf2f(static_cast<uint16_t>(yw[q] >> 16)), acc[2 * q + 1]);
+                }
+            }
+            const uint32_t rw[4] = {rq[u].x, rq[u].y, rq[u].z, rq[u].w};
+            float rv[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                rv[2 * q] = bf2f(static_cast<uint16_t>(rw[q] & 0xffffu));
+                rv[2 * q + 1] = bf2f(static_cast<uint16_t>(rw[q] >> 16));
+            }
+            uint4 o;
+            o.x = pack2(__fadd_rn(rv[0], acc[0]), __fadd_rn(rv[1], acc[1]));
+            o.y = pack2(__fadd_rn(rv[2], acc[2]), __fadd_rn(rv[3], acc[3]));
+            o.z = pack2(__fadd_rn(rv[4], acc[4]), __fadd_rn(rv[5], acc[5]));
+            o.w = pack2(__fadd_rn(rv[6], acc[6]), __fadd_rn(rv[7], acc[7]));
+            *reinterpret_cast<uint4*>(out + t * d + i * 8) = o;
+        }
     }
 }
 
@@ -719,6 +788,8 @@ extern "C" int64_t kl_permute_workspace_bytes(int64_t R, int E) {
     return (chunks * E + R) * static_cast<int64_t>(sizeof(int32_t)) + 256;
 }
 
+extern "C" int kl_permute_launches(int64_t R) { return R == 0 ? 1 : (R <= kChunk ? 2 : 3); }
+
 extern "C" int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uint16_t* x2, int d, int32_t* counts,
                           int32_t* offsets, int32_t* pos, int32_t* row_token, uint16_t* xp, void* workspace,
                           cudaStream_t stream) {
@@ -729,23 +800,29 @@ extern "C" int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uin
     int32_t* chunk_counts = static_cast<int32_t*>(workspace);
     int32_t* local_rank = chunk_counts + chunks * E;
     if (R > 0) {
-        permute_rank_kernel<<<static_cast<int>(chunks), kChunk, 0, stream>>>(idx, R, E, chunk_counts, local_rank);
+        // One chunk: rank + scan in a single launch.
+        permute_rank_kernel<<<static_cast<int>(chunks), kChunk, 0, stream>>>(
+            idx, R, E, chunk_counts, local_rank, chunks == 1 ? counts : nullptr, chunks == 1 ? offsets : nullptr);
         KL_CUDA_TRY(cudaGetLastError());
     }
-    permute_scan_kernel<<<1, 64, 0, stream>>>(chunk_counts, chunks, E, counts, offsets);
-    KL_CUDA_TRY(cudaGetLastError());
+    if (chunks != 1) {
+        permute_scan_kernel<<<1, 64, 0, stream>>>(chunk_counts, chunks, E, counts, offsets);
+        KL_CUDA_TRY(cudaGetLastError());
+    }
     if (R == 0) return KL_OK;
-    permute_scatter_kernel<<<grid_for(R, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(
-        idx, R, k, E, chunk_counts, local_rank, x2, d, pos, row_token, xp);
+    permute_scatter_kernel<<<static_cast<unsigned>(R), kRowThreads, 0, stream>>>(idx, R, k, E, chunk_counts,
+                                                                                local_rank, x2, d, pos, row_token, xp);
     return check_launch();
 }
 
 extern "C" int kl_combine(const uint16_t* y, const int32_t* pos, const float* weight, const uint16_t* resid, int64_t T,
                           int k, int d, uint16_t* out, cudaStream_t stream) {
-    if (T < 0 || k < 1 || k > 8 || d % 256 != 0 || !y || !pos || !weight || !resid || !out) return KL_EINVAL;
+    if (T < 0 || k < 1 || k > 8 || d % 8 != 0 || !y || !pos || !weight || !resid || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    combine_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(y, pos, weight, resid, T, k, d,
-                                                                                    out);
+    if (k <= 2)
+        combine_kernel<2><<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(y, pos, weight, resid, T, k, d, out);
+    else
+        combine_kernel<8><<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(y, pos, weight, resid, T, k, d, out);
     return check_launch();
 }
 

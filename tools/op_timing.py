@@ -69,6 +69,21 @@ def main():
             sel = [d for d, t in ex if lo < t <= hi]
             if sel:
                 print(f"  rows ({lo},{hi}]: n={len(sel)} mean {np.mean(sel):.1f} us")
+    # Expert ops split by whether they waited for their load: gap to the
+    # previous compute-stream op's end (small = weights were already there).
+    comp = sorted([r for r in rows if r["stream"] == "compute"], key=lambda r: int(r["start_ps"]))
+    waited, ready = [], []
+    for prev, r in zip(comp, comp[1:]):
+        if r["kind"] != "compute_expert":
+            continue
+        gap = (int(r["start_ps"]) - int(prev["end_ps"])) / 1e6
+        dur = (int(r["end_ps"]) - int(r["start_ps"])) / 1e6
+        (waited if gap > 5.0 else ready).append((dur, gap, prev["kind"]))
+    for name, v in (("waited for load", waited), ("load already done", ready)):
+        if v:
+            d = np.array([x[0] for x in v])
+            print(f"  {name:18s} n={len(d):4d} dur mean {d.mean():.1f} med {np.median(d):.1f} us;"
+                  f" gap med {np.median([x[1] for x in v]):.1f} us")
     diag = eng.report("diag").get("expert_op_us", [])
     if diag:
         a = np.array(diag)

@@ -251,14 +251,27 @@ def main():
         nw = torch.ones(d, dtype=bf, device=dev)
         wg = torch.randn(E, d, dtype=bf, device=dev) * 0.02
         x2 = torch.empty_like(h)
-        t = timed(lambda i: K.gate_topk(h[:bs], nw, wg, k, x2=x2[:bs]), args.iters, st)
+        t = timed_graph(lambda i: K.gate_topk(h[:bs], nw, wg, k, x2=x2[:bs]), args.iters)
         res["gate_topk_b64"] = {"us": t * 1e6}
         _, idx, wt = K.gate_topk(h, nw, wg, k, x2=x2)
-        t = timed(lambda i: K.permute(idx, E, x2=x2), args.iters, st)
+        t = timed_graph(lambda i: K.permute(idx, E, x2=x2), args.iters)
         res["permute_T512"] = {"us": t * 1e6, "GBs": (T * d * 2 + T * k * d * 2) / t / 1e9}
         _, _, p, _, xp = K.permute(idx, E, x2=x2)
-        t = timed(lambda i: K.combine(xp, p, wt, h, out=x2), args.iters, st)
+        t = timed_graph(lambda i: K.combine(xp, p, wt, h, out=x2), args.iters)
         res["combine_T512"] = {"us": t * 1e6, "GBs": (k * T * d * 2 + 2 * T * d * 2) / t / 1e9}
+        t = timed_graph(lambda i: K.rmsnorm(h[:bs], nw, out=x2[:bs]), args.iters)
+        res["rmsnorm_b64"] = {"us": t * 1e6, "GBs": 2 * bs * d * 2 / t / 1e9}
+        # prefill-sized group: bs 32 x n 8 x 512 tokens
+        TP = 32 * 8 * 512
+        hp = torch.randn(TP, d, dtype=bf, device=dev)
+        x2p = torch.empty_like(hp)
+        _, idxp, wtp = K.gate_topk(hp, nw, wg, k, x2=x2p)
+        t = timed(lambda i: K.permute(idxp, E, x2=x2p), max(2, args.iters // 4), st)
+        res["permute_T131072"] = {"us": t * 1e6, "GBs": (TP * d * 2 + TP * k * d * 2) / t / 1e9}
+        _, _, pp, _, xpp = K.permute(idxp, E, x2=x2p)
+        t = timed(lambda i: K.combine(xpp, pp, wtp, hp, out=x2p), max(2, args.iters // 4), st)
+        res["combine_T131072"] = {"us": t * 1e6, "GBs": (k * TP * d * 2 + 2 * TP * d * 2) / t / 1e9}
+        del hp, x2p, xpp
     print(json.dumps(res, indent=1))
     if args.json:
         with open(args.json, "w") as fh:
