@@ -167,7 +167,12 @@ def ffn_isolated(torch, dev, D, M, iters=20):
     d, f = D["d"], D["f"]
     ws = [torch.empty(3 * d * f, dtype=torch.bfloat16, device=dev) for _ in range(8)]
     for i, w in enumerate(ws):
-        K.fill_normal(w, 1000 + i, 0.02)
+        # the engine's expert format: K-blocked W13 [2f, d] and W2 [d, f]
+        raw = torch.empty(3 * d * f, dtype=torch.bfloat16, device=dev)
+        K.fill_normal(raw, 1000 + i, 0.02)
+        w[: 2 * f * d].view(2 * f, d).copy_(K.weights_kblock(raw[: 2 * f * d].view(2 * f, d)))
+        w[2 * f * d:].view(d, f).copy_(K.weights_kblock(raw[2 * f * d:].view(d, f)))
+        del raw
     xp = torch.empty(max(M, 1) * 8, d, dtype=torch.bfloat16, device=dev)
     K.fill_normal(xp, 999, 1.0)
     y = torch.empty_like(xp)
@@ -175,7 +180,7 @@ def ffn_isolated(torch, dev, D, M, iters=20):
 
     def run(i):
         w = ws[i % 8]
-        K.expert_ffn(xp, (i % 8) * M, M, w[: 2 * f * d].view(2 * f, d), w[2 * f * d:].view(d, f), y, h)
+        K.expert_ffn(xp, (i % 8) * M, M, w[: 2 * f * d].view(2 * f, d), w[2 * f * d:].view(d, f), y, h, kblocked=True)
     for i in range(4):
         run(i)
     torch.cuda.synchronize()

@@ -102,6 +102,25 @@ int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row_offset, in
                   int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
                   uint16_t* y, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
+/* K-blocked weights (the engine's expert storage format for bf16). A
+ * row-major [rows, cols] bf16 matrix stored as cols/64 slabs, slab j holding
+ * columns [64j, 64j+64) of every row, row-major inside the slab:
+ *   kb[(j*rows + r)*64 + c] = w[r*cols + 64j + c]
+ * Same bytes as row-major; a 128-row x 64-column weight tile is one
+ * contiguous 16 KB run, so the weight stream reads HBM in long runs instead
+ * of 128-byte pieces 2*cols bytes apart (tools/tma_pattern_probe.cu: 6.34 vs
+ * 5.60 TB/s). Results are bit-identical to the row-major entry points.
+ *   kl_weights_kblock: convert (src != dst, cols % 64 == 0, 16 B aligned).
+ *   kl_gemm_bf16_kb / kl_expert_ffn_kb: as kl_gemm_bf16 / kl_expert_ffn with
+ *   b (w13 = [W1; W3] as one [2f, d] matrix, w2 = [d, f]) K-blocked. */
+int kl_weights_kblock(const uint16_t* src, int64_t rows, int64_t cols, uint16_t* dst, cudaStream_t stream);
+int kl_gemm_bf16_kb(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                    const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
+                    int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+int kl_expert_ffn_kb(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
+                     int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
+                     uint16_t* y, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+
 /* ---- 4-bit expert streaming ----
  * Q4T layout: the reference's HQQ format (quant.cpp:197-252: 4-bit codes,
  * groups of 64 along K, fp16 scale and zero, w = scale * (code - zero))

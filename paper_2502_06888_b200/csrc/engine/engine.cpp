@@ -128,6 +128,11 @@ EngineConfig parse_config(const std::string& text) {
     c.disk_dir = j.value("disk_dir", std::string());
     c.expert_slots = j.value("expert_slots", 0);
     c.ffn_chunk_rows = j.value("ffn_chunk_rows", 4096);
+    {
+        const std::string lay = j.value("expert_layout", std::string("kblocked"));
+        if (lay != "kblocked" && lay != "row") throw ConfigError("engine: expert_layout must be 'kblocked' or 'row'");
+        c.kblocked_experts = lay == "kblocked";
+    }
     c.record_trace = j.value("record_trace", true);
     c.record_hidden = j.value("record_hidden", false);
     if (j.contains("ep")) {
@@ -651,10 +656,25 @@ void Engine::init_weights() {
     // 17.4M gate elements vs 16.8M attention): it is staged in its own slot.
     uint16_t* gate_stage = gate_slot_[0];
     uint8_t* qstage = reinterpret_cast<uint8_t*>(pool_.ptr[0]);
+    // bf16 experts are stored K-blocked (kl_weights_kblock: each 128-row x
+    // 64-column weight tile one contiguous 16 KB run for the streaming GEMM);
+    // converted from the row-major stage into a second pool slot.
+    const bool kb = expert_kblocked();
+    uint16_t* kb_stage = pool_.ptr[slots_ > 1 ? 1 : 0];
+    if (kb && kb_stage == stage) throw AccountingError("engine: no second slot to stage K-blocked experts");
+    auto kblock_expert = [&](const uint16_t* src, uint16_t* dst) {
+        kl_check(kl_weights_kblock(src, 2LL * D_.f, D_.d, dst, st), "kblock w13");
+        kl_check(kl_weights_kblock(src + 2LL * D_.f * D_.d, D_.d, D_.f, dst + 2LL * D_.f * D_.d, st), "kblock w2");
+    };
     // bf16 stage -> host copy in the streamed format.
     auto to_host = [&](void* host, bool expert) {
         if (!cfg_.quant) {
-            cuda_check(cudaMemcpyAsync(host, stage, expert ? spec_.expert_bytes : spec_.attention_bytes,
+            const uint16_t* src = stage;
+            if (expert && kb) {
+                kblock_expert(stage, kb_stage);
+                src = kb_stage;
+            }
+            cuda_check(cudaMemcpyAsync(host, src, expert ? spec_.expert_bytes : spec_.attention_bytes,
                                        cudaMemcpyDeviceToHost, st), "d2h");
             return;
         }
@@ -682,7 +702,12 @@ void Engine::init_weights() {
             // same weights the single-GPU engine would.
             const std::uint64_t seed = tensor_seed(ws, kKindExpert, l, ep_ ? e * G_ + rank_ : e);
             if (uint16_t* r = res_expert_[l * El_ + e]) {
-                kl_check(kl_fill_normal_bf16(r, D_.expert_elems(), seed, sd, st), "init expert");
+                if (kb) {
+                    kl_check(kl_fill_normal_bf16(stage, D_.expert_elems(), seed, sd, st), "init expert");
+                    kblock_expert(stage, r);
+                } else {
+                    kl_check(kl_fill_normal_bf16(r, D_.expert_elems(), seed, sd, st), "init expert");
+                }
                 if (uint16_t* h = host_expert_[l * El_ + e]) {
                     if (cfg_.quant) {
                         cuda_check(cudaMemcpyAsync(stage, r, spec_.expert_bytes, cudaMemcpyDeviceToDevice, st), "d2d");
@@ -816,6 +841,7 @@ std::string Engine::describe() const {
     j["expert_stream_bytes"] = expert_slot_bytes_;
     j["attention_stream_bytes"] = attn_slot_bytes_;
     j["quant_bits"] = cfg_.quant ? cfg_.quant->bits : 16;
+    j["expert_layout"] = expert_kblocked() ? "kblocked" : (cfg_.quant ? "q4t" : "row");
     j["gate_bytes"] = spec_.gate_bytes;
     j["shared_experts"] = {{"n", D_.n_shared}, {"f", D_.f_shared}};
     j["host_pinned_blocks"] = host_blocks_.size();

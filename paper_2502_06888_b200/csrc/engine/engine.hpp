@@ -77,6 +77,7 @@ struct EngineConfig {
     int host_distinct_layers = 0;
     int expert_slots = 0;
     int ffn_chunk_rows = 4096;
+    bool kblocked_experts = true;  // bf16 experts stored K-blocked (kl_weights_kblock); Q4T keeps its own tiles
     bool record_trace = true;
     bool record_hidden = false;
     int ep_rank = 0, ep_world = 1;
@@ -135,6 +136,7 @@ class Engine {
   private:
     // setup
     void plan_memory();
+    bool expert_kblocked() const { return cfg_.kblocked_experts && !cfg_.quant; }
     bool plan_at(int n, bool rethrow = false);
     void finish_plan();
     moesim::TraceStats stats_;

@@ -872,6 +872,9 @@ void Engine::exec_expert(const StreamOp& op) {
         if (q4 && M <= 256)
             kl_check(kl_expert_ffn_q4(xp_, block_rows_, row0 + c, m, D_.d, D_.f, q13, q2, hs_, y_, gemm_ws_,
                                       gemm_ws_bytes_, cs), "expert ffn q4");
+        else if (expert_kblocked())  // bf16 experts (resident or streamed) are stored K-blocked
+            kl_check(kl_expert_ffn_kb(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
+                                      gemm_ws_bytes_, cs), "expert ffn");
         else
             kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
                                    gemm_ws_bytes_, cs), "expert ffn");

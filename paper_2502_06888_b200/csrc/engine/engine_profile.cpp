@@ -179,8 +179,9 @@ MeasuredProfile measure_profile(const EngineConfig& cfg, const std::string& phas
     });
     out.expert_ms = time_ms(st, 2, prefill ? 3 : 20, [&] {
         for (int c = 0; c < M; c += chunk)
-            kl_check(kl_expert_ffn(xp, M, c, std::min(chunk, M - c), D.d, D.f, wexp, wexp + 2LL * D.f * D.d, hs, y, ws,
-                                   ws_bytes, st), "expert ffn");
+            kl_check((cfg.kblocked_experts && !cfg.quant ? kl_expert_ffn_kb : kl_expert_ffn)(
+                         xp, M, c, std::min(chunk, M - c), D.d, D.f, wexp, wexp + 2LL * D.f * D.d, hs, y, ws, ws_bytes,
+                         st), "expert ffn");
     });
 
     // Pinned H2D on one and on two concurrent copy streams.

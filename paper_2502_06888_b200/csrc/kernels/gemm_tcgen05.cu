@@ -110,11 +110,14 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
                 uint8_t* sb = sa + C::kABytes;
                 mbar_arrive_expect_tx(&full[s], C::kStageBytes);
                 tma_load_2d(sa, &tmap_a, &full[s], kc, a_row);
+                // Weights through a 3D (64, rows, k-blocks) view: the same
+                // smem image for row-major and K-blocked weight layouts.
                 if constexpr (PAIRED) {
-                    tma_load_2d(sb, &tmap_b, &full[s], kc, n_tile * (BN / 2));
-                    tma_load_2d(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], kc, b_half_rows + n_tile * (BN / 2));
+                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * (BN / 2), kc / BK, 0, false);
+                    tma_load_3d_k(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], b_half_rows + n_tile * (BN / 2), kc / BK, 0,
+                                  false);
                 } else {
-                    tma_load_2d(sb, &tmap_b, &full[s], kc, n_tile * BN);
+                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * BN, kc / BK, 0, false);
                 }
             }
         }
@@ -282,10 +285,11 @@ gemm_persistent_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid
                     mbar_arrive_expect_tx(&full[s], C::kStageBytes);
                     tma_load_2d(sa, &tmap_a, &full[s], kb * BK, a_row);
                     if constexpr (PAIRED) {
-                        tma_load_2d(sb, &tmap_b, &full[s], kb * BK, n_tile * (BN / 2));
-                        tma_load_2d(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], kb * BK, b_half_rows + n_tile * (BN / 2));
+                        tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * (BN / 2), kb, 0, false);
+                        tma_load_3d_k(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], b_half_rows + n_tile * (BN / 2), kb, 0,
+                                      false);
                     } else {
-                        tma_load_2d(sb, &tmap_b, &full[s], kb * BK, n_tile * BN);
+                        tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * BN, kb, 0, false);
                     }
                 }
             }
@@ -502,23 +506,6 @@ __device__ __forceinline__ int range_begin(int c, int units, int G) {
     return static_cast<int>(static_cast<int64_t>(c) * units / G);
 }
 
-// 3D tile load: box (64 columns, rows, k-chunks) of a [rows][K] matrix viewed
-// as (64, rows, K/64); lands as k-chunk slabs of [rows][64] 128B-swizzled.
-__device__ __forceinline__ void tma_load_3d_k(void* dst, const CUtensorMap* map, uint64_t* bar, int row, int kchunk,
-                                              uint64_t policy, bool hint) {
-    if (hint)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-            " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-            "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(row), "r"(kchunk), "l"(policy)
-            : "memory");
-    else
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-            "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(row), "r"(kchunk)
-            : "memory");
-}
 
 // 1D bulk copy global -> shared (async proxy), completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -639,12 +626,10 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                         if constexpr (Q4) {
                             const uint8_t* src = p.q4 + (static_cast<int64_t>(row / kWRows) * KB + kb) * kQ4Chunk;
                             bulk_g2s(raw + s * kRawStage + j * kQ4Chunk, src, kQ4Chunk, &raw_full[s]);
-                        } else if (p.ks > 1) {
-                            tma_load_3d_k(sw + j * wbytes, &tmap_w, &full[s], row, kb * p.ks, pol_w, hint);
-                        } else if (hint) {
-                            tma_load_2d_hint(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row, pol_w);
                         } else {
-                            tma_load_2d(sw + j * kWTileBytes, &tmap_w, &full[s], kb * BK, row);
+                            // 3D (64, rows, k-blocks) view of the weights, p.ks
+                            // k-blocks per box: row-major or K-blocked layout.
+                            tma_load_3d_k(sw + j * wbytes, &tmap_w, &full[s], row, kb * p.ks, pol_w, hint);
                         }
                     }
                     if (waited) {
@@ -982,7 +967,14 @@ struct Launch {
     int splits;
     float* ws;
     int ws_ld;
+    bool b_kblocked = false;  // weights in the K-blocked layout (make_map_kblocked)
 };
+
+// Weight (B operand) map: a 3D (64, rows, k-blocks) view, one k-block per box.
+inline int make_weight_map(CUtensorMap* m, const Launch& L, int box_rows) {
+    return L.b_kblocked ? make_map_kblocked(m, L.b, L.b_rows, L.K, box_rows, 1)
+                        : make_map_kchunks(m, L.b, L.b_rows, L.K, box_rows, 1);
+}
 
 template <int BN, int EPI, bool PAIRED, int STAGES>
 int launch(const Launch& L, cudaStream_t stream) {
@@ -990,7 +982,7 @@ int launch(const Launch& L, cudaStream_t stream) {
     CUtensorMap ma, mb;
     int rc = make_map(&ma, L.a, L.a_rows, L.K, BM);
     if (rc) return rc;
-    rc = make_map(&mb, L.b, L.b_rows, L.K, PAIRED ? BN / 2 : BN);
+    rc = make_weight_map(&mb, L, PAIRED ? BN / 2 : BN);
     if (rc) return rc;
     static bool configured = false;  // per template instance
     if (!configured) {
@@ -1014,7 +1006,7 @@ int launch_persistent(const Launch& L, cudaStream_t stream) {
     CUtensorMap ma, mb;
     int rc = make_map(&ma, L.a, L.a_rows, L.K, BM);
     if (rc) return rc;
-    rc = make_map(&mb, L.b, L.b_rows, L.K, PAIRED ? BN / 2 : BN);
+    rc = make_weight_map(&mb, L, PAIRED ? BN / 2 : BN);
     if (rc) return rc;
     static bool configured = false;
     if (!configured) {
@@ -1118,7 +1110,7 @@ int stream_grid(int N, int K, int epilogue) {
 template <int EPI, int NMMA, bool Q4 = false>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
                   int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
-                  cudaStream_t stream, const uint8_t* q4 = nullptr) {
+                  cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false) {
     StreamArgs p{};
     p.M = M;
     p.NP = stream_np(M);
@@ -1169,7 +1161,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     if (rc) return rc;
     if (Q4)
         mw = mx;  // unused: the Q4 variant bulk-copies packed tiles
-    else if ((rc = p.ks > 1 ? make_map_kchunks(&mw, b, b_rows, K, kWRows, p.ks) : make_map(&mw, b, b_rows, K, kWRows)))
+    else if ((rc = wkb ? make_map_kblocked(&mw, b, b_rows, K, kWRows, p.ks) : make_map_kchunks(&mw, b, b_rows, K, kWRows, p.ks)))
         return rc;
     const int smem = p.stages * per_stage + 1024 + 1024;  // rings + alignment + barriers
     static bool configured = false;  // per template instance
@@ -1193,21 +1185,22 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
 }
 
 int gemm_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int N,
-                uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+                uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                bool wkb) {
     const int nmma = stream_nmma(N, epilogue);
     if (epilogue == kSwiGLU)
         return launch_stream<kSwiGLU, 2>(a, a_rows, row_offset, M, K, b, N, N / 2 / kWRows, N / 2, c, ldc, r, ws,
-                                         ws_bytes, stream);
+                                         ws_bytes, stream, nullptr, wkb);
     const int n_tiles = N / (kWRows * nmma);
     if (epilogue == kResidual)
         return nmma == 2 ? launch_stream<kResidual, 2>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws,
-                                                       ws_bytes, stream)
+                                                       ws_bytes, stream, nullptr, wkb)
                          : launch_stream<kResidual, 1>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws,
-                                                       ws_bytes, stream);
+                                                       ws_bytes, stream, nullptr, wkb);
     return nmma == 2 ? launch_stream<kStore, 2>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws, ws_bytes,
-                                                stream)
+                                                stream, nullptr, wkb)
                      : launch_stream<kStore, 1>(a, a_rows, row_offset, M, K, b, N, n_tiles, 0, c, ldc, r, ws, ws_bytes,
-                                                stream);
+                                                stream, nullptr, wkb);
 }
 
 }  // namespace
@@ -1271,10 +1264,12 @@ extern "C" int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
     return s > 1 ? static_cast<int64_t>(s) * M * N * 4 : 0;
 }
 
-extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b,
-                            int N, uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace,
-                            int64_t workspace_bytes, cudaStream_t stream) {
-    using namespace kl;
+namespace kl {
+namespace {
+// kl_gemm_bf16 / kl_gemm_bf16_kb: b row-major [N, K] or K-blocked (wkb).
+int gemm_bf16_impl(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int N,
+                   uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace, int64_t workspace_bytes,
+                   cudaStream_t stream, bool wkb) {
     if (M < 0 || K <= 0 || N <= 0 || a == nullptr || b == nullptr || c == nullptr) return KL_EINVAL;
     if (M == 0) return KL_OK;
     if (K % BK != 0 || N % 64 != 0 || !aligned16(a) || !aligned16(b) || !aligned16(c) || ldc % 8 != 0)
@@ -1287,12 +1282,12 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
     if (workspace != nullptr && stream_eligible(M, N, K, epilogue) &&
         workspace_bytes >= kFlagBytes + stream_slot_bytes(M, stream_nmma(N, epilogue))) {
         const int rc = gemm_stream(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes,
-                                   stream);
+                                   stream, wkb);
         if (rc != KL_EUNSUPPORTED) return rc;
     }
     const int m_tiles = (M + BM - 1) / BM;
     const int kb = K / BK;
-    Launch L{a, a_rows, row_offset, M, K, b, N, 0, 0, c, ldc, r, 1, static_cast<float*>(workspace), N};
+    Launch L{a, a_rows, row_offset, M, K, b, N, 0, 0, c, ldc, r, 1, static_cast<float*>(workspace), N, wkb};
     const bool small_m = m_tiles <= 2 && N % 128 == 0;  // weight-streaming regime (decode)
     if (small_m) {
         // 128-wide tiles (activation:weight smem traffic 1:1), 2 CTAs per SM,
@@ -1331,6 +1326,22 @@ extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offse
     }
     L.n_tiles = N / 64;
     return epilogue == kResidual ? launch<64, kResidual, false, 6>(L, stream) : launch<64, kStore, false, 6>(L, stream);
+}
+}  // namespace
+}  // namespace kl
+
+extern "C" int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b,
+                            int N, uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace,
+                            int64_t workspace_bytes, cudaStream_t stream) {
+    return kl::gemm_bf16_impl(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes, stream,
+                              false);
+}
+
+extern "C" int kl_gemm_bf16_kb(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b,
+                               int N, uint16_t* c, int ldc, const uint16_t* r, int epilogue, void* workspace,
+                               int64_t workspace_bytes, cudaStream_t stream) {
+    return kl::gemm_bf16_impl(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes, stream,
+                              true);
 }
 
 extern "C" int kl_gemm_q4(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint8_t* bq,
@@ -1388,4 +1399,43 @@ extern "C" int kl_expert_ffn(const uint16_t* xp, int64_t rows_total, int64_t row
     if (rc) return rc;
     return kl_gemm_bf16(h_scratch, M, 0, M, f, w2, d, y + row_offset * d, d, nullptr, 0, workspace, workspace_bytes,
                         stream);
+}
+
+extern "C" int kl_expert_ffn_kb(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d, int f,
+                                const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch, uint16_t* y,
+                                void* workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    if (M == 0) return KL_OK;
+    if (y == nullptr || h_scratch == nullptr) return KL_EINVAL;
+    int rc = kl_gemm_bf16_kb(xp, rows_total, row_offset, M, d, w13, 2 * f, h_scratch, f, nullptr, 2, workspace,
+                             workspace_bytes, stream);
+    if (rc) return rc;
+    return kl_gemm_bf16_kb(h_scratch, M, 0, M, f, w2, d, y + row_offset * d, d, nullptr, 0, workspace, workspace_bytes,
+                           stream);
+}
+
+namespace kl {
+namespace {
+// Row-major [rows, cols] -> K-blocked (cols/64 slabs of [rows][64]); one
+// 16-byte vector per thread.
+__global__ void kblock_kernel(const uint4* __restrict__ src, int64_t rows, int64_t cols, uint4* __restrict__ dst) {
+    const int64_t n16 = rows * cols / 8;
+    const int64_t cpr = cols / 8;  // 16-byte vectors per source row
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = i / cpr, v = i % cpr;  // v: 16-byte vector within the row
+        const int64_t slab = v / 8, within = v % 8;
+        dst[(slab * rows + row) * 8 + within] = src[i];
+    }
+}
+}  // namespace
+}  // namespace kl
+
+extern "C" int kl_weights_kblock(const uint16_t* src, int64_t rows, int64_t cols, uint16_t* dst, cudaStream_t stream) {
+    using namespace kl;
+    if (src == nullptr || dst == nullptr || rows <= 0 || cols <= 0 || cols % 64 != 0 || src == dst) return KL_EINVAL;
+    if (!aligned16(src) || !aligned16(dst)) return KL_EINVAL;
+    const int64_t n16 = rows * cols / 8;
+    const int grid = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 148LL * 16));
+    kblock_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4*>(src), rows, cols, reinterpret_cast<uint4*>(dst));
+    return check_launch();
 }

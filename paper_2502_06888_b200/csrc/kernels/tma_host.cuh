@@ -41,8 +41,10 @@ struct MapKey {
     const void* base;
     int64_t rows, cols;
     int box_rows, kchunks;
+    int layout = 0;  // 0 = row-major [rows][cols], 1 = K-blocked (see make_map_kblocked)
     bool operator==(const MapKey& o) const {
-        return base == o.base && rows == o.rows && cols == o.cols && box_rows == o.box_rows && kchunks == o.kchunks;
+        return base == o.base && rows == o.rows && cols == o.cols && box_rows == o.box_rows && kchunks == o.kchunks &&
+               layout == o.layout;
     }
 };
 // Direct-mapped, 1024 entries, guarded by a mutex (launch paths may run on
@@ -57,7 +59,8 @@ inline bool map_cache_op(const MapKey& k, CUtensorMap* m, bool put) {
     static std::mutex mu;
     const uint64_t h = (reinterpret_cast<uint64_t>(k.base) >> 8) * 0x9E3779B97F4A7C15ull ^
                        static_cast<uint64_t>(k.rows) * 0xC2B2AE3D27D4EB4Full ^ static_cast<uint64_t>(k.cols) * 31u ^
-                       static_cast<uint64_t>(k.box_rows) * 131u ^ static_cast<uint64_t>(k.kchunks) * 7u;
+                       static_cast<uint64_t>(k.box_rows) * 131u ^ static_cast<uint64_t>(k.kchunks) * 7u ^
+                       static_cast<uint64_t>(k.layout) * 0x51ED27u;
     Entry& e = table[(h >> 32) & 1023];
     std::lock_guard<std::mutex> lock(mu);
     if (put) {
@@ -105,6 +108,34 @@ inline int make_map_kchunks(CUtensorMap* map, const void* base, int64_t rows, in
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTmaBoxK), static_cast<cuuint64_t>(rows),
                                 static_cast<cuuint64_t>(cols / kTmaBoxK)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, static_cast<cuuint64_t>(kTmaBoxK) * 2};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kTmaBoxK), static_cast<cuuint32_t>(box_rows),
+                               static_cast<cuuint32_t>(kchunks)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return KL_EINVAL;
+    map_cache_put(key, map);
+    return 0;
+}
+
+// K-blocked bf16 weights ("KB" layout, kl_weights_kblock): the [rows, cols]
+// matrix stored as cols/64 slabs, slab j = columns [64j, 64j+64) of every row,
+// row-major inside the slab (128 bytes per row). Viewed as (64, rows, cols/64)
+// with strides (128 B, rows*128 B), a box of box_rows x 64 x kchunks is
+// kchunks contiguous runs of box_rows*128 bytes (16 KB for a 128-row weight
+// tile) instead of box_rows strided 128-byte pieces, and lands in shared
+// memory exactly like the row-major box (same 128B swizzle).
+inline int make_map_kblocked(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows,
+                             int kchunks) {
+    MapKey key{base, rows, cols, box_rows, kchunks};
+    key.layout = 1;
+    if (map_cache_get(key, map)) return 0;
+    EncodeFn enc = encoder();
+    if (enc == nullptr) return KL_ENODEV;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTmaBoxK), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(cols / kTmaBoxK)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kTmaBoxK) * 2, static_cast<cuuint64_t>(rows) * kTmaBoxK * 2};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(kTmaBoxK), static_cast<cuuint32_t>(box_rows),
                                static_cast<cuuint32_t>(kchunks)};
     const cuuint32_t estr[3] = {1, 1, 1};

@@ -31,6 +31,9 @@ _lib.kl_error_string.argtypes = [_I]
 _gemm = _sig("kl_gemm_bf16", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P, _L, _P])
 _gemm_ws = _sig("kl_gemm_workspace_bytes", [_I, _I, _I, _I], C.c_int64)
 _ffn = _sig("kl_expert_ffn", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P, _L, _P])
+_ffn_kb = _sig("kl_expert_ffn_kb", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _P, _L, _P])
+_gemm_kb = _sig("kl_gemm_bf16_kb", [_P, _L, _L, _I, _I, _P, _I, _P, _I, _P, _I, _P, _L, _P])
+_kblock = _sig("kl_weights_kblock", [_P, _L, _L, _P, _P])
 _gate = _sig("kl_gate_topk", [_P, _P, _P, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P, _P])
 _perm_ws = _sig("kl_permute_workspace_bytes", [_L, _I], C.c_int64)
 _perm = _sig("kl_permute", [_P, _L, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P])
@@ -111,8 +114,19 @@ def workspace_bytes(M, N, K, epilogue=0):
     return int(_gemm_ws(M, N, K, epilogue))
 
 
-def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None, split_k=True, ws_bytes=None):
-    """C = A[row_offset:row_offset+m] @ B^T (bf16, fp32 accumulate) on tcgen05."""
+def weights_kblock(w, stream=None):
+    """Row-major bf16 [rows, cols] -> the K-blocked layout (kl_weights_kblock);
+    returned with the same shape (the bytes are reordered, not the meaning)."""
+    rows, cols = w.shape
+    out = torch.empty_like(w)
+    _chk(_kblock(_p(w), rows, cols, _p(out), _s(stream)), "kl_weights_kblock")
+    return out
+
+
+def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=None, split_k=True, ws_bytes=None,
+         kblocked=False):
+    """C = A[row_offset:row_offset+m] @ B^T (bf16, fp32 accumulate) on tcgen05.
+    kblocked: b holds the K-blocked layout of the [N, K] weights."""
     m = a.shape[0] - row_offset if m is None else m
     K = a.shape[1]
     N = b.shape[0]
@@ -123,18 +137,22 @@ def gemm(a, b, c=None, residual=None, epilogue=0, row_offset=0, m=None, stream=N
     if ws_bytes is not None and split_k:
         wsb = int(ws_bytes)
     ws = workspace(wsb, a.device) if wsb else None
-    _chk(_gemm(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue, _p(ws),
-               wsb, _s(stream)), "kl_gemm_bf16")
+    fn = _gemm_kb if kblocked else _gemm
+    _chk(fn(_p(a), a.shape[0], row_offset, m, K, _p(b), N, _p(c), c.stride(0), _p(residual), epilogue, _p(ws),
+            wsb, _s(stream)), "kl_gemm_bf16_kb" if kblocked else "kl_gemm_bf16")
     return c
 
 
-def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None, split_k=True):
+def expert_ffn(xp, row_offset, m, w13, w2, y, h_scratch, stream=None, split_k=True, kblocked=False):
+    """One expert's SwiGLU FFN (kl_expert_ffn); kblocked: w13 [2f, d] and
+    w2 [d, f] hold the K-blocked layout (kl_expert_ffn_kb)."""
     d = xp.shape[1]
     f = w2.shape[1]
     wsb = max(workspace_bytes(m, 2 * f, d, 2), workspace_bytes(m, d, f, 0)) if split_k else 0
     ws = workspace(wsb, xp.device) if wsb else None
-    _chk(_ffn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _p(ws), wsb,
-              _s(stream)), "kl_expert_ffn")
+    fn = _ffn_kb if kblocked else _ffn
+    _chk(fn(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y), _p(ws), wsb,
+            _s(stream)), "kl_expert_ffn_kb" if kblocked else "kl_expert_ffn")
 
 
 def q4_bytes(rows, K):

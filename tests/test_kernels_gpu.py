@@ -171,6 +171,54 @@ def test_expert_ffn(K, cuda, M, d, f):
     assert not to_bits(y)[:off].any() and not to_bits(y)[off + M:].any()
 
 
+def kblock_np(w):
+    """K-blocked layout restated: slab j = columns [64j, 64j+64) of every row."""
+    rows, cols = w.shape
+    return np.ascontiguousarray(w.reshape(rows, cols // 64, 64).transpose(1, 0, 2)).reshape(rows, cols)
+
+
+def test_weights_kblock_layout(K, cuda):
+    w = orc.normal_bf16(384 * 448, 41, 1.0).reshape(384, 448)
+    got = to_bits(K.weights_kblock(to_dev(w, cuda)))
+    assert np.array_equal(got, kblock_np(w))
+
+
+@pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (64, 4096, 4096, 1), (128, 28672, 4096, 2),
+                                         (128, 4096, 14336, 0), (200, 1024, 2048, 2), (300, 512, 1024, 1),
+                                         (700, 2048, 1024, 0), (2048, 4096, 512, 2), (2600, 2560, 256, 1),
+                                         (640, 320, 256, 0)])
+def test_gemm_kblocked_bit_identical(K, cuda, M, N, Kd, epi):
+    """kl_gemm_bf16_kb on K-blocked weights == kl_gemm_bf16 on the row-major
+    weights, bitwise, through every kernel family the shape selects (weight
+    streaming for M <= 256 with >= 40 MB or > 128 rows, one tile per CTA with
+    split-K, persistent for large M, 64-wide tiles for N % 256 != 0)."""
+    a = to_dev(orc.normal_bf16(M * Kd, 42, 1.0).reshape(M, Kd), cuda)
+    w = to_dev(orc.normal_bf16(N * Kd, 43, 0.03).reshape(N, Kd), cuda)
+    n_out = N // 2 if epi == 2 else N
+    r = to_dev(orc.normal_bf16(M * n_out, 44, 1.0).reshape(M, n_out), cuda) if epi == 1 else None
+    ref = K.gemm(a, w, residual=r, epilogue=epi)
+    got = K.gemm(a, K.weights_kblock(w), residual=r, epilogue=epi, kblocked=True)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("M,d,f", [(128, 4096, 14336), (8, 4096, 14336), (37, 512, 1792), (300, 512, 1792),
+                                   (128, 6144, 16384), (64, 2048, 1408)])
+def test_expert_ffn_kblocked_bit_identical(K, cuda, M, d, f):
+    """The engine's expert format: kl_expert_ffn_kb == kl_expert_ffn bitwise."""
+    rows, off = M + 30, 11
+    x = to_dev(orc.normal_bf16(rows * d, 51, 1.0).reshape(rows, d), cuda)
+    w13 = to_dev(orc.normal_bf16(2 * f * d, 52, 0.03).reshape(2 * f, d), cuda)
+    w2 = to_dev(orc.normal_bf16(d * f, 53, 0.03).reshape(d, f), cuda)
+    y0 = torch.zeros(rows, d, dtype=torch.bfloat16, device=cuda)
+    y1 = torch.zeros_like(y0)
+    h = torch.empty(M, f, dtype=torch.bfloat16, device=cuda)
+    K.expert_ffn(x, off, M, w13, w2, y0, h)
+    K.expert_ffn(x, off, M, K.weights_kblock(w13), K.weights_kblock(w2), y1, h, kblocked=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+
+
 @pytest.mark.parametrize("T,d,E,k,mode", [(64, 4096, 8, 2, 0), (300, 512, 8, 2, 0), (97, 2048, 64, 6, 1),
                                           (5, 256, 4, 4, 0), (1000, 512, 8, 2, 0), (700, 2048, 64, 6, 1),
                                           (64, 6144, 8, 2, 0), (512, 4096, 8, 2, 0), (64, 2048, 64, 6, 1)])

@@ -109,6 +109,29 @@ def main():
         out.append(a.elapsed_time(b) * 1e3 / 8)
     res["b2b_plain"] = med(out)
 
+    # the engine's K-blocked expert layout (kl_expert_ffn_kb), back to back
+    kbs = []
+    for sl in slots[:3]:
+        t = torch.empty_like(sl)
+        t[: 2 * f * d].view(2 * f, d).copy_(K.weights_kblock(sl[: 2 * f * d].view(2 * f, d)))
+        t[2 * f * d:].view(d, f).copy_(K.weights_kblock(sl[2 * f * d:].view(d, f)))
+        kbs.append(t)
+    out = []
+    for r in range(reps):
+        spin(cs)
+        a, b = ev(), ev()
+        a.record(cs)
+        for i in range(9):
+            w = kbs[i % 3]
+            K.expert_ffn(xp, 0, M, w[: 2 * f * d].view(2 * f, d), w[2 * f * d:].view(d, f), y, h,
+                         stream=cs.cuda_stream, kblocked=True)
+        b.record(cs)
+        release()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) * 1e3 / 9)
+    res["b2b_plain_kblocked"] = med(out)
+    del kbs
+
     def xwait(big, chain=False):
         out = []
         for r in range(reps):
