@@ -23,7 +23,9 @@
  * bubble_stats definitions.
  *
  * Conventions: opaque handle; 0 = success, non-zero = failure with the
- * message available from kl_engine_last_error(); strings returned through
+ * message available from kl_engine_last_error(). The code names the moesim
+ * exception class the C++ layer raised (reference error.hpp:11-49, plus
+ * DeviceError for CUDA / NCCL / OS failures), see KL_E* below; strings returned through
  * `char**` are malloc'd and released with kl_engine_free_string(). Host
  * buffers are plain pointers. Not thread-safe per handle.
  *
@@ -50,6 +52,17 @@
 #define KLOTSKI_ENGINE_H
 
 #include <stdint.h>
+
+/* Return codes of every kl_engine_* / kl_measure_profile entry point. */
+#define KL_OK 0
+#define KL_EOTHER 1         /* any other std::exception */
+#define KL_EMEMORY 2        /* moesim::MemoryInfeasible (model + workload do not fit) */
+#define KL_ECONFIG 3        /* moesim::ConfigError */
+#define KL_EVALIDATION 4    /* moesim::ValidationError */
+#define KL_EPARSE 5         /* moesim::ParseError */
+#define KL_ERANGE 6         /* moesim::RangeError */
+#define KL_EACCOUNTING 7    /* moesim::AccountingError (ledger / scheduler invariant) */
+#define KL_EDEVICE 8        /* moesim::DeviceError (CUDA / NCCL / OS) */
 
 #ifdef __cplusplus
 extern "C" {

@@ -30,11 +30,11 @@ using namespace moesim;
 namespace {
 
 void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw moesim::DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
 void kl_check(int rc, const char* what) {
-    if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
+    if (rc != 0) throw moesim::DeviceError(std::string(what) + ": " + kl_error_string(rc));
 }
 
 Dims preset_dims(const std::string& p) {
@@ -70,7 +70,12 @@ constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKi
 
 EngineConfig parse_config(const std::string& text) {
     EngineConfig c;
-    const json j = text.empty() ? json::object() : json::parse(text);
+    json j;
+    try {
+        j = text.empty() ? json::object() : json::parse(text);
+    } catch (const json::exception& x) {
+        throw ParseError(std::string("engine config: ") + x.what());
+    }
     const json m = j.value("model", json::object());
     c.name = m.value("preset", "tiny");
     c.dims = preset_dims(c.name);
@@ -219,7 +224,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     profile_.expert_compute_per_token = cfg_.expert_ps;
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    if (kl_device_supported() != 1) throw std::runtime_error("engine: device is not sm_100 (B200)");
+    if (kl_device_supported() != 1) throw moesim::DeviceError("engine: device is not sm_100 (B200)");
     if (!cfg_.measure_phase.empty()) {
         // Paper stage 1: the planner's rates are measured on
         // this GPU with this engine's kernels before n and placement are solved.
@@ -744,7 +749,7 @@ void Engine::init_weights() {
             int64_t left = disk_bytes(l), off = disk_off_[l];
             while (left > 0) {
                 const ssize_t w = ::pwrite(disk_fd_, src, static_cast<size_t>(left), off);
-                if (w <= 0) throw std::runtime_error(std::string("engine: disk store write: ") + std::strerror(errno));
+                if (w <= 0) throw moesim::DeviceError(std::string("engine: disk store write: ") + std::strerror(errno));
                 src += w;
                 off += w;
                 left -= w;

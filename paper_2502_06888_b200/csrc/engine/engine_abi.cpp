@@ -18,6 +18,38 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// Exception class -> return code (include/klotski/engine.h, KL_E*), with the
+// class name leading the message as the moesim Python module prints it.
+int error_code(std::exception_ptr p, std::string& msg) {
+    auto set = [&](const char* cls, const std::exception& x, int code) {
+        msg = std::string(cls) + ": " + x.what();
+        return code;
+    };
+    try {
+        std::rethrow_exception(p);
+    } catch (const moesim::MemoryInfeasible& x) {
+        return set("MemoryInfeasible", x, KL_EMEMORY);
+    } catch (const moesim::ConfigError& x) {
+        return set("ConfigError", x, KL_ECONFIG);
+    } catch (const moesim::ValidationError& x) {
+        return set("ValidationError", x, KL_EVALIDATION);
+    } catch (const moesim::ParseError& x) {
+        return set("ParseError", x, KL_EPARSE);
+    } catch (const moesim::RangeError& x) {
+        return set("RangeError", x, KL_ERANGE);
+    } catch (const moesim::AccountingError& x) {
+        return set("AccountingError", x, KL_EACCOUNTING);
+    } catch (const moesim::DeviceError& x) {
+        return set("DeviceError", x, KL_EDEVICE);
+    } catch (const std::exception& x) {
+        msg = x.what();
+        return KL_EOTHER;
+    } catch (...) {
+        msg = "unknown exception";
+        return KL_EOTHER;
+    }
+}
+
 char* dup_string(const std::string& s) {
     char* p = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(p, s.c_str(), s.size() + 1);
@@ -30,13 +62,9 @@ int guarded(kl_engine* e, F&& f) {
     try {
         f(*e->impl);
         e->error.clear();
-        return 0;
-    } catch (const moesim::MemoryInfeasible& x) {
-        e->error = std::string("MemoryInfeasible: ") + x.what();
-        return 2;
-    } catch (const std::exception& x) {
-        e->error = x.what();
-        return 1;
+        return KL_OK;
+    } catch (...) {
+        return error_code(std::current_exception(), e->error);
     }
 }
 
@@ -51,13 +79,9 @@ int kl_engine_create(const char* config_json, kl_engine** out) {
         auto* e = new kl_engine;
         e->impl = std::make_unique<klotski::Engine>(klotski::parse_config(config_json ? config_json : ""));
         *out = e;
-        return 0;
-    } catch (const moesim::MemoryInfeasible& x) {
-        g_create_error = std::string("MemoryInfeasible: ") + x.what();
-        return 2;
-    } catch (const std::exception& x) {
-        g_create_error = x.what();
-        return 1;
+        return KL_OK;
+    } catch (...) {
+        return error_code(std::current_exception(), g_create_error);
     }
 }
 
@@ -96,13 +120,12 @@ int kl_measure_profile(const char* config_json, const char* phase, char** json_o
     if (json_out == nullptr) return 1;
     *json_out = nullptr;
     try {
-        if (kl_device_supported() != 1) throw std::runtime_error("kl_measure_profile: device is not sm_100 (B200)");
+        if (kl_device_supported() != 1) throw moesim::DeviceError("kl_measure_profile: device is not sm_100 (B200)");
         const klotski::EngineConfig cfg = klotski::parse_config(config_json ? config_json : "");
         *json_out = dup_string(klotski::measure_profile(cfg, phase ? phase : "decode").to_json());
-        return 0;
-    } catch (const std::exception& x) {
-        g_create_error = x.what();
-        return 1;
+        return KL_OK;
+    } catch (...) {
+        return error_code(std::current_exception(), g_create_error);
     }
 }
 

@@ -81,7 +81,7 @@ const void* Engine::load_src(TensorClass cls, int layer, int e, cudaStream_t st)
 void Engine::enqueue_disk_read(char* dst, int64_t off, int64_t bytes, cudaStream_t st) {
     stage_jobs_.push_back({this, dst, off, bytes});
     const cudaError_t e = cudaLaunchHostFunc(st, &Engine::stage_host_fn, &stage_jobs_.back());
-    if (e != cudaSuccess) throw std::runtime_error(std::string("engine: disk read enqueue: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw moesim::DeviceError(std::string("engine: disk read enqueue: ") + cudaGetErrorString(e));
 }
 
 void Engine::open_disk_store() {
@@ -94,7 +94,7 @@ void Engine::open_disk_store() {
     std::vector<char> buf(path.begin(), path.end());
     buf.push_back('\0');
     disk_fd_ = ::mkstemp(buf.data());
-    if (disk_fd_ < 0) throw std::runtime_error("engine: cannot create the disk store in " + dir + ": " + std::strerror(errno));
+    if (disk_fd_ < 0) throw moesim::DeviceError("engine: cannot create the disk store in " + dir + ": " + std::strerror(errno));
     ::unlink(buf.data());
     disk_off_.assign(D_.L, 0);
     int64_t off = 0;
@@ -104,7 +104,7 @@ void Engine::open_disk_store() {
     }
     disk_bytes_total_ = off;
     if (::ftruncate(disk_fd_, off) != 0)
-        throw std::runtime_error(std::string("engine: cannot size the disk store: ") + std::strerror(errno));
+        throw moesim::DeviceError(std::string("engine: cannot size the disk store: ") + std::strerror(errno));
 }
 
 // Host-function body: runs on the CUDA driver's callback thread, so no CUDA

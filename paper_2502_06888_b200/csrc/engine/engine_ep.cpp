@@ -61,10 +61,10 @@ using namespace moesim;
 namespace {
 
 void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw moesim::DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 void kl_check_impl(int rc, const char* what) {
-    if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
+    if (rc != 0) throw moesim::DeviceError(std::string(what) + ": " + kl_error_string(rc));
 }
 #define kl_check(rc, what) (++launches_, kl_check_impl((rc), (what)))
 
@@ -89,10 +89,10 @@ NcclApi& nccl_api() {
     if (api.lib != nullptr) return api;
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
     if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (h == nullptr) throw std::runtime_error("engine EP: libnccl.so.2 not found");
+    if (h == nullptr) throw moesim::DeviceError("engine EP: libnccl.so.2 not found");
     auto sym = [&](const char* n) {
         void* p = dlsym(h, n);
-        if (p == nullptr) throw std::runtime_error(std::string("engine EP: NCCL symbol missing: ") + n);
+        if (p == nullptr) throw moesim::DeviceError(std::string("engine EP: NCCL symbol missing: ") + n);
         return p;
     };
     api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(sym("ncclGetUniqueId"));
@@ -109,7 +109,7 @@ NcclApi& nccl_api() {
 }
 
 void nccl_check(ncclResult_t r, const char* what) {
-    if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + nccl_api().error_string(r));
+    if (r != ncclSuccess) throw moesim::DeviceError(std::string(what) + ": " + nccl_api().error_string(r));
 }
 
 int hex_val(char c) {
@@ -197,7 +197,7 @@ struct LoopbackHub {
     // All G ranks arrive before any leaves (generation-counted, reusable).
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
-        if (broken) throw std::runtime_error("engine EP loopback: a peer left the group");
+        if (broken) throw moesim::DeviceError("engine EP loopback: a peer left the group");
         const uint64_t gen = generation;
         if (++arrived == G) {
             arrived = 0;
@@ -206,7 +206,7 @@ struct LoopbackHub {
             return;
         }
         cv.wait(lk, [&] { return generation != gen || broken; });
-        if (broken) throw std::runtime_error("engine EP loopback: a peer left the group");
+        if (broken) throw moesim::DeviceError("engine EP loopback: a peer left the group");
     }
     void abandon() {
         std::lock_guard<std::mutex> lk(mu);

@@ -23,6 +23,7 @@
 #include <stdexcept>
 
 #include <nlohmann/json.hpp>
+#include <nvtx3/nvToolsExt.h>
 
 #include "engine.hpp"
 #include "klotski/kernels.h"
@@ -36,14 +37,24 @@ using namespace moesim;
 namespace {
 
 void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw moesim::DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 void kl_check_impl(int rc, const char* what) {
-    if (rc != 0) throw std::runtime_error(std::string(what) + ": " + kl_error_string(rc));
+    if (rc != 0) throw moesim::DeviceError(std::string(what) + ": " + kl_error_string(rc));
 }
 // Every kernel entry point goes through here (inside Engine members), which
 // also counts launches for the bench's gpu_launches claim.
 #define kl_check(rc, what) (++launches_, kl_check_impl((rc), (what)))
+
+// NVTX3 range over a host-side scope: one per step and one per
+// executed op, named by the op kind, so an nsys / ncu --nvtx capture shows the
+// engine's enqueue structure over the kernels. A no-op without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int32_t kNoPos = 0x7f7f7f7f;  // memset(0x7f) sentinel for first_pos
 
@@ -170,6 +181,7 @@ PrefetchDecision Engine::decide(int /*step*/, int layer) const {
 }
 
 double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
+    const NvtxRange nvtx(step == 0 ? "klotski step (prefill)" : "klotski step (decode)");
     if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (no memory to run on)");
     if (step < 0 || step >= cfg_.workload.gen_len) throw RangeError("engine: step outside the batch group");
     if (step == 0 && !cfg_.prefill) throw ConfigError("engine: built without prefill support (prefill=false)");
@@ -355,7 +367,7 @@ void Engine::collect_step_times() {
     if (!kv_slot_of_.empty()) throw AccountingError("engine: KV slot still mapped at the end of a step");
     stage_jobs_.clear();
     if (const int e = stage_errno_.exchange(0))
-        throw std::runtime_error(std::string("engine: disk staging read failed: ") + std::strerror(e));
+        throw moesim::DeviceError(std::string("engine: disk staging read failed: ") + std::strerror(e));
 }
 
 // Enqueue every emitted-but-not-executed op. Cold computes of a reorder
@@ -391,6 +403,7 @@ void Engine::issue_pending() {
 
 void Engine::exec(std::int32_t id) {
     const StreamOp& op = em_->schedule().ops[id];
+    const NvtxRange nvtx(op_kind_name(op.kind));
     cudaStream_t st = stream_of(op.stream);
     for (std::int32_t d : op.deps) {
         if (d < timed_from_) continue;  // finished in an earlier (synchronized) step

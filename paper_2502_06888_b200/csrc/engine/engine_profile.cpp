@@ -34,10 +34,10 @@ namespace klotski {
 namespace {
 
 void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string("measure_profile: ") + what + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw moesim::DeviceError(std::string("measure_profile: ") + what + ": " + cudaGetErrorString(e));
 }
 void kl_check(int rc, const char* what) {
-    if (rc != 0) throw std::runtime_error(std::string("measure_profile: ") + what + ": " + kl_error_string(rc));
+    if (rc != 0) throw moesim::DeviceError(std::string("measure_profile: ") + what + ": " + kl_error_string(rc));
 }
 
 struct DevScratch {

@@ -47,23 +47,57 @@ def ep_unique_id():
 
 
 class EngineError(RuntimeError):
+    """Base of every engine failure; subclasses mirror the moesim exception
+    taxonomy (reference error.hpp:11-49) by the C-ABI return code (KL_E*)."""
+
+
+class ConfigError(EngineError, ValueError):
     pass
+
+
+class ValidationError(EngineError, ValueError):
+    pass
+
+
+class ParseError(EngineError, ValueError):
+    pass
+
+
+class RangeError(EngineError, IndexError):
+    pass
+
+
+class AccountingError(EngineError):
+    pass
+
+
+class DeviceError(EngineError):
+    """CUDA / NCCL / OS failure under the engine (fatal for the handle)."""
+
+
+class MemoryInfeasible(EngineError):
+    pass
+
+
+_ERRORS = {2: MemoryInfeasible, 3: ConfigError, 4: ValidationError, 5: ParseError, 6: RangeError,
+           7: AccountingError, 8: DeviceError}
+
+
+def _raise(rc, msg):
+    raise _ERRORS.get(rc, EngineError)(msg)
 
 
 def measure_profile(config, phase="decode"):
     """Planner stage 1: this GPU's per-token attention / gate / expert rates
     and pinned H2D bandwidth on the config's model shapes (kl_measure_profile)."""
     out = C.c_void_p()
-    if _lib.kl_measure_profile(json.dumps(config).encode(), phase.encode(), C.byref(out)) != 0:
-        raise EngineError(_lib.kl_engine_last_error(None).decode())
+    rc = _lib.kl_measure_profile(json.dumps(config).encode(), phase.encode(), C.byref(out))
+    if rc != 0:
+        _raise(rc, _lib.kl_engine_last_error(None).decode())
     try:
         return json.loads(C.string_at(out).decode())
     finally:
         _lib.kl_engine_free_string(out)
-
-
-class MemoryInfeasible(EngineError):
-    pass
 
 
 class Engine:
@@ -72,8 +106,7 @@ class Engine:
         text = json.dumps(config).encode()
         rc = _lib.kl_engine_create(text, C.byref(self._h))
         if rc != 0:
-            msg = _lib.kl_engine_last_error(None).decode()
-            raise (MemoryInfeasible if rc == 2 else EngineError)(msg)
+            _raise(rc, _lib.kl_engine_last_error(None).decode())
         self.info = self._json(_lib.kl_engine_describe)
         self.n_batches = self.info["n_batches"]
         self.batch_size = self.info["batch_size"]
@@ -81,8 +114,7 @@ class Engine:
 
     def _check(self, rc):
         if rc != 0:
-            msg = _lib.kl_engine_last_error(self._h).decode()
-            raise (MemoryInfeasible if rc == 2 else EngineError)(msg)
+            _raise(rc, _lib.kl_engine_last_error(self._h).decode())
 
     def _json(self, fn, *args):
         out = C.c_void_p()

@@ -47,9 +47,22 @@ def test_engine_create_fails_loudly_without_gpu(lib):
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    from paper_2502_06888_b200.engine import Engine, EngineError
-    with pytest.raises(EngineError):
+    from paper_2502_06888_b200.engine import DeviceError, Engine
+    with pytest.raises(DeviceError, match="DeviceError"):
         Engine({"model": {"preset": "tiny"}})
+
+
+def test_engine_errors_map_to_moesim_types(lib):
+    """Config errors raised before any device call arrive as the moesim class
+    (KL_ECONFIG / KL_EPARSE), not a generic failure."""
+    import ctypes as C
+    from paper_2502_06888_b200.engine import ConfigError, Engine, EngineError, ParseError
+    with pytest.raises(ConfigError):
+        Engine({"model": {"preset": "no-such-model"}})
+    h = C.c_void_p()
+    assert lib.kl_engine_create(b"{not json", C.byref(h)) == 5
+    assert not h.value
+    assert issubclass(ParseError, EngineError) and issubclass(ConfigError, ValueError)
 
 
 def test_package_has_no_cpu_fallback(monkeypatch, tmp_path):
