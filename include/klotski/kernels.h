@@ -87,6 +87,9 @@ int kl_tune(int knob, int value);
  * timing of the work queued behind it). */
 int kl_stream_trace(unsigned long long* host, int n_ctas);
 int kl_debug_spin_flag(const int* flag, cudaStream_t stream);
+/* Device timestamp: writes the GPU global timer (ns) into *dst (device
+ * memory) when `stream` reaches this point; the engine's op-boundary marks. */
+int kl_stamp(unsigned long long* dst, cudaStream_t stream);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
                  int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);

@@ -64,6 +64,13 @@ std::uint64_t tensor_seed(std::uint64_t base, int kind, int layer, int expert) {
 
 constexpr byte_count kGemmWorkspace = 40LL << 20;
 constexpr int kKvSlots = 3;  // device KV slots when the KV tier is DRAM  // split-K partials for decode-shaped GEMMs
+// Ops one step window can hold (op timestamps are sized by it): per layer n
+// attentions, gates, KV loads and stores, up to 3 ops (load, compute,
+// offload) per (expert, batch) for the per-batch variants, a few weight
+// loads / offloads / window stages; slack for ops emitted ahead.
+int64_t ops_per_step_bound(int layers, int64_t n, int64_t local_experts) {
+    return static_cast<int64_t>(layers) * (4 * n + 3 * local_experts * n + 8) + 256;
+}
 constexpr int kKindExpert = 1, kKindAttn = 2, kKindGate = 3, kKindEmbed = 4, kKindHead = 5;
 
 }  // namespace
@@ -191,7 +198,6 @@ void ExpertSlotPool::release_after(int slot, cudaEvent_t ev) {
 }
 
 Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
-    diag_ = std::getenv("KL_ENGINE_DIAG") != nullptr;
     spec_.name = cfg_.name;
     spec_.n_layers = D_.L;
     spec_.n_experts_per_layer = D_.E;
@@ -239,7 +245,8 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     allocate_device();
     allocate_host();
     for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaEventCreate(&t0_), "event");
+    cuda_check(cudaEventCreate(&step_begin_), "event");
+    cuda_check(cudaEventCreate(&step_end_), "event");
     ep_init();
     init_weights();
     const detail::GroupShape shape{cfg_.workload.gen_len, D_.L, plan_.n_batches, cfg_.workload.batch_size,
@@ -262,7 +269,8 @@ Engine::~Engine() {
         if (s) cudaStreamDestroy(s);
     for (auto& pool : event_pool_)
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
-    if (t0_) cudaEventDestroy(t0_);
+    if (step_begin_) cudaEventDestroy(step_begin_);
+    if (step_end_) cudaEventDestroy(step_end_);
     for (cudaEvent_t e : pool_.release) (void)e;
     if (arena_) cudaFree(arena_);
     for (void* p : host_blocks_) cudaFreeHost(p);
@@ -408,6 +416,7 @@ bool Engine::plan_at(int n, bool rethrow) {
         add(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + 64);                           // report
         add((static_cast<byte_count>(std::max(D_.L - 1, 0)) * D_.E * D_.E + D_.E) * 8);
         add(64 * 1024);
+        add((2 * ops_per_step_bound(D_.L, n, El_) + 8) * 8);                     // op timestamps
         if (kv_off)
             add(static_cast<byte_count>(kKvSlots) * w.batch_size *
                 cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
@@ -477,6 +486,8 @@ void Engine::allocate_device() {
     embed_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     head_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     h_ = bf(t_max_ * D_.d);
+    stamp_cap_ = ops_per_step_bound(D_.L, plan_.n_batches, El_);
+    stamps_dev_ = static_cast<unsigned long long*>(take((2 * stamp_cap_ + 8) * 8));
     x2_ = bf(t_max_ * D_.d);
     xa_ = bf(tb_max_ * D_.d);
     qkv_ = bf(tb_max_ * D_.qkv_width());
@@ -631,6 +642,7 @@ void Engine::allocate_host() {
         host_kv_.assign(static_cast<size_t>(L) * n, nullptr);
         for (size_t i = 0; i < host_kv_.size(); ++i) host_kv_[i] = static_cast<uint16_t*>(pinned(kv_slot_bytes_));
     }
+    stamps_host_ = static_cast<unsigned long long*>(pinned((2 * stamp_cap_ + 8) * 8));
     host_report_ = static_cast<int32_t*>(pinned(2LL * n * D_.E * 4 + 2LL * D_.E * 8 + D_.E * 4 + 128));
     if (ep_) host_recv_ids_ = static_cast<int32_t*>(pinned(std::max<int64_t>(r_recv_max_, 1) * 4));
     host_idx_ = static_cast<int32_t*>(pinned(t_max_ * D_.k * 4));

@@ -37,8 +37,6 @@
 
 namespace klotski {
 
-// Op event pairs of the previous step collected per routing wait.
-constexpr std::int32_t kCollectPerWait = 96;
 
 using moesim::byte_count;
 
@@ -160,8 +158,6 @@ class Engine {
     cudaStream_t stream_of(moesim::StreamId s) const { return streams_[static_cast<int>(s)]; }
     cudaEvent_t event();
     void collect_step_times();
-    void collect_some(std::int32_t budget);
-    void flush_times();
     int tokens_per_batch(int step) const { return cfg_.workload.batch_size * (step == 0 ? cfg_.workload.prompt_len : 1); }
     int n_batches() const { return plan_.n_batches; }
     const uint16_t* expert_weights(int layer, int e) const;
@@ -259,17 +255,24 @@ class Engine {
 
     // streams / events
     std::array<cudaStream_t, moesim::kNumStreams> streams_{};
-    // Two event pools alternate by step: the events of step N are turned into
-    // timeline entries while step N+1 runs (collect_some, in the host's
-    // routing waits), so the GPU does not idle between steps on ~2 event
-    // queries per op.
+    // Dependency / release events (cudaEventDisableTiming: recording one is
+    // free even while a copy engine streams, unlike a timed event). Two pools
+    // alternate by step so a step never reuses an event the previous one
+    // may still reference.
     std::array<std::vector<cudaEvent_t>, 2> event_pool_;
     int event_par_ = 0;
     std::size_t event_next_ = 0;
-    std::int32_t pend_from_ = 0, pend_to_ = 0;   // ops of the previous step not yet collected
-    cudaEvent_t t0_ = nullptr;
+    cudaEvent_t step_begin_ = nullptr, step_end_ = nullptr;  // timed: one pair per step
+    // Op timing: device timestamps (kl_stamp, GPU global timer in ns) at each
+    // op's start and end, indexed by op id - timed_from_; read back once the
+    // step has synchronized. [0, 2*cap): the window's stamps; [2*cap]: t0.
+    unsigned long long* stamps_dev_ = nullptr;
+    unsigned long long* stamps_host_ = nullptr;
+    std::int64_t stamp_cap_ = 0;  // ops per step window
     bool t0_recorded_ = false;
-    std::vector<cudaEvent_t> op_start_, op_end_;     // by op id (current step window)
+    unsigned long long t0_ns_ = 0;
+    void stamp(std::int32_t id, int side, cudaStream_t st);
+    std::vector<cudaEvent_t> op_end_;                 // by op id (current step window)
     std::vector<moesim::SimEvent> timeline_;          // measured, by op id
     std::int32_t timed_from_ = 0;
     std::int32_t log_from_ = 0;
@@ -289,15 +292,6 @@ class Engine {
     int kv_filled_positions_ = 0;
     int acquire_kv_slot(cudaStream_t st);
     std::set<int> executed_steps_;
-    // Diagnostics (KL_ENGINE_DIAG=1): events around each expert op's FFN kernels.
-    struct DiagEvent {
-        std::int32_t op;
-        cudaEvent_t before, after;
-    };
-    bool diag_ = false;
-    std::int32_t next_exec_diag_ = 0;
-    std::vector<DiagEvent> diag_events_, pend_diag_;
-    std::vector<std::array<float, 3>> diag_rows_;
     int idx_cur_ = 0;
     std::map<std::pair<int, int>, int> expert_slot_of_;   // (layer, e) -> pool slot
     std::map<int, int> attn_slot_of_;                      // layer -> attention slot

@@ -377,7 +377,6 @@ void Engine::ep_after_gates(int step, int layer) {
 
 detail::BlockRouting Engine::ep_read_routing(int step, int layer) {
     const std::int32_t last_gate = next_exec_ - 1;
-    collect_some(kCollectPerWait);
     cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     const int32_t* hist = host_report_;

@@ -130,10 +130,19 @@ cudaEvent_t Engine::event() {
     auto& pool = event_pool_[event_par_];
     if (event_next_ == pool.size()) {
         cudaEvent_t e;
-        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         pool.push_back(e);
     }
     return pool[event_next_++];
+}
+
+// Op boundary timestamp on the op's own stream (kl_stamp).
+void Engine::stamp(std::int32_t id, int side, cudaStream_t st) {
+    const std::int64_t slot = static_cast<std::int64_t>(id) - timed_from_;
+    if (slot < 0 || slot >= stamp_cap_)
+        throw AccountingError("engine: op " + std::to_string(id) + " outside the step's timestamp window (" +
+                              std::to_string(stamp_cap_) + " ops)");
+    kl_check(kl_stamp(stamps_dev_ + 2 * slot + side, st), "op stamp");
 }
 
 const uint16_t* Engine::expert_weights(int layer, int e) const {
@@ -200,11 +209,9 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     cudaStream_t cs = stream_of(StreamId::compute);
 
     cudaEvent_t begin = event();
+    cuda_check(cudaEventRecord(step_begin_, cs), "record");
+    if (!t0_recorded_) kl_check(kl_stamp(stamps_dev_ + 2 * stamp_cap_, cs), "t0 stamp");
     cuda_check(cudaEventRecord(begin, cs), "record");
-    if (!t0_recorded_) {
-        cuda_check(cudaEventRecord(t0_, cs), "record t0");
-        t0_recorded_ = true;
-    }
     for (int s = 1; s < kNumStreams; ++s) cuda_check(cudaStreamWaitEvent(streams_[s], begin, 0), "wait");
 
     // Token positions / cache rows; row order = batch-major, sequence-major.
@@ -302,11 +309,10 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
         cuda_check(cudaEventRecord(j, streams_[s]), "record");
         cuda_check(cudaStreamWaitEvent(cs, j, 0), "wait");
     }
-    cudaEvent_t end = event();
-    cuda_check(cudaEventRecord(end, cs), "record");
-    cuda_check(cudaEventSynchronize(end), "step sync");
+    cuda_check(cudaEventRecord(step_end_, cs), "record");
+    cuda_check(cudaEventSynchronize(step_end_), "step sync");
     float ms = 0.f;
-    cuda_check(cudaEventElapsedTime(&ms, begin, end), "elapsed");
+    cuda_check(cudaEventElapsedTime(&ms, step_begin_, step_end_), "elapsed");
     if (next_out != nullptr) std::memcpy(next_out, host_tokens_ + 3 * t_max_, seqs * 4);
     collect_step_times();
     tokens_generated_ += seqs;
@@ -314,47 +320,35 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     return ms;
 }
 
-// Turn up to `budget` op event pairs of the previous step into timeline
-// entries (the events completed at that step's end). Called from the host's
-// routing waits, where the host would otherwise only block.
-void Engine::collect_some(std::int32_t budget) {
+// End of a synchronized step: read back this step's op timestamps (one small
+// D2H), turn them into timeline entries, and recycle the step's events and
+// slot release markers.
+void Engine::collect_step_times() {
     const auto& ops = em_->schedule().ops;
+    const std::int64_t n_ops = next_exec_ - timed_from_;
+    if (!t0_recorded_) {
+        cuda_check(cudaMemcpy(stamps_host_ + 2 * stamp_cap_, stamps_dev_ + 2 * stamp_cap_, 8, cudaMemcpyDeviceToHost),
+                   "d2h t0");
+        t0_ns_ = stamps_host_[2 * stamp_cap_];
+        t0_recorded_ = true;
+    }
+    if (n_ops > 0)
+        cuda_check(cudaMemcpy(stamps_host_, stamps_dev_, static_cast<size_t>(n_ops) * 16, cudaMemcpyDeviceToHost),
+                   "d2h stamps");
     if (timeline_.size() < ops.size()) timeline_.resize(ops.size());
-    for (; pend_from_ < pend_to_ && budget > 0; ++pend_from_, --budget) {
-        const std::int32_t id = pend_from_;
-        float a = 0.f, b = 0.f;
-        cuda_check(cudaEventElapsedTime(&a, t0_, op_start_[id]), "elapsed");
-        cuda_check(cudaEventElapsedTime(&b, t0_, op_end_[id]), "elapsed");
+    auto ps = [&](unsigned long long ns) {
+        return static_cast<duration_ps>(static_cast<long long>(ns - t0_ns_)) * 1000;
+    };
+    for (std::int32_t id = timed_from_; id < next_exec_; ++id) {
+        const unsigned long long* t = stamps_host_ + 2 * (id - timed_from_);
         SimEvent& ev = timeline_[id];
         ev.op_id = id;
         ev.stream = ops[id].stream;
-        ev.start = std::llround(static_cast<double>(a) * 1e9);
-        ev.end = std::max(ev.start, static_cast<duration_ps>(std::llround(static_cast<double>(b) * 1e9)));
+        ev.start = ps(t[0]);
+        ev.end = std::max(ev.start, ps(t[1]));
         ev.bytes = ops[id].payload_bytes;
         ev.tokens = ops[id].token_count;
     }
-    if (pend_from_ < pend_to_) return;
-    for (const auto& de : pend_diag_) {
-        float a = 0.f, b = 0.f, c = 0.f;
-        cuda_check(cudaEventElapsedTime(&a, op_start_[de.op], de.before), "diag");
-        cuda_check(cudaEventElapsedTime(&b, de.before, de.after), "diag");
-        cuda_check(cudaEventElapsedTime(&c, de.after, op_end_[de.op]), "diag");
-        diag_rows_.push_back({a * 1e3f, b * 1e3f, c * 1e3f});
-    }
-    pend_diag_.clear();
-}
-
-void Engine::flush_times() { collect_some(std::numeric_limits<std::int32_t>::max()); }
-
-// End of a synchronized step: the previous step's leftovers are collected
-// now (its event pool is about to be reused), this step's ops become the
-// pending window, and slot release markers are recycled.
-void Engine::collect_step_times() {
-    flush_times();
-    pend_from_ = timed_from_;
-    pend_to_ = next_exec_;
-    pend_diag_ = std::move(diag_events_);
-    diag_events_.clear();
     timed_from_ = next_exec_;
     event_par_ ^= 1;
     event_next_ = 0;
@@ -378,10 +372,7 @@ void Engine::collect_step_times() {
 void Engine::issue_pending() {
     const auto& ops = em_->schedule().ops;
     const std::int32_t total = static_cast<std::int32_t>(ops.size());
-    if (static_cast<std::int32_t>(op_start_.size()) < total) {
-        op_start_.resize(total, nullptr);
-        op_end_.resize(total, nullptr);
-    }
+    if (static_cast<std::int32_t>(op_end_.size()) < total) op_end_.resize(total, nullptr);
     while (next_exec_ < total) {
         const StreamOp& op = ops[next_exec_];
         if (op.kind == OpKind::compute_expert && op.reorder_group >= 0 &&
@@ -410,7 +401,6 @@ void Engine::exec(std::int32_t id) {
         if (em_->schedule().ops[d].stream == op.stream) continue;  // FIFO on the same stream
         cuda_check(cudaStreamWaitEvent(st, op_end_[d], 0), "dep wait");
     }
-    op_start_[id] = event();
     op_end_[id] = event();
     const size_t E = static_cast<size_t>(El_);  // local expert shard
     auto wait_release = [&](cudaEvent_t ev) {
@@ -431,14 +421,14 @@ void Engine::exec(std::int32_t id) {
             if (op.cls == TensorClass::attention) {
                 const int s = pick2(attn_slot_busy_);
                 wait_release(attn_slot_release_[s]);
-                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                stamp(id, 0, st);
                 cuda_check(cudaMemcpyAsync(attn_slot_[s], load_src(TensorClass::attention, op.layer, 0, st), attn_slot_bytes_,
                                            cudaMemcpyHostToDevice, st), "h2d attention");
                 attn_slot_of_[op.layer] = s;
             } else if (op.cls == TensorClass::gate) {
                 const int s = pick2(gate_slot_busy_);
                 wait_release(gate_slot_release_[s]);
-                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                stamp(id, 0, st);
                 cuda_check(cudaMemcpyAsync(gate_slot_[s], load_src(TensorClass::gate, op.layer, 0, st), spec_.gate_bytes,
                                            cudaMemcpyHostToDevice, st), "h2d gate");
                 gate_slot_of_[op.layer] = s;
@@ -452,7 +442,7 @@ void Engine::exec(std::int32_t id) {
                     if (pool_.has_release[x]) wait_release(pool_.release[x]);
                     slots.push_back(x);
                 }
-                cuda_check(cudaEventRecord(op_start_[id], st), "record");
+                stamp(id, 0, st);
                 cuda_check(cudaMemcpyAsync(gate_slot_[s], load_src(TensorClass::gate, op.layer, 0, st), spec_.gate_bytes,
                                            cudaMemcpyHostToDevice, st), "h2d gate");
                 for (size_t e = 0; e < E; ++e) {
@@ -468,14 +458,14 @@ void Engine::exec(std::int32_t id) {
         case OpKind::load_expert: {
             const int s = pool_.acquire();
             if (pool_.has_release[s]) wait_release(pool_.release[s]);
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             cuda_check(cudaMemcpyAsync(pool_.ptr[s], load_src(TensorClass::expert, op.layer, op.expert, st), expert_slot_bytes_,
                                        cudaMemcpyHostToDevice, st), "h2d expert");
             expert_slot_of_[{op.layer, op.expert}] = s;
             break;
         }
         case OpKind::offload_expert: {
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             const auto it = expert_slot_of_.find({op.layer, op.expert});
             if (it == expert_slot_of_.end()) throw AccountingError("engine: offload of an unloaded expert");
             // The slot is free once the offload op itself has completed (the
@@ -485,7 +475,7 @@ void Engine::exec(std::int32_t id) {
             break;
         }
         case OpKind::offload_weights: {
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             cudaEvent_t after = op_end_[id];  // recorded after the dep wait above
             if (op.cls == TensorClass::attention) {
                 const int s = attn_slot_of_.at(op.layer);
@@ -513,7 +503,7 @@ void Engine::exec(std::int32_t id) {
             // free device slot (load_kv, schedule.cpp:255-268): rows
             // [0, history) of every sequence, one 2D copy each for K and V.
             const int slot = acquire_kv_slot(st);
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             const int history = plan_.placement.kv_retention.retained(cfg_.workload.prompt_len + op.step - 1);
             const size_t row = static_cast<size_t>(D_.Hkv) * D_.hd * 2, pitch = row * kv_cap_;
             const uint16_t* h = host_kv_[static_cast<size_t>(op.layer) * plan_.n_batches + op.batch];
@@ -528,7 +518,7 @@ void Engine::exec(std::int32_t id) {
         case OpKind::store_cache: {
             // This step's new K/V rows back to host (store_kv, schedule.cpp:270-288);
             // the slot is free once the copy has read it.
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             const auto it = kv_slot_of_.find({op.layer, op.batch});
             if (it == kv_slot_of_.end()) throw AccountingError("engine: KV store without a device slot");
             const int slot = it->second;
@@ -556,7 +546,7 @@ void Engine::exec(std::int32_t id) {
             // Evict op.batch's window slot (its loads of this pass are the
             // op's deps), then read the staged layer's disk region into a
             // free slot on the cpu_stage stream (schedule.cpp:374-426).
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             const int evict = op.batch;
             if (evict >= 0 && window_slot_of_[evict] >= 0) {
                 window_free_.push_back(window_slot_of_[evict]);
@@ -573,21 +563,21 @@ void Engine::exec(std::int32_t id) {
             break;
         }
         case OpKind::compute_attention:
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             exec_attention(op);
             break;
         case OpKind::compute_gate:
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
+            stamp(id, 0, st);
             exec_gate(op);
             break;
         case OpKind::compute_expert:
-            cuda_check(cudaEventRecord(op_start_[id], st), "record");
-            next_exec_diag_ = id;
+            stamp(id, 0, st);
             exec_expert(op);
             break;
         default:
             throw ConfigError(std::string("engine: op kind ") + op_kind_name(op.kind) + " is not executed on B200 yet");
     }
+    stamp(id, 1, st);
     cuda_check(cudaEventRecord(op_end_[id], st), "record");
     if (combine_step_ >= 0) {
         combine_block(combine_step_);
@@ -779,7 +769,6 @@ void Engine::after_batch_gate(int step, int layer, int b) {
 
 detail::BlockRouting Engine::read_routing_row(int step, int layer, int b) {
     const std::int32_t last_gate = next_exec_ - 1;
-    collect_some(kCollectPerWait);
     cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
@@ -818,7 +807,6 @@ detail::BlockRouting Engine::read_routing(int step, int layer) {
     // The last op issued on the compute stream is the block's last gate;
     // its end event covers the readback copies.
     const std::int32_t last_gate = next_exec_ - 1;
-    collect_some(kCollectPerWait);
     cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
@@ -874,12 +862,6 @@ void Engine::exec_expert(const StreamOp& op) {
         w = wscratch_;
     }
     const uint16_t* w2 = w + 2LL * D_.f * D_.d;
-    cudaEvent_t d0 = nullptr, d1 = nullptr;
-    if (diag_) {
-        d0 = event();
-        d1 = event();
-        cuda_check(cudaEventRecord(d0, cs), "diag");
-    }
     for (int64_t c = 0; c < M; c += cfg_.ffn_chunk_rows) {
         const int m = static_cast<int>(std::min<int64_t>(cfg_.ffn_chunk_rows, M - c));
         if (q4 && M <= 256)
@@ -892,10 +874,6 @@ void Engine::exec_expert(const StreamOp& op) {
             kl_check(kl_expert_ffn(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
                                    gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
-    }
-    if (diag_) {
-        cuda_check(cudaEventRecord(d1, cs), "diag");
-        diag_events_.push_back({static_cast<std::int32_t>(next_exec_diag_), d0, d1});
     }
     // The block's last expert op: the combine follows right after the op's
     // end event (so compute_expert events bracket the FFN kernels only).
@@ -941,7 +919,6 @@ void Engine::read_hidden(uint16_t* host, int64_t n) const {
 
 void Engine::reset_log() {
     if (cfg_.plan_only) return;
-    flush_times();
     // Keep the emitter (op ids keep growing); measurement restarts here.
     timed_from_ = next_exec_;
     log_from_ = next_exec_;
@@ -952,12 +929,10 @@ void Engine::reset_log() {
     ep_max_local_rows_ = 0;
     step_ms_.clear();
     hidden_dumps_.clear();
-    diag_rows_.clear();
 }
 
 std::string Engine::report(const std::string& what) {
     if (cfg_.plan_only) throw ConfigError("engine: created with plan_only (nothing executed to report)");
-    flush_times();
     const Schedule& s = em_->schedule();
     json j;
     std::vector<SimEvent> tl(timeline_.begin() + std::min<size_t>(log_from_, timeline_.size()),
@@ -1130,9 +1105,6 @@ std::string Engine::report(const std::string& what) {
         j["carried_in_frees"] = carried;
         j["arena_bytes_used"] = arena_used_;
         j["memory_csv"] = memory_timeline_csv(ledger);
-    } else if (what == "diag") {
-        // Expert-op breakdown (KL_ENGINE_DIAG=1): [start -> FFN launch, FFN kernels, FFN -> end] in us.
-        j["expert_op_us"] = diag_rows_;
     } else if (what == "hidden") {
         json arr = json::array();
         for (const auto& dmp : hidden_dumps_) arr.push_back(dmp);

@@ -36,3 +36,40 @@ extern "C" int kl_debug_spin_flag(const int* flag, cudaStream_t stream) {
     spin_flag_kernel<<<1, 1, 0, stream>>>(flag);
     return kl::check_launch();
 }
+
+// Device timestamp: one thread writes %globaltimer (ns, the clock cudaEvent
+// timestamps come from) into *dst once every earlier grid of the stream has
+// completed. The engine marks op boundaries with these instead of timed
+// cudaEvents: a timed event record stalls the stream for tens of microseconds
+// while a copy engine streams pinned host memory, and breaks programmatic
+// dependent launch (tools/dma_interference_probe.py). Launched as a PDL
+// secondary that releases its own dependents first, so the next kernel still
+// pre-launches while the previous one runs; griddepcontrol.wait then returns
+// when that previous grid has completed.
+namespace kl {
+int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
+}
+namespace {
+__global__ void stamp_kernel(unsigned long long* dst) {
+    kl::griddep_launch_dependents();
+    kl::griddep_wait();
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    *dst = t;
+}
+}  // namespace
+
+extern "C" int kl_stamp(unsigned long long* dst, cudaStream_t stream) {
+    if (dst == nullptr) return KL_EINVAL;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = kl::g_pdl ? 1 : 0;
+    KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, stamp_kernel, dst));
+    return kl::check_launch();
+}

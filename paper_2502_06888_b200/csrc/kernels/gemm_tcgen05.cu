@@ -28,6 +28,7 @@
 #include "tma_host.cuh"
 
 namespace kl {
+extern int g_pdl;  // kl_tune(KL_TUNE_PDL, ...): programmatic dependent launch (abi.cu)
 namespace {
 
 constexpr int BM = 128;
@@ -1054,7 +1055,6 @@ int g_stream_stages = 8;   // kl_tune(KL_TUNE_STREAM_STAGES, ...): cap on the sm
 int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/evict_last hints
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
-int g_pdl = 1;  // kl_tune(KL_TUNE_PDL, ...)
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
 int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...)
 int g_stream_ks = 2;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2): 2 where >= 3 stages still fit

@@ -84,11 +84,6 @@ def main():
             d = np.array([x[0] for x in v])
             print(f"  {name:18s} n={len(d):4d} dur mean {d.mean():.1f} med {np.median(d):.1f} us;"
                   f" gap med {np.median([x[1] for x in v]):.1f} us")
-    diag = eng.report("diag").get("expert_op_us", [])
-    if diag:
-        a = np.array(diag)
-        print("expert op breakdown (us): start->FFN %.1f  FFN kernels %.1f  FFN->end %.1f  (n=%d)" % (
-            *a.mean(0), len(a)))
     eng.close()
 
 

@@ -136,6 +136,7 @@ def main():
     ap.add_argument("--even", type=int, default=1, help="stream GEMM equal k-splits per tile")
     ap.add_argument("--whole", type=int, default=70, help="whole-tile grid when tiles >= pct%% of SMs")
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
+    ap.add_argument("--kb", type=int, default=1, help="expert weights in the K-blocked layout (the engine's)")
     ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
     args = ap.parse_args()
     K.tune(99, args.debug)
@@ -168,6 +169,10 @@ def main():
     if not args.only or args.only == "ffn":
         M = args.rows
         ws = [torch.randn(3 * d * f, dtype=bf, device=dev) * 0.02 for _ in range(E)]
+        if args.kb:
+            ws = [torch.cat([K.weights_kblock(w[: 2 * f * d].view(2 * f, d)).view(-1),
+                             K.weights_kblock(w[2 * f * d:].view(d, f)).view(-1)]) for w in ws]
+        kb = bool(args.kb)
         R = max(T * k, M)
         xp = torch.randn(R, d, dtype=bf, device=dev)
         y = torch.empty(R, d, dtype=bf, device=dev)
@@ -176,7 +181,7 @@ def main():
         def ffn(i):
             w = ws[i % E]
             K.expert_ffn(xp, (i % E) * M % (R - M + 1), M, w[: 2 * f * d].view(2 * f, d),
-                         w[2 * f * d:].view(d, f), y, h)
+                         w[2 * f * d:].view(d, f), y, h, kblocked=kb)
         t = timed(ffn, args.iters, st)
         byt = 3 * d * f * 2 + M * (2 * d * 2 + 2 * f * 2)
         res["expert_ffn"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9, "TFLOPs": 6 * M * d * f / t / 1e12}
@@ -185,7 +190,7 @@ def main():
 
         def g1(i):
             w = ws[i % E]
-            K.gemm(xp, w[: 2 * f * d].view(2 * f, d), c=h, epilogue=2, row_offset=0, m=M)
+            K.gemm(xp, w[: 2 * f * d].view(2 * f, d), c=h, epilogue=2, row_offset=0, m=M, kblocked=kb)
         t = timed(g1, args.iters, st)
         dump_trace("gemm_swiglu")
         res["gemm_swiglu"] = {"M": M, "us": t * 1e6, "GBs": (2 * d * f * 2) / t / 1e9}
@@ -194,7 +199,7 @@ def main():
 
         def g2(i):
             w = ws[i % E]
-            K.gemm(h, w[2 * f * d:].view(d, f), c=y[:M], m=M)
+            K.gemm(h, w[2 * f * d:].view(d, f), c=y[:M], m=M, kblocked=kb)
         t = timed(g2, args.iters, st)
         dump_trace("gemm_down")
         res["gemm_down"] = {"M": M, "us": t * 1e6, "GBs": (d * f * 2) / t / 1e9}
