@@ -29,6 +29,7 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ seq, float theta,
                                    uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int cap, int sink,
                                    int chunk_last_pos) {
+    pdl_enter();
     const int half = hd / 2;
     const int heads = Hq + Hkv;
     const int64_t per_tok = static_cast<int64_t>(heads) * half + static_cast<int64_t>(Hkv) * half;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kRopeThreads)
 rope_append_tok_kernel(uint16_t* __restrict__ qkv, int Hq, int Hkv, int hd, const int32_t* __restrict__ pos,
                        const int32_t* __restrict__ seq, float theta, uint16_t* __restrict__ kc,
                        uint16_t* __restrict__ vc, int cap, int sink, int chunk_last_pos) {
+    pdl_enter();
     extern __shared__ float cs_tab[];  // [half] cos, then [half] sin
     const int half = hd / 2;
     const int64_t t = blockIdx.x;
@@ -636,6 +638,7 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
                        const int32_t* __restrict__ seq, int Hq, int Hkv, int HG, int cap, float scale_log2,
                        float* part_o, float* part_ml, int n_chunks, int64_t n_items, uint16_t* __restrict__ out,
                        unsigned long long* counters, uint32_t tag, int whole, int nst, int mode) {
+    pdl_enter();
     const int G = Hq / Hkv, HGn = Hkv / HG;
     const uint32_t box_bytes = kDmSlots * HG * HD * 2;
     const int qelems = HG * G * HD;
@@ -1264,14 +1267,13 @@ extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int 
     // dozen tokens) spread better with a thread per element.
     if (g_rope_tok && T >= 4 * 148 && hd % 8 == 0 && T <= 0x7fffffff &&
         ((reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache)) & 15) == 0) {
-        rope_append_tok_kernel<<<static_cast<unsigned>(T), kRopeThreads, static_cast<size_t>(hd) * 4, stream>>>(
-            qkv, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink, chunk_last_pos);
+        if (int rc_ = launch_pdl(rope_append_tok_kernel, dim3(static_cast<unsigned>(T)), dim3(kRopeThreads), static_cast<size_t>(hd) * 4, stream, qkv, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink, chunk_last_pos)) return rc_;
         return check_launch();
     }
     const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
-    rope_append_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(qkv, T, Hq, Hkv, hd, pos, seq,
+    if (int rc_ = launch_pdl(rope_append_kernel, dim3(static_cast<int>((n + 255) / 256)), dim3(256), 0, stream, qkv, T, Hq, Hkv, hd, pos, seq,
                                                                                rope_theta, k_cache, v_cache, cap, sink,
-                                                                               chunk_last_pos);
+                                                                               chunk_last_pos)) return rc_;
     return check_launch();
 }
 
@@ -1406,10 +1408,9 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
         const uint32_t tag = 0x7FC00000u | (epoch.fetch_add(1) & 0x3FFFFFu);
         auto* counters = reinterpret_cast<unsigned long long*>(
             (reinterpret_cast<uintptr_t>(part_o + T * n_chunks * Hq * hd) + 7) & ~uintptr_t(7));
-        kern<<<ctas, (HG + 1) * 32, msmem, stream>>>(mk, mv, q, q_stride, pos, seq, Hq, Hkv, HG, cap,
-                                                     scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items,
-                                                     out, counters, tag, whole, nst, g_decode_mma);
-        return check_launch();
+        return launch_pdl(kern, dim3(ctas), dim3((HG + 1) * 32), msmem, stream, mk, mv, q, q_stride, pos, seq, Hq,
+                          Hkv, HG, cap, scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items, out, counters,
+                          tag, whole, nst, g_decode_mma);
     }
     auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;
     KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -137,6 +137,36 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void griddep_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Entry of a kernel launched by launch_pdl: release the next kernel of the
+// stream at once (it may become resident and wait), then wait for the
+// previous kernel to complete before any global memory access.
+__device__ __forceinline__ void pdl_enter() {
+    griddep_launch_dependents();
+    griddep_wait();
+}
+
+extern int g_pdl;  // kl_tune(KL_TUNE_PDL, ...), abi.cu
+
+// Launch as a programmatic-dependent-launch secondary (when g_pdl): the
+// kernel may be scheduled while the previous kernel of the stream drains,
+// hiding the launch latency between the short decode-path kernels. Every
+// kernel launched this way calls pdl_enter() first.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    return static_cast<int>(cudaGetLastError());
+}
+
 // Named barrier over a subset of warps (id 1..15; count = threads).
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

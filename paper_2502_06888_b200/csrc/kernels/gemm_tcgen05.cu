@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, STAGES>::kMinBlocks))
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   int a_row0, int M, int kb_per_split, int b_half_rows, uint16_t* __restrict__ c, int ldc,
                   const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld) {
+    pdl_enter();
     using C = Cfg<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -398,6 +399,7 @@ gemm_persistent_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid
 template <int EPI>
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int ws_ld, int n_out, int pair_bn,
                                      uint16_t* __restrict__ c, int ldc, const uint16_t* __restrict__ r) {
+    pdl_enter();
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int quads = n_out / 4;
     if (q >= static_cast<int64_t>(M) * quads) return;
@@ -992,9 +994,8 @@ int launch(const Launch& L, cudaStream_t stream) {
         configured = true;
     }
     const dim3 grid(L.n_tiles, (L.M + BM - 1) / BM, L.splits);
-    gemm_bf16_tcgen05<BN, EPI, PAIRED, STAGES><<<grid, kThreads, C::kSmemBytes, stream>>>(
-        ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK / L.splits, L.b_half_rows, L.c, L.ldc, L.r, L.ws,
-        L.ws_ld);
+    if (int rc_ = launch_pdl(gemm_bf16_tcgen05<BN, EPI, PAIRED, STAGES>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK / L.splits, L.b_half_rows, L.c, L.ldc, L.r, L.ws,
+        L.ws_ld)) return rc_;
     return check_launch();
 }
 
@@ -1026,8 +1027,7 @@ int launch_persistent(const Launch& L, cudaStream_t stream) {
 template <int EPI>
 int reduce(const Launch& L, int n_out, int pair_bn, cudaStream_t stream) {
     const int64_t threads = static_cast<int64_t>(L.M) * (n_out / 4);
-    splitk_reduce_kernel<EPI><<<static_cast<int>((threads + 255) / 256), 256, 0, stream>>>(
-        L.ws, L.splits, L.M, L.ws_ld, n_out, pair_bn, L.c, L.ldc, L.r);
+    if (int rc_ = launch_pdl(splitk_reduce_kernel<EPI>, dim3(static_cast<int>((threads + 255) / 256)), dim3(256), 0, stream, L.ws, L.splits, L.M, L.ws_ld, n_out, pair_bn, L.c, L.ldc, L.r)) return rc_;
     return check_launch();
 }
 

@@ -74,6 +74,7 @@ gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ no
                  const uint16_t* __restrict__ wg, int T, int d, int E, int k, float eps, int score_mode,
                  uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                  float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    pdl_enter();
     const int tok = blockIdx.x;
     const int wid = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -157,6 +158,7 @@ gate_topk_block_kernel(const uint16_t* __restrict__ h, const uint16_t* __restric
                        const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
                        uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                        float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    pdl_enter();
     constexpr int d = NC * 256;
     __shared__ float lg[64];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,6 +272,7 @@ gate_topk_warp_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict
                       const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
                       uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                       float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    pdl_enter();
     constexpr int d = NC * 256;
     __shared__ float lg_all[4][64];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -376,6 +379,7 @@ gate_topk_warp_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict
 
 __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int64_t T, int d,
                                float eps, uint16_t* __restrict__ out) {
+    pdl_enter();
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= T) return;
@@ -389,10 +393,10 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
 __global__ void __launch_bounds__(256)
 rmsnorm_row_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d, float eps,
                    uint16_t* __restrict__ out) {
-    // The QKV GEMM that follows (launched with programmatic dependent
-    // launch) may start now and prefetch its weights; it reads this
-    // kernel's output only after griddepcontrol.wait.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_enter();
+    // (pdl_enter released the QKV GEMM that follows: it may start now and
+    // prefetch its weights; it reads this kernel's output only after
+    // griddepcontrol.wait.)
     const int64_t row = blockIdx.x;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float rstd = row_rstd(x + row * d, d, eps, lane);
@@ -419,6 +423,7 @@ constexpr int kChunk = 1024;
 __global__ void __launch_bounds__(kChunk)
 permute_rank_kernel(const int32_t* __restrict__ idx, int64_t R, int E, int32_t* __restrict__ chunk_counts,
                     int32_t* __restrict__ local_rank, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+    pdl_enter();
     __shared__ int32_t warp_cnt[32][64];
     __shared__ int32_t tot[64];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -472,6 +477,7 @@ permute_rank_kernel(const int32_t* __restrict__ idx, int64_t R, int E, int32_t* 
 // One thread per expert: totals, exclusive offsets, per-chunk bases.
 __global__ void permute_scan_kernel(int32_t* __restrict__ chunk_counts, int64_t n_chunks, int E,
                                     int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+    pdl_enter();
     __shared__ int32_t total[64];
     const int e = threadIdx.x;
     if (e < E) {
@@ -513,6 +519,7 @@ permute_scatter_kernel(const int32_t* __restrict__ idx, int64_t R, int k, int E,
                        const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ local_rank,
                        const uint16_t* __restrict__ x2, int d, int32_t* __restrict__ pos,
                        int32_t* __restrict__ row_token, uint16_t* __restrict__ xp) {
+    pdl_enter();
     const int64_t r = blockIdx.x;
     if (r >= R) return;
     const int e = idx[r];
@@ -552,6 +559,7 @@ template <int KMAX>
 __global__ void __launch_bounds__(kRowThreads)
 combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos, const float* __restrict__ weight,
                const uint16_t* resid, int64_t T, int k, int d, uint16_t* out) {
+    pdl_enter();
     const int64_t t = blockIdx.x;
     if (t >= T) return;
     int32_t p[KMAX];
@@ -610,6 +618,7 @@ combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos, 
 // ------------------------------------------------------------ prefetcher --
 __global__ void coact_kernel(const int32_t* __restrict__ prev, const int32_t* __restrict__ cur, int64_t T, int k,
                              int E, int layer, int64_t* __restrict__ table, int64_t* __restrict__ marginal) {
+    pdl_enter();
     extern __shared__ int32_t cnt[];  // E*E (or E for the marginal)
     const int cells = layer == 0 ? E : E * E;
     for (int i = threadIdx.x; i < cells; i += blockDim.x) cnt[i] = 0;
@@ -634,6 +643,7 @@ __global__ void coact_kernel(const int32_t* __restrict__ prev, const int32_t* __
 
 __global__ void predict_kernel(const int32_t* __restrict__ hist, const int64_t* __restrict__ table, int E,
                                int layer, int64_t* __restrict__ score) {
+    pdl_enter();
     const int b = threadIdx.x;
     if (b >= E) return;
     const int64_t* tab = table + static_cast<int64_t>(layer - 1) * E * E;
@@ -672,6 +682,7 @@ __global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64
 __global__ void route_override_kernel(const int32_t* __restrict__ forced, const float* __restrict__ logits, int T,
                                       int E, int k, int32_t* __restrict__ idx, float* __restrict__ weight,
                                       int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+    pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
     float v[8], mx = -INFINITY, sum = 0.f;
@@ -693,6 +704,7 @@ __global__ void route_override_kernel(const int32_t* __restrict__ forced, const 
 
 __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __restrict__ table, int64_t T, int d,
                              uint16_t* __restrict__ out) {
+    pdl_enter();
     const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (t >= T) return;
@@ -704,6 +716,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const uint16_t* __
 
 // Greedy decode: first index of the row maximum (bf16 logits).
 __global__ void argmax_kernel(const uint16_t* __restrict__ logits, int64_t T, int V, int32_t* __restrict__ out) {
+    pdl_enter();
     const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (t >= T) return;
@@ -752,12 +765,10 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
 #define KL_GATE_WARP(NC)                                                                                          \
     case NC:                                                                                                      \
         if (per_block)                                                                                            \
-            gate_topk_block_kernel<NC><<<static_cast<unsigned>(T), 256, 0, stream>>>(                             \
-                h, norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);               \
-        else                                                                                                      \
-            gate_topk_warp_kernel<NC><<<blocks, 128, 0, stream>>>(h, norm_w, wg, T, E, k, eps, score_mode, x2,     \
-                                                                  logits, idx, weight, hist, first_pos);          \
-        return check_launch();
+            return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, h, \
+                              norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);     \
+        return launch_pdl(gate_topk_warp_kernel<NC>, dim3(blocks), dim3(128), 0, stream, h, norm_w, wg, T, E, k, eps, \
+                          score_mode, x2, logits, idx, weight, hist, first_pos);
     switch (d / 256) {
         KL_GATE_WARP(2)
         KL_GATE_WARP(4)
@@ -767,9 +778,8 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
         default: break;
     }
 #undef KL_GATE_WARP
-    gate_topk_kernel<<<T, kGateWarps * 32, 0, stream>>>(
-        h, norm_w, wg, T, d, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);
-    return check_launch();
+    return launch_pdl(gate_topk_kernel, dim3(T), dim3(kGateWarps * 32), 0, stream, h, norm_w, wg, T, d, E, k, eps,
+                      score_mode, x2, logits, idx, weight, hist, first_pos);
 }
 
 extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps, uint16_t* out,
@@ -777,10 +787,9 @@ extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d
     if (T < 0 || d <= 0 || d % 256 != 0 || !x || !w || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
     if (T <= 4 * 148)
-        rmsnorm_row_kernel<<<static_cast<unsigned>(T), 256, 0, stream>>>(x, w, d, eps, out);
-    else
-        rmsnorm_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(x, w, T, d, eps, out);
-    return check_launch();
+        return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out);
+    return launch_pdl(rmsnorm_kernel, dim3(grid_for(T, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), 0, stream, x, w, T,
+                      d, eps, out);
 }
 
 extern "C" int64_t kl_permute_workspace_bytes(int64_t R, int E) {
@@ -801,17 +810,16 @@ extern "C" int kl_permute(const int32_t* idx, int64_t T, int k, int E, const uin
     int32_t* local_rank = chunk_counts + chunks * E;
     if (R > 0) {
         // One chunk: rank + scan in a single launch.
-        permute_rank_kernel<<<static_cast<int>(chunks), kChunk, 0, stream>>>(
-            idx, R, E, chunk_counts, local_rank, chunks == 1 ? counts : nullptr, chunks == 1 ? offsets : nullptr);
+        if (int rc_ = launch_pdl(permute_rank_kernel, dim3(static_cast<int>(chunks)), dim3(kChunk), 0, stream, idx, R, E, chunk_counts, local_rank, chunks == 1 ? counts : nullptr, chunks == 1 ? offsets : nullptr)) return rc_;
         KL_CUDA_TRY(cudaGetLastError());
     }
     if (chunks != 1) {
-        permute_scan_kernel<<<1, 64, 0, stream>>>(chunk_counts, chunks, E, counts, offsets);
+        if (int rc_ = launch_pdl(permute_scan_kernel, dim3(1), dim3(64), 0, stream, chunk_counts, chunks, E, counts, offsets)) return rc_;
         KL_CUDA_TRY(cudaGetLastError());
     }
     if (R == 0) return KL_OK;
-    permute_scatter_kernel<<<static_cast<unsigned>(R), kRowThreads, 0, stream>>>(idx, R, k, E, chunk_counts,
-                                                                                local_rank, x2, d, pos, row_token, xp);
+    if (int rc_ = launch_pdl(permute_scatter_kernel, dim3(static_cast<unsigned>(R)), dim3(kRowThreads), 0, stream, idx, R, k, E, chunk_counts,
+                                                                                local_rank, x2, d, pos, row_token, xp)) return rc_;
     return check_launch();
 }
 
@@ -820,10 +828,10 @@ extern "C" int kl_combine(const uint16_t* y, const int32_t* pos, const float* we
     if (T < 0 || k < 1 || k > 8 || d % 8 != 0 || !y || !pos || !weight || !resid || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
     if (k <= 2)
-        combine_kernel<2><<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(y, pos, weight, resid, T, k, d, out);
-    else
-        combine_kernel<8><<<static_cast<unsigned>(T), kRowThreads, 0, stream>>>(y, pos, weight, resid, T, k, d, out);
-    return check_launch();
+        return launch_pdl(combine_kernel<2>, dim3(static_cast<unsigned>(T)), dim3(kRowThreads), 0, stream, y, pos,
+                          weight, resid, T, k, d, out);
+    return launch_pdl(combine_kernel<8>, dim3(static_cast<unsigned>(T)), dim3(kRowThreads), 0, stream, y, pos, weight,
+                      resid, T, k, d, out);
 }
 
 extern "C" int kl_coact_update(const int32_t* prev, const int32_t* cur, int64_t T, int k, int E, int layer,
@@ -833,14 +841,14 @@ extern "C" int kl_coact_update(const int32_t* prev, const int32_t* cur, int64_t 
     if (T == 0) return KL_OK;
     const int cells = layer == 0 ? E : E * E;
     const int blocks = static_cast<int>(T / 256 + 1 < 148 ? T / 256 + 1 : 148);
-    coact_kernel<<<blocks, 256, cells * sizeof(int32_t), stream>>>(prev, cur, T, k, E, layer, table, marginal);
+    if (int rc_ = launch_pdl(coact_kernel, dim3(blocks), dim3(256), cells * sizeof(int32_t), stream, prev, cur, T, k, E, layer, table, marginal)) return rc_;
     return check_launch();
 }
 
 extern "C" int kl_predict_scores(const int32_t* hist, const int64_t* table, int E, int layer, int64_t* score,
                                  cudaStream_t stream) {
     if (E < 1 || E > 1024 || layer < 1 || !hist || !table || !score) return KL_EINVAL;
-    predict_kernel<<<1, E < 32 ? 32 : E, 0, stream>>>(hist, table, E, layer, score);
+    if (int rc_ = launch_pdl(predict_kernel, dim3(1), dim3(E < 32 ? 32 : E), 0, stream, hist, table, E, layer, score)) return rc_;
     return check_launch();
 }
 
@@ -857,7 +865,7 @@ extern "C" int kl_route_override(const int32_t* forced, const float* logits, int
                                  float* weight, int32_t* hist, int32_t* first_pos, cudaStream_t stream) {
     if (T < 0 || E < 1 || k < 1 || k > 8 || !forced || !logits || !idx || !weight) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    route_override_kernel<<<(T + 127) / 128, 128, 0, stream>>>(forced, logits, T, E, k, idx, weight, hist, first_pos);
+    if (int rc_ = launch_pdl(route_override_kernel, dim3((T + 127) / 128), dim3(128), 0, stream, forced, logits, T, E, k, idx, weight, hist, first_pos)) return rc_;
     return check_launch();
 }
 
@@ -865,14 +873,14 @@ extern "C" int kl_embed(const int32_t* ids, const uint16_t* table, int64_t T, in
                         cudaStream_t stream) {
     if (T < 0 || d % 8 != 0 || !ids || !table || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    embed_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(ids, table, T, d, out);
+    if (int rc_ = launch_pdl(embed_kernel, dim3(grid_for(T, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), 0, stream, ids, table, T, d, out)) return rc_;
     return check_launch();
 }
 
 extern "C" int kl_argmax_bf16(const uint16_t* logits, int64_t T, int V, int32_t* out, cudaStream_t stream) {
     if (T < 0 || V < 1 || !logits || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    argmax_kernel<<<grid_for(T, kWarpsPerBlock), kWarpsPerBlock * 32, 0, stream>>>(logits, T, V, out);
+    if (int rc_ = launch_pdl(argmax_kernel, dim3(grid_for(T, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), 0, stream, logits, T, V, out)) return rc_;
     return check_launch();
 }
 

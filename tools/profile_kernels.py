@@ -251,6 +251,59 @@ def main():
         t = timed(att2, args.iters, st)
         K.tune(K.TUNE_DECODE_MMA, 1)
         res["attn_decode_split_cudacore_b64"] = {"us": t * 1e6, "GBs": bs * cap * Hkv * hd * 2 * 2 / t / 1e9}
+    if args.only == "attnop":
+        # The whole decode attention op as the engine issues it (rmsnorm, QKV
+        # GEMM, RoPE + KV append, decode attention, o-proj with the residual
+        # add), 8 batches x 4 layers with distinct weights and KV, one CUDA
+        # graph; variants: o-proj through the weight-streaming GEMM, PDL off.
+        width = (Hq + 2 * Hkv) * hd
+        L4 = 4
+        wqkv = [torch.randn(width, d, dtype=bf, device=dev) * 0.02 for _ in range(L4)]
+        wo = [torch.randn(d, Hq * hd, dtype=bf, device=dev) * 0.02 for _ in range(L4)]
+        nw = torch.ones(d, dtype=bf, device=dev)
+        cap = 260
+        kcs = [torch.randn(T * cap * Hkv * hd, dtype=bf, device=dev) for _ in range(L4)]
+        vcs = [torch.randn(T * cap * Hkv * hd, dtype=bf, device=dev) for _ in range(L4)]
+        h = torch.randn(T, d, dtype=bf, device=dev)
+        xa = torch.empty(bs, d, dtype=bf, device=dev)
+        qkv = torch.empty(bs, width, dtype=bf, device=dev)
+        ao = torch.empty(bs, Hq * hd, dtype=bf, device=dev)
+        pos = torch.full((bs,), 600, dtype=torch.int32, device=dev)
+        seqs = [torch.arange(bs, dtype=torch.int32, device=dev) + j * bs for j in range(n)]
+
+        def op(i):
+            l, b = (i // n) % L4, i % n
+            hb = h[b * bs:(b + 1) * bs]
+            K.rmsnorm(hb, nw, out=xa)
+            K.gemm(xa, wqkv[l], c=qkv)
+            K.rope_kv_append(qkv, Hq, Hkv, hd, pos, seqs[b], 1e6, kcs[l], vcs[l], cap, 4)
+            K.attn_decode_split(qkv, width, pos, seqs[b], Hq, Hkv, hd, kcs[l], vcs[l], cap, 4, hd ** -0.5, ao)
+            K.gemm(ao, wo[l], c=hb, residual=hb, epilogue=1)
+        per = 8 * L4
+        t = timed_graph(op, per)
+        res["attn_op_b64"] = {"us": t * 1e6, "floor_us": (width * d * 2 + d * Hq * hd * 2 + bs * cap * Hkv * hd * 4) / 6.5e6}
+        K.tune(K.TUNE_STREAM_GEMM, 2)
+        t = timed_graph(op, per)
+        res["attn_op_b64_oproj_stream"] = {"us": t * 1e6}
+        K.tune(K.TUNE_STREAM_GEMM, 1)
+        K.tune(K.TUNE_PDL, 0)
+        t = timed_graph(op, per)
+        res["attn_op_b64_no_pdl"] = {"us": t * 1e6}
+        K.tune(K.TUNE_PDL, 1)
+        for nm, fn in (("rmsnorm", lambda i: K.rmsnorm(h[(i % n) * bs:(i % n + 1) * bs], nw, out=xa)),
+                       ("qkv", lambda i: K.gemm(xa, wqkv[(i // n) % L4], c=qkv)),
+                       ("rope", lambda i: K.rope_kv_append(qkv, Hq, Hkv, hd, pos, seqs[i % n], 1e6, kcs[(i // n) % L4],
+                                                           vcs[(i // n) % L4], cap, 4)),
+                       ("attn", lambda i: K.attn_decode_split(qkv, width, pos, seqs[i % n], Hq, Hkv, hd, kcs[(i // n) % L4],
+                                                              vcs[(i // n) % L4], cap, 4, hd ** -0.5, ao)),
+                       ("oproj", lambda i: K.gemm(ao, wo[(i // n) % L4], c=h[(i % n) * bs:(i % n + 1) * bs],
+                                                  residual=h[(i % n) * bs:(i % n + 1) * bs], epilogue=1))):
+            res["attn_op_part_" + nm] = {"us": timed_graph(fn, per) * 1e6}
+        K.tune(K.TUNE_STREAM_GEMM, 2)
+        res["attn_op_part_oproj_stream"] = {"us": timed_graph(
+            lambda i: K.gemm(ao, wo[(i // n) % L4], c=h[(i % n) * bs:(i % n + 1) * bs],
+                             residual=h[(i % n) * bs:(i % n + 1) * bs], epilogue=1), per) * 1e6}
+        K.tune(K.TUNE_STREAM_GEMM, 1)
     if not args.only or args.only == "route":
         h = torch.randn(T, d, dtype=bf, device=dev)
         nw = torch.ones(d, dtype=bf, device=dev)
