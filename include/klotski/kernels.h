@@ -70,11 +70,13 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_STAGES 2 /* cap on the smem pipeline depth (2..16, default 8) */
 #define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints */
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */
-#define KL_TUNE_PDL 5 /* 1 = weight-streaming GEMMs use programmatic dependent launch (default) */
+#define KL_TUNE_PDL 5 /* 1 = decode-path kernels use programmatic dependent launch (default) */
 #define KL_TUNE_PREFILL_TC 6 /* tcgen05 prefill attention: 2 = 64-key blocks, two CTAs per SM (default), 1 = 128-key blocks, 0 = CUDA-core fallback */
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
-#define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 2 (default; 3D TMA boxes, used where >= 3 stages fit) or 1 */
-#define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 0 = one CTA per SM */
+#define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 3 (default) = 2 where >= 2 stages fit, 2 = 2 where >= 3 stages fit (3D TMA boxes), 1 */
+#define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 2 = also into k-ranges differing by one unit, 0 = one CTA per SM */
+#define KL_TUNE_STREAM_L2_AHEAD 14 /* weight-streaming GEMM: weight units prefetched into L2 ahead of the smem ring (0 = off) */
+#define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */

@@ -487,6 +487,9 @@ struct StreamArgs {
     int pdl;    // launched with programmatic stream serialization
     int ks;     // k-blocks per stage: 2 = one 3D TMA box covers two 64-column k-blocks (larger copies)
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
+    int l2_ahead;  // weight units prefetched into L2 ahead of the smem ring (0 = off)
+    int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
+    int owner_extra;  // tile-aligned splits: extra units of the owner's (last) range
     const uint8_t* q4;  // Q4 variant: weights in the tiled 4-bit layout (kQ4Chunk bytes per 128x64 tile)
 };
 
@@ -507,6 +510,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ int range_begin(int c, int units, int G) {
     return static_cast<int>(static_cast<int64_t>(c) * units / G);
+}
+// First unit of CTA c. With tile-aligned splits (p.split = S > 0, G = tiles
+// x S) the owner's range (the tile's last) is p.owner_extra units longer
+// than the S - 1 equal contributor ranges, so contributors publish their
+// partials while the owner is still streaming and the owner's fixup does
+// not wait on them.
+__device__ __forceinline__ int unit_begin(const StreamArgs& p, int c, int G) {
+    if (p.split <= 0) return range_begin(c, p.units, G);
+    const int t = c / p.split, j = c % p.split;
+    return t * p.KB + j * ((p.KB - p.owner_extra) / p.split);
 }
 
 
@@ -561,7 +574,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, cta = blockIdx.x;
     const int KB = p.KB;
-    const int u0 = range_begin(cta, p.units, G), u1 = range_begin(cta + 1, p.units, G);
+    const int u0 = unit_begin(p, cta, G), u1 = unit_begin(p, cta + 1, G);
     const int t_hi = u1 > u0 ? (u1 - 1) / KB : 0, t_lo = u1 > u0 ? u0 / KB : 1;  // tiles walked t_hi .. t_lo
     const int buf_cols = NMMA * p.acc_stride;
 
@@ -609,6 +622,36 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                     tma_load_2d(sx, &tmap_x, &full[s_], kb_ * BK, a_row0);
             };
             int xkb[16];  // k-block of each stage issued before the wait
+            // L2 prefetch cursor, l2_ahead units past the ring: walks the same
+            // (tile, k-block) order as the loads, so the smem loads of those
+            // units later hit L2 (more weight bytes in flight than the ring holds).
+            int pf_t = t_hi, pf_kb = max(u0, t_hi * KB) - t_hi * KB, pf_n = 0;
+            auto prefetch_next = [&]() {
+                if (pf_t < t_lo) return;
+#pragma unroll
+                for (int j = 0; j < NMMA; ++j) {
+                    const int row = EPI == kSwiGLU ? (j == 0 ? pf_t * kWRows : p.half_rows + pf_t * kWRows)
+                                                   : (pf_t * NMMA + j) * kWRows;
+                    tma_prefetch_3d(&tmap_w, row, pf_kb * p.ks);
+                }
+                ++pf_n;
+                if (++pf_kb >= min(u1, (pf_t + 1) * KB) - pf_t * KB) {
+                    --pf_t;
+                    if (pf_t >= t_lo) pf_kb = max(u0, pf_t * KB) - pf_t * KB;
+                }
+            };
+            auto skip_next = [&]() {  // advance the cursor over a unit the ring loads itself
+                if (pf_t < t_lo) return;
+                ++pf_n;
+                if (++pf_kb >= min(u1, (pf_t + 1) * KB) - pf_t * KB) {
+                    --pf_t;
+                    if (pf_t >= t_lo) pf_kb = max(u0, pf_t * KB) - pf_t * KB;
+                }
+            };
+            if (!Q4 && p.l2_ahead > 0) {
+                for (int i = 0; i < p.stages; ++i) skip_next();
+                for (int i = 0; i < p.l2_ahead; ++i) prefetch_next();
+            }
             for (int t = t_hi; t >= t_lo; --t) {
                 const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -618,6 +661,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                         waited = true;
                         for (int i = 0; i < pending_x; ++i) load_x(i, xkb[i]);
                     }
+                    if (!Q4 && p.l2_ahead > 0 && it >= p.stages) prefetch_next();
                     mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
                     uint8_t* sw = smem + s * stage_bytes;
                     mbar_arrive_expect_tx(&full[s], Q4 ? p.NP * BK * 2 : stage_bytes);
@@ -790,7 +834,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 if (etid == 0) STREAM_TRACE(3);
                 if (kb0 > 0) {
                     int c_lo = cta - 1;
-                    while (c_lo > 0 && range_begin(c_lo, p.units, G) > t * KB) --c_lo;
+                    while (c_lo > 0 && unit_begin(p, c_lo, G) > t * KB) --c_lo;
                     if (slot_f4 * 16 <= ring_bytes) {
                     const int slot_bytes = slot_f4 * 16;
                     const int per_batch = max(1, ring_bytes / slot_bytes);
@@ -1056,8 +1100,10 @@ int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
-int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...)
-int g_stream_ks = 2;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2): 2 where >= 3 stages still fit
+int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...): 1 = equal splits, 2 = also near-equal
+int g_stream_l2_ahead = 0;  // kl_tune(KL_TUNE_STREAM_L2_AHEAD, units)
+int g_stream_owner_extra = 0;  // kl_tune(KL_TUNE_STREAM_OWNER_EXTRA, units)
+int g_stream_ks = 3;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2|3): 2 k-blocks per stage where >= 3 (2) or >= 2 (3) stages fit
 
 int sm_count() {
     static const int n = [] {
@@ -1122,8 +1168,12 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     // 16 KB ones (tools/bw_probe.cu).
     {
         const int per_kb = NMMA * kWTileBytes + p.NP * BK * 2;
-        p.ks = (!Q4 && g_stream_ks == 2 && (K / BK) % 2 == 0 &&
-                std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / (2 * per_kb)) >= 3)
+        // Knob 3 (default): two k-blocks per stage down to 2 stages. The
+        // SwiGLU pair at M = 64..192 (2 x 96 KB stages) streams 2-3 us
+        // faster than with 3-5 single-k-block stages (tools/dev/swiglu_probe2.sh).
+        const int min_stages = g_stream_ks == 3 ? 2 : 3;
+        p.ks = (!Q4 && g_stream_ks >= 2 && (K / BK) % 2 == 0 &&
+                std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / (2 * per_kb)) >= min_stages)
                    ? 2
                    : 1;  // keep >= 3 stages in flight (the SwiGLU pair's 96 KB stages would leave 2)
     }
@@ -1137,16 +1187,30 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     // units) and as the bf16 output staging tile of the last segment.
     if (p.stages * stage_bytes < p.NP * kWRows * (EPI == kResidual ? 4 : 2)) return KL_EUNSUPPORTED;
     p.hint = g_stream_hint;
+    p.l2_ahead = g_stream_l2_ahead;
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
     if (p.stages > 16) p.stages = 16;
     int G = std::max(1, std::min(sm_count() * g_stream_ctas, p.units / 4));
     if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
         G = n_tiles;  // one whole tile per CTA: no split partials, the rest of the SMs idle
-    else if (g_stream_even_split && n_tiles < G && G / n_tiles >= 2 && p.KB % (G / n_tiles) == 0)
-        G = n_tiles * (G / n_tiles);  // every tile split into the same number of equal k-ranges
-    G = static_cast<int>(std::min<int64_t>(G, (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA)));
-    G = std::min(G, static_cast<int>(kFlagBytes / 4));
+    else if (g_stream_even_split && n_tiles < G && G / n_tiles >= 2 &&
+             (p.KB % (G / n_tiles) == 0 || g_stream_even_split == 2)) {
+        // Every tile split into the same number S of k-ranges cut at tile
+        // boundaries (unit_begin), equal when S divides KB (else the owner's
+        // range takes the remainder), the owner's optionally longer.
+        G = n_tiles * (G / n_tiles);
+        p.split = G / n_tiles;
+        // Owner bonus, capped so every contributor keeps at least one unit.
+        p.owner_extra = std::max(0, std::min(g_stream_owner_extra, p.KB - 2 * p.split));
+    }
+    const int G_ws = static_cast<int>(std::min<int64_t>((ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA),
+                                                        kFlagBytes / 4));
+    if (G > G_ws) {  // workspace-limited: plain stream-K ranges over fewer CTAs
+        G = G_ws;
+        p.split = 0;
+        p.owner_extra = 0;
+    }
     if (G < 1) return KL_EUNSUPPORTED;
     p.half_rows = half_rows;
     p.c = c;
@@ -1239,9 +1303,11 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
-        case KL_TUNE_STREAM_EVEN_SPLIT: g_stream_even_split = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_EVEN_SPLIT: g_stream_even_split = value; return KL_OK;
+        case KL_TUNE_STREAM_L2_AHEAD: g_stream_l2_ahead = value < 0 ? 0 : value; return KL_OK;
+        case KL_TUNE_STREAM_OWNER_EXTRA: g_stream_owner_extra = value < 0 ? 0 : value; return KL_OK;
         case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
-            if (value != 1 && value != 2) return KL_EINVAL;
+            if (value < 1 || value > 3) return KL_EINVAL;
             g_stream_ks = value;
             return KL_OK;
         case KL_TUNE_STREAM_CTAS_PER_SM:

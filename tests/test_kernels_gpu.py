@@ -89,7 +89,7 @@ def test_gemm_residual_and_row_offset(K, cuda):
     close_bf16(to_bits(c), ref)
 
 
-@pytest.mark.parametrize("ks", [1, 2])
+@pytest.mark.parametrize("ks", [1, 2, 3])
 @pytest.mark.parametrize("nmma", [1, 2])
 @pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (16, 4096, 4096, 0), (129, 1024, 2048, 1),
                                         (256, 2048, 1024, 2), (77, 28672 // 8, 4096, 2), (200, 384, 8192, 0)])
@@ -114,7 +114,7 @@ def test_gemm_weight_streaming(K, cuda, ks, nmma, M, N, Kd, epi):
     finally:
         K.tune(K.TUNE_STREAM_NMMA, 1)
         K.tune(K.TUNE_STREAM_GEMM, 1)
-        K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, 2)
+        K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, 3)
     assert torch.equal(c, c2)  # deterministic split reduction
     x = a[off:off + M]
     if epi == 2:

@@ -132,10 +132,13 @@ def main():
     ap.add_argument("--debug", type=int, default=0)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--persist", type=int, default=1)
-    ap.add_argument("--ks", type=int, default=2, help="stream GEMM k-blocks per stage")
+    ap.add_argument("--ks", type=int, default=3, help="stream GEMM k-blocks per stage (knob 1|2|3)")
     ap.add_argument("--even", type=int, default=1, help="stream GEMM equal k-splits per tile")
     ap.add_argument("--whole", type=int, default=70, help="whole-tile grid when tiles >= pct%% of SMs")
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
+    ap.add_argument("--l2-ahead", type=int, default=-1, help="stream GEMM L2 prefetch distance (units; -1 = default)")
+    ap.add_argument("--split", type=int, default=-1, help="stream GEMM even-split mode (-1 = default)")
+    ap.add_argument("--owner-extra", type=int, default=-1, help="stream GEMM owner-range bonus (units; -1 = default)")
     ap.add_argument("--kb", type=int, default=1, help="expert weights in the K-blocked layout (the engine's)")
     ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
     args = ap.parse_args()
@@ -144,7 +147,11 @@ def main():
     K.tune(K.TUNE_STREAM_WHOLE_TILES, args.whole)
     K.tune(K.TUNE_GEMM_PERSISTENT, args.persist)
     K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, args.ks)
-    K.tune(K.TUNE_STREAM_EVEN_SPLIT, args.even)
+    K.tune(K.TUNE_STREAM_EVEN_SPLIT, args.even if args.split < 0 else args.split)
+    if args.owner_extra >= 0:
+        K.tune(K.TUNE_STREAM_OWNER_EXTRA, args.owner_extra)
+    if args.l2_ahead >= 0:
+        K.tune(K.TUNE_STREAM_L2_AHEAD, args.l2_ahead)
     global TRACE, GAP_MS
     GAP_MS = args.gap_ms
     TRACE = bool(args.debug & 128)
@@ -290,6 +297,16 @@ def main():
         t = timed_graph(op, per)
         res["attn_op_b64_no_pdl"] = {"us": t * 1e6}
         K.tune(K.TUNE_PDL, 1)
+        K.tune(K.TUNE_STREAM_EVEN_SPLIT, 2)
+        t = timed_graph(op, per)
+        res["attn_op_b64_near_even"] = {"us": t * 1e6}
+        res["attn_op_part_qkv_near_even"] = {"us": timed_graph(lambda i: K.gemm(xa, wqkv[(i // n) % L4], c=qkv), per) * 1e6}
+        K.tune(K.TUNE_STREAM_GEMM, 2)
+        res["attn_op_part_oproj_stream_near_even"] = {"us": timed_graph(
+            lambda i: K.gemm(ao, wo[(i // n) % L4], c=h[(i % n) * bs:(i % n + 1) * bs],
+                             residual=h[(i % n) * bs:(i % n + 1) * bs], epilogue=1), per) * 1e6}
+        K.tune(K.TUNE_STREAM_GEMM, 1)
+        K.tune(K.TUNE_STREAM_EVEN_SPLIT, 1)
         for nm, fn in (("rmsnorm", lambda i: K.rmsnorm(h[(i % n) * bs:(i % n + 1) * bs], nw, out=xa)),
                        ("qkv", lambda i: K.gemm(xa, wqkv[(i // n) % L4], c=qkv)),
                        ("rope", lambda i: K.rope_kv_append(qkv, Hq, Hkv, hd, pos, seqs[i % n], 1e6, kcs[(i // n) % L4],
