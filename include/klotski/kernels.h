@@ -77,6 +77,8 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 2 = also into k-ranges differing by one unit, 0 = one CTA per SM */
 #define KL_TUNE_STREAM_L2_AHEAD 14 /* weight-streaming GEMM: weight units prefetched into L2 ahead of the smem ring (0 = off) */
 #define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
+#define KL_TUNE_STREAM_BULK_PUBLISH 17 /* weight-streaming GEMM: split contributors with an idle ring publish partials via smem + one bulk copy (1) or direct stores (0) */
+#define KL_TUNE_STREAM_FUSED_FIXUP 16 /* weight-streaming GEMM: 1 (default) = owners add split partials during the epilogue pass (dedicated staging region), 0 = TMEM fixup first */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */

@@ -490,6 +490,9 @@ struct StreamArgs {
     int l2_ahead;  // weight units prefetched into L2 ahead of the smem ring (0 = off)
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
     int owner_extra;  // tile-aligned splits: extra units of the owner's (last) range
+    int bulk_publish; // contributors whose ring is idle publish their partial with one bulk copy
+    int stage_off;    // > 0: byte offset of a dedicated output staging region (owner adds the
+                      // landed partials while it reads TMEM for the epilogue; no TMEM store-back)
     const uint8_t* q4;  // Q4 variant: weights in the tiled 4-bit layout (kQ4Chunk bytes per 128x64 tile)
 };
 
@@ -522,6 +525,13 @@ __device__ __forceinline__ int unit_begin(const StreamArgs& p, int c, int G) {
     return t * p.KB + j * ((p.KB - p.owner_extra) / p.split);
 }
 
+
+// 1D bulk copy shared -> global (async proxy, bulk group of the issuing thread).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(dst)),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
 
 // 1D bulk copy global -> shared (async proxy), completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -783,6 +793,45 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 // layout [j][16-column chunk][float4 i][feature row] so each
                 // warp store / load is 512 contiguous bytes.
                 if (etid == 0) STREAM_TRACE(8);
+                if (p.bulk_publish && t == t_lo && slot_f4 * 16 <= ring_bytes) {
+                    // Ring idle (last segment walked): stage the partial in
+                    // smem in the slot's layout, then one bulk copy to global.
+                    float4* sslot = reinterpret_cast<float4*>(smem);
+                    for (int j = 0; j < NMMA; ++j)
+                        for (int col = 0; col < cols; col += 32) {
+                            float v[32];
+                            tmem_ld32(acc0 + j * p.acc_stride + col, v);
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                if (col + 16 * h >= cols) break;
+                                float4* dst = sslot + (static_cast<int64_t>(j * nch + (col >> 4) + h) * 4) * kWRows + frow;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    dst[i * kWRows] = make_float4(v[16 * h + 4 * i], v[16 * h + 4 * i + 1],
+                                                                  v[16 * h + 4 * i + 2], v[16 * h + 4 * i + 3]);
+                            }
+                        }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[b]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    named_bar_sync(1, 128);
+                    if (etid == 0) {
+                        // Only the column chunks the epilogue reads: [j][chunk < nch_live][4][128].
+                        const int nch_live = cols / 16;
+                        for (int j = 0; j < NMMA; ++j) {
+                            const uint32_t bytes = static_cast<uint32_t>(nch_live * 4 * kWRows * 16);
+                            const int64_t off = static_cast<int64_t>(j * nch) * 4 * kWRows;
+                            bulk_s2g(slot4(cta) + off, sslot + off, bytes);
+                        }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        st_release_gpu(p.flags + cta, p.epoch);
+                        STREAM_TRACE(9);
+                    }
+                    continue;
+                }
                 float4* slot = slot4(cta);
                 for (int j = 0; j < NMMA; ++j) {
                     for (int col = 0; col < cols; col += 32) {
@@ -832,10 +881,36 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 // Last tile walked (ring idle from here on): owner fixup,
                 // then the epilogue staged through shared memory.
                 if (etid == 0) STREAM_TRACE(3);
+                int fused_nq = 0;  // contributors' partials landed in the ring, added in the epilogue pass
                 if (kb0 > 0) {
                     int c_lo = cta - 1;
                     while (c_lo > 0 && unit_begin(p, c_lo, G) > t * KB) --c_lo;
-                    if (slot_f4 * 16 <= ring_bytes) {
+                    if (p.stage_off > 0 && (cta - c_lo) * slot_f4 * 16 <= ring_bytes) {
+                        // Every partial lands at once; the epilogue below adds
+                        // them to the accumulator it reads (own partial first,
+                        // then ascending CTA, as the TMEM fixup would).
+                        const int slot_bytes = slot_f4 * 16;
+                        fused_nq = cta - c_lo;
+                        if (etid < 32) {
+                            // One lane per contributor: each polls its own flag and
+                            // pulls that partial as soon as it is published.
+                            if (etid == 0) mbar_arrive_expect_tx(part_bar, static_cast<uint32_t>(fused_nq * slot_bytes));
+                            __syncwarp();
+                            for (int qi = etid; qi < fused_nq; qi += 32) {
+                                while (ld_relaxed_gpu(p.flags + c_lo + qi) != p.epoch) {
+                                }
+                                fence_acq_rel_gpu();
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
+                                for (int off = 0; off < slot_bytes; off += 32768)
+                                    bulk_g2s(smem + qi * slot_bytes + off,
+                                             reinterpret_cast<const uint8_t*>(slot4(c_lo + qi)) + off,
+                                             static_cast<uint32_t>(min(32768, slot_bytes - off)), part_bar);
+                            }
+                        }
+                        if (etid == 0) STREAM_TRACE(4);
+                        mbar_wait(part_bar, 0);
+                        if (etid == 0) STREAM_TRACE(5);
+                    } else if (slot_f4 * 16 <= ring_bytes) {
                     const int slot_bytes = slot_f4 * 16;
                     const int per_batch = max(1, ring_bytes / slot_bytes);
                     int phase = 0;
@@ -940,8 +1015,10 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 if (etid == 0) STREAM_TRACE(6);
                 // Stage bf16 outputs [token][128 features] in smem, then
                 // coalesced 16-byte row stores.
-                uint16_t* stage = reinterpret_cast<uint16_t*>(smem);
-                float* stage_f = reinterpret_cast<float*>(smem);  // residual: fp32 staging, one rounding after the add
+                uint8_t* stage_base = smem + (fused_nq > 0 ? p.stage_off : 0);
+                uint16_t* stage = reinterpret_cast<uint16_t*>(stage_base);
+                float* stage_f = reinterpret_cast<float*>(stage_base);  // residual: fp32 staging, one rounding after the add
+                const float4* land = reinterpret_cast<const float4*>(smem);
                 constexpr int kOut = EPI == kSwiGLU ? 1 : NMMA;
                 for (int j = 0; j < kOut; ++j) {
                     const int64_t feat0 = static_cast<int64_t>(EPI == kSwiGLU ? t : t * NMMA + j) * kWRows;
@@ -949,7 +1026,21 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                         float acc[2][16];
 #pragma unroll
                         for (int jj = 0; jj < NMMA; ++jj)
-                            if (EPI == kSwiGLU || jj == j) tmem_ld16(acc0 + jj * p.acc_stride + col, acc[jj]);
+                            if (EPI == kSwiGLU || jj == j) {
+                                tmem_ld16(acc0 + jj * p.acc_stride + col, acc[jj]);
+                                for (int q = 0; q < fused_nq; ++q) {
+                                    const float4* src = land + static_cast<int64_t>(q) * slot_f4 +
+                                                        (static_cast<int64_t>(jj * nch + (col >> 4)) * 4) * kWRows + frow;
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        const float4 w = src[i * kWRows];
+                                        acc[jj][4 * i] += w.x;
+                                        acc[jj][4 * i + 1] += w.y;
+                                        acc[jj][4 * i + 2] += w.z;
+                                        acc[jj][4 * i + 3] += w.w;
+                                    }
+                                }
+                            }
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const float v = epi_value<EPI>(acc, j, i);
@@ -1103,6 +1194,8 @@ int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): who
 int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...): 1 = equal splits, 2 = also near-equal
 int g_stream_l2_ahead = 0;  // kl_tune(KL_TUNE_STREAM_L2_AHEAD, units)
 int g_stream_owner_extra = 0;  // kl_tune(KL_TUNE_STREAM_OWNER_EXTRA, units)
+int g_stream_fused_fixup = 1;  // kl_tune(KL_TUNE_STREAM_FUSED_FIXUP, 0|1)
+int g_stream_bulk_publish = 0;  // kl_tune(KL_TUNE_STREAM_BULK_PUBLISH, 0|1)
 int g_stream_ks = 3;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2|3): 2 k-blocks per stage where >= 3 (2) or >= 2 (3) stages fit
 
 int sm_count() {
@@ -1188,6 +1281,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     if (p.stages * stage_bytes < p.NP * kWRows * (EPI == kResidual ? 4 : 2)) return KL_EUNSUPPORTED;
     p.hint = g_stream_hint;
     p.l2_ahead = g_stream_l2_ahead;
+    p.bulk_publish = g_stream_bulk_publish;
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
     if (p.stages > 16) p.stages = 16;
@@ -1227,7 +1321,16 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
         mw = mx;  // unused: the Q4 variant bulk-copies packed tiles
     else if ((rc = wkb ? make_map_kblocked(&mw, b, b_rows, K, kWRows, p.ks) : make_map_kchunks(&mw, b, b_rows, K, kWRows, p.ks)))
         return rc;
-    const int smem = p.stages * per_stage + 1024 + 1024;  // rings + alignment + barriers
+    int smem = p.stages * per_stage + 1024 + 1024;  // rings + alignment + barriers
+    // A dedicated output staging region after the barriers when it fits:
+    // the owner then adds the landed partials during its epilogue pass.
+    {
+        const int stage_bytes = p.NP * kWRows * (EPI == kResidual ? 4 : 2);
+        if (g_stream_fused_fixup && smem + stage_bytes <= kStreamSmemBudget + 2048) {
+            p.stage_off = p.stages * per_stage + 1024;
+            smem += stage_bytes;
+        }
+    }
     static bool configured = false;  // per template instance
     if (!configured) {
         KL_CUDA_TRY(cudaFuncSetAttribute(gemm_stream_kernel<EPI, NMMA, Q4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1306,6 +1409,8 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_EVEN_SPLIT: g_stream_even_split = value; return KL_OK;
         case KL_TUNE_STREAM_L2_AHEAD: g_stream_l2_ahead = value < 0 ? 0 : value; return KL_OK;
         case KL_TUNE_STREAM_OWNER_EXTRA: g_stream_owner_extra = value < 0 ? 0 : value; return KL_OK;
+        case KL_TUNE_STREAM_FUSED_FIXUP: g_stream_fused_fixup = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_BULK_PUBLISH: g_stream_bulk_publish = value != 0; return KL_OK;
         case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
             if (value < 1 || value > 3) return KL_EINVAL;
             g_stream_ks = value;

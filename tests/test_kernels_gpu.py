@@ -89,11 +89,12 @@ def test_gemm_residual_and_row_offset(K, cuda):
     close_bf16(to_bits(c), ref)
 
 
+@pytest.mark.parametrize("fused", [0, 1])
 @pytest.mark.parametrize("ks", [1, 2, 3])
 @pytest.mark.parametrize("nmma", [1, 2])
 @pytest.mark.parametrize("M,N,Kd,epi", [(1, 256, 512, 0), (16, 4096, 4096, 0), (129, 1024, 2048, 1),
                                         (256, 2048, 1024, 2), (77, 28672 // 8, 4096, 2), (200, 384, 8192, 0)])
-def test_gemm_weight_streaming(K, cuda, ks, nmma, M, N, Kd, epi):
+def test_gemm_weight_streaming(K, cuda, fused, ks, nmma, M, N, Kd, epi):
     """Decode path (swap-AB, stream-K): every shape/epilogue against the
     oracle, and bit-identical to itself across NMMA settings' reruns."""
     rows, off = M + 40, 13
@@ -105,17 +106,31 @@ def test_gemm_weight_streaming(K, cuda, ks, nmma, M, N, Kd, epi):
     K.tune(K.TUNE_STREAM_NMMA, nmma)
     K.tune(K.TUNE_STREAM_GEMM, 2)  # force the streaming path at these small shapes
     K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, ks)
+    K.tune(K.TUNE_STREAM_FUSED_FIXUP, fused)
     try:
         assert K.workspace_bytes(M, N, Kd, epi) > 0
         rd = to_dev(r, cuda) if r is not None else None
         c = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
         c2 = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
+        c3 = None
+        c4 = None
+        if fused:  # partials added in the epilogue pass == TMEM fixup first, bit for bit
+            K.tune(K.TUNE_STREAM_FUSED_FIXUP, 0)
+            c3 = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
+            K.tune(K.TUNE_STREAM_FUSED_FIXUP, 1)
+            K.tune(K.TUNE_STREAM_BULK_PUBLISH, 1)  # contributors publish through smem + one bulk copy
+            c4 = K.gemm(ad, bd, residual=rd, epilogue=epi, row_offset=off, m=M)
+            K.tune(K.TUNE_STREAM_BULK_PUBLISH, 0)
         torch.cuda.synchronize()
     finally:
         K.tune(K.TUNE_STREAM_NMMA, 1)
         K.tune(K.TUNE_STREAM_GEMM, 1)
         K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, 3)
+        K.tune(K.TUNE_STREAM_FUSED_FIXUP, 1)
     assert torch.equal(c, c2)  # deterministic split reduction
+    if c3 is not None:
+        assert torch.equal(c, c3)
+        assert torch.equal(c, c4)
     x = a[off:off + M]
     if epi == 2:
         g = orc.gemm_f32(np.ascontiguousarray(x), np.ascontiguousarray(b[:n_out])).astype(np.float64)

@@ -32,7 +32,7 @@ def dump_trace(label):
     buf = (ctypes.c_ulonglong * (256 * 12))()
     K._lib.kl_stream_trace(buf, 256)
     a = np.array(buf, dtype=np.float64).reshape(256, 12)[:148]
-    t0 = a[:, 0].min()
+    t0 = a[:, 0][a[:, 0] > 0].min()
     rel = (a - t0) / 1e3
     rel[a == 0] = np.nan
     names = ["start", "mma0", "mma_end", "epi_last", "flags_ok", "landed", "sums_done", "end", "contrib0",
@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
     ap.add_argument("--l2-ahead", type=int, default=-1, help="stream GEMM L2 prefetch distance (units; -1 = default)")
     ap.add_argument("--split", type=int, default=-1, help="stream GEMM even-split mode (-1 = default)")
+    ap.add_argument("--bulk-publish", type=int, default=-1, help="stream GEMM contributors publish via smem + bulk copy")
+    ap.add_argument("--fused-fixup", type=int, default=-1, help="stream GEMM owners add partials in the epilogue pass")
     ap.add_argument("--owner-extra", type=int, default=-1, help="stream GEMM owner-range bonus (units; -1 = default)")
     ap.add_argument("--kb", type=int, default=1, help="expert weights in the K-blocked layout (the engine's)")
     ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
@@ -148,6 +150,10 @@ def main():
     K.tune(K.TUNE_GEMM_PERSISTENT, args.persist)
     K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, args.ks)
     K.tune(K.TUNE_STREAM_EVEN_SPLIT, args.even if args.split < 0 else args.split)
+    if args.bulk_publish >= 0:
+        K.tune(K.TUNE_STREAM_BULK_PUBLISH, args.bulk_publish)
+    if args.fused_fixup >= 0:
+        K.tune(K.TUNE_STREAM_FUSED_FIXUP, args.fused_fixup)
     if args.owner_extra >= 0:
         K.tune(K.TUNE_STREAM_OWNER_EXTRA, args.owner_extra)
     if args.l2_ahead >= 0:
