@@ -68,7 +68,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_GEMM 0 /* 1 = weight-streaming path for >= 40 MB of weights or M > 128 (default), 2 = always, 0 = off */
 #define KL_TUNE_STREAM_NMMA 1 /* 128-row weight sub-tiles per activation tile: 1 (default) or 2 */
 #define KL_TUNE_STREAM_STAGES 2 /* cap on the smem pipeline depth (2..16, default 8) */
-#define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints */
+#define KL_TUNE_STREAM_HINT 3   /* 1 = L2 evict_first (weights) / evict_last (activations) hints, 2 = weights evict_last too, 0 = none */
 #define KL_TUNE_STREAM_CTAS_PER_SM 4 /* persistent CTAs per SM: 1 (default) or 2 */
 #define KL_TUNE_PDL 5 /* 1 = decode-path kernels use programmatic dependent launch (default) */
 #define KL_TUNE_PREFILL_TC 6 /* tcgen05 prefill attention: 2 = 64-key blocks, two CTAs per SM (default), 1 = 128-key blocks, 0 = CUDA-core fallback */
@@ -79,6 +79,8 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
 #define KL_TUNE_STREAM_BULK_PUBLISH 17 /* weight-streaming GEMM: split contributors with an idle ring publish partials via smem + one bulk copy (1) or direct stores (0) */
 #define KL_TUNE_STREAM_FUSED_FIXUP 16 /* weight-streaming GEMM: 1 (default) = owners add split partials during the epilogue pass (dedicated staging region), 0 = TMEM fixup first */
+#define KL_TUNE_ATTN_KV_EVICT_FIRST 19 /* tensor-core decode attention: 1 (default) = K/V loads with an L2 evict-first policy, 0 = no hint */
+#define KL_TUNE_DECODE_HG 18 /* tensor-core decode attention: KV heads per work item (0 = auto) */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */
 #define KL_TUNE_GEMM_PERSISTENT 8 /* 1 = persistent double-buffered-TMEM kernel for compute-bound GEMMs (default) */
 #define KL_TUNE_STREAM_WHOLE_TILES 7 /* pct: one whole weight tile per CTA when tiles >= pct% of the SMs (default 70, 0 = off) */

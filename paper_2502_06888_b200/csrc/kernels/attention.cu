@@ -525,6 +525,14 @@ __device__ __forceinline__ void hmma(float (&c)[4], uint32_t a0, uint32_t a2, ui
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return static_cast<uint32_t>(f2bf(lo)) | (static_cast<uint32_t>(f2bf(hi)) << 16);
 }
+__device__ __forceinline__ void tma_load_3d_pol(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -666,6 +674,7 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
 
     if (warp == HG) {  // producer
         if (lane != 0) return;
+        const uint64_t kv_pol = l2_policy_evict_first();
         tma_prefetch_desc(&tmap_k);
         tma_prefetch_desc(&tmap_v);
         int64_t it = 0;
@@ -698,8 +707,13 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
             uint8_t* st = ring + static_cast<size_t>(s) * stage_bytes;
             mbar_arrive_expect_tx(&full[s], 2 * box_bytes + (seg_first ? qelems * 2u : 0u));
             const int row = row_t + j0, chunk = hg * HG * HD / 64;
-            tma_load_3d(st, &tmap_k, &full[s], 0, row, chunk);
-            tma_load_3d(st + box_bytes, &tmap_v, &full[s], 0, row, chunk);
+            if (mode & 4) {  // KV read once per step: L2 evict-first, so reused weights stay resident
+                tma_load_3d_pol(st, &tmap_k, &full[s], 0, row, chunk, kv_pol);
+                tma_load_3d_pol(st + box_bytes, &tmap_v, &full[s], 0, row, chunk, kv_pol);
+            } else {
+                tma_load_3d(st, &tmap_k, &full[s], 0, row, chunk);
+                tma_load_3d(st + box_bytes, &tmap_v, &full[s], 0, row, chunk);
+            }
             if (seg_first)
                 bulk_load(st + 2 * box_bytes, q + static_cast<int64_t>(t) * q_stride + static_cast<int64_t>(hg) * HG * G * HD,
                           qelems * 2u, &full[s]);
@@ -749,7 +763,7 @@ attn_decode_mma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_
             }
             uint8_t* Kb = ring + static_cast<size_t>(s) * stage_bytes;
             uint8_t* Vb = Kb + box_bytes;
-            if (mode >= 2) {  // load-only timing probe
+            if ((mode & 3) >= 2) {  // load-only timing probe
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
                 ++it;
@@ -1243,6 +1257,8 @@ using namespace kl;
 namespace kl {
 int g_prefill_tc = 2;  // kl_tune(KL_TUNE_PREFILL_TC, ...): 2 = 64-key blocks (default), 1 = 128-key blocks, 0 = CUDA cores
 int g_decode_mma = 1;  // kl_tune(KL_TUNE_DECODE_MMA, ...)
+int g_decode_hg = 0;   // kl_tune(KL_TUNE_DECODE_HG, ...): KV heads per decode work item (0 = auto)
+int g_attn_kv_evict_first = 1;  // kl_tune(KL_TUNE_ATTN_KV_EVICT_FIRST, ...): K/V read once per step
 int g_rope_tok = 1;    // kl_tune(KL_TUNE_ROPE_TOKEN_BLOCKS, ...)
 
 static int attn_sm_count() {
@@ -1352,12 +1368,14 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
     int whole = 0;
     for (int hg_try = HG; hg_try >= 1; hg_try /= 2) {
         if (Hkv % hg_try) continue;
+        if (g_decode_hg > 0 && hg_try != g_decode_hg) continue;  // forced group width (tuning)
         if (T * (Hkv / hg_try) * 5 >= static_cast<int64_t>(attn_sm_count()) * 4) {
             HG = hg_try;
             whole = 1;
             break;
         }
     }
+    if (g_decode_hg > 0 && Hkv % g_decode_hg == 0 && g_decode_hg <= kDmMaxHG) HG = g_decode_hg;
     if (g_decode_mma && cache_seqs > 0 && Hkv % HG == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
         static_assert(kDmSlots == kDecChunk, "workspace layout shared with the per-chunk kernel");
         auto ring_bytes = [&](int hg) {
@@ -1410,7 +1428,7 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
             (reinterpret_cast<uintptr_t>(part_o + T * n_chunks * Hq * hd) + 7) & ~uintptr_t(7));
         return launch_pdl(kern, dim3(ctas), dim3((HG + 1) * 32), msmem, stream, mk, mv, q, q_stride, pos, seq, Hq,
                           Hkv, HG, cap, scale * 1.4426950408889634f, part_o, part_ml, n_chunks, n_items, out, counters,
-                          tag, whole, nst, g_decode_mma);
+                          tag, whole, nst, g_decode_mma | (g_attn_kv_evict_first ? 4 : 0));
     }
     auto kern = hd == 128 ? attn_decode_split_kernel<128> : attn_decode_split_kernel<64>;
     KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

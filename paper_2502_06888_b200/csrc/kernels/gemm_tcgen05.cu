@@ -30,6 +30,9 @@
 namespace kl {
 extern int g_pdl;  // kl_tune(KL_TUNE_PDL, ...): programmatic dependent launch (abi.cu)
 namespace {
+// kl_tune(KL_TUNE_STREAM_HINT, ...): L2 policy hints on weight loads: 1 = weights
+// evict-first / activations evict-last, 2 = weights evict-last, 0 = none.
+int g_stream_hint = 1;
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle span
@@ -53,7 +56,7 @@ template <int BN, int EPI, bool PAIRED, int STAGES>
 __global__ void __launch_bounds__(kThreads, (Cfg<BN, STAGES>::kMinBlocks))
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   int a_row0, int M, int kb_per_split, int b_half_rows, uint16_t* __restrict__ c, int ldc,
-                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld) {
+                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld, int b_hint) {
     pdl_enter();
     using C = Cfg<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -103,6 +106,9 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
     if (warp == 0) {
         if (lane == 0) {
             const int a_row = a_row0 + m_tile * BM;
+            // Weights: no hint (1), L2 evict-last (2) when the caller reuses them soon.
+            const uint64_t pol_b = l2_policy_evict_last();
+            const bool hb = b_hint == 2;
             for (int i = 0; i < num_kb; ++i) {
                 const int s = i % STAGES;
                 const uint32_t phase = (i / STAGES) & 1;
@@ -115,11 +121,11 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
                 // Weights through a 3D (64, rows, k-blocks) view: the same
                 // smem image for row-major and K-blocked weight layouts.
                 if constexpr (PAIRED) {
-                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * (BN / 2), kc / BK, 0, false);
-                    tma_load_3d_k(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], b_half_rows + n_tile * (BN / 2), kc / BK, 0,
-                                  false);
+                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * (BN / 2), kc / BK, pol_b, hb);
+                    tma_load_3d_k(sb + (BN / 2) * BK * 2, &tmap_b, &full[s], b_half_rows + n_tile * (BN / 2), kc / BK,
+                                  pol_b, hb);
                 } else {
-                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * BN, kc / BK, 0, false);
+                    tma_load_3d_k(sb, &tmap_b, &full[s], n_tile * BN, kc / BK, pol_b, hb);
                 }
             }
         }
@@ -613,7 +619,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol_w = l2_policy_evict_first();
+            const uint64_t pol_w = p.hint == 2 ? l2_policy_evict_last() : l2_policy_evict_first();
             const uint64_t pol_x = l2_policy_evict_last();
             const bool hint = p.hint != 0;
             // Programmatic dependent launch: the weights do not depend on the
@@ -1130,7 +1136,7 @@ int launch(const Launch& L, cudaStream_t stream) {
     }
     const dim3 grid(L.n_tiles, (L.M + BM - 1) / BM, L.splits);
     if (int rc_ = launch_pdl(gemm_bf16_tcgen05<BN, EPI, PAIRED, STAGES>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK / L.splits, L.b_half_rows, L.c, L.ldc, L.r, L.ws,
-        L.ws_ld)) return rc_;
+        L.ws_ld, g_stream_hint)) return rc_;
     return check_launch();
 }
 
@@ -1187,7 +1193,6 @@ int choose_splits(int tiles, int kb, int M, int ws_cols, int64_t ws_bytes) {
 int g_stream_enabled = 1;  // kl_tune(KL_TUNE_STREAM_GEMM, ...)
 int g_stream_nmma = 1;     // kl_tune(KL_TUNE_STREAM_NMMA, ...): weight sub-tiles per activation tile
 int g_stream_stages = 8;   // kl_tune(KL_TUNE_STREAM_STAGES, ...): cap on the smem ring depth
-int g_stream_hint = 1;     // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 evict_first/evict_last hints
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
@@ -1383,6 +1388,8 @@ extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
 namespace kl {
 extern int g_prefill_tc;
 extern int g_decode_mma;
+extern int g_decode_hg;
+extern int g_attn_kv_evict_first;
 extern int g_rope_tok;
 }
 
@@ -1398,11 +1405,13 @@ extern "C" int kl_tune(int knob, int value) {
             if (value < 2 || value > 16) return KL_EINVAL;
             g_stream_stages = value;
             return KL_OK;
-        case KL_TUNE_STREAM_HINT: g_stream_hint = value != 0; return KL_OK;
+        case KL_TUNE_STREAM_HINT: g_stream_hint = value; return KL_OK;
         case 99: g_stream_debug = value; return KL_OK;
         case KL_TUNE_PDL: g_pdl = value != 0; return KL_OK;
         case KL_TUNE_PREFILL_TC: g_prefill_tc = value; return KL_OK;
         case KL_TUNE_DECODE_MMA: g_decode_mma = value; return KL_OK;
+        case KL_TUNE_DECODE_HG: g_decode_hg = value < 0 ? 0 : value; return KL_OK;
+        case KL_TUNE_ATTN_KV_EVICT_FIRST: g_attn_kv_evict_first = value != 0; return KL_OK;
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;

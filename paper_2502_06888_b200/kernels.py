@@ -73,6 +73,8 @@ TUNE_STREAM_L2_AHEAD = 14  # weight-streaming GEMM: units prefetched into L2 ahe
 TUNE_STREAM_BULK_PUBLISH = 17  # weight-streaming GEMM: contributors publish partials via smem + bulk copy
 TUNE_STREAM_FUSED_FIXUP = 16  # weight-streaming GEMM: owners add split partials in the epilogue pass
 TUNE_STREAM_OWNER_EXTRA = 15  # weight-streaming GEMM, tile-aligned splits: extra units of each tile's owner range
+TUNE_ATTN_KV_EVICT_FIRST = 19  # decode attention: K/V loads L2 evict-first
+TUNE_DECODE_HG = 18  # tensor-core decode attention: KV heads per work item (0 = auto)
 TUNE_DECODE_MMA = 9  # persistent mma.sync split-KV decode attention (1) or per-chunk CUDA-core kernel (0)
 
 

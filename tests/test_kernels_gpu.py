@@ -469,12 +469,18 @@ def test_decode_attention_split_kv(K, cuda, mma, T, Hq, Hkv, hd, cap, p):
     seq = np.array(list(range(T))[::-1], np.int32)
     out = torch.empty(T, Hq * hd, dtype=torch.bfloat16, device=cuda)
     K.tune(K.TUNE_DECODE_MMA, mma)
+    out_nohint = torch.empty_like(out)
     try:
-        K.attn_decode_split(to_dev(q, cuda), width, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda),
-                            Hq, Hkv, hd, to_dev(kc, cuda), to_dev(vc, cuda), cap, sink, hd ** -0.5, out)
+        args = (to_dev(q, cuda), width, torch.from_numpy(pos).to(cuda), torch.from_numpy(seq).to(cuda), Hq, Hkv, hd,
+                to_dev(kc, cuda), to_dev(vc, cuda), cap, sink, hd ** -0.5)
+        K.attn_decode_split(*args, out)
+        K.tune(K.TUNE_ATTN_KV_EVICT_FIRST, 0)  # the L2 policy on the K/V loads changes no result bit
+        K.attn_decode_split(*args, out_nohint)
         torch.cuda.synchronize()
     finally:
         K.tune(K.TUNE_DECODE_MMA, 1)
+        K.tune(K.TUNE_ATTN_KV_EVICT_FIRST, 1)
+    assert torch.equal(out, out_nohint)
     ref = orc.attn_decode(q, width, pos, seq, Hq, Hkv, hd, kc, vc, cap, hd ** -0.5)
     close_bf16(to_bits(out), orc.bits_to_f32(ref))
 

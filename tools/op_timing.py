@@ -20,9 +20,13 @@ def main():
     ap.add_argument("--hbm-cap", type=float, default=24e9)
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--trace", action="store_true", help="per-CTA phase trace of the step's last streaming GEMM")
+    ap.add_argument("--tune", action="append", default=[], help="kernel knob=value (kl_tune), repeatable")
     a = ap.parse_args()
     from paper_2502_06888_b200 import kernels as K
     K.tune(K.TUNE_PDL, a.pdl)
+    for kv in a.tune:
+        k, v = kv.split("=")
+        K.tune(int(k), int(v))
     if a.trace:
         K.tune(99, 128)
     ns = argparse.Namespace(model="mixtral-8x7b", batch_size=64, n_batches=8, prompt_len=512, hbm_cap=a.hbm_cap,
