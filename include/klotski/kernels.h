@@ -77,6 +77,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 2 = also into k-ranges differing by one unit, 0 = one CTA per SM */
 #define KL_TUNE_STREAM_L2_AHEAD 14 /* weight-streaming GEMM: weight units prefetched into L2 ahead of the smem ring (0 = off) */
 #define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
+#define KL_TUNE_SPLIT_FINISH 20 /* tcgen05 GEMM split-K: 1 = each tile finished by its last-arriving CTA, 0 (default) = separate reduce kernel */
 #define KL_TUNE_STREAM_BULK_PUBLISH 17 /* weight-streaming GEMM: split contributors with an idle ring publish partials via smem + one bulk copy (1) or direct stores (0) */
 #define KL_TUNE_STREAM_FUSED_FIXUP 16 /* weight-streaming GEMM: 1 (default) = owners add split partials during the epilogue pass (dedicated staging region), 0 = TMEM fixup first */
 #define KL_TUNE_ATTN_KV_EVICT_FIRST 19 /* tensor-core decode attention: 1 (default) = K/V loads with an L2 evict-first policy, 0 = no hint */

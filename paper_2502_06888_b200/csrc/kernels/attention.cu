@@ -46,13 +46,12 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
     if (rem < static_cast<int64_t>(heads) * half) {
         const int head = static_cast<int>(rem / half);
         const int i = static_cast<int>(rem % half);
-        const float inv = powf(theta, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
         float sn, cs;
-        sincosf(static_cast<float>(p) * inv, &sn, &cs);
+        rope_cs(p, i, hd, theta, cs, sn);
         uint16_t* base = row + static_cast<int64_t>(head) * hd;
         const float a = bf2f(base[i]), b = bf2f(base[i + half]);
-        const uint16_t ra = f2bf(a * cs - b * sn);
-        const uint16_t rb = f2bf(b * cs + a * sn);
+        const uint16_t ra = f2bf(rope_lo(a, b, cs, sn));
+        const uint16_t rb = f2bf(rope_hi(a, b, cs, sn));
         base[i] = ra;
         base[i + half] = rb;
         if (head >= Hq && to_cache) {  // rotated key -> cache
@@ -93,9 +92,8 @@ rope_append_tok_kernel(uint16_t* __restrict__ qkv, int Hq, int Hkv, int hd, cons
     const bool to_cache = chunk_last_pos < 0 || p < sink || p > chunk_last_pos - (cap - sink);
     const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot) * Hkv * hd;
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
-        const float inv = powf(theta, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
         float sn, cs;
-        sincosf(static_cast<float>(p) * inv, &sn, &cs);
+        rope_cs(p, i, hd, theta, cs, sn);
         cs_tab[i] = cs;
         cs_tab[half + i] = sn;
     }
@@ -113,8 +111,8 @@ rope_append_tok_kernel(uint16_t* __restrict__ qkv, int Hq, int Hkv, int hd, cons
             const float a = bf2f(static_cast<uint16_t>(e ? av >> 16 : av & 0xffffu));
             const float b = bf2f(static_cast<uint16_t>(e ? bv >> 16 : bv & 0xffffu));
             const float cs = cs_tab[i + e], sn = cs_tab[half + i + e];
-            ra[e] = f2bf(a * cs - b * sn);
-            rb[e] = f2bf(b * cs + a * sn);
+            ra[e] = f2bf(rope_lo(a, b, cs, sn));
+            rb[e] = f2bf(rope_hi(a, b, cs, sn));
         }
         const uint32_t ro = static_cast<uint32_t>(ra[0]) | (static_cast<uint32_t>(ra[1]) << 16);
         const uint32_t rbo = static_cast<uint32_t>(rb[0]) | (static_cast<uint32_t>(rb[1]) << 16);

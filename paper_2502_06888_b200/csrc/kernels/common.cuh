@@ -145,6 +145,23 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void griddep_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// RoPE (NeoX pairs i, i + hd/2) shared by the RoPE / KV-append kernels and the
+// QKV GEMM's fused epilogue, so every path rounds identically (no FMA
+// contraction: two products and one add, each rounded, as the oracle).
+__device__ __forceinline__ void rope_cs(int p, int i, int hd, float theta, float& cs, float& sn) {
+    const float inv = powf(theta, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
+    sincosf(static_cast<float>(p) * inv, &sn, &cs);
+}
+__device__ __forceinline__ float rope_lo(float a, float b, float cs, float sn) {
+    return __fsub_rn(__fmul_rn(a, cs), __fmul_rn(b, sn));
+}
+__device__ __forceinline__ float rope_hi(float a, float b, float cs, float sn) {
+    return __fadd_rn(__fmul_rn(b, cs), __fmul_rn(a, sn));
+}
+__device__ __forceinline__ int kv_slot_of(int p, int cap, int sink) {
+    return p < sink ? p : sink + (p - sink) % (cap - sink);
+}
+
 // Entry of a kernel launched by launch_pdl: release the next kernel of the
 // stream at once (it may become resident and wait), then wait for the
 // previous kernel to complete before any global memory access.

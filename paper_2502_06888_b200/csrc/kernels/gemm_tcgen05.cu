@@ -52,11 +52,108 @@ struct Cfg {
 
 // PAIRED: the B tile is two BN/2-row halves [W1 rows | W3 rows] of the same
 // output columns (SwiGLU gate/up), read at row offsets n and b_half_rows + n.
+// Tile arrival counter of a split-K launch: word = (epoch << 8) | arrivals,
+// a stale epoch counting as zero, so the workspace needs no clearing. True
+// for the n-th (last) arrival of this launch.
+__device__ __forceinline__ bool arrive_last(uint32_t* ctr, uint32_t epoch, uint32_t n) {
+    const uint32_t tag = (epoch & 0xFFFFFFu) << 8;
+    uint32_t cur = *reinterpret_cast<volatile uint32_t*>(ctr);
+    while (true) {
+        const uint32_t cnt = (cur & 0xFFFFFF00u) == tag ? (cur & 0xFFu) : 0u;
+        const uint32_t prev = atomicCAS(ctr, cur, tag | (cnt + 1));
+        if (prev == cur) return cnt + 1 == n;
+        cur = prev;
+    }
+}
+
+// Sum one (m_tile, n_tile) tile's split partials in split order and apply
+// the final epilogue (store / +residual / SwiGLU of the paired tile) with
+// 128 threads, coalesced float4 reads along each row.
+__device__ __forceinline__ void split_finish(const float* __restrict__ ws, int splits, int M, int ws_ld, int m_tile,
+                                             int n_tile, int bn, int fin, uint16_t* __restrict__ c, int ldc,
+                                             const uint16_t* __restrict__ r, int tid) {
+    // kU quads per thread per round, every split of them loaded before any
+    // add (up to kU * 16 float4 loads in flight: the finish is L2-latency
+    // bound, not bandwidth bound).
+    constexpr int kU = 4, kMaxSplits = 16;
+    const int rows = min(BM, M - m_tile * BM);
+    const int64_t split_stride = static_cast<int64_t>(M) * ws_ld;
+    const bool swiglu = fin == kSwiGLU;
+    const int half = bn / 2;
+    const int out_cols = swiglu ? half : bn;
+    const int quads = out_cols / 4;
+    const int total = rows * quads;
+    for (int base = tid; base < total; base += 128 * kU) {
+        float4 g[kU], u[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            u[k] = g[k];
+        }
+        for (int sp0 = 0; sp0 < splits; sp0 += kMaxSplits / kU) {
+            float4 tg[kMaxSplits / kU][kU], tu[kMaxSplits / kU][kU];
+#pragma unroll
+            for (int q = 0; q < kMaxSplits / kU; ++q)
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    const int idx = base + k * 128, sp = sp0 + q;
+                    if (idx >= total || sp >= splits) continue;
+                    const int m = m_tile * BM + idx / quads, w = (idx % quads) * 4;
+                    const float* p = ws + sp * split_stride + static_cast<int64_t>(m) * ws_ld +
+                                     static_cast<int64_t>(n_tile) * bn + w;
+                    tg[q][k] = *reinterpret_cast<const float4*>(p);
+                    if (swiglu) tu[q][k] = *reinterpret_cast<const float4*>(p + half);
+                }
+#pragma unroll
+            for (int q = 0; q < kMaxSplits / kU; ++q)
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    const int sp = sp0 + q;
+                    if (base + k * 128 >= total || sp >= splits) continue;
+                    // Split order, the first split as the initial value (as splitk_reduce_kernel).
+                    if (sp == 0) {
+                        g[k] = tg[q][k];
+                        if (swiglu) u[k] = tu[q][k];
+                    } else {
+                        g[k].x += tg[q][k].x; g[k].y += tg[q][k].y; g[k].z += tg[q][k].z; g[k].w += tg[q][k].w;
+                        if (swiglu) {
+                            u[k].x += tu[q][k].x; u[k].y += tu[q][k].y; u[k].z += tu[q][k].z; u[k].w += tu[q][k].w;
+                        }
+                    }
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const int idx = base + k * 128;
+            if (idx >= total) continue;
+            const int m = m_tile * BM + idx / quads, w = (idx % quads) * 4;
+            float out[4];
+            if (swiglu) {
+                const float gv[4] = {g[k].x, g[k].y, g[k].z, g[k].w}, uv[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) out[i] = gv[i] / (1.0f + expf(-gv[i])) * uv[i];
+            } else {
+                out[0] = g[k].x; out[1] = g[k].y; out[2] = g[k].z; out[3] = g[k].w;
+                if (fin == kResidual) {
+                    const uint2 rv = *reinterpret_cast<const uint2*>(r + static_cast<int64_t>(m) * ldc + n_tile * bn + w);
+                    out[0] += bf2f(static_cast<uint16_t>(rv.x & 0xffffu));
+                    out[1] += bf2f(static_cast<uint16_t>(rv.x >> 16));
+                    out[2] += bf2f(static_cast<uint16_t>(rv.y & 0xffffu));
+                    out[3] += bf2f(static_cast<uint16_t>(rv.y >> 16));
+                }
+            }
+            *reinterpret_cast<uint2*>(c + static_cast<int64_t>(m) * ldc + static_cast<int64_t>(n_tile) * out_cols + w) =
+                make_uint2(pack2(out[0], out[1]), pack2(out[2], out[3]));
+        }
+    }
+}
+
 template <int BN, int EPI, bool PAIRED, int STAGES>
 __global__ void __launch_bounds__(kThreads, (Cfg<BN, STAGES>::kMinBlocks))
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   int a_row0, int M, int kb_per_split, int b_half_rows, uint16_t* __restrict__ c, int ldc,
-                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld, int b_hint) {
+                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld, int b_hint, int fin,
+                  uint32_t* __restrict__ counters, uint32_t epoch) {
     pdl_enter();
     using C = Cfg<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -168,6 +265,22 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
                     float4* dst = reinterpret_cast<float4*>(out + col);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                }
+            }
+            if (fin >= 0) {
+                // Split-K finished by the last CTA of the tile to arrive (no
+                // reduce launch): partials summed in split order, exactly as
+                // splitk_reduce_kernel, then the final epilogue `fin`.
+                __threadfence();
+                named_bar_sync(1, 128);
+                volatile uint32_t* last = tmem_slot + 1;
+                if (warp == 2 && lane == 0)
+                    *last = arrive_last(counters + m_tile * gridDim.x + n_tile, epoch, gridDim.z) ? 1u : 0u;
+                named_bar_sync(1, 128);
+                if (*last) {
+                    __threadfence();
+                    split_finish(ws, static_cast<int>(gridDim.z), M, ws_ld, m_tile, n_tile, BN, fin, c, ldc, r,
+                                 threadIdx.x - 64);
                 }
             }
         } else if constexpr (EPI == kSwiGLU) {
@@ -1112,6 +1225,9 @@ struct Launch {
     float* ws;
     int ws_ld;
     bool b_kblocked = false;  // weights in the K-blocked layout (make_map_kblocked)
+    int fin = -1;                  // split-K: final epilogue run by each tile's last CTA (-1: reduce kernel)
+    uint32_t* counters = nullptr;  // split-K tile arrival counters (fin >= 0)
+    uint32_t epoch = 0;
 };
 
 // Weight (B operand) map: a 3D (64, rows, k-blocks) view, one k-block per box.
@@ -1136,7 +1252,7 @@ int launch(const Launch& L, cudaStream_t stream) {
     }
     const dim3 grid(L.n_tiles, (L.M + BM - 1) / BM, L.splits);
     if (int rc_ = launch_pdl(gemm_bf16_tcgen05<BN, EPI, PAIRED, STAGES>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK / L.splits, L.b_half_rows, L.c, L.ldc, L.r, L.ws,
-        L.ws_ld, g_stream_hint)) return rc_;
+        L.ws_ld, g_stream_hint, L.fin, L.counters, L.epoch)) return rc_;
     return check_launch();
 }
 
@@ -1201,6 +1317,7 @@ int g_stream_l2_ahead = 0;  // kl_tune(KL_TUNE_STREAM_L2_AHEAD, units)
 int g_stream_owner_extra = 0;  // kl_tune(KL_TUNE_STREAM_OWNER_EXTRA, units)
 int g_stream_fused_fixup = 1;  // kl_tune(KL_TUNE_STREAM_FUSED_FIXUP, 0|1)
 int g_stream_bulk_publish = 0;  // kl_tune(KL_TUNE_STREAM_BULK_PUBLISH, 0|1)
+int g_split_finish = 0;  // kl_tune(KL_TUNE_SPLIT_FINISH, 0|1): split-K tiles finished by their last CTA (measured slower: off)
 int g_stream_ks = 3;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2|3): 2 k-blocks per stage where >= 3 (2) or >= 2 (3) stages fit
 
 int sm_count() {
@@ -1420,6 +1537,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_OWNER_EXTRA: g_stream_owner_extra = value < 0 ? 0 : value; return KL_OK;
         case KL_TUNE_STREAM_FUSED_FIXUP: g_stream_fused_fixup = value != 0; return KL_OK;
         case KL_TUNE_STREAM_BULK_PUBLISH: g_stream_bulk_publish = value != 0; return KL_OK;
+        case KL_TUNE_SPLIT_FINISH: g_split_finish = value != 0; return KL_OK;
         case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
             if (value < 1 || value > 3) return KL_EINVAL;
             g_stream_ks = value;
@@ -1441,7 +1559,8 @@ extern "C" int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
     const int tiles = (N / 128) * m_tiles;
     const int s = choose_splits(tiles, K / BK, M, N, INT64_MAX);
     (void)epilogue;
-    return s > 1 ? static_cast<int64_t>(s) * M * N * 4 : 0;
+    // Partials, then one arrival counter per tile (last-arriver finish).
+    return s > 1 ? ((static_cast<int64_t>(s) * M * N * 4 + 15) & ~int64_t(15)) + static_cast<int64_t>(tiles) * 4 : 0;
 }
 
 namespace kl {
@@ -1477,6 +1596,15 @@ int gemm_bf16_impl(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M,
         const bool paired = epilogue == kSwiGLU;
         L.b_half_rows = paired ? N / 2 : 0;
         if (L.splits > 1) {
+            // Tile arrival counters after the partials: the last CTA of each
+            // tile finishes it (no reduce launch) when the workspace has room.
+            const int64_t part_bytes = (static_cast<int64_t>(L.splits) * M * N * 4 + 15) & ~int64_t(15);
+            if (g_split_finish && workspace_bytes >= part_bytes + static_cast<int64_t>(L.n_tiles) * m_tiles * 4) {
+                L.fin = epilogue;
+                L.counters = reinterpret_cast<uint32_t*>(static_cast<char*>(workspace) + part_bytes);
+                L.epoch = next_epoch();
+                return paired ? launch<128, kPartial, true, 3>(L, stream) : launch<128, kPartial, false, 3>(L, stream);
+            }
             int rc = paired ? launch<128, kPartial, true, 3>(L, stream) : launch<128, kPartial, false, 3>(L, stream);
             if (rc) return rc;
             if (epilogue == kSwiGLU) return reduce<kSwiGLU>(L, N / 2, 128, stream);
