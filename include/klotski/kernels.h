@@ -80,6 +80,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_SPLIT_FINISH 20 /* tcgen05 GEMM split-K: 1 = each tile finished by its last-arriving CTA, 0 (default) = separate reduce kernel */
 #define KL_TUNE_STREAM_BULK_PUBLISH 17 /* weight-streaming GEMM: split contributors with an idle ring publish partials via smem + one bulk copy (1) or direct stores (0) */
 #define KL_TUNE_STREAM_FUSED_FIXUP 16 /* weight-streaming GEMM: 1 (default) = owners add split partials during the epilogue pass (dedicated staging region), 0 = TMEM fixup first */
+#define KL_TUNE_DECODE_STAGES 21 /* tensor-core decode attention: ring stages (0 = default 3) */
 #define KL_TUNE_ATTN_KV_EVICT_FIRST 19 /* tensor-core decode attention: 1 (default) = K/V loads with an L2 evict-first policy, 0 = no hint */
 #define KL_TUNE_DECODE_HG 18 /* tensor-core decode attention: KV heads per work item (0 = auto) */
 #define KL_TUNE_DECODE_MMA 9 /* 1 = persistent mma.sync split-KV decode attention (default), 0 = per-chunk CUDA-core kernel */

@@ -1256,6 +1256,7 @@ namespace kl {
 int g_prefill_tc = 2;  // kl_tune(KL_TUNE_PREFILL_TC, ...): 2 = 64-key blocks (default), 1 = 128-key blocks, 0 = CUDA cores
 int g_decode_mma = 1;  // kl_tune(KL_TUNE_DECODE_MMA, ...)
 int g_decode_hg = 0;   // kl_tune(KL_TUNE_DECODE_HG, ...): KV heads per decode work item (0 = auto)
+int g_decode_stages = 0;  // kl_tune(KL_TUNE_DECODE_STAGES, ...): ring depth of the tensor-core decode kernel (0 = 3)
 int g_attn_kv_evict_first = 1;  // kl_tune(KL_TUNE_ATTN_KV_EVICT_FIRST, ...): K/V read once per step
 int g_rope_tok = 1;    // kl_tune(KL_TUNE_ROPE_TOKEN_BLOCKS, ...)
 
@@ -1376,10 +1377,11 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
     if (g_decode_hg > 0 && Hkv % g_decode_hg == 0 && g_decode_hg <= kDmMaxHG) HG = g_decode_hg;
     if (g_decode_mma && cache_seqs > 0 && Hkv % HG == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
         static_assert(kDmSlots == kDecChunk, "workspace layout shared with the per-chunk kernel");
+        const int nst = g_decode_stages > 0 ? g_decode_stages : kDmStages;
         auto ring_bytes = [&](int hg) {
             const size_t stage = (static_cast<size_t>(2) * kDmSlots * hg * hd * 2 + static_cast<size_t>(hg) * G * hd * 2 +
                                   1023) & ~static_cast<size_t>(1023);
-            return kDmStages * stage + 1024 + 2 * kDmStages * 8;
+            return nst * stage + 1024 + 2 * nst * 8;
         };
         // Wide GQA groups (e.g. 48 q / 8 kv heads with split tokens) can
         // overflow shared memory with all KV heads in one item: narrow the
@@ -1395,7 +1397,6 @@ extern "C" int kl_attn_decode_ws2(const uint16_t* q, int64_t q_stride, const int
         if (msmem > 227 * 1024) return KL_EUNSUPPORTED;
         // (A deeper ring at one CTA per SM measured the same as two CTAs with
         // three stages each.)
-        const int nst = kDmStages;
         auto kern = hd == 128 ? attn_decode_mma_kernel<128> : attn_decode_mma_kernel<64>;
         KL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
         // Occupancy per (hd, HG, smem), queried once; several host threads

@@ -1507,6 +1507,7 @@ extern int g_prefill_tc;
 extern int g_decode_mma;
 extern int g_decode_hg;
 extern int g_attn_kv_evict_first;
+extern int g_decode_stages;
 extern int g_rope_tok;
 }
 
@@ -1529,6 +1530,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_DECODE_MMA: g_decode_mma = value; return KL_OK;
         case KL_TUNE_DECODE_HG: g_decode_hg = value < 0 ? 0 : value; return KL_OK;
         case KL_TUNE_ATTN_KV_EVICT_FIRST: g_attn_kv_evict_first = value != 0; return KL_OK;
+        case KL_TUNE_DECODE_STAGES: g_decode_stages = value < 0 || value > 12 ? 0 : value; return KL_OK;
         case KL_TUNE_ROPE_TOKEN_BLOCKS: g_rope_tok = value != 0; return KL_OK;
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;

@@ -74,6 +74,7 @@ TUNE_SPLIT_FINISH = 20  # tcgen05 GEMM split-K: tiles finished by their last CTA
 TUNE_STREAM_BULK_PUBLISH = 17  # weight-streaming GEMM: contributors publish partials via smem + bulk copy
 TUNE_STREAM_FUSED_FIXUP = 16  # weight-streaming GEMM: owners add split partials in the epilogue pass
 TUNE_STREAM_OWNER_EXTRA = 15  # weight-streaming GEMM, tile-aligned splits: extra units of each tile's owner range
+TUNE_DECODE_STAGES = 21  # tensor-core decode attention: ring stages (0 = default)
 TUNE_ATTN_KV_EVICT_FIRST = 19  # decode attention: K/V loads L2 evict-first
 TUNE_DECODE_HG = 18  # tensor-core decode attention: KV heads per work item (0 = auto)
 TUNE_DECODE_MMA = 9  # persistent mma.sync split-KV decode attention (1) or per-chunk CUDA-core kernel (0)

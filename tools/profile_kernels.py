@@ -141,6 +141,7 @@ def main():
     ap.add_argument("--bulk-publish", type=int, default=-1, help="stream GEMM contributors publish via smem + bulk copy")
     ap.add_argument("--fused-fixup", type=int, default=-1, help="stream GEMM owners add partials in the epilogue pass")
     ap.add_argument("--kv-evict-first", type=int, default=-1, help="decode attention K/V loads evict-first")
+    ap.add_argument("--decode-stages", type=int, default=-1, help="decode attention ring stages (0 = default)")
     ap.add_argument("--decode-hg", type=int, default=-1, help="decode attention KV heads per work item (0 = auto)")
     ap.add_argument("--owner-extra", type=int, default=-1, help="stream GEMM owner-range bonus (units; -1 = default)")
     ap.add_argument("--kb", type=int, default=1, help="expert weights in the K-blocked layout (the engine's)")
@@ -158,6 +159,8 @@ def main():
         K.tune(K.TUNE_STREAM_FUSED_FIXUP, args.fused_fixup)
     if args.kv_evict_first >= 0:
         K.tune(K.TUNE_ATTN_KV_EVICT_FIRST, args.kv_evict_first)
+    if args.decode_stages >= 0:
+        K.tune(K.TUNE_DECODE_STAGES, args.decode_stages)
     if args.decode_hg >= 0:
         K.tune(K.TUNE_DECODE_HG, args.decode_hg)
     if args.owner_extra >= 0:
