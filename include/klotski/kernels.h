@@ -7,7 +7,8 @@
  *
  *   compute_gate      (schedule.cpp:340-353)  -> kl_gate_topk
  *   compute_expert    (schedule.cpp:355-372)  -> kl_permute + kl_expert_ffn + kl_combine
- *   compute_attention (schedule.cpp:313-338)  -> kl_rmsnorm, kl_gemm_bf16, kl_rope_kv_append,
+ *   compute_attention (schedule.cpp:313-338)  -> kl_rmsnorm, kl_gemm_bf16, kl_rope_kv_append
+ *                                               (decode: kl_rmsnorm_rope_table + kl_gemm_bf16_qkv_rope),
  *                                                kl_attn_decode / kl_attn_prefill
  *   update_table / predict_hot (correlation.cpp:74-140, invoked from
  *   make_table_prefetcher, schedule.cpp:60-91) -> kl_coact_update, kl_predict_scores
@@ -225,6 +226,27 @@ int kl_predict_scores(const int32_t* hist, const int64_t* table, int E, int laye
 /* out[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * w), d % 256 == 0. */
 int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps,
                uint16_t* out, cudaStream_t stream);
+
+/* kl_rmsnorm for decode-sized calls (T <= 592) that also writes each row's
+ * RoPE (cos, sin) table for kl_gemm_bf16_qkv_rope: table[t][i] (float pairs,
+ * i < hd/2) at position pos[t]. KL_EUNSUPPORTED for larger T. */
+int kl_rmsnorm_rope_table(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps,
+                          uint16_t* out, const int32_t* pos, float rope_theta, int hd, float* table,
+                          cudaStream_t stream);
+
+/* The QKV projection with kl_rope_kv_append fused into its epilogue:
+ * c[0:M] = a[row_offset:+M] @ b^T (b = [Hq+2Hkv heads * hd, K] row-major),
+ * q and k heads rotated with the table from kl_rmsnorm_rope_table, k and v
+ * rows appended to the caches (same layout and retention rule as
+ * kl_rope_kv_append). Results are bit-identical to kl_gemm_bf16 followed by
+ * kl_rope_kv_append. Weight-streaming path only (hd 128, decode-sized M,
+ * workspace of kl_gemm_workspace_bytes): KL_EUNSUPPORTED otherwise, and the
+ * caller runs the two separate calls. */
+int kl_gemm_bf16_qkv_rope(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                          const uint16_t* b, int Hq, int Hkv, int hd, uint16_t* c, int ldc,
+                          const float* rope_table, const int32_t* pos, const int32_t* seq,
+                          uint16_t* k_cache, uint16_t* v_cache, int cap, int sink, int chunk_last_pos,
+                          void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
 /* Rotary embedding on q/k of a fused qkv row [Hq*hd | Hkv*hd | Hkv*hd] at the
  * token's absolute position, rope applied in place to q; roped k and v are

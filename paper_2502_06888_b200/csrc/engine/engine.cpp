@@ -417,6 +417,7 @@ bool Engine::plan_at(int n, bool rethrow) {
         add((static_cast<byte_count>(std::max(D_.L - 1, 0)) * D_.E * D_.E + D_.E) * 8);
         add(64 * 1024);
         add((2 * ops_per_step_bound(D_.L, n, El_) + 8) * 8);                     // op timestamps
+        add(tb_max_ * D_.hd * 4);                                                // RoPE table
         if (kv_off)
             add(static_cast<byte_count>(kKvSlots) * w.batch_size *
                 cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
@@ -486,6 +487,11 @@ void Engine::allocate_device() {
     embed_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     head_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     h_ = bf(t_max_ * D_.d);
+    rope_tab_ = static_cast<float*>(take(tb_max_ * D_.hd * 4));  // [tb_max][hd/2] (cos, sin)
+    // Opt-in (KL_QKV_ROPE=1): bit-identical to the separate calls but no
+    // faster (attention op 56.6 vs 57.1 us as a graph: the owners' epilogue
+    // tail grows by what the RoPE launch cost).
+    rope_fused_ok_ = std::getenv("KL_QKV_ROPE") != nullptr;
     stamp_cap_ = ops_per_step_bound(D_.L, plan_.n_batches, El_);
     stamps_dev_ = static_cast<unsigned long long*>(take((2 * stamp_cap_ + 8) * 8));
     x2_ = bf(t_max_ * D_.d);

@@ -273,6 +273,8 @@ class Engine {
     unsigned long long t0_ns_ = 0;
     void stamp(std::int32_t id, int side, cudaStream_t st);
     std::vector<cudaEvent_t> op_end_;                 // by op id (current step window)
+    float* rope_tab_ = nullptr;   // decode RoPE (cos, sin) table of one batch [tb_max][hd/2][2]
+    bool rope_fused_ok_ = true;   // QKV GEMM with the fused RoPE / KV-append epilogue
     std::vector<moesim::SimEvent> timeline_;          // measured, by op id
     std::int32_t timed_from_ = 0;
     std::int32_t log_from_ = 0;

@@ -607,13 +607,6 @@ void Engine::exec_attention(const StreamOp& op) {
     const uint16_t* wqkv = w;
     const uint16_t* wo = w + static_cast<int64_t>(D_.qkv_width()) * D_.d;
     uint16_t* hb = h_ + row0 * D_.d;
-    kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
-    if (fused)
-        kl_check(kl_gemm_q4(xa_, tpb, 0, tpb, D_.d, q4qkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
-                            gemm_ws_bytes_, cs), "qkv q4");
-    else
-        kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
-                              gemm_ws_bytes_, cs), "qkv");
     const float scale = 1.0f / std::sqrt(static_cast<float>(D_.hd));
     const int last = step == 0 ? cfg_.workload.prompt_len - 1 : -1;
     uint16_t* kc = kc_[l];
@@ -630,8 +623,36 @@ void Engine::exec_attention(const StreamOp& op) {
         vc = kv_slot_v_[it->second];
         seq_idx = tok_seq_local_ + row0;
     }
-    kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, seq_idx, D_.theta, kc, vc, kv_cap_,
-                               kv_sink_, last, cs), "rope/kv");
+    // Decode with bf16 projections, opt-in (KL_QKV_ROPE=1): RMSNorm writes the
+    // RoPE table and the QKV GEMM rotates q / k and appends k / v in its
+    // epilogue (two launches instead of three); shapes off the weight-
+    // streaming path fall back.
+    if (step != 0 && !fused && rope_fused_ok_) {
+        kl_check(kl_rmsnorm_rope_table(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, tok_pos_ + row0, D_.theta, D_.hd,
+                                       rope_tab_, cs), "attn norm + rope table");
+        const int rc = kl_gemm_bf16_qkv_rope(xa_, tpb, 0, tpb, D_.d, wqkv, D_.Hq, D_.Hkv, D_.hd, qkv_, D_.qkv_width(),
+                                             rope_tab_, tok_pos_ + row0, seq_idx, kc, vc, kv_cap_, kv_sink_, -1,
+                                             gemm_ws_, gemm_ws_bytes_, cs);
+        if (rc == KL_EUNSUPPORTED) {
+            rope_fused_ok_ = false;  // this engine's shapes take the separate calls from now on
+            kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0,
+                                  gemm_ws_, gemm_ws_bytes_, cs), "qkv");
+            kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, seq_idx, D_.theta, kc, vc,
+                                       kv_cap_, kv_sink_, last, cs), "rope/kv");
+        } else {
+            kl_check(rc, "qkv + rope/kv");
+        }
+    } else {
+        kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
+        if (fused)
+            kl_check(kl_gemm_q4(xa_, tpb, 0, tpb, D_.d, q4qkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
+                                gemm_ws_bytes_, cs), "qkv q4");
+        else
+            kl_check(kl_gemm_bf16(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0,
+                                  gemm_ws_, gemm_ws_bytes_, cs), "qkv");
+        kl_check(kl_rope_kv_append(qkv_, tpb, D_.Hq, D_.Hkv, D_.hd, tok_pos_ + row0, seq_idx, D_.theta, kc, vc, kv_cap_,
+                                   kv_sink_, last, cs), "rope/kv");
+    }
     if (step == 0)
         kl_check(kl_attn_prefill(qkv_, cfg_.workload.batch_size, cfg_.workload.prompt_len, D_.Hq, D_.Hkv, D_.hd,
                                  kv_cap_, kv_sink_, scale, ao_, cs), "prefill attention");

@@ -610,6 +610,14 @@ struct StreamArgs {
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
     int owner_extra;  // tile-aligned splits: extra units of the owner's (last) range
     int bulk_publish; // contributors whose ring is idle publish their partial with one bulk copy
+    // Fused RoPE + KV append (QKV projection, one 128-row weight tile = one
+    // head of hd 128): rows [q heads | k heads | v heads], NeoX pairs.
+    const float2* rope_tab;  // [M][64] (cos, sin) per row and frequency; nullptr = plain store
+    const int32_t* rope_pos;
+    const int32_t* rope_seq;
+    uint16_t* kc;
+    uint16_t* vc;
+    int Hq, Hkv, cap, sink, chunk_last_pos;
     int stage_off;    // > 0: byte offset of a dedicated output staging region (owner adds the
                       // landed partials while it reads TMEM for the epilogue; no TMEM store-back)
     const uint8_t* q4;  // Q4 variant: weights in the tiled 4-bit layout (kQ4Chunk bytes per 128x64 tile)
@@ -678,6 +686,46 @@ __device__ __forceinline__ float epi_value(const float (&acc)[2][16], int j, int
         return __fdividef(g, 1.0f + __expf(-g)) * u;
     } else {
         return acc[j][i];
+    }
+}
+
+// One 16-byte vector (8 features) of a staged QKV row: rotate q / k heads
+// with the row's (cos, sin) table (same rope_lo / rope_hi as the RoPE
+// kernels), store to the QKV output, and append k / v heads to the cache.
+__device__ __forceinline__ void rope_row_store(const StreamArgs& p, const uint16_t* stage, int row, int x, int head,
+                                               uint16_t* o) {
+    const uint4 v = *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
+    uint4 r = v;
+    const int rot = p.Hq + p.Hkv;
+    if (head < rot) {
+        const uint4 w = *reinterpret_cast<const uint4*>(stage + row * kWRows + (x ^ 8) * 8);
+        const float2* tb = p.rope_tab + static_cast<int64_t>(row) * (kWRows / 2) + (x & 7) * 8;
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w}, ww[4] = {w.x, w.y, w.z, w.w};
+        uint32_t rr[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float out2[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float2 t = __ldg(tb + 2 * e + h);
+                const float self = bf2f(static_cast<uint16_t>(h ? vv[e] >> 16 : vv[e] & 0xffffu));
+                const float other = bf2f(static_cast<uint16_t>(h ? ww[e] >> 16 : ww[e] & 0xffffu));
+                out2[h] = x < 8 ? rope_lo(self, other, t.x, t.y) : rope_hi(other, self, t.x, t.y);
+            }
+            rr[e] = pack2(out2[0], out2[1]);
+        }
+        r = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+    }
+    *reinterpret_cast<uint4*>(o) = r;
+    if (head >= p.Hq) {
+        const int pp = p.rope_pos[row];
+        if (p.chunk_last_pos < 0 || pp < p.sink || pp > p.chunk_last_pos - (p.cap - p.sink)) {
+            const int64_t crow = (static_cast<int64_t>(p.rope_seq[row]) * p.cap + kv_slot_of(pp, p.cap, p.sink)) *
+                                 p.Hkv * kWRows;
+            uint16_t* dst = head < rot ? p.kc + crow + static_cast<int64_t>(head - p.Hq) * kWRows
+                                       : p.vc + crow + static_cast<int64_t>(head - rot) * kWRows;
+            *reinterpret_cast<uint4*>(dst + x * 8) = r;
+        }
     }
 }
 
@@ -978,7 +1026,9 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 continue;
             } else if (t != t_lo) {
                 // A whole tile in the middle of the range (only when a range
-                // spans more than a tile): direct, uncoalesced stores.
+                // spans more than a tile): direct, uncoalesced stores. (The
+                // host never lets the fused RoPE epilogue reach this path.)
+                if (p.rope_tab != nullptr) __trap();
                 for (int col = 0; col < cols; col += 16) {
                     float acc[2][16];
 #pragma unroll
@@ -1134,6 +1184,15 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 if (etid == 0) STREAM_TRACE(6);
                 // Stage bf16 outputs [token][128 features] in smem, then
                 // coalesced 16-byte row stores.
+                if (p.rope_tab != nullptr) {
+                    // Pull this thread's RoPE table lines toward L1 while the
+                    // accumulator is staged: the row-store pass then hits.
+                    const int vec = kWRows / 8;
+                    for (int v = etid; v < p.M * vec; v += 128) {
+                        const float2* tb = p.rope_tab + static_cast<int64_t>(v / vec) * (kWRows / 2) + (v % vec & 7) * 8;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(tb));
+                    }
+                }
                 uint8_t* stage_base = smem + (fused_nq > 0 ? p.stage_off : 0);
                 uint16_t* stage = reinterpret_cast<uint16_t*>(stage_base);
                 float* stage_f = reinterpret_cast<float*>(stage_base);  // residual: fp32 staging, one rounding after the add
@@ -1188,6 +1247,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                                 ow[e] = pack2(f[2 * e] + bf2f(static_cast<uint16_t>(rw[e] & 0xffffu)),
                                               f[2 * e + 1] + bf2f(static_cast<uint16_t>(rw[e] >> 16)));
                             *reinterpret_cast<uint4*>(o) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                        } else if (p.rope_tab != nullptr) {
+                            rope_row_store(p, stage, row, x, static_cast<int>(feat0 / kWRows), o);
                         } else {
                             *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
                         }
@@ -1368,11 +1429,32 @@ int stream_grid(int N, int K, int epilogue) {
     return std::max(1, std::min(sm_count() * g_stream_ctas, units / 4));
 }
 
+struct RopeArgs {
+    const float2* table;
+    const int32_t* pos;
+    const int32_t* seq;
+    uint16_t* kc;
+    uint16_t* vc;
+    int Hq, Hkv, cap, sink, chunk_last_pos;
+};
+
 template <int EPI, int NMMA, bool Q4 = false>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
                   int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
-                  cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false) {
+                  cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false, const RopeArgs* rope = nullptr) {
     StreamArgs p{};
+    if (rope != nullptr) {
+        p.rope_tab = rope->table;
+        p.rope_pos = rope->pos;
+        p.rope_seq = rope->seq;
+        p.kc = rope->kc;
+        p.vc = rope->vc;
+        p.Hq = rope->Hq;
+        p.Hkv = rope->Hkv;
+        p.cap = rope->cap;
+        p.sink = rope->sink;
+        p.chunk_last_pos = rope->chunk_last_pos;
+    }
     p.M = M;
     p.NP = stream_np(M);
     p.acc_stride = pow2ceil(std::max(32, p.NP));
@@ -1428,6 +1510,9 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
         p.owner_extra = 0;
     }
     if (G < 1) return KL_EUNSUPPORTED;
+    // The fused RoPE epilogue runs only on owners' staged path: no CTA range
+    // may contain a whole tile strictly inside it.
+    if (rope != nullptr && p.split == 0 && (p.units + G - 1) / G > p.KB + 1) return KL_EUNSUPPORTED;
     p.half_rows = half_rows;
     p.c = c;
     p.ldc = ldc;
@@ -1652,6 +1737,30 @@ extern "C" int kl_gemm_bf16_kb(const uint16_t* a, int64_t a_rows, int64_t row_of
                                int64_t workspace_bytes, cudaStream_t stream) {
     return kl::gemm_bf16_impl(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes, stream,
                               true);
+}
+
+extern "C" int kl_gemm_bf16_qkv_rope(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                                     const uint16_t* b, int Hq, int Hkv, int hd, uint16_t* c, int ldc,
+                                     const float* rope_table, const int32_t* pos, const int32_t* seq, uint16_t* k_cache,
+                                     uint16_t* v_cache, int cap, int sink, int chunk_last_pos, void* workspace,
+                                     int64_t workspace_bytes, cudaStream_t stream) {
+    using namespace kl;
+    if (M < 0 || K <= 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || !a || !b || !c || !rope_table || !pos || !seq || !k_cache ||
+        !v_cache || cap <= sink || sink < 0)
+        return KL_EINVAL;
+    if (M == 0) return KL_OK;
+    const int N = (Hq + 2 * Hkv) * hd;
+    // One 128-row weight tile per head, on the weight-streaming path.
+    if (hd != kWRows || K % BK != 0 || !aligned16(a) || !aligned16(b) || !aligned16(c) || ldc % 8 != 0 ||
+        !aligned16(k_cache) || !aligned16(v_cache) || row_offset < 0 || row_offset + M > a_rows)
+        return KL_EUNSUPPORTED;
+    if (workspace == nullptr || !aligned16(workspace) || !stream_eligible(M, N, K, kStore) ||
+        workspace_bytes < kFlagBytes + stream_slot_bytes(M, 1))
+        return KL_EUNSUPPORTED;
+    const RopeArgs ra{reinterpret_cast<const float2*>(rope_table), pos, seq, k_cache, v_cache, Hq, Hkv, cap, sink,
+                      chunk_last_pos};
+    return launch_stream<kStore, 1>(a, a_rows, row_offset, M, K, b, N, N / kWRows, 0, c, ldc, nullptr, workspace,
+                                    workspace_bytes, stream, nullptr, false, &ra);
 }
 
 extern "C" int kl_gemm_q4(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint8_t* bq,

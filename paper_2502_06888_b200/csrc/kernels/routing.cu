@@ -392,8 +392,15 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
 // span, so a 64-row call spreads over 64 SMs instead of 16.
 __global__ void __launch_bounds__(256)
 rmsnorm_row_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d, float eps,
-                   uint16_t* __restrict__ out) {
+                   uint16_t* __restrict__ out, const int32_t* __restrict__ rope_pos, float rope_theta, int rope_hd,
+                   float2* __restrict__ rope_table) {
     pdl_enter();
+    if (rope_table != nullptr && static_cast<int>(threadIdx.x) < rope_hd / 2) {
+        // This token's RoPE cos/sin table for the QKV GEMM's fused epilogue.
+        float cs, sn;
+        rope_cs(rope_pos[blockIdx.x], threadIdx.x, rope_hd, rope_theta, cs, sn);
+        rope_table[static_cast<int64_t>(blockIdx.x) * (rope_hd / 2) + threadIdx.x] = make_float2(cs, sn);
+    }
     // (pdl_enter released the QKV GEMM that follows: it may start now and
     // prefetch its weights; it reads this kernel's output only after
     // griddepcontrol.wait.)
@@ -787,9 +794,20 @@ extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d
     if (T < 0 || d <= 0 || d % 256 != 0 || !x || !w || !out) return KL_EINVAL;
     if (T == 0) return KL_OK;
     if (T <= 4 * 148)
-        return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out);
+        return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out,
+                          static_cast<const int32_t*>(nullptr), 0.0f, 0, static_cast<float2*>(nullptr));
     return launch_pdl(rmsnorm_kernel, dim3(grid_for(T, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), 0, stream, x, w, T,
                       d, eps, out);
+}
+
+extern "C" int kl_rmsnorm_rope_table(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps, uint16_t* out,
+                                     const int32_t* pos, float theta, int hd, float* table, cudaStream_t stream) {
+    if (T < 0 || d <= 0 || d % 256 != 0 || !x || !w || !out || !pos || !table || hd < 2 || hd > 512 || hd % 2)
+        return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    if (T > 4 * 148) return KL_EUNSUPPORTED;  // decode-sized calls (block per row) only
+    return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out, pos,
+                      theta, hd, reinterpret_cast<float2*>(table));
 }
 
 extern "C" int64_t kl_permute_workspace_bytes(int64_t R, int E) {

@@ -16,6 +16,7 @@ _P = C.c_void_p
 _I = C.c_int
 _L = C.c_int64
 _F = C.c_float
+KL_EUNSUPPORTED = -2  # klotski/kernels.h
 _U64 = C.c_uint64
 
 
@@ -42,6 +43,9 @@ _coact = _sig("kl_coact_update", [_P, _P, _L, _I, _I, _I, _P, _P, _P])
 _pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
 _rms = _sig("kl_rmsnorm", [_P, _P, _L, _I, _F, _P, _P])
 _rope = _sig("kl_rope_kv_append", [_P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _I, _I, _P])
+_rms_tab = _sig("kl_rmsnorm_rope_table", [_P, _P, _L, _I, _F, _P, _P, _F, _I, _P, _P])
+_qkv_rope = _sig("kl_gemm_bf16_qkv_rope", [_P, _L, _L, _I, _I, _P, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _I, _I, _I,
+                                           _P, _L, _P])
 _dec = _sig("kl_attn_decode", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P])
 _dec_ws_bytes = _sig("kl_attn_decode_workspace_bytes", [_L, _I, _I, _I], C.c_int64)
 _dec_ws = _sig("kl_attn_decode_ws", [_P, _L, _P, _P, _L, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _L, _P])
@@ -263,6 +267,36 @@ def rope_kv_append(qkv, Hq, Hkv, hd, pos, seq, theta, k_cache, v_cache, cap, sin
                    stream=None):
     _chk(_rope(_p(qkv), qkv.shape[0], Hq, Hkv, hd, _p(pos), _p(seq), theta, _p(k_cache), _p(v_cache), cap, sink,
                chunk_last_pos, _s(stream)), "kl_rope_kv_append")
+
+
+def rmsnorm_rope_table(x, w, pos, theta, hd, eps=1e-5, out=None, table=None, stream=None):
+    """kl_rmsnorm_rope_table: RMSNorm of decode-sized x plus each row's RoPE
+    (cos, sin) table [T, hd/2, 2] fp32 for qkv_rope."""
+    out = torch.empty_like(x) if out is None else out
+    if table is None:
+        table = torch.empty(x.shape[0], hd // 2, 2, dtype=torch.float32, device=x.device)
+    _chk(_rms_tab(_p(x), _p(w), x.shape[0], x.shape[1], eps, _p(out), _p(pos), theta, hd, _p(table), _s(stream)),
+         "kl_rmsnorm_rope_table")
+    return out, table
+
+
+def qkv_rope(a, b, Hq, Hkv, hd, table, pos, seq, k_cache, v_cache, cap, sink, chunk_last_pos=-1, c=None,
+             row_offset=0, m=None, stream=None):
+    """kl_gemm_bf16_qkv_rope: the QKV GEMM with RoPE + KV append in its
+    epilogue. Returns c, or None when the shape is not on the fused path
+    (KL_EUNSUPPORTED: the caller runs gemm + rope_kv_append)."""
+    m = a.shape[0] - row_offset if m is None else m
+    N = b.shape[0]
+    c = torch.empty(m, N, dtype=torch.bfloat16, device=a.device) if c is None else c
+    wsb = workspace_bytes(m, N, a.shape[1], 0)
+    ws = workspace(max(wsb, 1024), a.device)
+    rc = _qkv_rope(_p(a), a.shape[0], row_offset, m, a.shape[1], _p(b), Hq, Hkv, hd, _p(c), c.stride(0), _p(table),
+                   _p(pos), _p(seq), _p(k_cache), _p(v_cache), cap, sink, chunk_last_pos, _p(ws), max(wsb, 1024),
+                   _s(stream))
+    if rc == KL_EUNSUPPORTED:
+        return None
+    _chk(rc, "kl_gemm_bf16_qkv_rope")
+    return c
 
 
 def attn_decode(q, q_stride, pos, seq, Hq, Hkv, hd, k_cache, v_cache, cap, sink, scale, out, stream=None):

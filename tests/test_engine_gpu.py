@@ -414,3 +414,30 @@ def test_mixtral_shape_schedule_and_determinism(cuda):
         assert e.report("validate")["violations"] == []
         e.close()
     assert all(np.array_equal(a, b) for a, b in zip(outs[0], outs[1]))
+
+
+def test_fused_qkv_rope_matches_separate_calls(cuda, monkeypatch):
+    """Mixtral-8x7B dims (2 layers, bs 64 x n 2, gate routing): decode with
+    the QKV GEMM's fused RoPE / KV-append epilogue (KL_QKV_ROPE=1) gives the
+    same tokens and hidden states as RMSNorm + QKV GEMM + RoPE kernel."""
+    cfg = {"model": {"preset": "mixtral-8x7b", "n_layers": 2},
+           "workload": {"batch_size": 64, "n_batches": 2, "prompt_len": 16, "gen_len": 4},
+           "hbm_cap_bytes": 8_000_000_000, "host_distinct_layers": 2, "routing": "gate", "record_hidden": True}
+    runs = []
+    for env in ("1", None):
+        if env is None:
+            monkeypatch.delenv("KL_QKV_ROPE", raising=False)
+        else:
+            monkeypatch.setenv("KL_QKV_ROPE", env)
+        eng = make(cfg)
+        outs = run_all_steps(eng, cfg, seed=3)
+        dumps = eng.report("hidden")["dumps"]
+        assert eng.report("validate")["violations"] == []
+        eng.close()
+        runs.append((outs, dumps))
+    (o1, d1), (o2, d2) = runs
+    assert len(d1) == len(d2) > 0
+    for a, b in zip(o1, o2):
+        assert np.array_equal(a, b)
+    for a, b in zip(d1, d2):
+        assert np.array_equal(np.array(a), np.array(b))

@@ -440,6 +440,50 @@ def test_rope_token_blocks_bit_identical(K, cuda, T, Hq, Hkv, hd, cap, sink, las
     _rotated_close(gk, kc)
 
 
+@pytest.mark.parametrize("M,Hq,Hkv,d,pos0", [(64, 32, 8, 4096, 600), (1, 32, 8, 4096, 3), (200, 32, 8, 4096, 100),
+                                             (64, 48, 8, 6144, 259)])
+def test_qkv_rope_fused_bit_identical(K, cuda, M, Hq, Hkv, d, pos0):
+    """RMSNorm + RoPE table, then the QKV GEMM with RoPE and the KV append in
+    its epilogue (kl_rmsnorm_rope_table + kl_gemm_bf16_qkv_rope) equals
+    kl_rmsnorm + kl_gemm_bf16 + kl_rope_kv_append bit for bit: the normed
+    rows, the roped qkv rows and both caches (ring wrap, sink, permuted
+    sequences)."""
+    hd, cap, sink, theta = 128, 260, 4, 1e6
+    width = (Hq + 2 * Hkv) * hd
+    h = to_dev(orc.normal_bf16(M * d, 81, 1.0).reshape(M, d), cuda)
+    nw = to_dev(orc.normal_bf16(d, 82, 0.5), cuda)
+    w = to_dev(orc.normal_bf16(width * d, 83, 0.02).reshape(width, d), cuda)
+    pos = torch.tensor([pos0 + (i * 37) % 300 for i in range(M)], dtype=torch.int32, device=cuda)
+    seq = torch.tensor([(i * 7) % M for i in range(M)], dtype=torch.int32, device=cuda)
+    seq = torch.argsort(seq).to(torch.int32)  # a permutation of 0..M-1
+    kc1 = torch.zeros(M * cap * Hkv * hd, dtype=torch.bfloat16, device=cuda)
+    vc1, kc2, vc2 = torch.zeros_like(kc1), torch.zeros_like(kc1), torch.zeros_like(kc1)
+    xa1 = K.rmsnorm(h, nw)
+    q1 = K.gemm(xa1, w)
+    K.rope_kv_append(q1, Hq, Hkv, hd, pos, seq, theta, kc1, vc1, cap, sink)
+    xa2, tab = K.rmsnorm_rope_table(h, nw, pos, theta, hd)
+    q2 = K.qkv_rope(xa2, w, Hq, Hkv, hd, tab, pos, seq, kc2, vc2, cap, sink)
+    torch.cuda.synchronize()
+    assert q2 is not None, "the fused path must cover the bench's QKV shapes"
+    assert torch.equal(xa1, xa2)
+    assert torch.equal(q1, q2)
+    assert torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
+    assert bool((kc2 != 0).any())
+
+
+def test_qkv_rope_fused_declines_small_shapes(K, cuda):
+    """Below the weight-streaming threshold the fused entry reports
+    KL_EUNSUPPORTED (the engine then issues the separate calls)."""
+    M, Hq, Hkv, hd, d = 4, 8, 2, 128, 512
+    width = (Hq + 2 * Hkv) * hd
+    a = to_dev(orc.normal_bf16(M * d, 84, 1.0).reshape(M, d), cuda)
+    w = to_dev(orc.normal_bf16(width * d, 85, 0.02).reshape(width, d), cuda)
+    pos = torch.arange(M, dtype=torch.int32, device=cuda)
+    kc = torch.zeros(M * 20 * Hkv * hd, dtype=torch.bfloat16, device=cuda)
+    tab = torch.zeros(M, hd // 2, 2, dtype=torch.float32, device=cuda)
+    assert K.qkv_rope(a, w, Hq, Hkv, hd, tab, pos, pos, kc, kc.clone(), 20, 4) is None
+
+
 def test_rope_append_and_decode_attention(K, cuda):
     n_seq, Hq, Hkv, hd, cap, sink = 6, 8, 2, 128, 20, 4
     width = (Hq + 2 * Hkv) * hd

@@ -302,6 +302,27 @@ def main():
             K.attn_decode_split(qkv, width, pos, seqs[b], Hq, Hkv, hd, kcs[l], vcs[l], cap, 4, hd ** -0.5, ao)
             K.gemm(ao, wo[l], c=hb, residual=hb, epilogue=1)
         per = 8 * L4
+        tab = torch.empty(bs, hd // 2, 2, dtype=torch.float32, device=dev)
+
+        def op_fused(i):
+            # As the engine issues decode: RMSNorm + RoPE table, QKV GEMM with
+            # the RoPE / KV-append epilogue, attention, o-proj.
+            l, b = (i // n) % L4, i % n
+            hb = h[b * bs:(b + 1) * bs]
+            K.rmsnorm_rope_table(hb, nw, pos, 1e6, hd, out=xa, table=tab)
+            assert K.qkv_rope(xa, wqkv[l], Hq, Hkv, hd, tab, pos, seqs[b], kcs[l], vcs[l], cap, 4, c=qkv) is not None
+            K.attn_decode_split(qkv, width, pos, seqs[b], Hq, Hkv, hd, kcs[l], vcs[l], cap, 4, hd ** -0.5, ao)
+            K.gemm(ao, wo[l], c=hb, residual=hb, epilogue=1)
+        res["attn_op_b64_fused_rope"] = {"us": timed_graph(op_fused, per) * 1e6}
+
+        def op_keep(i):
+            # The layer's projection weights kept in L2 (evict-last) for all
+            # but its last batch, which reads them evict-first.
+            K.tune(K.TUNE_STREAM_HINT, 2 if i % n < n - 1 else 1)
+            op(i)
+            K.tune(K.TUNE_STREAM_HINT, 1)
+        t = timed_graph(op_keep, per)
+        res["attn_op_b64_l2keep"] = {"us": t * 1e6}
         t = timed_graph(op, per)
         res["attn_op_b64"] = {"us": t * 1e6, "floor_us": (width * d * 2 + d * Hq * hd * 2 + bs * cap * Hkv * hd * 4) / 6.5e6}
         K.tune(K.TUNE_STREAM_GEMM, 2)
