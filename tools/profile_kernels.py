@@ -235,6 +235,7 @@ def main():
         qkv = torch.empty(bs, width, dtype=bf, device=dev)
         t = timed(lambda i: K.gemm(x, wqkv[i % 4], c=qkv), args.iters, st)
         res["gemm_qkv_M64"] = {"us": t * 1e6, "GBs": width * d * 2 / t / 1e9}
+        dump_trace("qkv")
         wo = [torch.randn(d, Hq * hd, dtype=bf, device=dev) * 0.02 for _ in range(4)]
         ao = torch.randn(bs, Hq * hd, dtype=bf, device=dev)
         hres = torch.randn(bs, d, dtype=bf, device=dev)
