@@ -248,6 +248,24 @@ int kl_gemm_bf16_qkv_rope(const uint16_t* a, int64_t a_rows, int64_t row_offset,
                           uint16_t* k_cache, uint16_t* v_cache, int cap, int sink, int chunk_last_pos,
                           void* workspace, int64_t workspace_bytes, cudaStream_t stream);
 
+/* Deferred-reduction expert FFN for decode (weight-streaming path, K-blocked
+ * weights): the down projection's tile-aligned k-splits each write their fp32
+ * accumulator rows to y_part[split][row][d] (split stride part_rows * d) and
+ * no CTA waits for another; kl_combine_deferred sums them in the owner's
+ * order, so FFN + combine are bit-identical to kl_expert_ffn_kb + kl_combine.
+ * `splits` must be kl_expert_ffn_deferred_splits(M, d, f) (0 = this shape
+ * does not run as tile-aligned splits: use kl_expert_ffn_kb). */
+int kl_expert_ffn_deferred_splits(int M, int d, int f);
+int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d, int f,
+                              const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch, float* y_part,
+                              int64_t part_rows, int splits, void* workspace, int64_t workspace_bytes,
+                              cudaStream_t stream);
+/* kl_combine over the fp32 split partials of kl_expert_ffn_kb_deferred
+ * (1 <= splits <= 4, split stride split_rows * d). */
+int kl_combine_deferred(const float* y_part, int splits, int64_t split_rows, const int32_t* pos,
+                        const float* weight, const uint16_t* resid, int64_t T, int k, int d, uint16_t* out,
+                        cudaStream_t stream);
+
 /* Rotary embedding on q/k of a fused qkv row [Hq*hd | Hkv*hd | Hkv*hd] at the
  * token's absolute position, rope applied in place to q; roped k and v are
  * written to the KV cache slot of that position. Cache layout per layer:

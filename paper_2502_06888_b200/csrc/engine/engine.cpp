@@ -418,6 +418,8 @@ bool Engine::plan_at(int n, bool rethrow) {
         add(64 * 1024);
         add((2 * ops_per_step_bound(D_.L, n, El_) + 8) * 8);                     // op timestamps
         add(tb_max_ * D_.hd * 4);                                                // RoPE table
+        if (defer_possible())                                                    // deferred split partials
+            add(4LL * n * w.batch_size * D_.k * D_.d * 4);
         if (kv_off)
             add(static_cast<byte_count>(kKvSlots) * w.batch_size *
                 cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
@@ -436,6 +438,12 @@ bool Engine::plan_at(int n, bool rethrow) {
         kv_off = off_now;     // KV slots join the working set
     }
     return true;
+}
+
+// Deferred split reduction applies to decode blocks of bf16 K-blocked experts
+// on one GPU with one combine per block (not the per-batch simple variant).
+bool Engine::defer_possible() const {
+    return !cfg_.quant && !ep_ && cfg_.kblocked_experts && cfg_.variant != Variant::simple;
 }
 
 void Engine::finish_plan() {
@@ -488,6 +496,11 @@ void Engine::allocate_device() {
     head_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     h_ = bf(t_max_ * D_.d);
     rope_tab_ = static_cast<float*>(take(tb_max_ * D_.hd * 4));  // [tb_max][hd/2] (cos, sin)
+    if (defer_possible()) {
+        ypart_rows_ = static_cast<int64_t>(plan_.n_batches) * cfg_.workload.batch_size * D_.k;  // a decode step's rows
+        ypart_ = static_cast<float*>(take(4 * ypart_rows_ * D_.d * 4));
+        defer_ok_ = std::getenv("KL_NO_DEFER") == nullptr;
+    }
     // Opt-in (KL_QKV_ROPE=1): bit-identical to the separate calls but no
     // faster (attention op 56.6 vs 57.1 us as a graph: the owners' epilogue
     // tail grows by what the RoPE launch cost).

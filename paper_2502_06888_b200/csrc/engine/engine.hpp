@@ -274,6 +274,16 @@ class Engine {
     void stamp(std::int32_t id, int side, cudaStream_t st);
     std::vector<cudaEvent_t> op_end_;                 // by op id (current step window)
     float* rope_tab_ = nullptr;   // decode RoPE (cos, sin) table of one batch [tb_max][hd/2][2]
+    // Deferred down-projection reduction (decode, bf16 K-blocked experts):
+    // the split partials of every expert of a block [4][ypart_rows_][d] fp32,
+    // summed by kl_combine_deferred. block_defer_ = their split count for the
+    // block being executed (0 = plain kl_expert_ffn_kb + kl_combine).
+    float* ypart_ = nullptr;
+    int64_t ypart_rows_ = 0;
+    bool defer_ok_ = false;
+    int block_defer_ = 0;
+    bool defer_possible() const;
+    int block_defer_splits(std::int32_t first_op) const;
     bool rope_fused_ok_ = true;   // QKV GEMM with the fused RoPE / KV-append epilogue
     std::vector<moesim::SimEvent> timeline_;          // measured, by op id
     std::int32_t timed_from_ = 0;

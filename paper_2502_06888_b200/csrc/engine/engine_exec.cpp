@@ -266,6 +266,7 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
                 const detail::BlockRouting routing = read_routing_row(step, layer, b);
                 const std::int32_t first = static_cast<std::int32_t>(em_->schedule().ops.size());
                 em_->simple_close(row, routing);
+                block_defer_ = 0;
                 exec_expert_left_ = 0;
                 for (std::int32_t id = first; id < static_cast<std::int32_t>(em_->schedule().ops.size()); ++id)
                     exec_expert_left_ += em_->schedule().ops[id].kind == OpKind::compute_expert;
@@ -288,6 +289,7 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
         exec_expert_left_ = 0;
         for (std::int32_t id = closed.first_op; id < static_cast<std::int32_t>(em_->schedule().ops.size()); ++id)
             exec_expert_left_ += em_->schedule().ops[id].kind == OpKind::compute_expert;
+        block_defer_ = block_defer_splits(closed.first_op);
         if (ep_) ep_dispatch();  // routed rows to their expert's rank (every rank, every layer)
         issue_pending();
         if (ep_) ep_return(T);   // expert outputs back + weighted combine
@@ -577,12 +579,14 @@ void Engine::exec(std::int32_t id) {
         default:
             throw ConfigError(std::string("engine: op kind ") + op_kind_name(op.kind) + " is not executed on B200 yet");
     }
-    stamp(id, 1, st);
-    cuda_check(cudaEventRecord(op_end_[id], st), "record");
     if (combine_step_ >= 0) {
+        // The block's weighted combine (and, with deferred splits, the
+        // down-projection reduction it carries) belongs to its last expert op.
         combine_block(combine_step_);
         combine_step_ = -1;
     }
+    stamp(id, 1, st);
+    cuda_check(cudaEventRecord(op_end_[id], st), "record");
 }
 
 void Engine::exec_attention(const StreamOp& op) {
@@ -868,6 +872,24 @@ detail::BlockRouting Engine::read_routing(int step, int layer) {
     return r;
 }
 
+// Split count shared by every expert FFN of the block just closed when all of
+// them can leave their down-projection splits for the combine (decode-sized
+// rows, one chunk each, the same tile-aligned split); 0 otherwise.
+int Engine::block_defer_splits(std::int32_t first_op) const {
+    if (!defer_ok_ || ypart_ == nullptr || block_rows_ > ypart_rows_) return 0;
+    const auto& ops = em_->schedule().ops;
+    int S = -1;
+    for (std::int32_t id = first_op; id < static_cast<std::int32_t>(ops.size()); ++id) {
+        const StreamOp& o = ops[id];
+        if (o.kind != OpKind::compute_expert || o.token_count == 0) continue;
+        if (o.token_count > cfg_.ffn_chunk_rows) return 0;
+        const int s = kl_expert_ffn_deferred_splits(static_cast<int>(o.token_count), D_.d, D_.f);
+        if (s < 2 || (S >= 0 && s != S)) return 0;
+        S = s;
+    }
+    return S > 0 ? S : 0;
+}
+
 void Engine::exec_expert(const StreamOp& op) {
     cudaStream_t cs = stream_of(StreamId::compute);
     const int l = op.layer, e = op.expert;
@@ -888,6 +910,10 @@ void Engine::exec_expert(const StreamOp& op) {
         if (q4 && M <= 256)
             kl_check(kl_expert_ffn_q4(xp_, block_rows_, row0 + c, m, D_.d, D_.f, q13, q2, hs_, y_, gemm_ws_,
                                       gemm_ws_bytes_, cs), "expert ffn q4");
+        else if (block_defer_ > 0)  // down-projection splits left for the block's combine to sum
+            kl_check(kl_expert_ffn_kb_deferred(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, ypart_,
+                                               ypart_rows_, block_defer_, gemm_ws_, gemm_ws_bytes_, cs),
+                     "expert ffn (deferred splits)");
         else if (expert_kblocked())  // bf16 experts (resident or streamed) are stored K-blocked
             kl_check(kl_expert_ffn_kb(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
                                       gemm_ws_bytes_, cs), "expert ffn");
@@ -896,8 +922,8 @@ void Engine::exec_expert(const StreamOp& op) {
                                    gemm_ws_bytes_, cs), "expert ffn");
         ++launches_;  // gate/up (SwiGLU) GEMM + down GEMM
     }
-    // The block's last expert op: the combine follows right after the op's
-    // end event (so compute_expert events bracket the FFN kernels only).
+    // The block's last expert op also runs the combine (exec(), before the
+    // op's end stamp).
     if (--exec_expert_left_ == 0 && !ep_) {
         combine_step_ = op.step;
         combine_batch_ = cfg_.variant == Variant::simple ? op.batch : -1;
@@ -922,7 +948,11 @@ void Engine::combine_block(int step) {
         return;
     }
     const int64_t T = static_cast<int64_t>(plan_.n_batches) * tokens_per_batch(step);
-    kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
+    if (block_defer_ > 0)
+        kl_check(kl_combine_deferred(ypart_, block_defer_, ypart_rows_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs),
+                 "combine (deferred splits)");
+    else
+        kl_check(kl_combine(y_, pos_, weight_, h_, T, D_.k, D_.d, h_, cs), "combine");
     if (cfg_.record_hidden) {
         std::vector<uint16_t> dump(static_cast<size_t>(T) * D_.d);
         cuda_check(cudaMemcpyAsync(dump.data(), h_, dump.size() * 2, cudaMemcpyDeviceToHost, cs), "dump");

@@ -610,6 +610,12 @@ struct StreamArgs {
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
     int owner_extra;  // tile-aligned splits: extra units of the owner's (last) range
     int bulk_publish; // contributors whose ring is idle publish their partial with one bulk copy
+    // Deferred split reduction (kStore, NMMA 1, tile-aligned splits): every CTA
+    // writes its fp32 accumulator to defer[split][row][feature] (row pitch
+    // defer_ld) and the consumer sums the splits; no flags, no fixup.
+    float* defer;
+    int64_t defer_split_elems;
+    int defer_ld;
     // Fused RoPE + KV append (QKV projection, one 128-row weight tile = one
     // head of hd 128): rows [q heads | k heads | v heads], NeoX pairs.
     const float2* rope_tab;  // [M][64] (cos, sin) per row and frequency; nullptr = plain store
@@ -955,6 +961,16 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
             const uint32_t acc0 = tmem_base + lane_off + b * buf_cols;
             const bool has_last = kb1 == KB;
             if (p.debug & 2) {
+            } else if (p.defer != nullptr) {
+                float* dst = p.defer + static_cast<int64_t>(cta % p.split) * p.defer_split_elems +
+                             static_cast<int64_t>(t) * kWRows + frow;
+                for (int col = 0; col < cols; col += 16) {
+                    float v[16];
+                    tmem_ld16(acc0 + col, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (col + i < p.M) __stcg(dst + static_cast<int64_t>(col + i) * p.defer_ld, v[i]);
+                }
             } else if (!has_last) {
                 // Contributor: publish the fp32 partial of this tile. Slot
                 // layout [j][16-column chunk][float4 i][feature row] so each
@@ -1441,8 +1457,12 @@ struct RopeArgs {
 template <int EPI, int NMMA, bool Q4 = false>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
                   int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
-                  cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false, const RopeArgs* rope = nullptr) {
+                  cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false, const RopeArgs* rope = nullptr,
+                  float* defer = nullptr, int64_t defer_split_elems = 0, int defer_splits = 0) {
     StreamArgs p{};
+    p.defer = defer;
+    p.defer_split_elems = defer_split_elems;
+    p.defer_ld = static_cast<int>(n_tiles) * kWRows * NMMA;
     if (rope != nullptr) {
         p.rope_tab = rope->table;
         p.rope_pos = rope->pos;
@@ -1502,8 +1522,14 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
         // Owner bonus, capped so every contributor keeps at least one unit.
         p.owner_extra = std::max(0, std::min(g_stream_owner_extra, p.KB - 2 * p.split));
     }
-    const int G_ws = static_cast<int>(std::min<int64_t>((ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA),
-                                                        kFlagBytes / 4));
+    if (defer != nullptr) {
+        // Deferred splits need exactly the tile-aligned split count the
+        // caller sized its partial buffer for; no workspace slots are used.
+        if (EPI != kStore || NMMA != 1 || Q4 || p.split != defer_splits || p.owner_extra != 0) return KL_EUNSUPPORTED;
+    }
+    const int G_ws = defer != nullptr ? G
+                                      : static_cast<int>(std::min<int64_t>(
+                                            (ws_bytes - kFlagBytes) / stream_slot_bytes(M, NMMA), kFlagBytes / 4));
     if (G > G_ws) {  // workspace-limited: plain stream-K ranges over fewer CTAs
         G = G_ws;
         p.split = 0;
@@ -1830,6 +1856,50 @@ extern "C" int kl_expert_ffn_kb(const uint16_t* xp, int64_t rows_total, int64_t 
     if (rc) return rc;
     return kl_gemm_bf16_kb(h_scratch, M, 0, M, f, w2, d, y + row_offset * d, d, nullptr, 0, workspace, workspace_bytes,
                            stream);
+}
+
+// Split count of the down projection [d, f] for kl_expert_ffn_kb_deferred
+// at M rows (the tile-aligned split launch_stream will choose), 0 when that
+// GEMM would not run as tile-aligned splits of the weight-streaming kernel.
+extern "C" int kl_expert_ffn_deferred_splits(int M, int d, int f) {
+    using namespace kl;
+    if (M < 1 || M > 256 || d % kWRows != 0 || f % BK != 0 || !stream_eligible(M, d, f, kStore)) return 0;
+    if (stream_nmma(d, kStore) != 1) return 0;
+    const int NP = stream_np(M);
+    const int per_kb = kWTileBytes + NP * BK * 2;
+    const int min_stages = g_stream_ks == 3 ? 2 : 3;
+    const int ks = (g_stream_ks >= 2 && (f / BK) % 2 == 0 &&
+                    std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / (2 * per_kb)) >= min_stages)
+                       ? 2
+                       : 1;
+    const int KB = f / BK / ks, n_tiles = d / kWRows;
+    const int G = std::max(1, std::min(sm_count() * g_stream_ctas, n_tiles * KB / 4));
+    if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
+        return 0;
+    if (!(g_stream_even_split && n_tiles < G && G / n_tiles >= 2 &&
+          (KB % (G / n_tiles) == 0 || g_stream_even_split == 2)))
+        return 0;
+    if (g_stream_owner_extra != 0) return 0;
+    const int S = G / n_tiles;
+    return S <= 4 ? S : 0;
+}
+
+extern "C" int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
+                                         int f, const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch,
+                                         float* y_part, int64_t part_rows, int splits, void* workspace,
+                                         int64_t workspace_bytes, cudaStream_t stream) {
+    using namespace kl;
+    if (M == 0) return KL_OK;
+    if (y_part == nullptr || h_scratch == nullptr || splits < 2 || splits > 4 || row_offset < 0 ||
+        row_offset + M > part_rows || !aligned16(h_scratch) || !aligned16(w2))
+        return KL_EINVAL;
+    if (kl_expert_ffn_deferred_splits(M, d, f) != splits) return KL_EUNSUPPORTED;
+    int rc = kl_gemm_bf16_kb(xp, rows_total, row_offset, M, d, w13, 2 * f, h_scratch, f, nullptr, 2, workspace,
+                             workspace_bytes, stream);
+    if (rc) return rc;
+    return launch_stream<kStore, 1>(h_scratch, M, 0, M, f, w2, d, d / kWRows, 0, nullptr, d, nullptr, workspace,
+                                    workspace_bytes, stream, nullptr, true, nullptr, y_part + row_offset * d,
+                                    part_rows * d, splits);
 }
 
 namespace kl {

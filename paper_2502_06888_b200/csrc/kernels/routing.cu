@@ -622,6 +622,71 @@ combine_kernel(const uint16_t* __restrict__ y, const int32_t* __restrict__ pos, 
     }
 }
 
+// combine_kernel over a down projection left as S fp32 split partials
+// (kl_expert_ffn_kb_deferred): y = bf16(((p[S-1] + p[0]) + p[1]) + ...), the
+// order the streaming GEMM's owner would have summed them in (its own split
+// last in the k range, then the contributors ascending), then the same
+// weighted sum as combine_kernel: bit-identical to the non-deferred path.
+template <int KMAX>
+__global__ void __launch_bounds__(kRowThreads)
+combine_deferred_kernel(const float* __restrict__ yp, int S, int64_t split_elems, const int32_t* __restrict__ pos,
+                        const float* __restrict__ weight, const uint16_t* resid, int64_t T, int k, int d,
+                        uint16_t* out) {
+    pdl_enter();
+    const int64_t t = blockIdx.x;
+    if (t >= T) return;
+    int32_t p[KMAX];
+    float w[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        p[j] = j < k ? pos[t * k + j] : 0;
+        w[j] = j < k ? weight[t * k + j] : 0.f;
+    }
+    const int n8 = d / 8;
+    for (int i = threadIdx.x; i < n8; i += kRowThreads) {
+        const uint4 rq = *reinterpret_cast<const uint4*>(resid + t * d + i * 8);
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            if (j >= k) break;
+            const float* base = yp + static_cast<int64_t>(p[j]) * d + i * 8;
+            const float4* own = reinterpret_cast<const float4*>(base + static_cast<int64_t>(S - 1) * split_elems);
+            const float4 o0 = __ldg(own), o1 = __ldg(own + 1);
+            float4 q0[3], q1[3];
+#pragma unroll
+            for (int sp = 0; sp < 3; ++sp)
+                if (sp < S - 1) {
+                    const float4* src = reinterpret_cast<const float4*>(base + sp * split_elems);
+                    q0[sp] = __ldg(src);
+                    q1[sp] = __ldg(src + 1);
+                }
+            float y[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+            for (int sp = 0; sp < 3; ++sp) {
+                if (sp >= S - 1) break;
+                const float q[8] = {q0[sp].x, q0[sp].y, q0[sp].z, q0[sp].w, q1[sp].x, q1[sp].y, q1[sp].z, q1[sp].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = __fadd_rn(y[e], q[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = fmaf(w[j], bf2f(f2bf(y[e])), acc[e]);
+        }
+        const uint32_t rw[4] = {rq.x, rq.y, rq.z, rq.w};
+        float rv[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            rv[2 * q] = bf2f(static_cast<uint16_t>(rw[q] & 0xffffu));
+            rv[2 * q + 1] = bf2f(static_cast<uint16_t>(rw[q] >> 16));
+        }
+        uint4 o;
+        o.x = pack2(__fadd_rn(rv[0], acc[0]), __fadd_rn(rv[1], acc[1]));
+        o.y = pack2(__fadd_rn(rv[2], acc[2]), __fadd_rn(rv[3], acc[3]));
+        o.z = pack2(__fadd_rn(rv[4], acc[4]), __fadd_rn(rv[5], acc[5]));
+        o.w = pack2(__fadd_rn(rv[6], acc[6]), __fadd_rn(rv[7], acc[7]));
+        *reinterpret_cast<uint4*>(out + t * d + i * 8) = o;
+    }
+}
+
 // ------------------------------------------------------------ prefetcher --
 __global__ void coact_kernel(const int32_t* __restrict__ prev, const int32_t* __restrict__ cur, int64_t T, int k,
                              int E, int layer, int64_t* __restrict__ table, int64_t* __restrict__ marginal) {
@@ -850,6 +915,21 @@ extern "C" int kl_combine(const uint16_t* y, const int32_t* pos, const float* we
                           weight, resid, T, k, d, out);
     return launch_pdl(combine_kernel<8>, dim3(static_cast<unsigned>(T)), dim3(kRowThreads), 0, stream, y, pos, weight,
                       resid, T, k, d, out);
+}
+
+extern "C" int kl_combine_deferred(const float* y_part, int splits, int64_t split_rows, const int32_t* pos,
+                                   const float* weight, const uint16_t* resid, int64_t T, int k, int d, uint16_t* out,
+                                   cudaStream_t stream) {
+    if (T < 0 || k < 1 || k > 8 || d % 8 != 0 || splits < 1 || splits > 4 || split_rows < 0 || !y_part || !pos ||
+        !weight || !resid || !out)
+        return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int64_t se = split_rows * d;
+    if (k <= 2)
+        return launch_pdl(combine_deferred_kernel<2>, dim3(static_cast<unsigned>(T)), dim3(kRowThreads), 0, stream,
+                          y_part, splits, se, pos, weight, resid, T, k, d, out);
+    return launch_pdl(combine_deferred_kernel<8>, dim3(static_cast<unsigned>(T)), dim3(kRowThreads), 0, stream, y_part,
+                      splits, se, pos, weight, resid, T, k, d, out);
 }
 
 extern "C" int kl_coact_update(const int32_t* prev, const int32_t* cur, int64_t T, int k, int E, int layer,

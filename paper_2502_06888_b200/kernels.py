@@ -39,6 +39,9 @@ _gate = _sig("kl_gate_topk", [_P, _P, _P, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P
 _perm_ws = _sig("kl_permute_workspace_bytes", [_L, _I], C.c_int64)
 _perm = _sig("kl_permute", [_P, _L, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P])
 _comb = _sig("kl_combine", [_P, _P, _P, _P, _L, _I, _I, _P, _P])
+_comb_def = _sig("kl_combine_deferred", [_P, _I, _L, _P, _P, _P, _L, _I, _I, _P, _P])
+_ffn_def = _sig("kl_expert_ffn_kb_deferred", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _L, _I, _P, _L, _P])
+_ffn_def_splits = _sig("kl_expert_ffn_deferred_splits", [_I, _I, _I])
 _coact = _sig("kl_coact_update", [_P, _P, _L, _I, _I, _I, _P, _P, _P])
 _pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
 _rms = _sig("kl_rmsnorm", [_P, _P, _L, _I, _F, _P, _P])
@@ -243,6 +246,30 @@ def combine(y, pos, weight, resid, out=None, stream=None):
     d = resid.shape[1]
     out = torch.empty_like(resid) if out is None else out
     _chk(_comb(_p(y), _p(pos), _p(weight), _p(resid), T, k, d, _p(out), _s(stream)), "kl_combine")
+    return out
+
+
+def expert_ffn_deferred_splits(M, d, f):
+    return int(_ffn_def_splits(M, d, f))
+
+
+def expert_ffn_deferred(xp, row_offset, m, w13, w2, y_part, h_scratch, splits, stream=None):
+    """kl_expert_ffn_kb_deferred: K-blocked weights, down-projection splits
+    left as fp32 partials in y_part [splits, rows, d]."""
+    d = xp.shape[1]
+    f = w2.shape[1]
+    wsb = workspace_bytes(m, 2 * f, d, 2)
+    ws = workspace(max(wsb, 1024), xp.device)
+    _chk(_ffn_def(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y_part),
+                  y_part.shape[1], splits, _p(ws), max(wsb, 1024), _s(stream)), "kl_expert_ffn_kb_deferred")
+
+
+def combine_deferred(y_part, splits, pos, weight, resid, out=None, stream=None):
+    T, k = weight.shape
+    d = resid.shape[1]
+    out = torch.empty_like(resid) if out is None else out
+    _chk(_comb_def(_p(y_part), splits, y_part.shape[1], _p(pos), _p(weight), _p(resid), T, k, d, _p(out), _s(stream)),
+         "kl_combine_deferred")
     return out
 
 

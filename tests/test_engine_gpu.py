@@ -441,3 +441,33 @@ def test_fused_qkv_rope_matches_separate_calls(cuda, monkeypatch):
         assert np.array_equal(a, b)
     for a, b in zip(d1, d2):
         assert np.array_equal(np.array(a), np.array(b))
+
+
+def test_deferred_split_reduction_matches_owner_fixup(cuda, monkeypatch):
+    """Mixtral-8x7B dims (2 layers, bs 64 x n 2, gate routing, experts
+    streamed and resident): leaving the down projection's k-splits as fp32
+    partials for the block's combine gives the same tokens and hidden states
+    as the owner-fixup FFN (KL_NO_DEFER), and the same executed op log."""
+    cfg = {"model": {"preset": "mixtral-8x7b", "n_layers": 2},
+           "workload": {"batch_size": 64, "n_batches": 2, "prompt_len": 16, "gen_len": 4},
+           "hbm_cap_bytes": 8_000_000_000, "host_distinct_layers": 2, "routing": "gate", "record_hidden": True}
+    runs = []
+    for env in (None, "1"):
+        if env is None:
+            monkeypatch.delenv("KL_NO_DEFER", raising=False)
+        else:
+            monkeypatch.setenv("KL_NO_DEFER", env)
+        eng = make(cfg)
+        outs = run_all_steps(eng, cfg, seed=4)
+        dumps = eng.report("hidden")["dumps"]
+        sched = eng.report("schedule")["text"]
+        assert eng.report("validate")["violations"] == []
+        eng.close()
+        runs.append((outs, dumps, sched))
+    (o1, d1, s1), (o2, d2, s2) = runs
+    assert s1 == s2
+    assert len(d1) == len(d2) > 0
+    for a, b in zip(o1, o2):
+        assert np.array_equal(a, b)
+    for a, b in zip(d1, d2):
+        assert np.array_equal(np.array(a), np.array(b))

@@ -198,6 +198,52 @@ def test_gemm_split_finish_bit_identical(K, cuda, M, N, Kd, epi):
     close_bf16(to_bits(fin[0]), ref)
 
 
+def test_deferred_ffn_and_combine_bit_identical(K, cuda):
+    """Mixtral-8x7B experts on skewed decode routing (512 tokens, top-2, per
+    expert ~90..~190 rows): FFN with the down projection's splits left as fp32
+    partials + the deferred combine equal the owner-fixup FFN + combine bit
+    for bit, row by row and after the weighted combine."""
+    T, k, E, d, f = 512, 2, 8, 4096, 14336
+    rng = np.random.default_rng(5)
+    p = np.array([0.18, 0.16, 0.14, 0.13, 0.12, 0.1, 0.09, 0.08])
+    idx = np.stack([rng.choice(E, 2, replace=False, p=p) for _ in range(T)]).astype(np.int32)
+    wt = rng.random((T, k)).astype(np.float32)
+    wt /= wt.sum(1, keepdims=True)
+    x2 = torch.randn(T, d, dtype=torch.bfloat16, device=cuda)
+    resid = torch.randn(T, d, dtype=torch.bfloat16, device=cuda)
+    counts, offsets, pos, _, xp = K.permute(torch.from_numpy(idx).to(cuda), E, x2=x2)
+    counts, offsets = counts.cpu().numpy(), offsets.cpu().numpy()
+    R = T * k
+    y = torch.zeros(R, d, dtype=torch.bfloat16, device=cuda)
+    h = torch.empty(R, f, dtype=torch.bfloat16, device=cuda)
+    ypart = torch.zeros(4, R, d, dtype=torch.float32, device=cuda)
+    S_seen = set()
+    for e in range(E):
+        m, off = int(counts[e]), int(offsets[e])
+        w = torch.empty(3 * d * f, dtype=torch.bfloat16, device=cuda)
+        K.fill_normal(w, 90 + e, 0.02)
+        w13 = K.weights_kblock(w[:2 * f * d].view(2 * f, d))
+        w2 = K.weights_kblock(w[2 * f * d:].view(d, f))
+        K.expert_ffn(xp, off, m, w13, w2, y, h, kblocked=True)
+        S = K.expert_ffn_deferred_splits(m, d, f)
+        assert S >= 2, (m, S)
+        S_seen.add(S)
+        K.expert_ffn_deferred(xp, off, m, w13, w2, ypart, h, S)
+        del w, w13, w2
+    assert len(S_seen) == 1
+    S = S_seen.pop()
+    wd = torch.from_numpy(wt).to(cuda)
+    out1 = K.combine(y, pos, wd, resid)
+    out2 = K.combine_deferred(ypart, S, pos, wd, resid)
+    torch.cuda.synchronize()
+    order = [S - 1] + list(range(S - 1))
+    acc = ypart[order[0]].clone()
+    for s_ in order[1:]:
+        acc += ypart[s_]
+    assert torch.equal(acc.to(torch.bfloat16), y)
+    assert torch.equal(out1, out2)
+
+
 @pytest.mark.parametrize("M,d,f", [(128, 512, 1792), (37, 256, 512), (260, 1024, 2048), (128, 4096, 1024),
                                    (64, 2048, 1408), (300, 512, 1792), (8, 4096, 14336), (21, 4096, 14336),
                                    (128, 4096, 14336), (8, 6144, 16384), (128, 6144, 16384)])

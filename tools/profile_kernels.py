@@ -209,6 +209,17 @@ def main():
         res["expert_ffn"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9, "TFLOPs": 6 * M * d * f / t / 1e12}
         t = timed_graph(ffn, 16)
         res["expert_ffn_graph"] = {"M": M, "us": t * 1e6, "GBs": byt / t / 1e9}
+        S = K.expert_ffn_deferred_splits(M, d, f)
+        if kb and S:
+            ypart = torch.empty(S, R, d, dtype=torch.float32, device=dev)
+
+            def ffn_def(i):
+                w = ws[i % E]
+                K.expert_ffn_deferred(xp, (i % E) * M % (R - M + 1), M, w[: 2 * f * d].view(2 * f, d),
+                                      w[2 * f * d:].view(d, f), ypart, h, S)
+            t = timed_graph(ffn_def, 16)
+            res["expert_ffn_deferred_graph"] = {"M": M, "splits": S, "us": t * 1e6, "GBs": byt / t / 1e9}
+            del ypart
 
         def g1(i):
             w = ws[i % E]
@@ -371,6 +382,10 @@ def main():
         _, _, p, _, xp = K.permute(idx, E, x2=x2)
         t = timed_graph(lambda i: K.combine(xp, p, wt, h, out=x2), args.iters)
         res["combine_T512"] = {"us": t * 1e6, "GBs": (k * T * d * 2 + 2 * T * d * 2) / t / 1e9}
+        ypart = torch.randn(4, T * k, d, dtype=torch.float32, device=dev)
+        t = timed_graph(lambda i: K.combine_deferred(ypart, 4, p, wt, h, out=x2), args.iters)
+        res["combine_deferred4_T512"] = {"us": t * 1e6, "GBs": (4 * k * T * d * 4 + 2 * T * d * 2) / t / 1e9}
+        del ypart
         t = timed_graph(lambda i: K.rmsnorm(h[:bs], nw, out=x2[:bs]), args.iters)
         res["rmsnorm_b64"] = {"us": t * 1e6, "GBs": 2 * bs * d * 2 / t / 1e9}
         # prefill-sized group: bs 32 x n 8 x 512 tokens
