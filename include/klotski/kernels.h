@@ -75,7 +75,7 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_PREFILL_TC 6 /* tcgen05 prefill attention: 2 = 64-key blocks, two CTAs per SM (default), 1 = 128-key blocks, 0 = CUDA-core fallback */
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
 #define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 3 (default) = 2 where >= 2 stages fit, 2 = 2 where >= 3 stages fit (3D TMA boxes), 1 */
-#define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: 1 (default) = grid of tiles x floor(SMs / tiles) when that splits each tile into equal k-ranges, 2 = also into k-ranges differing by one unit, 0 = one CTA per SM */
+#define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: grid of tiles x floor(SMs / tiles), each tile split into equal k-ranges (1) or, default, also near-equal ones (2: the last range takes the remainder); 0 = stream-K ranges over one CTA per SM */
 #define KL_TUNE_STREAM_L2_AHEAD 14 /* weight-streaming GEMM: weight units prefetched into L2 ahead of the smem ring (0 = off) */
 #define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
 #define KL_TUNE_SPLIT_FINISH 20 /* tcgen05 GEMM split-K: 1 = each tile finished by its last-arriving CTA, 0 (default) = separate reduce kernel */
@@ -256,6 +256,22 @@ int kl_gemm_bf16_qkv_rope(const uint16_t* a, int64_t a_rows, int64_t row_offset,
  * `splits` must be kl_expert_ffn_deferred_splits(M, d, f) (0 = this shape
  * does not run as tile-aligned splits: use kl_expert_ffn_kb). */
 int kl_expert_ffn_deferred_splits(int M, int d, int f);
+/* Deferred split reduction for any decode-sized [N, K] weight-streaming GEMM
+ * (e.g. the QKV projection): c_part[split][row][N] fp32 (split stride
+ * part_rows * N); splits = kl_gemm_deferred_splits(M, N, K) (0 = not on the
+ * tile-aligned split path). b_kblocked: weights in the K-blocked layout. */
+int kl_gemm_deferred_splits(int M, int N, int K);
+int kl_gemm_bf16_deferred(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                          const uint16_t* b, int N, int b_kblocked, float* c_part, int64_t part_rows,
+                          int splits, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+/* kl_rope_kv_append over the fp32 split partials of a deferred QKV GEMM:
+ * each element summed in the owner's order and rounded to bf16 (what the
+ * GEMM would have stored), then RoPE / KV append as kl_rope_kv_append; the
+ * full qkv rows are written. */
+int kl_rope_kv_append_deferred(const float* qkv_part, int splits, int64_t part_rows, uint16_t* qkv, int64_t T,
+                               int Hq, int Hkv, int hd, const int32_t* pos, const int32_t* seq,
+                               float rope_theta, uint16_t* k_cache, uint16_t* v_cache, int cap, int sink,
+                               int chunk_last_pos, cudaStream_t stream);
 int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d, int f,
                               const uint16_t* w13, const uint16_t* w2, uint16_t* h_scratch, float* y_part,
                               int64_t part_rows, int splits, void* workspace, int64_t workspace_bytes,

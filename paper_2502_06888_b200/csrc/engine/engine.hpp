@@ -278,6 +278,8 @@ class Engine {
     // the split partials of every expert of a block [4][ypart_rows_][d] fp32,
     // summed by kl_combine_deferred. block_defer_ = their split count for the
     // block being executed (0 = plain kl_expert_ffn_kb + kl_combine).
+    float* qkvpart_ = nullptr;    // deferred QKV split partials of one decode batch [4][bs][qkv_width]
+    int qkv_defer_ = -1;          // split count of the decode QKV GEMM (-1: not yet queried, 0: off)
     float* ypart_ = nullptr;
     int64_t ypart_rows_ = 0;
     bool defer_ok_ = false;

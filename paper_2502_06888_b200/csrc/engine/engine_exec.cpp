@@ -646,6 +646,18 @@ void Engine::exec_attention(const StreamOp& op) {
         } else {
             kl_check(rc, "qkv + rope/kv");
         }
+    } else if (step != 0 && !fused && defer_ok_ && qkvpart_ != nullptr &&
+               (qkv_defer_ < 0 ? (qkv_defer_ = kl_gemm_deferred_splits(tpb, D_.qkv_width(), D_.d)) : qkv_defer_) > 0) {
+        // Decode: the QKV GEMM leaves its tile-aligned k-splits as fp32
+        // partials and the RoPE / KV-append kernel sums them (no fixup tail).
+        kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
+        kl_check(kl_gemm_bf16_deferred(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), 0, qkvpart_,
+                                       cfg_.workload.batch_size, qkv_defer_, gemm_ws_, gemm_ws_bytes_, cs),
+                 "qkv (deferred splits)");
+        kl_check(kl_rope_kv_append_deferred(qkvpart_, qkv_defer_, cfg_.workload.batch_size, qkv_, tpb, D_.Hq, D_.Hkv,
+                                            D_.hd, tok_pos_ + row0, seq_idx, D_.theta, kc, vc, kv_cap_, kv_sink_, -1,
+                                            cs),
+                 "rope/kv (deferred splits)");
     } else {
         kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
         if (fused)

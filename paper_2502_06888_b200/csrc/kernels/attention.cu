@@ -71,6 +71,72 @@ __global__ void rope_append_kernel(uint16_t* __restrict__ qkv, int64_t T, int Hq
     }
 }
 
+// rope_append_kernel over a QKV projection left as S fp32 split partials
+// (kl_gemm_bf16_deferred): each element is first summed in the owner's order
+// (own split S-1, then 0..S-2) and rounded to bf16 -- the value the GEMM's
+// fixup would have stored -- then rotated / appended exactly as
+// rope_append_kernel, and the full qkv row is written.
+__device__ __forceinline__ float sum_split_elem(const float* __restrict__ part, int S, int64_t se, int64_t off) {
+    float v = part[static_cast<int64_t>(S - 1) * se + off];
+    for (int sp = 0; sp < S - 1; ++sp) v = __fadd_rn(v, part[sp * se + off]);
+    return bf2f(f2bf(v));
+}
+
+__global__ void rope_append_deferred_kernel(const float* __restrict__ part, int S, int64_t split_elems,
+                                            uint16_t* __restrict__ qkv, int64_t T, int Hq, int Hkv, int hd,
+                                            const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+                                            float theta, uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+                                            int cap, int sink, int chunk_last_pos) {
+    pdl_enter();
+    const int half = hd / 2;
+    const int heads = Hq + Hkv;
+    const int64_t per_tok = static_cast<int64_t>(heads) * half + static_cast<int64_t>(Hkv) * half;
+    const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= T * per_tok) return;
+    const int64_t t = id / per_tok;
+    int64_t rem = id % per_tok;
+    const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * hd;
+    uint16_t* row = qkv + t * width;
+    const int64_t prow = t * width;
+    const int p = pos[t];
+    const int slot = slot_of(p, cap, sink);
+    const bool to_cache = chunk_last_pos < 0 || p < sink || p > chunk_last_pos - (cap - sink);
+    const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot) * Hkv * hd;
+    if (rem < static_cast<int64_t>(heads) * half) {
+        const int head = static_cast<int>(rem / half);
+        const int i = static_cast<int>(rem % half);
+        float sn, cs;
+        rope_cs(p, i, hd, theta, cs, sn);
+        const int64_t b0 = prow + static_cast<int64_t>(head) * hd;
+        const float a = sum_split_elem(part, S, split_elems, b0 + i);
+        const float b = sum_split_elem(part, S, split_elems, b0 + i + half);
+        const uint16_t ra = f2bf(rope_lo(a, b, cs, sn));
+        const uint16_t rb = f2bf(rope_hi(a, b, cs, sn));
+        uint16_t* base = row + static_cast<int64_t>(head) * hd;
+        base[i] = ra;
+        base[i + half] = rb;
+        if (head >= Hq && to_cache) {
+            uint16_t* dst = kc + cache_row + static_cast<int64_t>(head - Hq) * hd;
+            dst[i] = ra;
+            dst[i + half] = rb;
+        }
+    } else {
+        rem -= static_cast<int64_t>(heads) * half;
+        const int kvh = static_cast<int>(rem / half);
+        const int i = static_cast<int>(rem % half);
+        const int64_t b0 = prow + static_cast<int64_t>(Hq + Hkv + kvh) * hd;
+        const uint16_t v0 = f2bf(sum_split_elem(part, S, split_elems, b0 + i));
+        const uint16_t v1 = f2bf(sum_split_elem(part, S, split_elems, b0 + i + half));
+        uint16_t* src = row + static_cast<int64_t>(Hq + Hkv + kvh) * hd;
+        src[i] = v0;
+        src[i + half] = v1;
+        if (!to_cache) return;
+        uint16_t* dst = vc + cache_row + static_cast<int64_t>(kvh) * hd;
+        dst[i] = v0;
+        dst[i + half] = v1;
+    }
+}
+
 // Token-per-block RoPE + KV append: the token's cos/sin table (hd/2 entries,
 // the same powf / sincosf per element as rope_append_kernel, so results are
 // bit-identical) is computed once into shared memory and shared by all
@@ -1290,6 +1356,22 @@ extern "C" int kl_rope_kv_append(uint16_t* qkv, int64_t T, int Hq, int Hkv, int 
                                                                                rope_theta, k_cache, v_cache, cap, sink,
                                                                                chunk_last_pos)) return rc_;
     return check_launch();
+}
+
+extern "C" int kl_rope_kv_append_deferred(const float* qkv_part, int splits, int64_t part_rows, uint16_t* qkv,
+                                          int64_t T, int Hq, int Hkv, int hd, const int32_t* pos, const int32_t* seq,
+                                          float rope_theta, uint16_t* k_cache, uint16_t* v_cache, int cap, int sink,
+                                          int chunk_last_pos, cudaStream_t stream) {
+    if (T < 0 || Hq < 1 || Hkv < 1 || Hq % Hkv || hd % 2 || cap <= sink || sink < 0 || splits < 1 || splits > 4 ||
+        T > part_rows)
+        return KL_EINVAL;
+    if (!qkv_part || !qkv || !pos || !seq || !k_cache || !v_cache) return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
+    const int64_t se = part_rows * (static_cast<int64_t>(Hq) + 2 * Hkv) * hd;
+    return launch_pdl(rope_append_deferred_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
+                      qkv_part, splits, se, qkv, T, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink,
+                      chunk_last_pos);
 }
 
 extern "C" int kl_attn_decode(const uint16_t* q, int64_t q_stride, const int32_t* pos, const int32_t* seq, int64_t T,

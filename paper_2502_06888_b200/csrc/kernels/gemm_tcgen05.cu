@@ -1389,7 +1389,7 @@ int g_stream_stages = 8;   // kl_tune(KL_TUNE_STREAM_STAGES, ...): cap on the sm
 int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
-int g_stream_even_split = 1;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...): 1 = equal splits, 2 = also near-equal
+int g_stream_even_split = 2;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...): 1 = equal splits only, 2 (default) = also near-equal
 int g_stream_l2_ahead = 0;  // kl_tune(KL_TUNE_STREAM_L2_AHEAD, units)
 int g_stream_owner_extra = 0;  // kl_tune(KL_TUNE_STREAM_OWNER_EXTRA, units)
 int g_stream_fused_fixup = 1;  // kl_tune(KL_TUNE_STREAM_FUSED_FIXUP, 0|1)
@@ -1513,7 +1513,7 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
         G = n_tiles;  // one whole tile per CTA: no split partials, the rest of the SMs idle
     else if (g_stream_even_split && n_tiles < G && G / n_tiles >= 2 &&
-             (p.KB % (G / n_tiles) == 0 || g_stream_even_split == 2)) {
+             (p.KB % (G / n_tiles) == 0 || g_stream_even_split == 2 || defer != nullptr)) {
         // Every tile split into the same number S of k-ranges cut at tile
         // boundaries (unit_begin), equal when S divides KB (else the owner's
         // range takes the remainder), the owner's optionally longer.
@@ -1858,30 +1858,44 @@ extern "C" int kl_expert_ffn_kb(const uint16_t* xp, int64_t rows_total, int64_t 
                            stream);
 }
 
-// Split count of the down projection [d, f] for kl_expert_ffn_kb_deferred
-// at M rows (the tile-aligned split launch_stream will choose), 0 when that
-// GEMM would not run as tile-aligned splits of the weight-streaming kernel.
-extern "C" int kl_expert_ffn_deferred_splits(int M, int d, int f) {
+// Tile-aligned split count launch_stream picks for a deferred [N, K]
+// weight-streaming GEMM at M rows (near-equal splits allowed), 0 when that
+// GEMM would not run as tile-aligned splits (or S > 4).
+extern "C" int kl_gemm_deferred_splits(int M, int N, int K) {
     using namespace kl;
-    if (M < 1 || M > 256 || d % kWRows != 0 || f % BK != 0 || !stream_eligible(M, d, f, kStore)) return 0;
-    if (stream_nmma(d, kStore) != 1) return 0;
+    if (M < 1 || M > 256 || N % kWRows != 0 || K % BK != 0 || !stream_eligible(M, N, K, kStore)) return 0;
+    if (stream_nmma(N, kStore) != 1) return 0;
     const int NP = stream_np(M);
     const int per_kb = kWTileBytes + NP * BK * 2;
     const int min_stages = g_stream_ks == 3 ? 2 : 3;
-    const int ks = (g_stream_ks >= 2 && (f / BK) % 2 == 0 &&
+    const int ks = (g_stream_ks >= 2 && (K / BK) % 2 == 0 &&
                     std::min(g_stream_stages, kStreamSmemBudget / g_stream_ctas / (2 * per_kb)) >= min_stages)
                        ? 2
                        : 1;
-    const int KB = f / BK / ks, n_tiles = d / kWRows;
+    const int KB = K / BK / ks, n_tiles = N / kWRows;
     const int G = std::max(1, std::min(sm_count() * g_stream_ctas, n_tiles * KB / 4));
     if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
         return 0;
-    if (!(g_stream_even_split && n_tiles < G && G / n_tiles >= 2 &&
-          (KB % (G / n_tiles) == 0 || g_stream_even_split == 2)))
-        return 0;
+    if (!(g_stream_even_split && n_tiles < G && G / n_tiles >= 2)) return 0;
     if (g_stream_owner_extra != 0) return 0;
     const int S = G / n_tiles;
     return S <= 4 ? S : 0;
+}
+
+extern "C" int kl_expert_ffn_deferred_splits(int M, int d, int f) { return kl_gemm_deferred_splits(M, d, f); }
+
+extern "C" int kl_gemm_bf16_deferred(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
+                                     const uint16_t* b, int N, int b_kblocked, float* c_part, int64_t part_rows,
+                                     int splits, void* workspace, int64_t workspace_bytes, cudaStream_t stream) {
+    using namespace kl;
+    if (M == 0) return KL_OK;
+    if (c_part == nullptr || a == nullptr || b == nullptr || splits < 2 || splits > 4 || M > part_rows ||
+        row_offset < 0 || row_offset + M > a_rows || !aligned16(a) || !aligned16(b))
+        return KL_EINVAL;
+    if (kl_gemm_deferred_splits(M, N, K) != splits) return KL_EUNSUPPORTED;
+    return launch_stream<kStore, 1>(a, a_rows, row_offset, M, K, b, N, N / kWRows, 0, nullptr, N, nullptr, workspace,
+                                    workspace_bytes, stream, nullptr, b_kblocked != 0, nullptr, c_part,
+                                    part_rows * N, splits);
 }
 
 extern "C" int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,

@@ -42,6 +42,9 @@ _comb = _sig("kl_combine", [_P, _P, _P, _P, _L, _I, _I, _P, _P])
 _comb_def = _sig("kl_combine_deferred", [_P, _I, _L, _P, _P, _P, _L, _I, _I, _P, _P])
 _ffn_def = _sig("kl_expert_ffn_kb_deferred", [_P, _L, _L, _I, _I, _I, _P, _P, _P, _P, _L, _I, _P, _L, _P])
 _ffn_def_splits = _sig("kl_expert_ffn_deferred_splits", [_I, _I, _I])
+_gemm_def_splits = _sig("kl_gemm_deferred_splits", [_I, _I, _I])
+_gemm_def = _sig("kl_gemm_bf16_deferred", [_P, _L, _L, _I, _I, _P, _I, _I, _P, _L, _I, _P, _L, _P])
+_rope_def = _sig("kl_rope_kv_append_deferred", [_P, _I, _L, _P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _I, _I, _P])
 _coact = _sig("kl_coact_update", [_P, _P, _L, _I, _I, _I, _P, _P, _P])
 _pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
 _rms = _sig("kl_rmsnorm", [_P, _P, _L, _I, _F, _P, _P])
@@ -262,6 +265,26 @@ def expert_ffn_deferred(xp, row_offset, m, w13, w2, y_part, h_scratch, splits, s
     ws = workspace(max(wsb, 1024), xp.device)
     _chk(_ffn_def(_p(xp), xp.shape[0], row_offset, m, d, f, _p(w13), _p(w2), _p(h_scratch), _p(y_part),
                   y_part.shape[1], splits, _p(ws), max(wsb, 1024), _s(stream)), "kl_expert_ffn_kb_deferred")
+
+
+def gemm_deferred_splits(M, N, K):
+    return int(_gemm_def_splits(M, N, K))
+
+
+def gemm_deferred(a, b, c_part, splits, row_offset=0, m=None, kblocked=False, stream=None):
+    """kl_gemm_bf16_deferred: fp32 split partials into c_part [splits, rows, N]."""
+    m = a.shape[0] - row_offset if m is None else m
+    N, K = b.shape[0], a.shape[1]
+    _chk(_gemm_def(_p(a), a.shape[0], row_offset, m, K, _p(b), N, int(kblocked), _p(c_part), c_part.shape[1], splits,
+                   None, 0, _s(stream)), "kl_gemm_bf16_deferred")
+    return c_part
+
+
+def rope_kv_append_deferred(qkv_part, splits, qkv, Hq, Hkv, hd, pos, seq, theta, k_cache, v_cache, cap, sink,
+                            chunk_last_pos=-1, stream=None):
+    _chk(_rope_def(_p(qkv_part), splits, qkv_part.shape[1], _p(qkv), qkv.shape[0], Hq, Hkv, hd, _p(pos), _p(seq),
+                   theta, _p(k_cache), _p(v_cache), cap, sink, chunk_last_pos, _s(stream)),
+         "kl_rope_kv_append_deferred")
 
 
 def combine_deferred(y_part, splits, pos, weight, resid, out=None, stream=None):

@@ -517,6 +517,36 @@ def test_qkv_rope_fused_bit_identical(K, cuda, M, Hq, Hkv, d, pos0):
     assert bool((kc2 != 0).any())
 
 
+@pytest.mark.parametrize("M,Hq,Hkv,d", [(64, 32, 8, 4096), (1, 32, 8, 4096), (200, 32, 8, 4096), (64, 48, 8, 6144)])
+def test_qkv_deferred_rope_bit_identical(K, cuda, M, Hq, Hkv, d):
+    """QKV GEMM with its tile-aligned k-splits left as fp32 partials, summed by
+    the RoPE / KV-append kernel, equals the same split GEMM with the owner
+    fixup followed by kl_rope_kv_append: qkv rows and both caches."""
+    hd, cap, sink, theta = 128, 260, 4, 1e6
+    width = (Hq + 2 * Hkv) * hd
+    S = K.gemm_deferred_splits(M, width, d)
+    assert S >= 2
+    xa = to_dev(orc.normal_bf16(M * d, 91, 1.0).reshape(M, d), cuda)
+    w = to_dev(orc.normal_bf16(width * d, 92, 0.02).reshape(width, d), cuda)
+    pos = torch.tensor([300 + (i * 37) % 300 for i in range(M)], dtype=torch.int32, device=cuda)
+    seq = torch.randperm(M, device=cuda).to(torch.int32)
+    kc1 = torch.zeros(M * cap * Hkv * hd, dtype=torch.bfloat16, device=cuda)
+    vc1, kc2, vc2 = torch.zeros_like(kc1), torch.zeros_like(kc1), torch.zeros_like(kc1)
+    K.tune(K.TUNE_STREAM_EVEN_SPLIT, 2)  # (the default) the owner-fixup GEMM on the same tile-aligned splits
+    try:
+        q1 = K.gemm(xa, w)
+    finally:
+        K.tune(K.TUNE_STREAM_EVEN_SPLIT, 2)
+    K.rope_kv_append(q1, Hq, Hkv, hd, pos, seq, theta, kc1, vc1, cap, sink)
+    part = torch.empty(S, M, width, dtype=torch.float32, device=cuda)
+    K.gemm_deferred(xa, w, part, S)
+    q2 = torch.empty_like(q1)
+    K.rope_kv_append_deferred(part, S, q2, Hq, Hkv, hd, pos, seq, theta, kc2, vc2, cap, sink)
+    torch.cuda.synchronize()
+    assert torch.equal(q1, q2)
+    assert torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
+
+
 def test_qkv_rope_fused_declines_small_shapes(K, cuda):
     """Below the weight-streaming threshold the fused entry reports
     KL_EUNSUPPORTED (the engine then issues the separate calls)."""

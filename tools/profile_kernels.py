@@ -133,7 +133,7 @@ def main():
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--persist", type=int, default=1)
     ap.add_argument("--ks", type=int, default=3, help="stream GEMM k-blocks per stage (knob 1|2|3)")
-    ap.add_argument("--even", type=int, default=1, help="stream GEMM equal k-splits per tile")
+    ap.add_argument("--even", type=int, default=2, help="stream GEMM tile-aligned k-splits: 1 equal only, 2 near-equal too")
     ap.add_argument("--whole", type=int, default=70, help="whole-tile grid when tiles >= pct%% of SMs")
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
     ap.add_argument("--l2-ahead", type=int, default=-1, help="stream GEMM L2 prefetch distance (units; -1 = default)")
@@ -326,6 +326,23 @@ def main():
             K.attn_decode_split(qkv, width, pos, seqs[b], Hq, Hkv, hd, kcs[l], vcs[l], cap, 4, hd ** -0.5, ao)
             K.gemm(ao, wo[l], c=hb, residual=hb, epilogue=1)
         res["attn_op_b64_fused_rope"] = {"us": timed_graph(op_fused, per) * 1e6}
+        Sq = K.gemm_deferred_splits(bs, width, d)
+        if Sq:
+            qpart = torch.empty(Sq, bs, width, dtype=torch.float32, device=dev)
+
+            def op_defer(i):
+                # As the engine issues decode: QKV splits left as fp32 partials,
+                # summed by the RoPE / KV-append kernel.
+                l, b = (i // n) % L4, i % n
+                hb = h[b * bs:(b + 1) * bs]
+                K.rmsnorm(hb, nw, out=xa)
+                K.gemm_deferred(xa, wqkv[l], qpart, Sq)
+                K.rope_kv_append_deferred(qpart, Sq, qkv, Hq, Hkv, hd, pos, seqs[b], 1e6, kcs[l], vcs[l], cap, 4)
+                K.attn_decode_split(qkv, width, pos, seqs[b], Hq, Hkv, hd, kcs[l], vcs[l], cap, 4, hd ** -0.5, ao)
+                K.gemm(ao, wo[l], c=hb, residual=hb, epilogue=1)
+            res["attn_op_b64_deferred_qkv"] = {"us": timed_graph(op_defer, per) * 1e6, "splits": Sq}
+            res["attn_op_part_qkv_deferred"] = {"us": timed_graph(
+                lambda i: K.gemm_deferred(xa, wqkv[(i // n) % L4], qpart, Sq), per) * 1e6}
 
         def op_keep(i):
             # The layer's projection weights kept in L2 (evict-last) for all
@@ -354,7 +371,7 @@ def main():
             lambda i: K.gemm(ao, wo[(i // n) % L4], c=h[(i % n) * bs:(i % n + 1) * bs],
                              residual=h[(i % n) * bs:(i % n + 1) * bs], epilogue=1), per) * 1e6}
         K.tune(K.TUNE_STREAM_GEMM, 1)
-        K.tune(K.TUNE_STREAM_EVEN_SPLIT, 1)
+        K.tune(K.TUNE_STREAM_EVEN_SPLIT, 2)
         for nm, fn in (("rmsnorm", lambda i: K.rmsnorm(h[(i % n) * bs:(i % n + 1) * bs], nw, out=xa)),
                        ("qkv", lambda i: K.gemm(xa, wqkv[(i // n) % L4], c=qkv)),
                        ("rope", lambda i: K.rope_kv_append(qkv, Hq, Hkv, hd, pos, seqs[i % n], 1e6, kcs[(i // n) % L4],
