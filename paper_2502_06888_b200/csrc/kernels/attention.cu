@@ -82,6 +82,71 @@ __device__ __forceinline__ float sum_split_elem(const float* __restrict__ part, 
     return bf2f(f2bf(v));
 }
 
+// Four pairs per thread: float4 loads of each split's partials (the same
+// sums and roundings as the scalar form).
+__device__ __forceinline__ float4 sum_split_vec4(const float* __restrict__ part, int S, int64_t se, int64_t off) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(part + static_cast<int64_t>(S - 1) * se + off));
+    for (int sp = 0; sp < S - 1; ++sp) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(part + sp * se + off));
+        v.x = __fadd_rn(v.x, q.x);
+        v.y = __fadd_rn(v.y, q.y);
+        v.z = __fadd_rn(v.z, q.z);
+        v.w = __fadd_rn(v.w, q.w);
+    }
+    return make_float4(bf2f(f2bf(v.x)), bf2f(f2bf(v.y)), bf2f(f2bf(v.z)), bf2f(f2bf(v.w)));
+}
+
+__global__ void rope_append_deferred_vec_kernel(const float* __restrict__ part, int S, int64_t split_elems,
+                                                uint16_t* __restrict__ qkv, int64_t T, int Hq, int Hkv, int hd,
+                                                const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+                                                float theta, uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+                                                int cap, int sink, int chunk_last_pos) {
+    pdl_enter();
+    const int half = hd / 2, q4 = half / 4;
+    const int heads = Hq + Hkv;
+    const int64_t per_tok = static_cast<int64_t>(heads + Hkv) * q4;
+    const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= T * per_tok) return;
+    const int64_t t = id / per_tok;
+    const int unit = static_cast<int>(id % per_tok);
+    const int64_t width = static_cast<int64_t>(Hq + 2 * Hkv) * hd;
+    uint16_t* row = qkv + t * width;
+    const int64_t prow = t * width;
+    const int p = pos[t];
+    const bool to_cache = chunk_last_pos < 0 || p < sink || p > chunk_last_pos - (cap - sink);
+    const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot_of(p, cap, sink)) * Hkv * hd;
+    const int head = unit / q4, i0 = (unit % q4) * 4;  // head in [0, Hq + 2 Hkv)
+    const int64_t b0 = prow + static_cast<int64_t>(head) * hd;
+    const float4 a4 = sum_split_vec4(part, S, split_elems, b0 + i0);
+    const float4 b4 = sum_split_vec4(part, S, split_elems, b0 + i0 + half);
+    uint16_t ra[4], rb[4];
+    if (head < heads) {
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float sn, cs;
+            rope_cs(p, i0 + e, hd, theta, cs, sn);
+            ra[e] = f2bf(rope_lo(av[e], bv[e], cs, sn));
+            rb[e] = f2bf(rope_hi(av[e], bv[e], cs, sn));
+        }
+    } else {
+        ra[0] = f2bf(a4.x); ra[1] = f2bf(a4.y); ra[2] = f2bf(a4.z); ra[3] = f2bf(a4.w);
+        rb[0] = f2bf(b4.x); rb[1] = f2bf(b4.y); rb[2] = f2bf(b4.z); rb[3] = f2bf(b4.w);
+    }
+    const uint2 lo = make_uint2(static_cast<uint32_t>(ra[0]) | (static_cast<uint32_t>(ra[1]) << 16),
+                                static_cast<uint32_t>(ra[2]) | (static_cast<uint32_t>(ra[3]) << 16));
+    const uint2 hi = make_uint2(static_cast<uint32_t>(rb[0]) | (static_cast<uint32_t>(rb[1]) << 16),
+                                static_cast<uint32_t>(rb[2]) | (static_cast<uint32_t>(rb[3]) << 16));
+    uint16_t* base = row + static_cast<int64_t>(head) * hd;
+    *reinterpret_cast<uint2*>(base + i0) = lo;
+    *reinterpret_cast<uint2*>(base + i0 + half) = hi;
+    if (head < Hq || !to_cache) return;
+    uint16_t* dst = head < heads ? kc + cache_row + static_cast<int64_t>(head - Hq) * hd
+                                 : vc + cache_row + static_cast<int64_t>(head - heads) * hd;
+    *reinterpret_cast<uint2*>(dst + i0) = lo;
+    *reinterpret_cast<uint2*>(dst + i0 + half) = hi;
+}
+
 __global__ void rope_append_deferred_kernel(const float* __restrict__ part, int S, int64_t split_elems,
                                             uint16_t* __restrict__ qkv, int64_t T, int Hq, int Hkv, int hd,
                                             const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
@@ -1367,8 +1432,15 @@ extern "C" int kl_rope_kv_append_deferred(const float* qkv_part, int splits, int
         return KL_EINVAL;
     if (!qkv_part || !qkv || !pos || !seq || !k_cache || !v_cache) return KL_EINVAL;
     if (T == 0) return KL_OK;
-    const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
     const int64_t se = part_rows * (static_cast<int64_t>(Hq) + 2 * Hkv) * hd;
+    if (hd % 8 == 0 && (reinterpret_cast<uintptr_t>(qkv_part) & 15) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 7) == 0 &&
+        ((reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache)) & 7) == 0) {
+        const int64_t nv = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 8));
+        return launch_pdl(rope_append_deferred_vec_kernel, dim3(static_cast<unsigned>((nv + 255) / 256)), dim3(256),
+                          0, stream, qkv_part, splits, se, qkv, T, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache,
+                          cap, sink, chunk_last_pos);
+    }
+    const int64_t n = T * ((static_cast<int64_t>(Hq) + 2 * Hkv) * (hd / 2));
     return launch_pdl(rope_append_deferred_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, stream,
                       qkv_part, splits, se, qkv, T, Hq, Hkv, hd, pos, seq, rope_theta, k_cache, v_cache, cap, sink,
                       chunk_last_pos);
