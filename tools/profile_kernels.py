@@ -218,6 +218,7 @@ def main():
                 K.expert_ffn_deferred(xp, (i % E) * M % (R - M + 1), M, w[: 2 * f * d].view(2 * f, d),
                                       w[2 * f * d:].view(d, f), ypart, h, S)
             t = timed_graph(ffn_def, 16)
+            dump_trace("down_deferred")
             res["expert_ffn_deferred_graph"] = {"M": M, "splits": S, "us": t * 1e6, "GBs": byt / t / 1e9}
             del ypart
 
