@@ -76,10 +76,6 @@ int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 #define KL_TUNE_ROPE_TOKEN_BLOCKS 11 /* 1 = RoPE/KV append with a block per token and a shared cos/sin table (default), 0 = thread per element */
 #define KL_TUNE_STREAM_KBLOCKS_PER_STAGE 12 /* weight-streaming GEMM: 64-column k-blocks per pipeline stage: 3 (default) = 2 where >= 2 stages fit, 2 = 2 where >= 3 stages fit (3D TMA boxes), 1 */
 #define KL_TUNE_STREAM_EVEN_SPLIT 13 /* weight-streaming GEMM: grid of tiles x floor(SMs / tiles), each tile split into equal k-ranges (1) or, default, also near-equal ones (2: the last range takes the remainder); 0 = stream-K ranges over one CTA per SM */
-#define KL_TUNE_STREAM_L2_AHEAD 14 /* weight-streaming GEMM: weight units prefetched into L2 ahead of the smem ring (0 = off) */
-#define KL_TUNE_STREAM_OWNER_EXTRA 15 /* weight-streaming GEMM, tile-aligned splits: extra k-units of each tile's owner range */
-#define KL_TUNE_SPLIT_FINISH 20 /* tcgen05 GEMM split-K: 1 = each tile finished by its last-arriving CTA, 0 (default) = separate reduce kernel */
-#define KL_TUNE_STREAM_BULK_PUBLISH 17 /* weight-streaming GEMM: split contributors with an idle ring publish partials via smem + one bulk copy (1) or direct stores (0) */
 #define KL_TUNE_STREAM_FUSED_FIXUP 16 /* weight-streaming GEMM: 1 (default) = owners add split partials during the epilogue pass (dedicated staging region), 0 = TMEM fixup first */
 #define KL_TUNE_DECODE_STAGES 21 /* tensor-core decode attention: ring stages (0 = default 3) */
 #define KL_TUNE_ATTN_KV_EVICT_FIRST 19 /* tensor-core decode attention: 1 (default) = K/V loads with an L2 evict-first policy, 0 = no hint */

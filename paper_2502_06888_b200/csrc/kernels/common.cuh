@@ -106,14 +106,6 @@ __device__ __forceinline__ void tma_load_3d_k(void* dst, const CUtensorMap* map,
             : "memory");
 }
 
-// L2 prefetch of one 3D box (no shared-memory destination, no barrier).
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int row, int kchunk) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(0), "r"(row), "r"(kchunk)
-                 : "memory");
-}
-
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

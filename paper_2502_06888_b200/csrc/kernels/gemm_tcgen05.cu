@@ -52,108 +52,11 @@ struct Cfg {
 
 // PAIRED: the B tile is two BN/2-row halves [W1 rows | W3 rows] of the same
 // output columns (SwiGLU gate/up), read at row offsets n and b_half_rows + n.
-// Tile arrival counter of a split-K launch: word = (epoch << 8) | arrivals,
-// a stale epoch counting as zero, so the workspace needs no clearing. True
-// for the n-th (last) arrival of this launch.
-__device__ __forceinline__ bool arrive_last(uint32_t* ctr, uint32_t epoch, uint32_t n) {
-    const uint32_t tag = (epoch & 0xFFFFFFu) << 8;
-    uint32_t cur = *reinterpret_cast<volatile uint32_t*>(ctr);
-    while (true) {
-        const uint32_t cnt = (cur & 0xFFFFFF00u) == tag ? (cur & 0xFFu) : 0u;
-        const uint32_t prev = atomicCAS(ctr, cur, tag | (cnt + 1));
-        if (prev == cur) return cnt + 1 == n;
-        cur = prev;
-    }
-}
-
-// Sum one (m_tile, n_tile) tile's split partials in split order and apply
-// the final epilogue (store / +residual / SwiGLU of the paired tile) with
-// 128 threads, coalesced float4 reads along each row.
-__device__ __forceinline__ void split_finish(const float* __restrict__ ws, int splits, int M, int ws_ld, int m_tile,
-                                             int n_tile, int bn, int fin, uint16_t* __restrict__ c, int ldc,
-                                             const uint16_t* __restrict__ r, int tid) {
-    // kU quads per thread per round, every split of them loaded before any
-    // add (up to kU * 16 float4 loads in flight: the finish is L2-latency
-    // bound, not bandwidth bound).
-    constexpr int kU = 4, kMaxSplits = 16;
-    const int rows = min(BM, M - m_tile * BM);
-    const int64_t split_stride = static_cast<int64_t>(M) * ws_ld;
-    const bool swiglu = fin == kSwiGLU;
-    const int half = bn / 2;
-    const int out_cols = swiglu ? half : bn;
-    const int quads = out_cols / 4;
-    const int total = rows * quads;
-    for (int base = tid; base < total; base += 128 * kU) {
-        float4 g[kU], u[kU];
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-            g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            u[k] = g[k];
-        }
-        for (int sp0 = 0; sp0 < splits; sp0 += kMaxSplits / kU) {
-            float4 tg[kMaxSplits / kU][kU], tu[kMaxSplits / kU][kU];
-#pragma unroll
-            for (int q = 0; q < kMaxSplits / kU; ++q)
-#pragma unroll
-                for (int k = 0; k < kU; ++k) {
-                    const int idx = base + k * 128, sp = sp0 + q;
-                    if (idx >= total || sp >= splits) continue;
-                    const int m = m_tile * BM + idx / quads, w = (idx % quads) * 4;
-                    const float* p = ws + sp * split_stride + static_cast<int64_t>(m) * ws_ld +
-                                     static_cast<int64_t>(n_tile) * bn + w;
-                    tg[q][k] = *reinterpret_cast<const float4*>(p);
-                    if (swiglu) tu[q][k] = *reinterpret_cast<const float4*>(p + half);
-                }
-#pragma unroll
-            for (int q = 0; q < kMaxSplits / kU; ++q)
-#pragma unroll
-                for (int k = 0; k < kU; ++k) {
-                    const int sp = sp0 + q;
-                    if (base + k * 128 >= total || sp >= splits) continue;
-                    // Split order, the first split as the initial value (as splitk_reduce_kernel).
-                    if (sp == 0) {
-                        g[k] = tg[q][k];
-                        if (swiglu) u[k] = tu[q][k];
-                    } else {
-                        g[k].x += tg[q][k].x; g[k].y += tg[q][k].y; g[k].z += tg[q][k].z; g[k].w += tg[q][k].w;
-                        if (swiglu) {
-                            u[k].x += tu[q][k].x; u[k].y += tu[q][k].y; u[k].z += tu[q][k].z; u[k].w += tu[q][k].w;
-                        }
-                    }
-                }
-        }
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-            const int idx = base + k * 128;
-            if (idx >= total) continue;
-            const int m = m_tile * BM + idx / quads, w = (idx % quads) * 4;
-            float out[4];
-            if (swiglu) {
-                const float gv[4] = {g[k].x, g[k].y, g[k].z, g[k].w}, uv[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) out[i] = gv[i] / (1.0f + expf(-gv[i])) * uv[i];
-            } else {
-                out[0] = g[k].x; out[1] = g[k].y; out[2] = g[k].z; out[3] = g[k].w;
-                if (fin == kResidual) {
-                    const uint2 rv = *reinterpret_cast<const uint2*>(r + static_cast<int64_t>(m) * ldc + n_tile * bn + w);
-                    out[0] += bf2f(static_cast<uint16_t>(rv.x & 0xffffu));
-                    out[1] += bf2f(static_cast<uint16_t>(rv.x >> 16));
-                    out[2] += bf2f(static_cast<uint16_t>(rv.y & 0xffffu));
-                    out[3] += bf2f(static_cast<uint16_t>(rv.y >> 16));
-                }
-            }
-            *reinterpret_cast<uint2*>(c + static_cast<int64_t>(m) * ldc + static_cast<int64_t>(n_tile) * out_cols + w) =
-                make_uint2(pack2(out[0], out[1]), pack2(out[2], out[3]));
-        }
-    }
-}
-
 template <int BN, int EPI, bool PAIRED, int STAGES>
 __global__ void __launch_bounds__(kThreads, (Cfg<BN, STAGES>::kMinBlocks))
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   int a_row0, int M, int kb_per_split, int b_half_rows, uint16_t* __restrict__ c, int ldc,
-                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld, int b_hint, int fin,
-                  uint32_t* __restrict__ counters, uint32_t epoch) {
+                  const uint16_t* __restrict__ r, float* __restrict__ ws, int ws_ld, int b_hint) {
     pdl_enter();
     using C = Cfg<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -265,22 +168,6 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
                     float4* dst = reinterpret_cast<float4*>(out + col);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                }
-            }
-            if (fin >= 0) {
-                // Split-K finished by the last CTA of the tile to arrive (no
-                // reduce launch): partials summed in split order, exactly as
-                // splitk_reduce_kernel, then the final epilogue `fin`.
-                __threadfence();
-                named_bar_sync(1, 128);
-                volatile uint32_t* last = tmem_slot + 1;
-                if (warp == 2 && lane == 0)
-                    *last = arrive_last(counters + m_tile * gridDim.x + n_tile, epoch, gridDim.z) ? 1u : 0u;
-                named_bar_sync(1, 128);
-                if (*last) {
-                    __threadfence();
-                    split_finish(ws, static_cast<int>(gridDim.z), M, ws_ld, m_tile, n_tile, BN, fin, c, ldc, r,
-                                 threadIdx.x - 64);
                 }
             }
         } else if constexpr (EPI == kSwiGLU) {
@@ -606,10 +493,7 @@ struct StreamArgs {
     int pdl;    // launched with programmatic stream serialization
     int ks;     // k-blocks per stage: 2 = one 3D TMA box covers two 64-column k-blocks (larger copies)
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
-    int l2_ahead;  // weight units prefetched into L2 ahead of the smem ring (0 = off)
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
-    int owner_extra;  // tile-aligned splits: extra units of the owner's (last) range
-    int bulk_publish; // contributors whose ring is idle publish their partial with one bulk copy
     // Deferred split reduction (kStore, NMMA 1, tile-aligned splits): every CTA
     // writes its fp32 accumulator to defer[split][row][feature] (row pitch
     // defer_ld) and the consumer sums the splits; no flags, no fixup.
@@ -648,23 +532,14 @@ __device__ __forceinline__ int range_begin(int c, int units, int G) {
     return static_cast<int>(static_cast<int64_t>(c) * units / G);
 }
 // First unit of CTA c. With tile-aligned splits (p.split = S > 0, G = tiles
-// x S) the owner's range (the tile's last) is p.owner_extra units longer
-// than the S - 1 equal contributor ranges, so contributors publish their
-// partials while the owner is still streaming and the owner's fixup does
-// not wait on them.
+// x S) each tile's k-blocks are cut into S ranges, the last (the owner's)
+// taking the remainder when S does not divide KB.
 __device__ __forceinline__ int unit_begin(const StreamArgs& p, int c, int G) {
     if (p.split <= 0) return range_begin(c, p.units, G);
     const int t = c / p.split, j = c % p.split;
-    return t * p.KB + j * ((p.KB - p.owner_extra) / p.split);
+    return t * p.KB + j * (p.KB / p.split);
 }
 
-
-// 1D bulk copy shared -> global (async proxy, bulk group of the issuing thread).
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(dst)),
-                 "r"(smem_u32(src)), "r"(bytes)
-                 : "memory");
-}
 
 // 1D bulk copy global -> shared (async proxy), completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -805,36 +680,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                     tma_load_2d(sx, &tmap_x, &full[s_], kb_ * BK, a_row0);
             };
             int xkb[16];  // k-block of each stage issued before the wait
-            // L2 prefetch cursor, l2_ahead units past the ring: walks the same
-            // (tile, k-block) order as the loads, so the smem loads of those
-            // units later hit L2 (more weight bytes in flight than the ring holds).
-            int pf_t = t_hi, pf_kb = max(u0, t_hi * KB) - t_hi * KB, pf_n = 0;
-            auto prefetch_next = [&]() {
-                if (pf_t < t_lo) return;
-#pragma unroll
-                for (int j = 0; j < NMMA; ++j) {
-                    const int row = EPI == kSwiGLU ? (j == 0 ? pf_t * kWRows : p.half_rows + pf_t * kWRows)
-                                                   : (pf_t * NMMA + j) * kWRows;
-                    tma_prefetch_3d(&tmap_w, row, pf_kb * p.ks);
-                }
-                ++pf_n;
-                if (++pf_kb >= min(u1, (pf_t + 1) * KB) - pf_t * KB) {
-                    --pf_t;
-                    if (pf_t >= t_lo) pf_kb = max(u0, pf_t * KB) - pf_t * KB;
-                }
-            };
-            auto skip_next = [&]() {  // advance the cursor over a unit the ring loads itself
-                if (pf_t < t_lo) return;
-                ++pf_n;
-                if (++pf_kb >= min(u1, (pf_t + 1) * KB) - pf_t * KB) {
-                    --pf_t;
-                    if (pf_t >= t_lo) pf_kb = max(u0, pf_t * KB) - pf_t * KB;
-                }
-            };
-            if (!Q4 && p.l2_ahead > 0) {
-                for (int i = 0; i < p.stages; ++i) skip_next();
-                for (int i = 0; i < p.l2_ahead; ++i) prefetch_next();
-            }
             for (int t = t_hi; t >= t_lo; --t) {
                 const int kb0 = max(u0, t * KB) - t * KB, kb1 = min(u1, (t + 1) * KB) - t * KB;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -844,7 +689,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                         waited = true;
                         for (int i = 0; i < pending_x; ++i) load_x(i, xkb[i]);
                     }
-                    if (!Q4 && p.l2_ahead > 0 && it >= p.stages) prefetch_next();
                     mbar_wait(&empty[s], ((it / p.stages) & 1) ^ 1);
                     uint8_t* sw = smem + s * stage_bytes;
                     mbar_arrive_expect_tx(&full[s], Q4 ? p.NP * BK * 2 : stage_bytes);
@@ -976,45 +820,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                 // layout [j][16-column chunk][float4 i][feature row] so each
                 // warp store / load is 512 contiguous bytes.
                 if (etid == 0) STREAM_TRACE(8);
-                if (p.bulk_publish && t == t_lo && slot_f4 * 16 <= ring_bytes) {
-                    // Ring idle (last segment walked): stage the partial in
-                    // smem in the slot's layout, then one bulk copy to global.
-                    float4* sslot = reinterpret_cast<float4*>(smem);
-                    for (int j = 0; j < NMMA; ++j)
-                        for (int col = 0; col < cols; col += 32) {
-                            float v[32];
-                            tmem_ld32(acc0 + j * p.acc_stride + col, v);
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                if (col + 16 * h >= cols) break;
-                                float4* dst = sslot + (static_cast<int64_t>(j * nch + (col >> 4) + h) * 4) * kWRows + frow;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i)
-                                    dst[i * kWRows] = make_float4(v[16 * h + 4 * i], v[16 * h + 4 * i + 1],
-                                                                  v[16 * h + 4 * i + 2], v[16 * h + 4 * i + 3]);
-                            }
-                        }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[b]);
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    named_bar_sync(1, 128);
-                    if (etid == 0) {
-                        // Only the column chunks the epilogue reads: [j][chunk < nch_live][4][128].
-                        const int nch_live = cols / 16;
-                        for (int j = 0; j < NMMA; ++j) {
-                            const uint32_t bytes = static_cast<uint32_t>(nch_live * 4 * kWRows * 16);
-                            const int64_t off = static_cast<int64_t>(j * nch) * 4 * kWRows;
-                            bulk_s2g(slot4(cta) + off, sslot + off, bytes);
-                        }
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-                        asm volatile("fence.proxy.async.global;" ::: "memory");
-                        st_release_gpu(p.flags + cta, p.epoch);
-                        STREAM_TRACE(9);
-                    }
-                    continue;
-                }
                 float4* slot = slot4(cta);
                 for (int j = 0; j < NMMA; ++j) {
                     for (int col = 0; col < cols; col += 32) {
@@ -1302,9 +1107,6 @@ struct Launch {
     float* ws;
     int ws_ld;
     bool b_kblocked = false;  // weights in the K-blocked layout (make_map_kblocked)
-    int fin = -1;                  // split-K: final epilogue run by each tile's last CTA (-1: reduce kernel)
-    uint32_t* counters = nullptr;  // split-K tile arrival counters (fin >= 0)
-    uint32_t epoch = 0;
 };
 
 // Weight (B operand) map: a 3D (64, rows, k-blocks) view, one k-block per box.
@@ -1329,7 +1131,7 @@ int launch(const Launch& L, cudaStream_t stream) {
     }
     const dim3 grid(L.n_tiles, (L.M + BM - 1) / BM, L.splits);
     if (int rc_ = launch_pdl(gemm_bf16_tcgen05<BN, EPI, PAIRED, STAGES>, dim3(grid), dim3(kThreads), C::kSmemBytes, stream, ma, mb, static_cast<int>(L.row_offset), L.M, L.K / BK / L.splits, L.b_half_rows, L.c, L.ldc, L.r, L.ws,
-        L.ws_ld, g_stream_hint, L.fin, L.counters, L.epoch)) return rc_;
+        L.ws_ld, g_stream_hint)) return rc_;
     return check_launch();
 }
 
@@ -1390,11 +1192,7 @@ int g_stream_ctas = 1;     // kl_tune(KL_TUNE_STREAM_CTAS_PER_SM, ...)
 int g_stream_debug = 0;
 int g_stream_whole_tiles = 70;  // kl_tune(KL_TUNE_STREAM_WHOLE_TILES, pct): whole tiles when n_tiles >= pct% of SMs
 int g_stream_even_split = 2;  // kl_tune(KL_TUNE_STREAM_EVEN_SPLIT, ...): 1 = equal splits only, 2 (default) = also near-equal
-int g_stream_l2_ahead = 0;  // kl_tune(KL_TUNE_STREAM_L2_AHEAD, units)
-int g_stream_owner_extra = 0;  // kl_tune(KL_TUNE_STREAM_OWNER_EXTRA, units)
 int g_stream_fused_fixup = 1;  // kl_tune(KL_TUNE_STREAM_FUSED_FIXUP, 0|1)
-int g_stream_bulk_publish = 0;  // kl_tune(KL_TUNE_STREAM_BULK_PUBLISH, 0|1)
-int g_split_finish = 0;  // kl_tune(KL_TUNE_SPLIT_FINISH, 0|1): split-K tiles finished by their last CTA (measured slower: off)
 int g_stream_ks = 3;  // kl_tune(KL_TUNE_STREAM_KBLOCKS_PER_STAGE, 1|2|3): 2 k-blocks per stage where >= 3 (2) or >= 2 (3) stages fit
 
 int sm_count() {
@@ -1504,8 +1302,6 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     // units) and as the bf16 output staging tile of the last segment.
     if (p.stages * stage_bytes < p.NP * kWRows * (EPI == kResidual ? 4 : 2)) return KL_EUNSUPPORTED;
     p.hint = g_stream_hint;
-    p.l2_ahead = g_stream_l2_ahead;
-    p.bulk_publish = g_stream_bulk_publish;
     p.debug = g_stream_debug;
     p.pdl = g_pdl;
     if (p.stages > 16) p.stages = 16;
@@ -1519,13 +1315,11 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
         // range takes the remainder), the owner's optionally longer.
         G = n_tiles * (G / n_tiles);
         p.split = G / n_tiles;
-        // Owner bonus, capped so every contributor keeps at least one unit.
-        p.owner_extra = std::max(0, std::min(g_stream_owner_extra, p.KB - 2 * p.split));
     }
     if (defer != nullptr) {
         // Deferred splits need exactly the tile-aligned split count the
         // caller sized its partial buffer for; no workspace slots are used.
-        if (EPI != kStore || NMMA != 1 || Q4 || p.split != defer_splits || p.owner_extra != 0) return KL_EUNSUPPORTED;
+        if (EPI != kStore || NMMA != 1 || Q4 || p.split != defer_splits) return KL_EUNSUPPORTED;
     }
     const int G_ws = defer != nullptr ? G
                                       : static_cast<int>(std::min<int64_t>(
@@ -1533,7 +1327,6 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     if (G > G_ws) {  // workspace-limited: plain stream-K ranges over fewer CTAs
         G = G_ws;
         p.split = 0;
-        p.owner_extra = 0;
     }
     if (G < 1) return KL_EUNSUPPORTED;
     // The fused RoPE epilogue runs only on owners' staged path: no CTA range
@@ -1646,11 +1439,7 @@ extern "C" int kl_tune(int knob, int value) {
         case KL_TUNE_STREAM_WHOLE_TILES: g_stream_whole_tiles = value; return KL_OK;
         case KL_TUNE_GEMM_PERSISTENT: g_persistent = value != 0; return KL_OK;
         case KL_TUNE_STREAM_EVEN_SPLIT: g_stream_even_split = value; return KL_OK;
-        case KL_TUNE_STREAM_L2_AHEAD: g_stream_l2_ahead = value < 0 ? 0 : value; return KL_OK;
-        case KL_TUNE_STREAM_OWNER_EXTRA: g_stream_owner_extra = value < 0 ? 0 : value; return KL_OK;
         case KL_TUNE_STREAM_FUSED_FIXUP: g_stream_fused_fixup = value != 0; return KL_OK;
-        case KL_TUNE_STREAM_BULK_PUBLISH: g_stream_bulk_publish = value != 0; return KL_OK;
-        case KL_TUNE_SPLIT_FINISH: g_split_finish = value != 0; return KL_OK;
         case KL_TUNE_STREAM_KBLOCKS_PER_STAGE:
             if (value < 1 || value > 3) return KL_EINVAL;
             g_stream_ks = value;
@@ -1672,8 +1461,7 @@ extern "C" int64_t kl_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
     const int tiles = (N / 128) * m_tiles;
     const int s = choose_splits(tiles, K / BK, M, N, INT64_MAX);
     (void)epilogue;
-    // Partials, then one arrival counter per tile (last-arriver finish).
-    return s > 1 ? ((static_cast<int64_t>(s) * M * N * 4 + 15) & ~int64_t(15)) + static_cast<int64_t>(tiles) * 4 : 0;
+    return s > 1 ? static_cast<int64_t>(s) * M * N * 4 : 0;
 }
 
 namespace kl {
@@ -1709,15 +1497,6 @@ int gemm_bf16_impl(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M,
         const bool paired = epilogue == kSwiGLU;
         L.b_half_rows = paired ? N / 2 : 0;
         if (L.splits > 1) {
-            // Tile arrival counters after the partials: the last CTA of each
-            // tile finishes it (no reduce launch) when the workspace has room.
-            const int64_t part_bytes = (static_cast<int64_t>(L.splits) * M * N * 4 + 15) & ~int64_t(15);
-            if (g_split_finish && workspace_bytes >= part_bytes + static_cast<int64_t>(L.n_tiles) * m_tiles * 4) {
-                L.fin = epilogue;
-                L.counters = reinterpret_cast<uint32_t*>(static_cast<char*>(workspace) + part_bytes);
-                L.epoch = next_epoch();
-                return paired ? launch<128, kPartial, true, 3>(L, stream) : launch<128, kPartial, false, 3>(L, stream);
-            }
             int rc = paired ? launch<128, kPartial, true, 3>(L, stream) : launch<128, kPartial, false, 3>(L, stream);
             if (rc) return rc;
             if (epilogue == kSwiGLU) return reduce<kSwiGLU>(L, N / 2, 128, stream);
@@ -1877,7 +1656,6 @@ extern "C" int kl_gemm_deferred_splits(int M, int N, int K) {
     if (g_stream_whole_tiles > 0 && n_tiles <= sm_count() && n_tiles * 100 >= g_stream_whole_tiles * sm_count())
         return 0;
     if (!(g_stream_even_split && n_tiles < G && G / n_tiles >= 2)) return 0;
-    if (g_stream_owner_extra != 0) return 0;
     const int S = G / n_tiles;
     return S <= 4 ? S : 0;
 }

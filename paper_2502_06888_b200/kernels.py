@@ -79,11 +79,7 @@ TUNE_GEMM_PERSISTENT = 8
 TUNE_ROPE_TOKEN_BLOCKS = 11  # RoPE/KV append: block per token (1) or thread per element (0)
 TUNE_STREAM_KBLOCKS_PER_STAGE = 12  # weight-streaming GEMM k-blocks per stage: 1, 2 (if >= 3 stages), 3 (default: 2 if >= 2 stages)
 TUNE_STREAM_EVEN_SPLIT = 13  # weight-streaming GEMM: equal (1) or near-equal (2) k-splits per tile
-TUNE_STREAM_L2_AHEAD = 14  # weight-streaming GEMM: units prefetched into L2 ahead of the smem ring
-TUNE_SPLIT_FINISH = 20  # tcgen05 GEMM split-K: tiles finished by their last CTA (1) or a reduce kernel (0)
-TUNE_STREAM_BULK_PUBLISH = 17  # weight-streaming GEMM: contributors publish partials via smem + bulk copy
 TUNE_STREAM_FUSED_FIXUP = 16  # weight-streaming GEMM: owners add split partials in the epilogue pass
-TUNE_STREAM_OWNER_EXTRA = 15  # weight-streaming GEMM, tile-aligned splits: extra units of each tile's owner range
 TUNE_DECODE_STAGES = 21  # tensor-core decode attention: ring stages (0 = default)
 TUNE_ATTN_KV_EVICT_FIRST = 19  # decode attention: K/V loads L2 evict-first
 TUNE_DECODE_HG = 18  # tensor-core decode attention: KV heads per work item (0 = auto)

@@ -136,14 +136,11 @@ def main():
     ap.add_argument("--even", type=int, default=2, help="stream GEMM tile-aligned k-splits: 1 equal only, 2 near-equal too")
     ap.add_argument("--whole", type=int, default=70, help="whole-tile grid when tiles >= pct%% of SMs")
     ap.add_argument("--gap-ms", type=float, default=0.0, help="host sleep between timed launches")
-    ap.add_argument("--l2-ahead", type=int, default=-1, help="stream GEMM L2 prefetch distance (units; -1 = default)")
     ap.add_argument("--split", type=int, default=-1, help="stream GEMM even-split mode (-1 = default)")
-    ap.add_argument("--bulk-publish", type=int, default=-1, help="stream GEMM contributors publish via smem + bulk copy")
     ap.add_argument("--fused-fixup", type=int, default=-1, help="stream GEMM owners add partials in the epilogue pass")
     ap.add_argument("--kv-evict-first", type=int, default=-1, help="decode attention K/V loads evict-first")
     ap.add_argument("--decode-stages", type=int, default=-1, help="decode attention ring stages (0 = default)")
     ap.add_argument("--decode-hg", type=int, default=-1, help="decode attention KV heads per work item (0 = auto)")
-    ap.add_argument("--owner-extra", type=int, default=-1, help="stream GEMM owner-range bonus (units; -1 = default)")
     ap.add_argument("--kb", type=int, default=1, help="expert weights in the K-blocked layout (the engine's)")
     ap.add_argument("--h2d", action="store_true", help="keep a pinned-host -> HBM copy running on a side stream")
     args = ap.parse_args()
@@ -153,8 +150,6 @@ def main():
     K.tune(K.TUNE_GEMM_PERSISTENT, args.persist)
     K.tune(K.TUNE_STREAM_KBLOCKS_PER_STAGE, args.ks)
     K.tune(K.TUNE_STREAM_EVEN_SPLIT, args.even if args.split < 0 else args.split)
-    if args.bulk_publish >= 0:
-        K.tune(K.TUNE_STREAM_BULK_PUBLISH, args.bulk_publish)
     if args.fused_fixup >= 0:
         K.tune(K.TUNE_STREAM_FUSED_FIXUP, args.fused_fixup)
     if args.kv_evict_first >= 0:
@@ -163,10 +158,6 @@ def main():
         K.tune(K.TUNE_DECODE_STAGES, args.decode_stages)
     if args.decode_hg >= 0:
         K.tune(K.TUNE_DECODE_HG, args.decode_hg)
-    if args.owner_extra >= 0:
-        K.tune(K.TUNE_STREAM_OWNER_EXTRA, args.owner_extra)
-    if args.l2_ahead >= 0:
-        K.tune(K.TUNE_STREAM_L2_AHEAD, args.l2_ahead)
     global TRACE, GAP_MS
     GAP_MS = args.gap_ms
     TRACE = bool(args.debug & 128)

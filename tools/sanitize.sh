@@ -5,8 +5,8 @@
 # gpurun_out/sanitize_*.log. Usage (on the GPU box): bash tools/sanitize.sh
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
-SEL_ALL="test_gemm_split_finish or test_gemm_weight_streaming or test_expert_ffn or test_permute or test_combine or test_decode_attention_split_kv or test_gemm_split_k or test_gemm_residual or test_gate_topk or test_coact or test_prefill_attention_window or test_rope or test_q4 or test_gemm_store or test_gemm_persistent"
-SEL_SMALL="test_gemm_split_finish or test_gemm_weight_streaming or test_expert_ffn or test_permute or test_combine or test_decode_attention_split_kv or test_gemm_split_k or test_prefill_attention_window"
+SEL_ALL="test_gemm_weight_streaming or test_expert_ffn or test_permute or test_combine or test_decode_attention_split_kv or test_gemm_split_k or test_gemm_residual or test_gate_topk or test_coact or test_prefill_attention_window or test_rope or test_q4 or test_gemm_store or test_gemm_persistent"
+SEL_SMALL="test_gemm_weight_streaming or test_expert_ffn or test_permute or test_combine or test_decode_attention_split_kv or test_gemm_split_k or test_prefill_attention_window"
 run() {  # tool, selection, timeout
     timeout "$3" $CS --tool "$1" --target-processes all --print-limit 20 \
         python -m pytest tests/test_kernels_gpu.py -m gpu -q -p no:cacheprovider -k "$2" \
