@@ -260,6 +260,15 @@ int kl_gemm_deferred_splits(int M, int N, int K);
 int kl_gemm_bf16_deferred(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                           const uint16_t* b, int N, int b_kblocked, float* c_part, int64_t part_rows,
                           int splits, void* workspace, int64_t workspace_bytes, cudaStream_t stream);
+/* kl_gate_topk (decode-sized T <= 592, block-per-token path) whose input row
+ * is first completed from a deferred o-projection: h = bf16(Σ splits in the
+ * owner's order + h), written back to h, then RMSNorm / router / top-k as
+ * kl_gate_topk. Equal bit for bit to the streaming GEMM's residual epilogue
+ * on the same splits followed by kl_gate_topk. KL_EUNSUPPORTED off that path. */
+int kl_gate_topk_deferred(uint16_t* h, const float* h_part, int splits, int64_t part_rows,
+                          const uint16_t* norm_w, const uint16_t* wg, int T, int d, int E, int k, float eps,
+                          int score_mode, uint16_t* x2, float* logits, int32_t* idx, float* weight,
+                          int32_t* hist, int32_t* first_pos, cudaStream_t stream);
 /* kl_rope_kv_append over the fp32 split partials of a deferred QKV GEMM:
  * each element summed in the owner's order and rounded to bf16 (what the
  * GEMM would have stored), then RoPE / KV append as kl_rope_kv_append; the

@@ -419,7 +419,8 @@ bool Engine::plan_at(int n, bool rethrow) {
         add((2 * ops_per_step_bound(D_.L, n, El_) + 8) * 8);                     // op timestamps
         add(tb_max_ * D_.hd * 4);                                                // RoPE table
         if (defer_possible())                                                    // deferred split partials
-            add(4LL * n * w.batch_size * D_.k * D_.d * 4 + 4LL * w.batch_size * D_.qkv_width() * 4);
+            add(4LL * n * w.batch_size * D_.k * D_.d * 4 + 4LL * w.batch_size * D_.qkv_width() * 4 +
+                4LL * n * w.batch_size * D_.d * 4);
         if (kv_off)
             add(static_cast<byte_count>(kKvSlots) * w.batch_size *
                 cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
@@ -500,6 +501,8 @@ void Engine::allocate_device() {
         ypart_rows_ = static_cast<int64_t>(plan_.n_batches) * cfg_.workload.batch_size * D_.k;  // a decode step's rows
         ypart_ = static_cast<float*>(take(4 * ypart_rows_ * D_.d * 4));
         qkvpart_ = static_cast<float*>(take(4LL * cfg_.workload.batch_size * D_.qkv_width() * 4));
+        opart_ = static_cast<float*>(take(4LL * plan_.n_batches * cfg_.workload.batch_size * D_.d * 4));
+        o_deferred_.assign(static_cast<size_t>(plan_.n_batches), 0);
         defer_ok_ = std::getenv("KL_NO_DEFER") == nullptr;
     }
     // Opt-in (KL_QKV_ROPE=1): bit-identical to the separate calls but no

@@ -279,6 +279,9 @@ class Engine {
     // summed by kl_combine_deferred. block_defer_ = their split count for the
     // block being executed (0 = plain kl_expert_ffn_kb + kl_combine).
     float* qkvpart_ = nullptr;    // deferred QKV split partials of one decode batch [4][bs][qkv_width]
+    float* opart_ = nullptr;      // deferred o-proj split partials per batch [n][4][bs][d], summed by the gate
+    int o_defer_ = -1;            // split count of the decode o-proj (-1: not yet queried, 0: off)
+    std::vector<int> o_deferred_; // per batch: its o-proj partials await the gate (split count, 0 = none)
     int qkv_defer_ = -1;          // split count of the decode QKV GEMM (-1: not yet queried, 0: off)
     float* ypart_ = nullptr;
     int64_t ypart_rows_ = 0;

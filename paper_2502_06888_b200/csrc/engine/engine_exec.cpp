@@ -677,12 +677,24 @@ void Engine::exec_attention(const StreamOp& op) {
                                     static_cast<int64_t>(cfg_.workload.batch_size) * (kv_offload_ ? 1 : plan_.n_batches),
                                     kv_cap_, kv_sink_, scale, ao_, gemm_ws_, gemm_ws_bytes_, cs),
                  "decode attention");
-    if (fused)
+    const int64_t wo_k2 = static_cast<int64_t>(D_.Hq) * D_.hd;
+    if (fused) {
         kl_check(kl_gemm_q4(ao_, tpb, 0, tpb, D_.Hq * D_.hd, q4o, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),
                  "o proj q4");
-    else
+    } else if (step != 0 && defer_ok_ && opart_ != nullptr && tpb <= 4 * 148 && D_.d % 256 == 0 &&
+               (D_.d / 256 == 2 || D_.d / 256 == 4 || D_.d / 256 == 8 || D_.d / 256 == 16 || D_.d / 256 == 24) &&
+               (o_defer_ < 0 ? (o_defer_ = kl_gemm_deferred_splits(tpb, D_.d, static_cast<int>(wo_k2))) : o_defer_) > 0) {
+        // Decode: the o-proj leaves its tile-aligned k-splits as fp32 partials;
+        // this batch's gate op completes h (+ residual) before its router.
+        kl_check(kl_gemm_bf16_deferred(ao_, tpb, 0, tpb, static_cast<int>(wo_k2), wo, D_.d, 0,
+                                       opart_ + static_cast<int64_t>(b) * 4 * cfg_.workload.batch_size * D_.d,
+                                       cfg_.workload.batch_size, o_defer_, gemm_ws_, gemm_ws_bytes_, cs),
+                 "o proj (deferred splits)");
+        o_deferred_[static_cast<size_t>(b)] = o_defer_;
+    } else {
         kl_check(kl_gemm_bf16(ao_, tpb, 0, tpb, D_.Hq * D_.hd, wo, D_.d, hb, D_.d, hb, 1, gemm_ws_, gemm_ws_bytes_, cs),
                  "o proj");
+    }
 }
 
 void Engine::exec_gate(const StreamOp& op) {
@@ -713,7 +725,20 @@ void Engine::exec_gate(const StreamOp& op) {
     const uint16_t* wg = gate_slot_[gate_slot_of_.at(l)];
     int32_t* idx = idx_[idx_cur_] + row0 * D_.k;
     float* wt = weight_ + row0 * D_.k;
-    if (cfg_.replay) {
+    const int odef = o_deferred_.empty() || simple ? 0 : o_deferred_[static_cast<size_t>(b)];
+    if (odef > 0) {
+        // This batch's o-proj left split partials: the router kernel completes h first.
+        o_deferred_[static_cast<size_t>(b)] = 0;
+        const float* part = opart_ + static_cast<int64_t>(b) * 4 * cfg_.workload.batch_size * D_.d;
+        kl_check(kl_gate_topk_deferred(h_ + row0 * D_.d, part, odef, cfg_.workload.batch_size, norm_ffn_[l], wg, tpb,
+                                       D_.d, D_.E, D_.k, D_.eps, D_.score_mode, x2_ + row0 * D_.d,
+                                       cfg_.replay ? router_logits_ + row0 * D_.E : nullptr, idx, wt,
+                                       cfg_.replay ? nullptr : hist, cfg_.replay ? nullptr : first, cs),
+                 "gate (deferred o-proj)");
+        if (cfg_.replay)
+            kl_check(kl_route_override(forced_ + row0 * D_.k, router_logits_ + row0 * D_.E, tpb, D_.E, D_.k, idx, wt,
+                                       hist, first, cs), "route override");
+    } else if (cfg_.replay) {
         kl_check(kl_gate_topk(h_ + row0 * D_.d, norm_ffn_[l], wg, tpb, D_.d, D_.E, D_.k, D_.eps, D_.score_mode,
                               x2_ + row0 * D_.d, router_logits_ + row0 * D_.E, idx, wt, nullptr, nullptr, cs), "gate");
         kl_check(kl_route_override(forced_ + row0 * D_.k, router_logits_ + row0 * D_.E, tpb, D_.E, D_.k, idx, wt, hist,

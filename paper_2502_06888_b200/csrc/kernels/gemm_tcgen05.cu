@@ -1642,7 +1642,9 @@ extern "C" int kl_expert_ffn_kb(const uint16_t* xp, int64_t rows_total, int64_t 
 // GEMM would not run as tile-aligned splits (or S > 4).
 extern "C" int kl_gemm_deferred_splits(int M, int N, int K) {
     using namespace kl;
-    if (M < 1 || M > 256 || N % kWRows != 0 || K % BK != 0 || !stream_eligible(M, N, K, kStore)) return 0;
+    // No size threshold here: the small-GEMM reason to avoid the streaming
+    // kernel (its split fixup tail) does not exist when splits are deferred.
+    if (M < 1 || M > 256 || N % kWRows != 0 || K % BK != 0 || !g_stream_enabled) return 0;
     if (stream_nmma(N, kStore) != 1) return 0;
     const int NP = stream_np(M);
     const int per_kb = kWTileBytes + NP * BK * 2;

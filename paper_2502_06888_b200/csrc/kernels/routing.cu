@@ -154,10 +154,11 @@ gate_topk_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ no
 // 0 then runs the same top-k / weights code.
 template <int NC>
 __global__ void __launch_bounds__(256)
-gate_topk_block_kernel(const uint16_t* __restrict__ h, const uint16_t* __restrict__ norm_w,
+gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
                        const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
                        uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
-                       float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos) {
+                       float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos,
+                       const float* __restrict__ hpart, int S, int64_t part_split_elems) {
     pdl_enter();
     constexpr int d = NC * 256;
     __shared__ float lg[64];
@@ -165,8 +166,41 @@ gate_topk_block_kernel(const uint16_t* __restrict__ h, const uint16_t* __restric
     const int tok = blockIdx.x;
     const uint16_t* hrow = h + static_cast<int64_t>(tok) * d;
     uint4 hv[NC];
+    if (hpart != nullptr) {
+        // Deferred o-proj: the row is first completed from the projection's
+        // fp32 split partials (the owner's order: its own split S-1, then
+        // 0..S-2) plus the residual, rounded once -- what the streaming
+        // GEMM's residual epilogue would have stored -- and written back.
+        __shared__ uint4 hrow_s[NC * 32];
+        for (int j = wid; j < NC; j += 8) {
+            const int64_t off = static_cast<int64_t>(tok) * d + lane * 8 + 256 * j;
+            const float4* own = reinterpret_cast<const float4*>(hpart + static_cast<int64_t>(S - 1) * part_split_elems + off);
+            float4 v0 = own[0], v1 = own[1];
+            for (int sp = 0; sp < S - 1; ++sp) {
+                const float4* q = reinterpret_cast<const float4*>(hpart + sp * part_split_elems + off);
+                const float4 a = q[0], b = q[1];
+                v0.x = __fadd_rn(v0.x, a.x); v0.y = __fadd_rn(v0.y, a.y); v0.z = __fadd_rn(v0.z, a.z); v0.w = __fadd_rn(v0.w, a.w);
+                v1.x = __fadd_rn(v1.x, b.x); v1.y = __fadd_rn(v1.y, b.y); v1.z = __fadd_rn(v1.z, b.z); v1.w = __fadd_rn(v1.w, b.w);
+            }
+            const uint4 r = *reinterpret_cast<const uint4*>(h + off);
+            const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+            uint32_t o[4];
 #pragma unroll
-    for (int j = 0; j < NC; ++j) hv[j] = __ldg(reinterpret_cast<const uint4*>(hrow + lane * 8 + 256 * j));
+            for (int e = 0; e < 4; ++e)
+                o[e] = pack2(__fadd_rn(f[2 * e], bf2f(static_cast<uint16_t>(rw[e] & 0xffffu))),
+                             __fadd_rn(f[2 * e + 1], bf2f(static_cast<uint16_t>(rw[e] >> 16))));
+            const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+            hrow_s[j * 32 + lane] = ov;
+            *reinterpret_cast<uint4*>(h + off) = ov;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < NC; ++j) hv[j] = hrow_s[j * 32 + lane];
+    } else {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) hv[j] = __ldg(reinterpret_cast<const uint4*>(hrow + lane * 8 + 256 * j));
+    }
     float ss = 0.f;
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
@@ -837,8 +871,9 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
 #define KL_GATE_WARP(NC)                                                                                          \
     case NC:                                                                                                      \
         if (per_block)                                                                                            \
-            return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, h, \
-                              norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos);     \
+            return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream,   \
+                              const_cast<uint16_t*>(h), norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx,       \
+                              weight, hist, first_pos, static_cast<const float*>(nullptr), 0, int64_t{0});           \
         return launch_pdl(gate_topk_warp_kernel<NC>, dim3(blocks), dim3(128), 0, stream, h, norm_w, wg, T, E, k, eps, \
                           score_mode, x2, logits, idx, weight, hist, first_pos);
     switch (d / 256) {
@@ -852,6 +887,33 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
 #undef KL_GATE_WARP
     return launch_pdl(gate_topk_kernel, dim3(T), dim3(kGateWarps * 32), 0, stream, h, norm_w, wg, T, d, E, k, eps,
                       score_mode, x2, logits, idx, weight, hist, first_pos);
+}
+
+extern "C" int kl_gate_topk_deferred(uint16_t* h, const float* h_part, int splits, int64_t part_rows,
+                                     const uint16_t* norm_w, const uint16_t* wg, int T, int d, int E, int k, float eps,
+                                     int score_mode, uint16_t* x2, float* logits, int32_t* idx, float* weight,
+                                     int32_t* hist, int32_t* first_pos, cudaStream_t stream) {
+    if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 64 || k < 1 || k > 8 || k > E) return KL_EINVAL;
+    if (!h || !h_part || !norm_w || !wg || !x2 || !idx || !weight || splits < 1 || splits > 4 || T > part_rows)
+        return KL_EINVAL;
+    if (T == 0) return KL_OK;
+    if (T > 4 * 148) return KL_EUNSUPPORTED;  // decode-sized calls (block per token) only
+    const int64_t pse = part_rows * d;
+#define KL_GATE_DEF(NC)                                                                                           \
+    case NC:                                                                                                      \
+        return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, h,     \
+                          norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos, h_part,   \
+                          splits, pse);
+    switch (d / 256) {
+        KL_GATE_DEF(2)
+        KL_GATE_DEF(4)
+        KL_GATE_DEF(8)
+        KL_GATE_DEF(16)
+        KL_GATE_DEF(24)
+        default: break;
+    }
+#undef KL_GATE_DEF
+    return KL_EUNSUPPORTED;
 }
 
 extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d, float eps, uint16_t* out,

@@ -44,6 +44,8 @@ _ffn_def = _sig("kl_expert_ffn_kb_deferred", [_P, _L, _L, _I, _I, _I, _P, _P, _P
 _ffn_def_splits = _sig("kl_expert_ffn_deferred_splits", [_I, _I, _I])
 _gemm_def_splits = _sig("kl_gemm_deferred_splits", [_I, _I, _I])
 _gemm_def = _sig("kl_gemm_bf16_deferred", [_P, _L, _L, _I, _I, _P, _I, _I, _P, _L, _I, _P, _L, _P])
+_gate_def = _sig("kl_gate_topk_deferred", [_P, _P, _I, _L, _P, _P, _I, _I, _I, _I, _F, _I, _P, _P, _P, _P, _P, _P,
+                                           _P])
 _rope_def = _sig("kl_rope_kv_append_deferred", [_P, _I, _L, _P, _L, _I, _I, _I, _P, _P, _F, _P, _P, _I, _I, _I, _P])
 _coact = _sig("kl_coact_update", [_P, _P, _L, _I, _I, _I, _P, _P, _P])
 _pred = _sig("kl_predict_scores", [_P, _P, _I, _I, _P, _P])
@@ -274,6 +276,20 @@ def gemm_deferred(a, b, c_part, splits, row_offset=0, m=None, kblocked=False, st
     _chk(_gemm_def(_p(a), a.shape[0], row_offset, m, K, _p(b), N, int(kblocked), _p(c_part), c_part.shape[1], splits,
                    None, 0, _s(stream)), "kl_gemm_bf16_deferred")
     return c_part
+
+
+def gate_topk_deferred(h, h_part, splits, norm_w, wg, k, eps=1e-5, score_mode=0, x2=None, logits=None, hist=None,
+                       first_pos=None, stream=None):
+    """kl_gate_topk_deferred: completes h in place from o-proj split partials
+    h_part [splits, rows, d], then the router; returns (x2, idx, weight)."""
+    T, d = h.shape
+    E = wg.shape[0]
+    x2 = torch.empty_like(h) if x2 is None else x2
+    idx = torch.empty(T, k, dtype=torch.int32, device=h.device)
+    wt = torch.empty(T, k, dtype=torch.float32, device=h.device)
+    _chk(_gate_def(_p(h), _p(h_part), splits, h_part.shape[1], _p(norm_w), _p(wg), T, d, E, k, eps, score_mode, _p(x2),
+                   _p(logits), _p(idx), _p(wt), _p(hist), _p(first_pos), _s(stream)), "kl_gate_topk_deferred")
+    return x2, idx, wt
 
 
 def rope_kv_append_deferred(qkv_part, splits, qkv, Hq, Hkv, hd, pos, seq, theta, k_cache, v_cache, cap, sink,

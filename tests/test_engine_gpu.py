@@ -445,9 +445,13 @@ def test_fused_qkv_rope_matches_separate_calls(cuda, monkeypatch):
 
 def test_deferred_split_reduction_matches_owner_fixup(cuda, monkeypatch):
     """Mixtral-8x7B dims (2 layers, bs 64 x n 2, gate routing, experts
-    streamed and resident): leaving the down projection's k-splits as fp32
-    partials for the block's combine gives the same tokens and hidden states
-    as the owner-fixup FFN (KL_NO_DEFER), and the same executed op log."""
+    streamed and resident): leaving the k-splits of the QKV projection, the
+    o-projection and every expert's down projection as fp32 partials (summed
+    by the RoPE kernel, the router kernel and the block's combine) gives the
+    same tokens and hidden states as the owner-fixup GEMMs on the same splits
+    (KL_NO_DEFER, with the o-projection forced onto the streaming kernel), and
+    the same executed op log."""
+    from paper_2502_06888_b200 import kernels as K
     cfg = {"model": {"preset": "mixtral-8x7b", "n_layers": 2},
            "workload": {"batch_size": 64, "n_batches": 2, "prompt_len": 16, "gen_len": 4},
            "hbm_cap_bytes": 8_000_000_000, "host_distinct_layers": 2, "routing": "gate", "record_hidden": True}
@@ -457,12 +461,16 @@ def test_deferred_split_reduction_matches_owner_fixup(cuda, monkeypatch):
             monkeypatch.delenv("KL_NO_DEFER", raising=False)
         else:
             monkeypatch.setenv("KL_NO_DEFER", env)
-        eng = make(cfg)
-        outs = run_all_steps(eng, cfg, seed=4)
-        dumps = eng.report("hidden")["dumps"]
-        sched = eng.report("schedule")["text"]
-        assert eng.report("validate")["violations"] == []
-        eng.close()
+            K.tune(K.TUNE_STREAM_GEMM, 2)  # o-proj (< 40 MB) on the streaming kernel, as when deferred
+        try:
+            eng = make(cfg)
+            outs = run_all_steps(eng, cfg, seed=4)
+            dumps = eng.report("hidden")["dumps"]
+            sched = eng.report("schedule")["text"]
+            assert eng.report("validate")["violations"] == []
+            eng.close()
+        finally:
+            K.tune(K.TUNE_STREAM_GEMM, 1)
         runs.append((outs, dumps, sched))
     (o1, d1, s1), (o2, d2, s2) = runs
     assert s1 == s2

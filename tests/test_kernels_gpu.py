@@ -507,6 +507,37 @@ def test_qkv_deferred_rope_bit_identical(K, cuda, M, Hq, Hkv, d):
     assert torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
 
 
+@pytest.mark.parametrize("M,d,Hq,E,k", [(64, 4096, 32, 8, 2), (37, 6144, 48, 8, 2), (64, 2048, 16, 64, 6)])
+def test_oproj_deferred_into_gate_bit_identical(K, cuda, M, d, Hq, E, k):
+    """o-projection splits left as fp32 partials and completed (+ residual) by
+    the router kernel equal the streaming GEMM's residual epilogue on the same
+    splits followed by the router: h, x2, ids, weights and logits."""
+    hd = 128
+    ao = to_dev(orc.normal_bf16(M * Hq * hd, 93, 1.0).reshape(M, Hq * hd), cuda)
+    wo = to_dev(orc.normal_bf16(d * Hq * hd, 94, 0.02).reshape(d, Hq * hd), cuda)
+    h0 = to_dev(orc.normal_bf16(M * d, 95, 1.0).reshape(M, d), cuda)
+    nw = to_dev(orc.normal_bf16(d, 96, 0.5), cuda)
+    wg = to_dev(orc.normal_bf16(E * d, 97, 0.05).reshape(E, d), cuda)
+    S = K.gemm_deferred_splits(M, d, Hq * hd)
+    assert S >= 2
+    h1 = h0.clone()
+    K.tune(K.TUNE_STREAM_GEMM, 2)  # the owner-fixup residual GEMM on the same splits (below 40 MB)
+    try:
+        K.gemm(ao, wo, c=h1, residual=h1, epilogue=1)
+    finally:
+        K.tune(K.TUNE_STREAM_GEMM, 1)
+    lg1 = torch.empty(M, E, dtype=torch.float32, device=cuda)
+    x21, i1, w1 = K.gate_topk(h1, nw, wg, k, logits=lg1)
+    part = torch.empty(S, M, d, dtype=torch.float32, device=cuda)
+    K.gemm_deferred(ao, wo, part, S)
+    h2 = h0.clone()
+    lg2 = torch.empty_like(lg1)
+    x22, i2, w2 = K.gate_topk_deferred(h2, part, S, nw, wg, k, logits=lg2)
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2)
+    assert torch.equal(x21, x22) and torch.equal(i1, i2) and torch.equal(w1, w2) and torch.equal(lg1, lg2)
+
+
 def test_qkv_rope_fused_declines_small_shapes(K, cuda):
     """Below the weight-streaming threshold the fused entry reports
     KL_EUNSUPPORTED (the engine then issues the separate calls)."""
