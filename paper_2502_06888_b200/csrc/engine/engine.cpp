@@ -245,6 +245,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     allocate_device();
     allocate_host();
     for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&routing_ready_, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreate(&step_begin_), "event");
     cuda_check(cudaEventCreate(&step_end_), "event");
     ep_init();
@@ -269,6 +270,7 @@ Engine::~Engine() {
         if (s) cudaStreamDestroy(s);
     for (auto& pool : event_pool_)
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    if (routing_ready_) cudaEventDestroy(routing_ready_);
     if (step_begin_) cudaEventDestroy(step_begin_);
     if (step_end_) cudaEventDestroy(step_end_);
     for (cudaEvent_t e : pool_.release) (void)e;
@@ -418,9 +420,9 @@ bool Engine::plan_at(int n, bool rethrow) {
         add(64 * 1024);
         add((2 * ops_per_step_bound(D_.L, n, El_) + 8) * 8);                     // op timestamps
         add(tb_max_ * D_.hd * 4);                                                // RoPE table
-        if (defer_possible())                                                    // deferred split partials
-            add(4LL * n * w.batch_size * D_.k * D_.d * 4 + 4LL * w.batch_size * D_.qkv_width() * 4 +
-                4LL * n * w.batch_size * D_.d * 4);
+        if (defer_possible()) add(4LL * n * w.batch_size * D_.k * D_.d * 4);    // deferred FFN split partials
+        if (defer_attn_possible())                                               // deferred QKV / o-proj partials
+            add(4LL * w.batch_size * D_.qkv_width() * 4 + 4LL * n * w.batch_size * D_.d * 4);
         if (kv_off)
             add(static_cast<byte_count>(kKvSlots) * w.batch_size *
                 cfg_.retention.retained(w.prompt_len + w.gen_len - 1) * spec_.kv_bytes_per_token);
@@ -446,6 +448,10 @@ bool Engine::plan_at(int n, bool rethrow) {
 bool Engine::defer_possible() const {
     return !cfg_.quant && !ep_ && cfg_.kblocked_experts && cfg_.variant != Variant::simple;
 }
+// The attention projections defer in every variant and under expert
+// parallelism (each batch's router op follows its attention op); not with
+// Q4T-streamed attention weights.
+bool Engine::defer_attn_possible() const { return !cfg_.quant; }
 
 void Engine::finish_plan() {
     kv_offload_ = plan_.placement.kv_tier == Tier::dram;
@@ -497,13 +503,15 @@ void Engine::allocate_device() {
     head_ = bf(static_cast<int64_t>(D_.V) * D_.d);
     h_ = bf(t_max_ * D_.d);
     rope_tab_ = static_cast<float*>(take(tb_max_ * D_.hd * 4));  // [tb_max][hd/2] (cos, sin)
+    defer_ok_ = std::getenv("KL_NO_DEFER") == nullptr;
     if (defer_possible()) {
         ypart_rows_ = static_cast<int64_t>(plan_.n_batches) * cfg_.workload.batch_size * D_.k;  // a decode step's rows
         ypart_ = static_cast<float*>(take(4 * ypart_rows_ * D_.d * 4));
+    }
+    if (defer_attn_possible()) {
         qkvpart_ = static_cast<float*>(take(4LL * cfg_.workload.batch_size * D_.qkv_width() * 4));
         opart_ = static_cast<float*>(take(4LL * plan_.n_batches * cfg_.workload.batch_size * D_.d * 4));
         o_deferred_.assign(static_cast<size_t>(plan_.n_batches), 0);
-        defer_ok_ = std::getenv("KL_NO_DEFER") == nullptr;
     }
     // Opt-in (KL_QKV_ROPE=1): bit-identical to the separate calls but no
     // faster (attention op 56.6 vs 57.1 us as a graph: the owners' epilogue

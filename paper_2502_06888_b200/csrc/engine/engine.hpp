@@ -287,7 +287,8 @@ class Engine {
     int64_t ypart_rows_ = 0;
     bool defer_ok_ = false;
     int block_defer_ = 0;
-    bool defer_possible() const;
+    bool defer_possible() const;       // FFN down projection -> combine
+    bool defer_attn_possible() const;  // QKV -> RoPE kernel, o-projection -> router kernel
     int block_defer_splits(std::int32_t first_op) const;
     bool rope_fused_ok_ = true;   // QKV GEMM with the fused RoPE / KV-append epilogue
     std::vector<moesim::SimEvent> timeline_;          // measured, by op id
@@ -322,6 +323,13 @@ class Engine {
     int block_layer_ = -1;
     int exec_expert_left_ = 0;
     std::vector<int64_t> host_scores_, host_marginal_;
+    // Routing readback in two parts (non-EP blocks): the per-batch histogram /
+    // first demand (and recorded ids) right after the last gate, so the host
+    // emits the expert half while the GPU permutes; the prefetcher's next-layer
+    // scores with the rest of the op, read before the next block's decision.
+    cudaEvent_t routing_ready_ = nullptr;
+    std::int32_t scores_op_ = -1;  // op whose end covers the pending scores readback (-1: none)
+    void take_scores();
     bool scores_valid_ = false;
     int64_t tokens_generated_ = 0;
     int64_t launches_ = 0;  // sm_100a kernel launches since the last reset

@@ -275,6 +275,7 @@ double Engine::step(int step, const int32_t* tokens_in, int32_t* next_out) {
     }
     for (int layer = 0; layer < D_.L && cfg_.variant != Variant::simple; ++layer) {
         PrefetchDecision d;
+        if (!ep_) take_scores();  // the previous block's scores (its gate op has long been enqueued)
         if (split) d = decide(step, layer);
         if (cfg_.replay) {
             // Forced routing of this (step, layer) from the replay trace.
@@ -725,7 +726,7 @@ void Engine::exec_gate(const StreamOp& op) {
     const uint16_t* wg = gate_slot_[gate_slot_of_.at(l)];
     int32_t* idx = idx_[idx_cur_] + row0 * D_.k;
     float* wt = weight_ + row0 * D_.k;
-    const int odef = o_deferred_.empty() || simple ? 0 : o_deferred_[static_cast<size_t>(b)];
+    const int odef = o_deferred_.empty() ? 0 : o_deferred_[static_cast<size_t>(b)];
     if (odef > 0) {
         // This batch's o-proj left split partials: the router kernel completes h first.
         o_deferred_[static_cast<size_t>(b)] = 0;
@@ -766,6 +767,12 @@ void Engine::after_layer_gates(int step, int layer) {
     const int64_t T = static_cast<int64_t>(n) * tokens_per_batch(step);
     int32_t* cur = idx_[idx_cur_];
     int32_t* prev = idx_[idx_cur_ ^ 1];
+    // Part 1 of the readback: what close_block needs (per-batch histogram and
+    // first demand, recorded ids), ahead of the permutation.
+    cuda_check(cudaMemcpyAsync(host_report_, report_, 2LL * n * D_.E * 4, cudaMemcpyDeviceToHost, cs), "d2h routing");
+    if (cfg_.record_trace)
+        cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, cs), "d2h idx");
+    cuda_check(cudaEventRecord(routing_ready_, cs), "routing ready");
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
     shared_experts(layer, T, 0);
@@ -778,11 +785,25 @@ void Engine::after_layer_gates(int step, int layer) {
         kl_check(kl_predict_scores(counts_, table_, D_.E, layer + 1, scores, cs), "predict");
     }
     cuda_check(cudaMemcpyAsync(marg_copy, marginal_, D_.E * 8, cudaMemcpyDeviceToDevice, cs), "marginal");
-    const size_t report_bytes = reinterpret_cast<char*>(marg_copy + D_.E) - reinterpret_cast<char*>(report_);
-    cuda_check(cudaMemcpyAsync(host_report_, report_, report_bytes, cudaMemcpyDeviceToHost, cs), "d2h report");
-    if (cfg_.record_trace)
-        cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, cs), "d2h idx");
+    // Part 2: the next layer's prefetch scores and the marginal (take_scores).
+    const size_t head = reinterpret_cast<char*>(scores) - reinterpret_cast<char*>(report_);
+    cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(host_report_) + head, scores, 2LL * D_.E * 8,
+                               cudaMemcpyDeviceToHost, cs), "d2h scores");
+    scores_op_ = next_exec_ - 1;  // this (last gate) op; its end event covers the copy
     idx_cur_ ^= 1;  // this layer's ids become "prev" for the next layer
+}
+
+// The prefetcher's next-layer scores of the last closed block (readback part
+// 2), once its gate op has completed; before the next block's decision.
+void Engine::take_scores() {
+    if (scores_op_ < 0) return;
+    cuda_check(cudaEventSynchronize(op_end_[scores_op_]), "scores sync");
+    scores_op_ = -1;
+    const int n = plan_.n_batches, E = D_.E;
+    const int64_t* scores =
+        reinterpret_cast<const int64_t*>(host_report_ + 2LL * n * E + 16 - ((2LL * n * E) % 16));
+    host_scores_.assign(scores, scores + E);
+    host_marginal_.assign(scores + E, scores + 2 * E);
 }
 
 // Shared experts (always active): h += FFN_shared(x2) on every token of the
@@ -830,8 +851,8 @@ void Engine::after_batch_gate(int step, int layer, int b) {
 }
 
 detail::BlockRouting Engine::read_routing_row(int step, int layer, int b) {
-    const std::int32_t last_gate = next_exec_ - 1;
-    cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
+    // The row's gate op (the last op issued) ends after its readback copies.
+    cuda_check(cudaEventSynchronize(op_end_[next_exec_ - 1]), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
     r.group_hist.assign(E, 0);
@@ -868,8 +889,7 @@ detail::BlockRouting Engine::read_routing_row(int step, int layer, int b) {
 detail::BlockRouting Engine::read_routing(int step, int layer) {
     // The last op issued on the compute stream is the block's last gate;
     // its end event covers the readback copies.
-    const std::int32_t last_gate = next_exec_ - 1;
-    cuda_check(cudaEventSynchronize(op_end_[last_gate]), "routing sync");
+    cuda_check(cudaEventSynchronize(routing_ready_), "routing sync");
     const int n = plan_.n_batches, E = D_.E;
     detail::BlockRouting r;
     r.group_hist.assign(E, 0);
@@ -890,10 +910,6 @@ detail::BlockRouting Engine::read_routing(int step, int layer) {
         std::sort(firsts.begin(), firsts.end());
         for (const auto& [f, e] : firsts) r.demand[b].push_back(e);
     }
-    const int64_t* scores =
-        reinterpret_cast<const int64_t*>(host_report_ + 2LL * n * E + 16 - ((2LL * n * E) % 16));
-    host_scores_.assign(scores, scores + E);
-    host_marginal_.assign(scores + E, scores + 2 * E);
     // Expert segment starts of the stable counting sort (== device offsets).
     row_offset_.assign(E, 0);
     for (int e = 1; e < E; ++e) row_offset_[e] = row_offset_[e - 1] + r.group_hist[e - 1];

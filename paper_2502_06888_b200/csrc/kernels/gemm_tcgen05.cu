@@ -1662,7 +1662,12 @@ extern "C" int kl_gemm_deferred_splits(int M, int N, int K) {
     return S <= 4 ? S : 0;
 }
 
-extern "C" int kl_expert_ffn_deferred_splits(int M, int d, int f) { return kl_gemm_deferred_splits(M, d, f); }
+// The down projection defers only where the owner-fixup form would also run
+// on the streaming kernel (>= 40 MB of weights or M > 128), so a deferred and
+// a non-deferred FFN (e.g. an expert-parallel shard) share split partitions.
+extern "C" int kl_expert_ffn_deferred_splits(int M, int d, int f) {
+    return kl::stream_eligible(M, d, f, kl::kStore) ? kl_gemm_deferred_splits(M, d, f) : 0;
+}
 
 extern "C" int kl_gemm_bf16_deferred(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                                      const uint16_t* b, int N, int b_kblocked, float* c_part, int64_t part_rows,
