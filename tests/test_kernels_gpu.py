@@ -158,6 +158,27 @@ def test_gemm_weight_streaming_small_workspace_and_off(K, cuda):
     close_bf16(to_bits(off), ref)
 
 
+@pytest.mark.parametrize("T,k,S,d", [(64, 6, 3, 2048), (33, 2, 2, 512), (200, 8, 4, 1024)])
+def test_combine_deferred_matches_combine_of_summed_rows(K, cuda, T, k, S, d):
+    """kl_combine_deferred over random fp32 split partials equals kl_combine
+    over y = bf16(((p[S-1] + p[0]) + p[1]) + ...) for top-k up to 8 (the
+    fine-grained DeepSeek shape uses k 6)."""
+    R = T * k
+    rng = np.random.default_rng(7)
+    pos = torch.from_numpy(rng.permutation(R).astype(np.int32)).to(cuda)
+    wt = torch.from_numpy(rng.random((T, k)).astype(np.float32)).to(cuda)
+    part = torch.randn(S, R, d, dtype=torch.float32, device=cuda)
+    resid = torch.randn(T, d, dtype=torch.bfloat16, device=cuda)
+    acc = part[S - 1].clone()
+    for sp in range(S - 1):
+        acc += part[sp]
+    y = acc.to(torch.bfloat16)
+    out1 = K.combine(y, pos, wt, resid)
+    out2 = K.combine_deferred(part, S, pos, wt, resid)
+    torch.cuda.synchronize()
+    assert torch.equal(out1, out2)
+
+
 def test_deferred_ffn_and_combine_bit_identical(K, cuda):
     """Mixtral-8x7B experts on skewed decode routing (512 tokens, top-2, per
     expert ~90..~190 rows): FFN with the down projection's splits left as fp32

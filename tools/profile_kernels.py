@@ -211,6 +211,23 @@ def main():
             t = timed_graph(ffn_def, 16)
             dump_trace("down_deferred")
             res["expert_ffn_deferred_graph"] = {"M": M, "splits": S, "us": t * 1e6, "GBs": byt / t / 1e9}
+            if R >= E * M:
+                # One layer block as the engine runs it at decode: 8 experts'
+                # deferred FFNs, then the combine summing their split partials.
+                Tt = R // k
+                pos_b = torch.randperm(R, device=dev).to(torch.int32)
+                wt_b = torch.rand(Tt, k, device=dev)
+                res_b = torch.randn(Tt, d, dtype=bf, device=dev)
+                out_b = torch.empty_like(res_b)
+
+                def block(i):
+                    for e in range(E):
+                        w = ws[e]
+                        K.expert_ffn_deferred(xp, e * M, M, w[: 2 * f * d].view(2 * f, d), w[2 * f * d:].view(d, f),
+                                              ypart, h, S)
+                    K.combine_deferred(ypart, S, pos_b, wt_b, res_b, out=out_b)
+                t = timed_graph(block, 4)
+                res["block_8ffn_deferred_combine"] = {"M": M, "us": t * 1e6, "us_per_ffn": t * 1e6 / E}
             del ypart
 
         def g1(i):
