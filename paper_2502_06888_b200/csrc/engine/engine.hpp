@@ -272,6 +272,7 @@ class Engine {
     bool t0_recorded_ = false;
     unsigned long long t0_ns_ = 0;
     void stamp(std::int32_t id, int side, cudaStream_t st);
+    void stamp_next_launch(std::int32_t id);  // the op's first GEMM writes its start mark
     std::vector<cudaEvent_t> op_end_;                 // by op id (current step window)
     float* rope_tab_ = nullptr;   // decode RoPE (cos, sin) table of one batch [tb_max][hd/2][2]
     // Deferred down-projection reduction (decode, bf16 K-blocked experts):

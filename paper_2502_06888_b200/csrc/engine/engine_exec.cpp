@@ -145,6 +145,13 @@ void Engine::stamp(std::int32_t id, int side, cudaStream_t st) {
     kl_check(kl_stamp(stamps_dev_ + 2 * slot + side, st), "op stamp");
 }
 
+void Engine::stamp_next_launch(std::int32_t id) {
+    const std::int64_t slot = static_cast<std::int64_t>(id) - timed_from_;
+    if (slot < 0 || slot >= stamp_cap_)
+        throw AccountingError("engine: op " + std::to_string(id) + " outside the step's timestamp window");
+    kl_stamp_next_launch(stamps_dev_ + 2 * slot);
+}
+
 const uint16_t* Engine::expert_weights(int layer, int e) const {
     if (const uint16_t* r = res_expert_[static_cast<size_t>(layer) * El_ + e]) return r;
     const auto it = expert_slot_of_.find({layer, e});
@@ -574,7 +581,11 @@ void Engine::exec(std::int32_t id) {
             exec_gate(op);
             break;
         case OpKind::compute_expert:
-            stamp(id, 0, st);
+            // bf16 experts: the op's first GEMM marks its start itself.
+            if (op.token_count > 0 && !cfg_.quant)
+                stamp_next_launch(id);
+            else
+                stamp(id, 0, st);
             exec_expert(op);
             break;
         default:

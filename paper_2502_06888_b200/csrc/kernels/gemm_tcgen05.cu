@@ -29,6 +29,9 @@
 
 namespace kl {
 extern int g_pdl;  // kl_tune(KL_TUNE_PDL, ...): programmatic dependent launch (abi.cu)
+// kl_stamp_next_launch: the next GEMM this host thread launches marks the op
+// start itself (one kernel fewer in the op's launch chain).
+thread_local unsigned long long* t_next_start = nullptr;
 namespace {
 // kl_tune(KL_TUNE_STREAM_HINT, ...): L2 policy hints on weight loads: 1 = weights
 // evict-first / activations evict-last, 2 = weights evict-last, 0 = none.
@@ -494,6 +497,7 @@ struct StreamArgs {
     int ks;     // k-blocks per stage: 2 = one 3D TMA box covers two 64-column k-blocks (larger copies)
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
+    unsigned long long* t_start;  // op start mark: %globaltimer once the previous grid is done (kl_stamp_next_launch)
     // Deferred split reduction (kStore, NMMA 1, tile-aligned splits): every CTA
     // writes its fp32 accumulator to defer[split][row][feature] (row pitch
     // defer_ld) and the consumer sums the splits; no flags, no fixup.
@@ -755,6 +759,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
         __syncwarp();
     } else {
         if (p.pdl) griddep_wait();
+        if (p.t_start != nullptr && blockIdx.x == 0 && threadIdx.x == 64) *p.t_start = gtimer();
         const int quarter = warp & 3;
         const int frow = quarter * 32 + lane;  // feature row inside a 128-row sub-tile
         const int etid = threadIdx.x - 64;     // 0..127 across the epilogue warps
@@ -1373,6 +1378,8 @@ int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = p.pdl ? 1 : 0;
+    p.t_start = t_next_start;
+    t_next_start = nullptr;
     KL_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_stream_kernel<EPI, NMMA, Q4>, mw, mx, static_cast<int>(row_offset), p));
     return check_launch();
 }
@@ -1398,6 +1405,11 @@ int gemm_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, in
 
 }  // namespace
 }  // namespace kl
+
+extern "C" int kl_stamp_next_launch(unsigned long long* dst) {
+    kl::t_next_start = dst;
+    return KL_OK;
+}
 
 extern "C" int kl_stream_trace(unsigned long long* host, int n_ctas) {
     const int rc = static_cast<int>(cudaMemcpyFromSymbol(host, kl::g_stream_trace, static_cast<size_t>(n_ctas) * 12 * 8));
@@ -1484,6 +1496,11 @@ int gemm_bf16_impl(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M,
         const int rc = gemm_stream(a, a_rows, row_offset, M, K, b, N, c, ldc, r, epilogue, workspace, workspace_bytes,
                                    stream, wkb);
         if (rc != KL_EUNSUPPORTED) return rc;
+    }
+    if (t_next_start != nullptr) {  // a pending op-start mark on a non-streaming path: a separate stamp
+        unsigned long long* ts = t_next_start;
+        t_next_start = nullptr;
+        if (const int rc = kl_stamp(ts, stream)) return rc;
     }
     const int m_tiles = (M + BM - 1) / BM;
     const int kb = K / BK;
