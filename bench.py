@@ -663,6 +663,11 @@ def run_ours(args):
             torch.cuda.synchronize()
 
     # Timed region 1: inputs resident in HBM (device-fed greedy tokens).
+    # (Python's cyclic GC stays off inside both timed regions: a collection
+    # pause would land in the end-to-end wall time.)
+    import gc
+    gc.collect()
+    gc.disable()
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -698,6 +703,7 @@ def run_ours(args):
         step += 1
     barrier()
     e2e_wall = time.perf_counter() - t1
+    gc.enable()
 
     total_ms = max_over_ranks(total_ms, world, dev)
     e2e_total_ms = max_over_ranks(max(sum(e2e_ms), e2e_wall * 1e3), world, dev)
