@@ -96,6 +96,37 @@ __device__ __forceinline__ float4 sum_split_vec4(const float* __restrict__ part,
     return make_float4(bf2f(f2bf(v.x)), bf2f(f2bf(v.y)), bf2f(f2bf(v.z)), bf2f(f2bf(v.w)));
 }
 
+// Both halves of a rotation pair (offsets oa, ob) summed as sum_split_vec4
+// does; for S <= 4 every split's loads are issued before the first add (one
+// memory latency instead of a chain of S).
+__device__ __forceinline__ void sum_split_pair4(const float* __restrict__ part, int S, int64_t se, int64_t oa,
+                                                int64_t ob, float4& a, float4& b) {
+    if (S > 4) {
+        a = sum_split_vec4(part, S, se, oa);
+        b = sum_split_vec4(part, S, se, ob);
+        return;
+    }
+    float4 qa[4], qb[4];
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl)
+        if (sl < S) {
+            const int64_t sp = sl == 0 ? S - 1 : sl - 1;  // the owner's split first, then 0..S-2
+            qa[sl] = __ldg(reinterpret_cast<const float4*>(part + sp * se + oa));
+            qb[sl] = __ldg(reinterpret_cast<const float4*>(part + sp * se + ob));
+        }
+    float4 va = qa[0], vb = qb[0];
+#pragma unroll
+    for (int sl = 1; sl < 4; ++sl)
+        if (sl < S) {
+            va.x = __fadd_rn(va.x, qa[sl].x); va.y = __fadd_rn(va.y, qa[sl].y);
+            va.z = __fadd_rn(va.z, qa[sl].z); va.w = __fadd_rn(va.w, qa[sl].w);
+            vb.x = __fadd_rn(vb.x, qb[sl].x); vb.y = __fadd_rn(vb.y, qb[sl].y);
+            vb.z = __fadd_rn(vb.z, qb[sl].z); vb.w = __fadd_rn(vb.w, qb[sl].w);
+        }
+    a = make_float4(bf2f(f2bf(va.x)), bf2f(f2bf(va.y)), bf2f(f2bf(va.z)), bf2f(f2bf(va.w)));
+    b = make_float4(bf2f(f2bf(vb.x)), bf2f(f2bf(vb.y)), bf2f(f2bf(vb.z)), bf2f(f2bf(vb.w)));
+}
+
 __global__ void rope_append_deferred_vec_kernel(const float* __restrict__ part, int S, int64_t split_elems,
                                                 uint16_t* __restrict__ qkv, int64_t T, int Hq, int Hkv, int hd,
                                                 const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
@@ -117,8 +148,8 @@ __global__ void rope_append_deferred_vec_kernel(const float* __restrict__ part, 
     const int64_t cache_row = (static_cast<int64_t>(seq[t]) * cap + slot_of(p, cap, sink)) * Hkv * hd;
     const int head = unit / q4, i0 = (unit % q4) * 4;  // head in [0, Hq + 2 Hkv)
     const int64_t b0 = prow + static_cast<int64_t>(head) * hd;
-    const float4 a4 = sum_split_vec4(part, S, split_elems, b0 + i0);
-    const float4 b4 = sum_split_vec4(part, S, split_elems, b0 + i0 + half);
+    float4 a4, b4;
+    sum_split_pair4(part, S, split_elems, b0 + i0, b0 + i0 + half, a4, b4);
     uint16_t ra[4], rb[4];
     if (head < heads) {
         const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};

@@ -172,17 +172,7 @@ gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
         // 0..S-2) plus the residual, rounded once -- what the streaming
         // GEMM's residual epilogue would have stored -- and written back.
         __shared__ uint4 hrow_s[NC * 32];
-        for (int j = wid; j < NC; j += 8) {
-            const int64_t off = static_cast<int64_t>(tok) * d + lane * 8 + 256 * j;
-            const float4* own = reinterpret_cast<const float4*>(hpart + static_cast<int64_t>(S - 1) * part_split_elems + off);
-            float4 v0 = own[0], v1 = own[1];
-            for (int sp = 0; sp < S - 1; ++sp) {
-                const float4* q = reinterpret_cast<const float4*>(hpart + sp * part_split_elems + off);
-                const float4 a = q[0], b = q[1];
-                v0.x = __fadd_rn(v0.x, a.x); v0.y = __fadd_rn(v0.y, a.y); v0.z = __fadd_rn(v0.z, a.z); v0.w = __fadd_rn(v0.w, a.w);
-                v1.x = __fadd_rn(v1.x, b.x); v1.y = __fadd_rn(v1.y, b.y); v1.z = __fadd_rn(v1.z, b.z); v1.w = __fadd_rn(v1.w, b.w);
-            }
-            const uint4 r = *reinterpret_cast<const uint4*>(h + off);
+        auto finish = [&](int j, int64_t off, float4 v0, float4 v1, uint4 r) {
             const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
             uint32_t o[4];
@@ -193,6 +183,57 @@ gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
             const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
             hrow_s[j * 32 + lane] = ov;
             *reinterpret_cast<uint4*>(h + off) = ov;
+        };
+        auto add4 = [](float4& v, const float4& a) {
+            v.x = __fadd_rn(v.x, a.x); v.y = __fadd_rn(v.y, a.y); v.z = __fadd_rn(v.z, a.z); v.w = __fadd_rn(v.w, a.w);
+        };
+        if (S <= 4) {
+            // Every load of this warp's chunks issued before the first add
+            // (slot 0 = the owner's split S-1, slot i = split i-1): one
+            // memory latency instead of a chain of S x chunks.
+            constexpr int kJ = (NC + 7) / 8;
+            float4 pa[kJ][4][2];
+            uint4 rr[kJ];
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) {
+                const int j = wid + 8 * jj;
+                if (j >= NC) continue;
+                const int64_t off = static_cast<int64_t>(tok) * d + lane * 8 + 256 * j;
+#pragma unroll
+                for (int sl = 0; sl < 4; ++sl)
+                    if (sl < S) {
+                        const int sp = sl == 0 ? S - 1 : sl - 1;
+                        const float4* q = reinterpret_cast<const float4*>(hpart + sp * part_split_elems + off);
+                        pa[jj][sl][0] = q[0];
+                        pa[jj][sl][1] = q[1];
+                    }
+                rr[jj] = *reinterpret_cast<const uint4*>(h + off);
+            }
+#pragma unroll
+            for (int jj = 0; jj < kJ; ++jj) {
+                const int j = wid + 8 * jj;
+                if (j >= NC) continue;
+                float4 v0 = pa[jj][0][0], v1 = pa[jj][0][1];
+#pragma unroll
+                for (int sl = 1; sl < 4; ++sl)
+                    if (sl < S) {
+                        add4(v0, pa[jj][sl][0]);
+                        add4(v1, pa[jj][sl][1]);
+                    }
+                finish(j, static_cast<int64_t>(tok) * d + lane * 8 + 256 * j, v0, v1, rr[jj]);
+            }
+        } else {
+            for (int j = wid; j < NC; j += 8) {
+                const int64_t off = static_cast<int64_t>(tok) * d + lane * 8 + 256 * j;
+                const float4* own = reinterpret_cast<const float4*>(hpart + static_cast<int64_t>(S - 1) * part_split_elems + off);
+                float4 v0 = own[0], v1 = own[1];
+                for (int sp = 0; sp < S - 1; ++sp) {
+                    const float4* q = reinterpret_cast<const float4*>(hpart + sp * part_split_elems + off);
+                    add4(v0, q[0]);
+                    add4(v1, q[1]);
+                }
+                finish(j, off, v0, v1, *reinterpret_cast<const uint4*>(h + off));
+            }
         }
         __syncthreads();
 #pragma unroll
