@@ -245,7 +245,9 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg), D_(cfg.dims) {
     allocate_device();
     allocate_host();
     for (auto& s : streams_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaEventCreateWithFlags(&routing_ready_, cudaEventDisableTiming), "event");
+    cuda_check(cudaStreamCreateWithFlags(&rb_stream_, cudaStreamNonBlocking), "stream");
+    for (cudaEvent_t* e : {&routing_ready_, &gates_done_, &scores_done_, &scores_ready_})
+        cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreate(&step_begin_), "event");
     cuda_check(cudaEventCreate(&step_end_), "event");
     ep_init();
@@ -270,7 +272,9 @@ Engine::~Engine() {
         if (s) cudaStreamDestroy(s);
     for (auto& pool : event_pool_)
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
-    if (routing_ready_) cudaEventDestroy(routing_ready_);
+    if (rb_stream_) cudaStreamDestroy(rb_stream_);
+    for (cudaEvent_t e : {routing_ready_, gates_done_, scores_done_, scores_ready_})
+        if (e) cudaEventDestroy(e);
     if (step_begin_) cudaEventDestroy(step_begin_);
     if (step_end_) cudaEventDestroy(step_end_);
     for (cudaEvent_t e : pool_.release) (void)e;

@@ -328,8 +328,14 @@ class Engine {
     // first demand (and recorded ids) right after the last gate, so the host
     // emits the expert half while the GPU permutes; the prefetcher's next-layer
     // scores with the rest of the op, read before the next block's decision.
-    cudaEvent_t routing_ready_ = nullptr;
-    std::int32_t scores_op_ = -1;  // op whose end covers the pending scores readback (-1: none)
+    // Both parts are copied on their own stream (rb_stream_), behind events
+    // recorded on the compute stream, so the compute stream never waits for
+    // a PCIe round trip; the next block's first histogram reset waits for
+    // readback_done_ before it rewrites the device report.
+    cudaStream_t rb_stream_ = nullptr;
+    cudaEvent_t routing_ready_ = nullptr, gates_done_ = nullptr, scores_done_ = nullptr, scores_ready_ = nullptr;
+    bool scores_pending_ = false;   // a scores readback is in flight (take_scores syncs scores_ready_)
+    bool readback_pending_ = false;  // scores_ready_ recorded and not yet waited for by the compute stream
     void take_scores();
     bool scores_valid_ = false;
     int64_t tokens_generated_ = 0;

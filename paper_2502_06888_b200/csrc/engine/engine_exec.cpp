@@ -727,6 +727,10 @@ void Engine::exec_gate(const StreamOp& op) {
                                        static_cast<size_t>(tpb) * D_.k * 4, cudaMemcpyHostToDevice, cs),
                        "h2d forced routing");
     } else if (b == 0) {
+        if (readback_pending_) {  // the previous block's readback copies have read the report
+            cuda_check(cudaStreamWaitEvent(cs, scores_ready_, 0), "wait readback");
+            readback_pending_ = false;
+        }
         cuda_check(cudaMemsetAsync(report_, 0, static_cast<size_t>(n) * D_.E * 4, cs), "memset hist");
         cuda_check(cudaMemsetAsync(report_ + static_cast<int64_t>(n) * D_.E, 0x7f, static_cast<size_t>(n) * D_.E * 4, cs),
                    "memset first");
@@ -780,10 +784,15 @@ void Engine::after_layer_gates(int step, int layer) {
     int32_t* prev = idx_[idx_cur_ ^ 1];
     // Part 1 of the readback: what close_block needs (per-batch histogram and
     // first demand, recorded ids), ahead of the permutation.
-    cuda_check(cudaMemcpyAsync(host_report_, report_, 2LL * n * D_.E * 4, cudaMemcpyDeviceToHost, cs), "d2h routing");
+    // Copied on rb_stream_ behind gates_done_: the compute stream goes on to
+    // the permutation without waiting for the PCIe round trip.
+    cuda_check(cudaEventRecord(gates_done_, cs), "gates done");
+    cuda_check(cudaStreamWaitEvent(rb_stream_, gates_done_, 0), "wait gates");
+    cuda_check(cudaMemcpyAsync(host_report_, report_, 2LL * n * D_.E * 4, cudaMemcpyDeviceToHost, rb_stream_),
+               "d2h routing");
     if (cfg_.record_trace)
-        cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, cs), "d2h idx");
-    cuda_check(cudaEventRecord(routing_ready_, cs), "routing ready");
+        cuda_check(cudaMemcpyAsync(host_idx_, cur, T * D_.k * 4, cudaMemcpyDeviceToHost, rb_stream_), "d2h idx");
+    cuda_check(cudaEventRecord(routing_ready_, rb_stream_), "routing ready");
     kl_check(kl_permute(cur, T, D_.k, D_.E, x2_, D_.d, counts_, offsets_, pos_, row_token_, xp_, perm_ws_, cs),
              "permute");
     shared_experts(layer, T, 0);
@@ -798,18 +807,22 @@ void Engine::after_layer_gates(int step, int layer) {
     cuda_check(cudaMemcpyAsync(marg_copy, marginal_, D_.E * 8, cudaMemcpyDeviceToDevice, cs), "marginal");
     // Part 2: the next layer's prefetch scores and the marginal (take_scores).
     const size_t head = reinterpret_cast<char*>(scores) - reinterpret_cast<char*>(report_);
+    cuda_check(cudaEventRecord(scores_done_, cs), "scores done");
+    cuda_check(cudaStreamWaitEvent(rb_stream_, scores_done_, 0), "wait scores");
     cuda_check(cudaMemcpyAsync(reinterpret_cast<char*>(host_report_) + head, scores, 2LL * D_.E * 8,
-                               cudaMemcpyDeviceToHost, cs), "d2h scores");
-    scores_op_ = next_exec_ - 1;  // this (last gate) op; its end event covers the copy
+                               cudaMemcpyDeviceToHost, rb_stream_), "d2h scores");
+    cuda_check(cudaEventRecord(scores_ready_, rb_stream_), "scores ready");
+    scores_pending_ = true;
+    readback_pending_ = true;
     idx_cur_ ^= 1;  // this layer's ids become "prev" for the next layer
 }
 
 // The prefetcher's next-layer scores of the last closed block (readback part
 // 2), once its gate op has completed; before the next block's decision.
 void Engine::take_scores() {
-    if (scores_op_ < 0) return;
-    cuda_check(cudaEventSynchronize(op_end_[scores_op_]), "scores sync");
-    scores_op_ = -1;
+    if (!scores_pending_) return;
+    cuda_check(cudaEventSynchronize(scores_ready_), "scores sync");
+    scores_pending_ = false;
     const int n = plan_.n_batches, E = D_.E;
     const int64_t* scores =
         reinterpret_cast<const int64_t*>(host_report_ + 2LL * n * E + 16 - ((2LL * n * E) % 16));
