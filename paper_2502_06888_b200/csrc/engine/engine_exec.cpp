@@ -142,6 +142,8 @@ void Engine::stamp(std::int32_t id, int side, cudaStream_t st) {
     if (slot < 0 || slot >= stamp_cap_)
         throw AccountingError("engine: op " + std::to_string(id) + " outside the step's timestamp window (" +
                               std::to_string(stamp_cap_) + " ops)");
+    static const bool off = std::getenv("KL_PROBE_NO_STAMPS") != nullptr;  // overhead probe only: no timeline
+    if (off) return;
     kl_check(kl_stamp(stamps_dev_ + 2 * slot + side, st), "op stamp");
 }
 
@@ -402,6 +404,17 @@ void Engine::issue_pending() {
     }
 }
 
+// A dependency whose event has already completed needs no stream wait; a
+// skipped wait keeps the stream's programmatic-dependent-launch chain intact
+// (a cudaStreamWaitEvent between two kernels makes the second one wait for
+// the first to finish before it can launch).
+static void wait_unless_done(cudaStream_t st, cudaEvent_t ev, const char* what) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) cuda_check(q, what);
+    cuda_check(cudaStreamWaitEvent(st, ev, 0), what);
+}
+
 void Engine::exec(std::int32_t id) {
     const StreamOp& op = em_->schedule().ops[id];
     const NvtxRange nvtx(op_kind_name(op.kind));
@@ -409,12 +422,12 @@ void Engine::exec(std::int32_t id) {
     for (std::int32_t d : op.deps) {
         if (d < timed_from_) continue;  // finished in an earlier (synchronized) step
         if (em_->schedule().ops[d].stream == op.stream) continue;  // FIFO on the same stream
-        cuda_check(cudaStreamWaitEvent(st, op_end_[d], 0), "dep wait");
+        wait_unless_done(st, op_end_[d], "dep wait");
     }
     op_end_[id] = event();
     const size_t E = static_cast<size_t>(El_);  // local expert shard
     auto wait_release = [&](cudaEvent_t ev) {
-        if (ev != nullptr) cuda_check(cudaStreamWaitEvent(st, ev, 0), "slot wait");
+        if (ev != nullptr) wait_unless_done(st, ev, "slot wait");
     };
     auto pick2 = [](std::vector<int>& busy) {
         for (int i = 0; i < 2; ++i)
