@@ -95,10 +95,12 @@ int kl_debug_spin_flag(const int* flag, cudaStream_t stream);
 /* Device timestamp: writes the GPU global timer (ns) into *dst (device
  * memory) when `stream` reaches this point; the engine's op-boundary marks. */
 int kl_stamp(unsigned long long* dst, cudaStream_t stream);
-/* The next GEMM launched by the calling host thread writes the same mark into
- * *dst itself -- from its first CTA once its stream predecessor is done --
- * instead of a separate kl_stamp kernel (the op's first kernel is then one
- * launch earlier); a non-streaming GEMM issues kl_stamp(dst) before itself. */
+/* The next launch by the calling host thread of a kernel that supports it
+ * (weight-streaming GEMM, decode-sized row RMSNorm, block-per-token router)
+ * writes the same mark into *dst itself -- from its first CTA once its stream
+ * predecessor is done -- instead of a separate kl_stamp kernel (the op's first
+ * kernel is then one launch earlier); the other launch paths of those entry
+ * points issue kl_stamp(dst) before themselves. */
 int kl_stamp_next_launch(unsigned long long* dst);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,

@@ -334,6 +334,8 @@ class Engine {
     // readback_done_ before it rewrites the device report.
     cudaStream_t rb_stream_ = nullptr;
     cudaEvent_t routing_ready_ = nullptr, gates_done_ = nullptr, scores_done_ = nullptr, scores_ready_ = nullptr;
+    std::int32_t start_mark_ = -1;  // op whose start the next kernel writes (take_start_mark before it)
+    void take_start_mark();
     bool scores_pending_ = false;   // a scores readback is in flight (take_scores syncs scores_ready_)
     bool readback_pending_ = false;  // scores_ready_ recorded and not yet waited for by the compute stream
     void take_scores();

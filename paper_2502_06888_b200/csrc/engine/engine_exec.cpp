@@ -147,6 +147,13 @@ void Engine::stamp(std::int32_t id, int side, cudaStream_t st) {
     kl_check(kl_stamp(stamps_dev_ + 2 * slot + side, st), "op stamp");
 }
 
+// The op whose start mark the next kernel launch writes (set by exec()).
+void Engine::take_start_mark() {
+    if (start_mark_ < 0) return;
+    stamp_next_launch(start_mark_);
+    start_mark_ = -1;
+}
+
 void Engine::stamp_next_launch(std::int32_t id) {
     const std::int64_t slot = static_cast<std::int64_t>(id) - timed_from_;
     if (slot < 0 || slot >= stamp_cap_)
@@ -586,12 +593,22 @@ void Engine::exec(std::int32_t id) {
             break;
         }
         case OpKind::compute_attention:
-            stamp(id, 0, st);
+            // bf16 decode: the op's first kernel (row RMSNorm) marks its start.
+            if (op.step != 0 && !cfg_.quant)
+                start_mark_ = id;
+            else
+                stamp(id, 0, st);
             exec_attention(op);
+            if (start_mark_ >= 0) throw AccountingError("engine: attention op start mark not taken");
             break;
         case OpKind::compute_gate:
-            stamp(id, 0, st);
+            // The router kernel marks the start when it is the op's first launch.
+            if (cfg_.variant != Variant::simple && !cfg_.replay && op.batch != 0)
+                start_mark_ = id;
+            else
+                stamp(id, 0, st);
             exec_gate(op);
+            if (start_mark_ >= 0) throw AccountingError("engine: gate op start mark not taken");
             break;
         case OpKind::compute_expert:
             // bf16 experts: the op's first GEMM marks its start itself.
@@ -657,6 +674,7 @@ void Engine::exec_attention(const StreamOp& op) {
     // epilogue (two launches instead of three); shapes off the weight-
     // streaming path fall back.
     if (step != 0 && !fused && rope_fused_ok_) {
+        take_start_mark();
         kl_check(kl_rmsnorm_rope_table(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, tok_pos_ + row0, D_.theta, D_.hd,
                                        rope_tab_, cs), "attn norm + rope table");
         const int rc = kl_gemm_bf16_qkv_rope(xa_, tpb, 0, tpb, D_.d, wqkv, D_.Hq, D_.Hkv, D_.hd, qkv_, D_.qkv_width(),
@@ -675,6 +693,7 @@ void Engine::exec_attention(const StreamOp& op) {
                (qkv_defer_ < 0 ? (qkv_defer_ = kl_gemm_deferred_splits(tpb, D_.qkv_width(), D_.d)) : qkv_defer_) > 0) {
         // Decode: the QKV GEMM leaves its tile-aligned k-splits as fp32
         // partials and the RoPE / KV-append kernel sums them (no fixup tail).
+        take_start_mark();
         kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
         kl_check(kl_gemm_bf16_deferred(xa_, tpb, 0, tpb, D_.d, wqkv, D_.qkv_width(), 0, qkvpart_,
                                        cfg_.workload.batch_size, qkv_defer_, gemm_ws_, gemm_ws_bytes_, cs),
@@ -684,6 +703,7 @@ void Engine::exec_attention(const StreamOp& op) {
                                             cs),
                  "rope/kv (deferred splits)");
     } else {
+        take_start_mark();
         kl_check(kl_rmsnorm(hb, norm_attn_[l], tpb, D_.d, D_.eps, xa_, cs), "attn norm");
         if (fused)
             kl_check(kl_gemm_q4(xa_, tpb, 0, tpb, D_.d, q4qkv, D_.qkv_width(), qkv_, D_.qkv_width(), nullptr, 0, gemm_ws_,
@@ -755,6 +775,7 @@ void Engine::exec_gate(const StreamOp& op) {
     int32_t* idx = idx_[idx_cur_] + row0 * D_.k;
     float* wt = weight_ + row0 * D_.k;
     const int odef = o_deferred_.empty() ? 0 : o_deferred_[static_cast<size_t>(b)];
+    take_start_mark();
     if (odef > 0) {
         // This batch's o-proj left split partials: the router kernel completes h first.
         o_deferred_[static_cast<size_t>(b)] = 0;

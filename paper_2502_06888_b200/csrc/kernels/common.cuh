@@ -157,6 +157,25 @@ __device__ __forceinline__ int kv_slot_of(int p, int cap, int sink) {
 // Entry of a kernel launched by launch_pdl: release the next kernel of the
 // stream at once (it may become resident and wait), then wait for the
 // previous kernel to complete before any global memory access.
+// Op start marks written by the op's first kernel (kl_stamp_next_launch):
+// the pending destination of this host thread, taken by the next launch of a
+// kernel that writes it (weight-streaming GEMM, row RMSNorm, block router);
+// other launch paths write it with a separate kl_stamp first.
+extern thread_local unsigned long long* t_next_start;
+inline unsigned long long* take_next_start() {
+    unsigned long long* p = t_next_start;
+    t_next_start = nullptr;
+    return p;
+}
+// CTA 0 / thread 0, after the kernel's dependency wait: the op start mark.
+__device__ __forceinline__ void write_start_mark(unsigned long long* t_start) {
+    if (t_start != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        *t_start = t;
+    }
+}
+
 __device__ __forceinline__ void pdl_enter() {
     griddep_launch_dependents();
     griddep_wait();

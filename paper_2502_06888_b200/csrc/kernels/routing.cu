@@ -158,8 +158,10 @@ gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
                        const uint16_t* __restrict__ wg, int T, int E, int k, float eps, int score_mode,
                        uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                        float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos,
-                       const float* __restrict__ hpart, int S, int64_t part_split_elems) {
+                       const float* __restrict__ hpart, int S, int64_t part_split_elems,
+                       unsigned long long* t_start) {
     pdl_enter();
+    write_start_mark(t_start);
     constexpr int d = NC * 256;
     __shared__ float lg[64];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -468,8 +470,9 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
 __global__ void __launch_bounds__(256)
 rmsnorm_row_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int d, float eps,
                    uint16_t* __restrict__ out, const int32_t* __restrict__ rope_pos, float rope_theta, int rope_hd,
-                   float2* __restrict__ rope_table) {
+                   float2* __restrict__ rope_table, unsigned long long* t_start) {
     pdl_enter();
+    write_start_mark(t_start);
     if (rope_table != nullptr && static_cast<int>(threadIdx.x) < rope_hd / 2) {
         // This token's RoPE cos/sin table for the QKV GEMM's fused epilogue.
         float cs, sn;
@@ -914,7 +917,10 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
         if (per_block)                                                                                            \
             return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream,   \
                               const_cast<uint16_t*>(h), norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx,       \
-                              weight, hist, first_pos, static_cast<const float*>(nullptr), 0, int64_t{0});           \
+                              weight, hist, first_pos, static_cast<const float*>(nullptr), 0, int64_t{0},            \
+                              take_next_start());                                                                  \
+        if (unsigned long long* ts = take_next_start())                                                           \
+            if (const int rc = kl_stamp(ts, stream)) return rc;                                                   \
         return launch_pdl(gate_topk_warp_kernel<NC>, dim3(blocks), dim3(128), 0, stream, h, norm_w, wg, T, E, k, eps, \
                           score_mode, x2, logits, idx, weight, hist, first_pos);
     switch (d / 256) {
@@ -926,6 +932,8 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
         default: break;
     }
 #undef KL_GATE_WARP
+    if (unsigned long long* ts = take_next_start())
+        if (const int rc = kl_stamp(ts, stream)) return rc;
     return launch_pdl(gate_topk_kernel, dim3(T), dim3(kGateWarps * 32), 0, stream, h, norm_w, wg, T, d, E, k, eps,
                       score_mode, x2, logits, idx, weight, hist, first_pos);
 }
@@ -944,7 +952,7 @@ extern "C" int kl_gate_topk_deferred(uint16_t* h, const float* h_part, int split
     case NC:                                                                                                      \
         return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, h,     \
                           norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos, h_part,   \
-                          splits, pse);
+                          splits, pse, take_next_start());
     switch (d / 256) {
         KL_GATE_DEF(2)
         KL_GATE_DEF(4)
@@ -963,7 +971,10 @@ extern "C" int kl_rmsnorm(const uint16_t* x, const uint16_t* w, int64_t T, int d
     if (T == 0) return KL_OK;
     if (T <= 4 * 148)
         return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out,
-                          static_cast<const int32_t*>(nullptr), 0.0f, 0, static_cast<float2*>(nullptr));
+                          static_cast<const int32_t*>(nullptr), 0.0f, 0, static_cast<float2*>(nullptr),
+                          take_next_start());
+    if (unsigned long long* ts = take_next_start())
+        if (const int rc = kl_stamp(ts, stream)) return rc;
     return launch_pdl(rmsnorm_kernel, dim3(grid_for(T, kWarpsPerBlock)), dim3(kWarpsPerBlock * 32), 0, stream, x, w, T,
                       d, eps, out);
 }
@@ -975,7 +986,7 @@ extern "C" int kl_rmsnorm_rope_table(const uint16_t* x, const uint16_t* w, int64
     if (T == 0) return KL_OK;
     if (T > 4 * 148) return KL_EUNSUPPORTED;  // decode-sized calls (block per row) only
     return launch_pdl(rmsnorm_row_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, x, w, d, eps, out, pos,
-                      theta, hd, reinterpret_cast<float2*>(table));
+                      theta, hd, reinterpret_cast<float2*>(table), take_next_start());
 }
 
 extern "C" int64_t kl_permute_workspace_bytes(int64_t R, int E) {
