@@ -102,6 +102,15 @@ int kl_stamp(unsigned long long* dst, cudaStream_t stream);
  * kernel is then one launch earlier); the other launch paths of those entry
  * points issue kl_stamp(dst) before themselves. */
 int kl_stamp_next_launch(unsigned long long* dst);
+/* The op-END counterpart: the next launch by the calling host thread of a
+ * kernel that supports it (the deferred-split GEMMs' streaming launch -- for
+ * kl_expert_ffn_kb_deferred its down projection -- and the block-per-token
+ * router) has its last CTA to finish write %globaltimer into *dst, counted on
+ * *counter (device u32, zero before first use; the writer resets it).
+ * kl_stamp_end_pending() clears a mark no launch took and returns 1 if there
+ * was one (the caller then issues kl_stamp itself). */
+int kl_stamp_end_next_launch(unsigned long long* dst, unsigned* counter);
+int kl_stamp_end_pending(void);
 int kl_gemm_bf16(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K,
                  const uint16_t* b, int N, uint16_t* c, int ldc, const uint16_t* r,
                  int epilogue, void* workspace, int64_t workspace_bytes, cudaStream_t stream);

@@ -686,6 +686,10 @@ void Engine::allocate_host() {
 }
 
 void Engine::init_weights() {
+    // Op end-mark counter (kl_stamp_end_next_launch): zero before first use,
+    // reset by each end-marking kernel's last CTA.
+    end_cnt_ = reinterpret_cast<unsigned*>(stamps_dev_ + 2 * stamp_cap_ + 4);
+    cuda_check(cudaMemset(end_cnt_, 0, sizeof(unsigned)), "end counter");
     cudaStream_t st = streams_[0];
     const std::uint64_t ws = cfg_.weight_seed;
     const float sd = 0.02f;

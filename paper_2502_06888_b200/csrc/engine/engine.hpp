@@ -335,6 +335,12 @@ class Engine {
     cudaStream_t rb_stream_ = nullptr;
     cudaEvent_t routing_ready_ = nullptr, gates_done_ = nullptr, scores_done_ = nullptr, scores_ready_ = nullptr;
     std::int32_t start_mark_ = -1;  // op whose start the next kernel writes (take_start_mark before it)
+    // Op end written by the op's last kernel (end_mark_next right before it);
+    // exec() falls back to a stamp kernel when no launch took the mark.
+    std::int32_t cur_op_ = -1;
+    bool end_set_ = false;
+    unsigned* end_cnt_ = nullptr;
+    void end_mark_next();
     void take_start_mark();
     bool scores_pending_ = false;   // a scores readback is in flight (take_scores syncs scores_ready_)
     bool readback_pending_ = false;  // scores_ready_ recorded and not yet waited for by the compute stream

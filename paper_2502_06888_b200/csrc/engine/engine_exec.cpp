@@ -154,6 +154,13 @@ void Engine::take_start_mark() {
     start_mark_ = -1;
 }
 
+void Engine::end_mark_next() {
+    const std::int64_t slot = static_cast<std::int64_t>(cur_op_) - timed_from_;
+    if (slot < 0 || slot >= stamp_cap_) return;  // exec() then stamps (and reports the window error)
+    kl_check(kl_stamp_end_next_launch(stamps_dev_ + 2 * slot + 1, end_cnt_), "end mark");
+    end_set_ = true;
+}
+
 void Engine::stamp_next_launch(std::int32_t id) {
     const std::int64_t slot = static_cast<std::int64_t>(id) - timed_from_;
     if (slot < 0 || slot >= stamp_cap_)
@@ -432,6 +439,8 @@ void Engine::exec(std::int32_t id) {
         wait_unless_done(st, op_end_[d], "dep wait");
     }
     op_end_[id] = event();
+    cur_op_ = id;
+    end_set_ = false;
     const size_t E = static_cast<size_t>(El_);  // local expert shard
     auto wait_release = [&](cudaEvent_t ev) {
         if (ev != nullptr) wait_unless_done(st, ev, "slot wait");
@@ -627,7 +636,8 @@ void Engine::exec(std::int32_t id) {
         combine_block(combine_step_);
         combine_step_ = -1;
     }
-    stamp(id, 1, st);
+    if (!end_set_ || kl_stamp_end_pending()) stamp(id, 1, st);
+    end_set_ = false;
     cuda_check(cudaEventRecord(op_end_[id], st), "record");
 }
 
@@ -731,6 +741,7 @@ void Engine::exec_attention(const StreamOp& op) {
                (o_defer_ < 0 ? (o_defer_ = kl_gemm_deferred_splits(tpb, D_.d, static_cast<int>(wo_k2))) : o_defer_) > 0) {
         // Decode: the o-proj leaves its tile-aligned k-splits as fp32 partials;
         // this batch's gate op completes h (+ residual) before its router.
+        end_mark_next();  // the op's last launch
         kl_check(kl_gemm_bf16_deferred(ao_, tpb, 0, tpb, static_cast<int>(wo_k2), wo, D_.d, 0,
                                        opart_ + static_cast<int64_t>(b) * 4 * cfg_.workload.batch_size * D_.d,
                                        cfg_.workload.batch_size, o_defer_, gemm_ws_, gemm_ws_bytes_, cs),
@@ -776,6 +787,7 @@ void Engine::exec_gate(const StreamOp& op) {
     float* wt = weight_ + row0 * D_.k;
     const int odef = o_deferred_.empty() ? 0 : o_deferred_[static_cast<size_t>(b)];
     take_start_mark();
+    if (!simple && !cfg_.replay && b != n - 1) end_mark_next();  // the router is the op's only launch
     if (odef > 0) {
         // This batch's o-proj left split partials: the router kernel completes h first.
         o_deferred_[static_cast<size_t>(b)] = 0;
@@ -1021,10 +1033,13 @@ void Engine::exec_expert(const StreamOp& op) {
         if (q4 && M <= 256)
             kl_check(kl_expert_ffn_q4(xp_, block_rows_, row0 + c, m, D_.d, D_.f, q13, q2, hs_, y_, gemm_ws_,
                                       gemm_ws_bytes_, cs), "expert ffn q4");
-        else if (block_defer_ > 0)  // down-projection splits left for the block's combine to sum
+        else if (block_defer_ > 0) {  // down-projection splits left for the block's combine to sum
+            // The down GEMM is the op's last launch unless the block's combine follows.
+            if (c + m >= M && !ep_ && exec_expert_left_ > 1) end_mark_next();
             kl_check(kl_expert_ffn_kb_deferred(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, ypart_,
                                                ypart_rows_, block_defer_, gemm_ws_, gemm_ws_bytes_, cs),
                      "expert ffn (deferred splits)");
+        }
         else if (expert_kblocked())  // bf16 experts (resident or streamed) are stored K-blocked
             kl_check(kl_expert_ffn_kb(xp_, block_rows_, row0 + c, m, D_.d, D_.f, w, w2, hs_, y_, gemm_ws_,
                                       gemm_ws_bytes_, cs), "expert ffn");

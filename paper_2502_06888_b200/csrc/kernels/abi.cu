@@ -59,6 +59,22 @@ __global__ void stamp_kernel(unsigned long long* dst) {
 }
 }  // namespace
 
+namespace kl {
+thread_local EndMark t_next_end{nullptr, nullptr};
+}
+
+extern "C" int kl_stamp_end_next_launch(unsigned long long* dst, unsigned* counter) {
+    if ((dst == nullptr) != (counter == nullptr)) return KL_EINVAL;
+    kl::t_next_end = kl::EndMark{dst, counter};
+    return KL_OK;
+}
+
+extern "C" int kl_stamp_end_pending(void) {
+    const bool pending = kl::t_next_end.t != nullptr;
+    kl::t_next_end = kl::EndMark{nullptr, nullptr};
+    return pending ? 1 : 0;
+}
+
 extern "C" int kl_stamp(unsigned long long* dst, cudaStream_t stream) {
     if (dst == nullptr) return KL_EINVAL;
     cudaLaunchConfig_t cfg{};

@@ -167,6 +167,31 @@ inline unsigned long long* take_next_start() {
     t_next_start = nullptr;
     return p;
 }
+// Op end marks written by the op's last kernel (kl_stamp_end_next_launch):
+// the last CTA to finish (a counter the engine owns, reset by that CTA)
+// writes %globaltimer. Taken explicitly by the launch paths that support it.
+struct EndMark {
+    unsigned long long* t;
+    unsigned* cnt;
+};
+extern thread_local EndMark t_next_end;
+inline EndMark take_next_end() {
+    const EndMark m = t_next_end;
+    t_next_end = EndMark{nullptr, nullptr};
+    return m;
+}
+// One thread per CTA, after every other thread of the CTA is done.
+__device__ __forceinline__ void write_end_mark(unsigned long long* t_end, unsigned* cnt) {
+    if (t_end == nullptr) return;
+    __threadfence();
+    const unsigned v = atomicAdd(cnt, 1u);
+    if (v == gridDim.x * gridDim.y * gridDim.z - 1) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        *t_end = t;
+        *cnt = 0u;
+    }
+}
 // CTA 0 / thread 0, after the kernel's dependency wait: the op start mark.
 __device__ __forceinline__ void write_start_mark(unsigned long long* t_start) {
     if (t_start != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {

@@ -498,6 +498,8 @@ struct StreamArgs {
     int debug;  // benchmarking only: bit0 skip MMAs, bit1 skip epilogue work
     int split;        // > 0: tile-aligned splits, S per tile (G = tiles x S); 0: stream-K ranges
     unsigned long long* t_start;  // op start mark: %globaltimer once the previous grid is done (kl_stamp_next_launch)
+    unsigned long long* t_end;    // op end mark: written by the last CTA to finish (kl_stamp_end_next_launch)
+    unsigned* end_cnt;
     // Deferred split reduction (kStore, NMMA 1, tile-aligned splits): every CTA
     // writes its fp32 accumulator to defer[split][row][feature] (row pitch
     // defer_ld) and the consumer sums the splits; no flags, no fixup.
@@ -1090,6 +1092,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
     if (threadIdx.x == 64) STREAM_TRACE(7);
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) write_end_mark(p.t_end, p.end_cnt);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, p.tmem_cols);
@@ -1261,8 +1264,11 @@ template <int EPI, int NMMA, bool Q4 = false>
 int launch_stream(const uint16_t* a, int64_t a_rows, int64_t row_offset, int M, int K, const uint16_t* b, int64_t b_rows,
                   int n_tiles, int half_rows, uint16_t* c, int ldc, const uint16_t* r, void* ws, int64_t ws_bytes,
                   cudaStream_t stream, const uint8_t* q4 = nullptr, bool wkb = false, const RopeArgs* rope = nullptr,
-                  float* defer = nullptr, int64_t defer_split_elems = 0, int defer_splits = 0) {
+                  float* defer = nullptr, int64_t defer_split_elems = 0, int defer_splits = 0,
+                  EndMark end = EndMark{nullptr, nullptr}) {
     StreamArgs p{};
+    p.t_end = end.t;
+    p.end_cnt = end.cnt;
     p.defer = defer;
     p.defer_split_elems = defer_split_elems;
     p.defer_ld = static_cast<int>(n_tiles) * kWRows * NMMA;
@@ -1697,7 +1703,7 @@ extern "C" int kl_gemm_bf16_deferred(const uint16_t* a, int64_t a_rows, int64_t 
     if (kl_gemm_deferred_splits(M, N, K) != splits) return KL_EUNSUPPORTED;
     return launch_stream<kStore, 1>(a, a_rows, row_offset, M, K, b, N, N / kWRows, 0, nullptr, N, nullptr, workspace,
                                     workspace_bytes, stream, nullptr, b_kblocked != 0, nullptr, c_part,
-                                    part_rows * N, splits);
+                                    part_rows * N, splits, take_next_end());
 }
 
 extern "C" int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total, int64_t row_offset, int M, int d,
@@ -1715,7 +1721,7 @@ extern "C" int kl_expert_ffn_kb_deferred(const uint16_t* xp, int64_t rows_total,
     if (rc) return rc;
     return launch_stream<kStore, 1>(h_scratch, M, 0, M, f, w2, d, d / kWRows, 0, nullptr, d, nullptr, workspace,
                                     workspace_bytes, stream, nullptr, true, nullptr, y_part + row_offset * d,
-                                    part_rows * d, splits);
+                                    part_rows * d, splits, take_next_end());
 }
 
 namespace kl {

@@ -159,7 +159,7 @@ gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
                        uint16_t* __restrict__ x2, float* __restrict__ logits_out, int32_t* __restrict__ idx,
                        float* __restrict__ weight, int32_t* __restrict__ hist, int32_t* __restrict__ first_pos,
                        const float* __restrict__ hpart, int S, int64_t part_split_elems,
-                       unsigned long long* t_start) {
+                       unsigned long long* t_start, EndMark end) {
     pdl_enter();
     write_start_mark(t_start);
     constexpr int d = NC * 256;
@@ -336,6 +336,7 @@ gate_topk_block_kernel(uint16_t* h, const uint16_t* __restrict__ norm_w,
         if (hist != nullptr) atomicAdd(&hist[sel[j]], 1);
         if (first_pos != nullptr) atomicMin(&first_pos[sel[j]], static_cast<int32_t>(r));
     }
+    write_end_mark(end.t, end.cnt);  // thread 0: the block's last live thread
 }
 
 // Latency-optimised router: one warp per token, the row held in registers
@@ -918,7 +919,7 @@ extern "C" int kl_gate_topk(const uint16_t* h, const uint16_t* norm_w, const uin
             return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream,   \
                               const_cast<uint16_t*>(h), norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx,       \
                               weight, hist, first_pos, static_cast<const float*>(nullptr), 0, int64_t{0},            \
-                              take_next_start());                                                                  \
+                              take_next_start(), take_next_end());                                                 \
         if (unsigned long long* ts = take_next_start())                                                           \
             if (const int rc = kl_stamp(ts, stream)) return rc;                                                   \
         return launch_pdl(gate_topk_warp_kernel<NC>, dim3(blocks), dim3(128), 0, stream, h, norm_w, wg, T, E, k, eps, \
@@ -952,7 +953,7 @@ extern "C" int kl_gate_topk_deferred(uint16_t* h, const float* h_part, int split
     case NC:                                                                                                      \
         return launch_pdl(gate_topk_block_kernel<NC>, dim3(static_cast<unsigned>(T)), dim3(256), 0, stream, h,     \
                           norm_w, wg, T, E, k, eps, score_mode, x2, logits, idx, weight, hist, first_pos, h_part,   \
-                          splits, pse, take_next_start());
+                          splits, pse, take_next_start(), take_next_end());
     switch (d / 256) {
         KL_GATE_DEF(2)
         KL_GATE_DEF(4)
