@@ -770,3 +770,43 @@ def test_gemm_persistent_large_m(K, cuda, M, N, Kd, epi):
         ref = orc.gemm_f32(a, b) + (orc.bits_to_f32(r) if epi == 1 else 0)
     close_bf16(to_bits(c), ref)
     assert torch.equal(c, c2)  # same per-tile arithmetic, different schedule
+
+
+@pytest.mark.gpu
+def test_kernel_written_op_marks(cuda, K):
+    """kl_stamp_next_launch / kl_stamp_end_next_launch: the row RMSNorm and
+    the block router write the start mark (after their dependency wait) and
+    the router's last CTA the end mark, on the caller's host thread only;
+    a launch path that cannot take an end mark leaves it pending."""
+    import ctypes as C
+    lib = K._lib
+    lib.kl_stamp_next_launch.argtypes = [C.c_void_p]
+    lib.kl_stamp_end_next_launch.argtypes = [C.c_void_p, C.c_void_p]
+    lib.kl_stamp_end_pending.restype = C.c_int
+    dev = torch.device("cuda:0")
+    T, d, E, k = 64, 4096, 8, 2
+    g = torch.Generator(device="cpu").manual_seed(3)
+    h = (torch.randn(T, d, generator=g) * 0.5).to(torch.bfloat16).to(dev)
+    nw = torch.ones(d, dtype=torch.bfloat16, device=dev)
+    wg = (torch.randn(E, d, generator=g) * 0.02).to(torch.bfloat16).to(dev)
+    marks = torch.zeros(4, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    x2_ref, idx_ref, w_ref = K.gate_topk(h.clone(), nw, wg, k)
+    assert lib.kl_stamp_next_launch(C.c_void_p(marks.data_ptr())) == 0
+    assert lib.kl_stamp_end_next_launch(C.c_void_p(marks.data_ptr() + 8), C.c_void_p(cnt.data_ptr())) == 0
+    x2, idx, w = K.gate_topk(h.clone(), nw, wg, k)
+    torch.cuda.synchronize()
+    assert lib.kl_stamp_end_pending() == 0  # the router took it
+    t = marks.cpu().tolist()
+    assert t[0] > 0 and t[1] >= t[0] and t[1] - t[0] < 10**9
+    assert int(cnt.item()) == 0  # reset by the last CTA
+    assert torch.equal(idx, idx_ref) and torch.equal(w, w_ref) and torch.equal(x2, x2_ref)
+    # RMSNorm takes a start mark but not an end mark: the end stays pending.
+    assert lib.kl_stamp_next_launch(C.c_void_p(marks.data_ptr() + 16)) == 0
+    assert lib.kl_stamp_end_next_launch(C.c_void_p(marks.data_ptr() + 24), C.c_void_p(cnt.data_ptr())) == 0
+    K.rmsnorm(h, nw)
+    torch.cuda.synchronize()
+    assert lib.kl_stamp_end_pending() == 1
+    assert lib.kl_stamp_end_pending() == 0
+    t = marks.cpu().tolist()
+    assert t[2] > 0 and t[3] == 0
