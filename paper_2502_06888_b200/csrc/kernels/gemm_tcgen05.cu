@@ -1056,8 +1056,31 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                                 stage[(col + i) * kWRows + frow] = f2bf(v);
                         }
                     }
+                    if (etid == 0) STREAM_TRACE(10);
                     named_bar_sync(1, 128);
                     const int vec = kWRows / 8;  // 16-byte vectors per token row
+                    if (EPI != kResidual && p.rope_tab == nullptr) {
+                        // Plain rows: four 16-byte vectors per thread in flight
+                        // (smem loads first, then the global stores).
+                        const int nv = p.M * vec;
+                        int v = etid;
+                        for (; v + 3 * 128 < nv; v += 4 * 128) {
+                            uint4 q[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int vv = v + u * 128;
+                                q[u] = *reinterpret_cast<const uint4*>(stage + (vv / vec) * kWRows + (vv % vec) * 8);
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int vv = v + u * 128;
+                                *reinterpret_cast<uint4*>(p.c + static_cast<int64_t>(vv / vec) * p.ldc + feat0 + (vv % vec) * 8) = q[u];
+                            }
+                        }
+                        for (; v < nv; v += 128)
+                            *reinterpret_cast<uint4*>(p.c + static_cast<int64_t>(v / vec) * p.ldc + feat0 + (v % vec) * 8) =
+                                *reinterpret_cast<const uint4*>(stage + (v / vec) * kWRows + (v % vec) * 8);
+                    } else
                     for (int v = etid; v < p.M * vec; v += 128) {
                         const int row = v / vec, x = v % vec;
                         uint16_t* o = p.c + static_cast<int64_t>(row) * p.ldc + feat0 + x * 8;
@@ -1081,6 +1104,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_cons
                             *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(stage + row * kWRows + x * 8);
                         }
                     }
+                    if (etid == 0) STREAM_TRACE(11);
                     named_bar_sync(1, 128);
                 }
             }

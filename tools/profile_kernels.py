@@ -36,7 +36,7 @@ def dump_trace(label):
     rel = (a - t0) / 1e3
     rel[a == 0] = np.nan
     names = ["start", "mma0", "mma_end", "epi_last", "flags_ok", "landed", "sums_done", "end", "contrib0",
-             "published"]
+             "published", "staged", "stored"]
     print(f"trace {label} (us from first CTA start)")
     for i, nm in enumerate(names):
         col = rel[:, i]
