@@ -725,30 +725,44 @@ combine_deferred_kernel(const float* __restrict__ yp, int S, int64_t split_elems
     for (int i = threadIdx.x; i < n8; i += kRowThreads) {
         const uint4 rq = *reinterpret_cast<const uint4*>(resid + t * d + i * 8);
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // Up to two routed rows' partials loaded before the first add (one
+        // memory latency per pair of rows instead of one per row).
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            if (j >= k) break;
-            const float* base = yp + static_cast<int64_t>(p[j]) * d + i * 8;
-            const float4* own = reinterpret_cast<const float4*>(base + static_cast<int64_t>(S - 1) * split_elems);
-            const float4 o0 = __ldg(own), o1 = __ldg(own + 1);
-            float4 q0[3], q1[3];
+        for (int j0 = 0; j0 < KMAX; j0 += 2) {
+            if (j0 >= k) break;
+            float4 o0[2], o1[2], q0[2][3], q1[2][3];
 #pragma unroll
-            for (int sp = 0; sp < 3; ++sp)
-                if (sp < S - 1) {
-                    const float4* src = reinterpret_cast<const float4*>(base + sp * split_elems);
-                    q0[sp] = __ldg(src);
-                    q1[sp] = __ldg(src + 1);
-                }
-            float y[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = j0 + jj;
+                if (j >= k) break;
+                const float* base = yp + static_cast<int64_t>(p[j]) * d + i * 8;
+                const float4* own = reinterpret_cast<const float4*>(base + static_cast<int64_t>(S - 1) * split_elems);
+                o0[jj] = __ldg(own);
+                o1[jj] = __ldg(own + 1);
 #pragma unroll
-            for (int sp = 0; sp < 3; ++sp) {
-                if (sp >= S - 1) break;
-                const float q[8] = {q0[sp].x, q0[sp].y, q0[sp].z, q0[sp].w, q1[sp].x, q1[sp].y, q1[sp].z, q1[sp].w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) y[e] = __fadd_rn(y[e], q[e]);
+                for (int sp = 0; sp < 3; ++sp)
+                    if (sp < S - 1) {
+                        const float4* src = reinterpret_cast<const float4*>(base + sp * split_elems);
+                        q0[jj][sp] = __ldg(src);
+                        q1[jj][sp] = __ldg(src + 1);
+                    }
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = fmaf(w[j], bf2f(f2bf(y[e])), acc[e]);
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = j0 + jj;
+                if (j >= k) break;
+                float y[8] = {o0[jj].x, o0[jj].y, o0[jj].z, o0[jj].w, o1[jj].x, o1[jj].y, o1[jj].z, o1[jj].w};
+#pragma unroll
+                for (int sp = 0; sp < 3; ++sp) {
+                    if (sp >= S - 1) break;
+                    const float q[8] = {q0[jj][sp].x, q0[jj][sp].y, q0[jj][sp].z, q0[jj][sp].w,
+                                        q1[jj][sp].x, q1[jj][sp].y, q1[jj][sp].z, q1[jj][sp].w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) y[e] = __fadd_rn(y[e], q[e]);
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = fmaf(w[j], bf2f(f2bf(y[e])), acc[e]);
+            }
         }
         const uint32_t rw[4] = {rq.x, rq.y, rq.z, rq.w};
         float rv[8];
